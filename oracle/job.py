@@ -1,0 +1,80 @@
+"""CPU oracle job: train one task in numpy (test infrastructure / CPU baseline).
+
+``python -m oracle.job --model cnn --seed 3 --steps 20 [--bf16 0|1] [--json]``
+accepts the same flags as the product's job entry point
+(``python -m paper_2410_22254_b200.job``), so one parametric task list drives
+the packed runtime, the K-process PyTorch baseline and this CPU path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+
+import numpy as np
+
+from . import models, optim, rng
+
+
+def add_job_args(ap: argparse.ArgumentParser) -> None:
+    ap.add_argument("--model", choices=sorted(models.MODEL_NAMES), default="mlp")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--optim", choices=sorted(optim.OPT_NAMES), default="adam")
+    ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--beta1", type=float, default=0.9)
+    ap.add_argument("--beta2", type=float, default=0.999)
+    ap.add_argument("--eps", type=float, default=1e-8)
+    ap.add_argument("--wd", type=float, default=0.0)
+    ap.add_argument("--momentum", type=float, default=0.0)
+
+
+def train(model: int, seed: int, steps: int, batch: int, opt: optim.OptState,
+          bf16: bool = True, timer: bool = False):
+    """Run ``steps`` steps; returns (losses [steps], final flat params, seconds/step)."""
+    params = models.init_params(model, seed)
+    flat = models.flatten_params(model, params)
+    step_fn = models.STEP_FNS[model]
+    losses = np.zeros(steps, np.float32)
+    t_first = None
+    t0 = time.perf_counter()
+    for t in range(steps):
+        if t == 1:
+            t_first = time.perf_counter()
+        px, y = rng.batch(seed, t, batch)
+        loss, g = step_fn(models.unflatten(model, flat), px, y, bf16=bf16)
+        gflat = models.flatten_params(model, g)
+        flat = optim.step(opt, flat, gflat)
+        losses[t] = loss
+    t1 = time.perf_counter()
+    per_step = (t1 - (t_first if t_first is not None else t0)) / max(1, steps - (1 if t_first else 0))
+    return losses, flat, per_step
+
+
+def opt_from_args(a) -> optim.OptState:
+    return optim.OptState(kind=optim.OPT_NAMES[a.optim], lr=a.lr, beta1=a.beta1, beta2=a.beta2,
+                          eps=a.eps, weight_decay=a.wd, momentum=a.momentum)
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="oracle.job")
+    add_job_args(ap)
+    ap.add_argument("--bf16", type=int, default=1)
+    ap.add_argument("--json", action="store_true")
+    a = ap.parse_args(argv)
+    model = models.MODEL_NAMES[a.model]
+    losses, _, per_step = train(model, a.seed, a.steps, a.batch, opt_from_args(a), bool(a.bf16))
+    out = {
+        "model": a.model, "seed": a.seed, "steps": a.steps, "batch": a.batch,
+        "samples_per_s": a.batch / per_step if per_step > 0 else None,
+        "first_loss": float(losses[0]), "last_loss": float(losses[-1]),
+    }
+    print(json.dumps(out) if a.json else out)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

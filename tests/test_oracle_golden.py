@@ -1,0 +1,76 @@
+"""Pin the numpy oracle against PyTorch CPU golden vectors (tests/golden/torch_golden.npz).
+
+The reference has no training arithmetic; the paper's jobs are
+PyTorch trainings, so PyTorch fp32 is the authority.  The
+oracle in plain-fp32 mode must reproduce torch's loss curve and final weights
+for MLP (Adam, AdamW, SGD-momentum+wd) and CNN (Adam).
+
+Tolerances: loss |d| <= 1e-5; sampled final weights |d| <= 5e-5 absolute
+(= 5% of one lr=1e-3 Adam step; Adam's m/sqrt(v) amplifies fp32 summation-order
+noise on near-zero gradients), per-tensor norms rel <= 1e-4.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import job, models, optim, rng
+from oracle.bf16 import round_bf16, to_bf16_bits
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "torch_golden.npz"))
+RUNS = [
+    ("mlp_adam", models.MODEL_MLP, 16, 6, "adam", dict(lr=1e-3)),
+    ("mlp_adamw", models.MODEL_MLP, 16, 4, "adamw", dict(lr=2e-3, weight_decay=0.1)),
+    ("mlp_sgd", models.MODEL_MLP, 16, 4, "sgd", dict(lr=0.05, momentum=0.9, weight_decay=1e-4)),
+    ("cnn_adam", models.MODEL_CNN, 4, 3, "adam", dict(lr=1e-3)),
+]
+
+
+@pytest.mark.parametrize("run", RUNS, ids=[r[0] for r in RUNS])
+def test_oracle_matches_torch(run):
+    name, model, batch, steps, opt, kw = run
+    st = optim.OptState(kind=optim.OPT_NAMES[opt], **kw)
+    losses, flat, _ = job.train(model, 11, steps, batch, st, bf16=False)
+    np.testing.assert_allclose(losses, G[f"{name}/losses"], atol=1e-5, rtol=0)
+    idx = G[f"{name}/idx"]
+    np.testing.assert_allclose(flat[idx], G[f"{name}/sample"], atol=5e-5, rtol=0)
+    params = models.unflatten(model, flat)
+    norms = [np.linalg.norm(params[t.name]) for t in models.TENSORS[model]]
+    np.testing.assert_allclose(norms, G[f"{name}/norms"], rtol=1e-4)
+
+
+def test_param_counts_match_survey():
+    # SURVEY.md Appendix B
+    assert models.layout(models.MODEL_MLP)[1] == 669_706
+    assert models.layout(models.MODEL_CNN)[1] == 1_199_882
+    for m in (models.MODEL_MLP, models.MODEL_CNN):
+        lay, _, stride = models.layout(m)
+        assert all(off % models.ALIGN == 0 for _, off in lay) and stride % models.ALIGN == 0
+
+
+def test_rng_known_answers():
+    # splitmix64 reference value (Vigna's test vector for seed 0 first output)
+    assert rng.splitmix64_int(0) == 0xE220A8397B1DCDAF
+    px, y = rng.batch(0, 0, 64)
+    assert px.dtype == np.uint8 and px.shape == (64, 784)
+    assert np.bincount(y, minlength=10).min() > 0  # every class appears
+    # labels are exact integer argmax
+    s = (2 * px.astype(np.int64) - 255) @ rng.teacher().T.astype(np.int64)
+    assert (np.argmax(s, axis=1) == y).all()
+
+
+def test_bf16_rounding_rne():
+    x = np.array([1.0, 1.00390625, 1.01171875, -2.5, 3.0e-3, 65504.0], np.float32)
+    r = round_bf16(x)
+    assert r[1] == 1.0  # tie -> even
+    assert r[2] == np.float32(1.015625)
+    assert to_bf16_bits(np.float32([1.0]))[0] == 0x3F80
+
+
+def test_oracle_bf16_mode_close_to_fp32():
+    st1 = optim.OptState(kind=optim.ADAM, lr=1e-3)
+    st2 = optim.OptState(kind=optim.ADAM, lr=1e-3)
+    l1, _, _ = job.train(models.MODEL_CNN, 3, 3, 8, st1, bf16=True)
+    l2, _, _ = job.train(models.MODEL_CNN, 3, 3, 8, st2, bf16=False)
+    np.testing.assert_allclose(l1, l2, atol=2e-2)
