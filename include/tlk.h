@@ -53,6 +53,7 @@ extern "C" {
 #define TLK_BUF_LOSS 5    /* fp32 [lanes, max_steps] per-step mean loss  */
 #define TLK_BUF_PIXELS 6  /* u8   [lanes, batch, 784] current input batch */
 #define TLK_BUF_LABELS 7  /* i32  [lanes, batch] current labels          */
+#define TLK_BUF_ACTS 8    /* model activation scratch (debug/tests; layout per model) */
 
 typedef struct tlk_ctx tlk_ctx;
 

@@ -1,0 +1,393 @@
+// Model-independent kernels of a pack step: synthetic inputs, lane init,
+// fused classifier head (Linear + softmax-CE + its backward), batched
+// optimizer over every lane's flat parameter arena, step bookkeeping.
+#include <cmath>
+
+#include "pack.cuh"
+#include "rng.cuh"
+#include "tlk_ptx.cuh"
+
+namespace tlk {
+
+// ------------------------------------------------------------ teacher -------
+int build_teacher(int8_t** dev_out) {
+  std::vector<int8_t> t(CLASSES * PIXELS);
+  const uint64_t k = rng_key(TEACHER_SEED, STREAM_TEACHER, 0);
+  for (int i = 0; i < CLASSES * PIXELS; ++i)
+    t[i] = int8_t(int((rng_bits(k, uint64_t(i)) >> 60) & 15) - 8);
+  TLK_CUDA(cudaMalloc(reinterpret_cast<void**>(dev_out), t.size()));
+  TLK_CUDA(cudaMemcpy(*dev_out, t.data(), t.size(), cudaMemcpyHostToDevice));
+  return TLK_OK;
+}
+
+// ------------------------------------------------------------ inputs --------
+// One CTA per (sample, lane).  Generates (or takes from the host-input
+// buffers) the sample's 784 pixel codes, writes them as bf16 k/256 into x and
+// computes the teacher label with exact int32 arithmetic.
+__global__ void __launch_bounds__(128) inputs_kernel(const LaneState* __restrict__ lanes,
+                                                     uint64_t seed, int step, int batch,
+                                                     const int8_t* __restrict__ teacher,
+                                                     uint8_t* __restrict__ px,
+                                                     int32_t* __restrict__ labels,
+                                                     uint16_t* __restrict__ x, int host_input) {
+  const int s = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  if (lanes) {
+    if (!lanes[j].active) return;
+    seed = lanes[j].seed;
+    step = lanes[j].steps_done;
+  }
+  __shared__ __align__(16) uint8_t pix[PIXELS];
+  __shared__ int part[4][CLASSES];
+  const size_t row = size_t(j) * batch + s;
+  uint64_t* px_row = reinterpret_cast<uint64_t*>(px + row * PIXELS);
+  if (!host_input) {
+    const uint64_t key = rng_key(seed, STREAM_DATA, uint64_t(step));
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x) {
+      uint64_t h = rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
+      reinterpret_cast<uint64_t*>(pix)[q] = h;
+      px_row[q] = h;
+    }
+  } else {
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x)
+      reinterpret_cast<uint64_t*>(pix)[q] = px_row[q];
+  }
+  __syncthreads();
+  if (x) {
+    uint4* xr = reinterpret_cast<uint4*>(x + row * PIXELS);
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[i] = pack_bf2(float(pix[q * 8 + 2 * i]) * (1.0f / 256.0f),
+                        float(pix[q * 8 + 2 * i + 1]) * (1.0f / 256.0f));
+      xr[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  if (host_input) return;
+  int acc[CLASSES];
+#pragma unroll
+  for (int c = 0; c < CLASSES; ++c) acc[c] = 0;
+  for (int i = tid; i < PIXELS; i += blockDim.x) {
+    const int v = 2 * int(pix[i]) - 255;
+#pragma unroll
+    for (int c = 0; c < CLASSES; ++c) acc[c] += int(teacher[c * PIXELS + i]) * v;
+  }
+#pragma unroll
+  for (int c = 0; c < CLASSES; ++c) {
+    int a = acc[c];
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((tid & 31) == 0) part[tid >> 5][c] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int best = 0, bestv = 0;
+    for (int c = 0; c < CLASSES; ++c) {
+      int v = part[0][c] + part[1][c] + part[2][c] + part[3][c];
+      if (c == 0 || v > bestv) {
+        best = c;
+        bestv = v;
+      }
+    }
+    labels[row] = best;
+  }
+}
+
+int enqueue_inputs(Pack& p, cudaStream_t st) {
+  inputs_kernel<<<dim3(p.batch, p.lanes), 128, 0, st>>>(p.lane_dev, 0, 0, p.batch, p.teacher,
+                                                       p.pixels, p.labels, p.x, p.host_input);
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teacher, uint8_t* px,
+                        int32_t* labels, cudaStream_t st) {
+  inputs_kernel<<<dim3(batch, 1), 128, 0, st>>>(nullptr, seed, step, batch, teacher, px, labels,
+                                                nullptr, 0);
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+// ----------------------------------------------------- transposed shadows --
+// Model-specific bf16 copies in a second layout, refreshed wherever the bf16
+// shadow is written.  CNN: conv2.w (oc, tap, ic) -> wt (ic, tap, oc) so that
+// the conv2 dgrad GEMM reads its B operand K-major.
+struct WtHook {
+  uint16_t* wt;
+  int64_t wt_stride;
+  int64_t off;    // start of the source tensor in the arena
+  int64_t count;  // its element count
+};
+__device__ __forceinline__ void wt_write(const WtHook& h, int lane, int64_t e, uint16_t b) {
+  if (!h.wt) return;
+  int64_t r = e - h.off;
+  if (r < 0 || r >= h.count) return;
+  int oc = int(r / 288), t = int(r % 288), tap = t >> 5, ic = t & 31;
+  h.wt[lane * h.wt_stride + ic * 576 + tap * 64 + oc] = b;
+}
+static WtHook wt_hook(const Pack& p) {
+  WtHook h{nullptr, 0, 0, 0};
+  if (p.model == TLK_MODEL_CNN && p.wt) {
+    h.wt = p.wt;
+    h.wt_stride = p.wt_stride;
+    h.off = tensor_offset(*p.def, 2);
+    h.count = p.def->t[2].count;
+  }
+  return h;
+}
+
+// ------------------------------------------------------------ lane init -----
+TensorTable make_tensor_table(const ModelDef& d) {
+  TensorTable t{};
+  t.n = d.ntensors;
+  for (int i = 0; i < d.ntensors; ++i) {
+    t.off[i] = tensor_offset(d, i);
+    t.count[i] = d.t[i].count;
+    t.bound[i] = float(1.0 / std::sqrt(double(d.t[i].fan_in)));
+  }
+  return t;
+}
+
+__global__ void lane_init_kernel(TensorTable tt, uint64_t seed, int lane, int64_t stride,
+                                 float* params, float* grads, float* m1, float* m2,
+                                 uint16_t* wbf, WtHook hook) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < stride;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    float v = 0.0f;
+#pragma unroll 1
+    for (int t = 0; t < tt.n; ++t) {
+      int64_t r = e - tt.off[t];
+      if (r >= 0 && r < tt.count[t]) {
+        v = init_value(rng_key(seed, STREAM_INIT + t, 0), uint64_t(r), tt.bound[t]);
+        break;
+      }
+    }
+    const int64_t i = lane * stride + e;
+    params[i] = v;
+    grads[i] = 0.0f;
+    m1[i] = 0.0f;
+    m2[i] = 0.0f;
+    const uint16_t b = f2bf(v);
+    wbf[i] = b;
+    wt_write(hook, lane, e, b);
+  }
+}
+
+int enqueue_lane_init(Pack& p, int lane, cudaStream_t st) {
+  TensorTable tt = make_tensor_table(*p.def);
+  int blocks = int((p.stride + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  lane_init_kernel<<<blocks, 256, 0, st>>>(tt, p.lane_host[lane].seed, lane, p.stride, p.params,
+                                            p.grads, p.mom1, p.mom2, p.wbf, wt_hook(p));
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+// ------------------------------------------------------------ head ----------
+// Fused classifier head for one lane per CTA:
+//   logits = h W^T + b (fp32 master W), loss = mean CE, dlogits = (softmax -
+//   onehot)/B, dW = dlogits^T h, db = sum_b dlogits,
+//   dz_prev = bf16(dlogits W * [h > 0]), db_prev = sum_b dz_prev.
+// Also derives the lane's optimizer scalars for this step.
+template <int H>
+__global__ void __launch_bounds__(256) head_kernel(LaneState* __restrict__ lanes, int B,
+                                                   const uint16_t* __restrict__ h,
+                                                   const float* __restrict__ params,
+                                                   float* __restrict__ grads, int64_t stride,
+                                                   int64_t w_off, int64_t b_off,
+                                                   const int32_t* __restrict__ labels,
+                                                   uint16_t* __restrict__ dz_prev,
+                                                   int64_t db_prev_off, float* __restrict__ loss,
+                                                   int max_steps, float* __restrict__ last_loss) {
+  constexpr int C = CLASSES;
+  const int j = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!lanes[j].active) return;
+  extern __shared__ float sh[];
+  float* logit = sh;          // [B][C]
+  float* d = sh + B * C;      // [B][C]
+  float* lossb = d + B * C;   // [B]
+  const float* W = params + j * stride + w_off;
+  const float* bias = params + j * stride + b_off;
+  const uint16_t* hj = h + size_t(j) * B * H;
+
+  for (int b = warp; b < B; b += 8) {
+    float acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0f;
+    for (int k = lane; k < H; k += 32) {
+      const float hv = bf2f(hj[b * H + k]);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] += hv * W[c * H + k];
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float a = acc[c];
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) logit[b * C + c] = a + bias[c];
+    }
+  }
+  __syncthreads();
+  if (tid < B) {
+    const int y = labels[size_t(j) * B + tid];
+    const float* l = logit + tid * C;
+    float m = l[0];
+    for (int c = 1; c < C; ++c) m = fmaxf(m, l[c]);
+    float e[C], s = 0.0f;
+    for (int c = 0; c < C; ++c) {
+      e[c] = expf(l[c] - m);
+      s += e[c];
+    }
+    lossb[tid] = (m + logf(s)) - l[y];
+    for (int c = 0; c < C; ++c) d[tid * C + c] = (e[c] / s - (c == y ? 1.0f : 0.0f)) / float(B);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += lossb[b];
+    const float L = s / float(B);
+    LaneState& ls = lanes[j];
+    loss[size_t(j) * max_steps + ls.steps_done] = L;
+    last_loss[j] = L;
+    lane_step_scalars(ls);
+  }
+  float* G = grads + j * stride;
+  for (int k = tid; k < H; k += blockDim.x) {
+    float acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0f;
+    float dbp = 0.0f;
+    for (int b = 0; b < B; ++b) {
+      const float hv = bf2f(hj[b * H + k]);
+      float dh = 0.0f;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float dv = d[b * C + c];
+        acc[c] += dv * hv;
+        dh += dv * W[c * H + k];
+      }
+      const uint16_t zb = f2bf(hv > 0.0f ? dh : 0.0f);
+      dz_prev[size_t(j) * B * H + b * H + k] = zb;
+      dbp += bf2f(zb);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) G[w_off + c * H + k] = acc[c];
+    G[db_prev_off + k] = dbp;
+  }
+  if (tid < C) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += d[b * C + tid];
+    G[b_off + tid] = s;
+  }
+}
+
+int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_t w_off,
+                 int64_t b_off, uint16_t* dz_prev, int64_t db_prev_off) {
+  const size_t smem = size_t(p.batch) * (2 * CLASSES + 1) * sizeof(float);
+  if (hidden == 512)
+    head_kernel<512><<<p.lanes, 256, smem, st>>>(p.lane_dev, p.batch, h, p.params, p.grads,
+                                                 p.stride, w_off, b_off, p.labels, dz_prev,
+                                                 db_prev_off, p.loss, p.max_steps, p.last_loss);
+  else if (hidden == 128)
+    head_kernel<128><<<p.lanes, 256, smem, st>>>(p.lane_dev, p.batch, h, p.params, p.grads,
+                                                 p.stride, w_off, b_off, p.labels, dz_prev,
+                                                 db_prev_off, p.loss, p.max_steps, p.last_loss);
+  else
+    return fail(TLK_EINVAL, "head: unsupported hidden %d", hidden);
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+// ------------------------------------------------------------ optimizer -----
+// One launch over every lane's padded fp32 arena (float4 per thread): reads
+// p, g, m, v (16 B/param), writes p, m, v (12 B) + the bf16 GEMM shadow (2 B).
+// Every op is an explicit IEEE-rounded intrinsic in the same order as
+// oracle/optim.py, so the update is bit-exact given identical gradients.
+__device__ __forceinline__ void opt_one(const LaneState& s, float& p, float g, float& m, float& v) {
+  if (s.optimizer == TLK_OPT_SGD) {
+    if (s.wd != 0.0f) g = __fadd_rn(g, __fmul_rn(p, s.wd));
+    if (s.momentum != 0.0f) {
+      m = s.first_step ? g : __fadd_rn(__fmul_rn(m, s.momentum), g);
+      g = m;
+    }
+    p = __fsub_rn(p, __fmul_rn(s.lr, g));
+    return;
+  }
+  if (s.optimizer == TLK_OPT_ADAMW)
+    p = __fmul_rn(p, s.decay);
+  else if (s.wd != 0.0f)
+    g = __fadd_rn(g, __fmul_rn(p, s.wd));
+  m = __fadd_rn(m, __fmul_rn(s.w1, __fsub_rn(g, m)));
+  v = __fadd_rn(__fmul_rn(v, s.b2f), __fmul_rn(__fmul_rn(g, g), s.w2));
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), s.bc2s), s.eps);
+  p = __fsub_rn(p, __fmul_rn(s.step_size, __fdiv_rn(m, denom)));
+}
+
+__global__ void __launch_bounds__(256) optimizer_kernel(const LaneState* __restrict__ lanes,
+                                                        int nlanes, int64_t stride,
+                                                        float4* __restrict__ P,
+                                                        const float4* __restrict__ Gr,
+                                                        float4* __restrict__ M,
+                                                        float4* __restrict__ V,
+                                                        uint2* __restrict__ Wb, WtHook hook) {
+  const int64_t n4 = int64_t(nlanes) * stride / 4;
+  const int64_t s4 = stride / 4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = int(i / s4);
+    const LaneState& s = lanes[lane];
+    if (!s.active) continue;
+    float4 p = P[i], m = M[i], v = V[i];
+    const float4 g = Gr[i];
+    opt_one(s, p.x, g.x, m.x, v.x);
+    opt_one(s, p.y, g.y, m.y, v.y);
+    opt_one(s, p.z, g.z, m.z, v.z);
+    opt_one(s, p.w, g.w, m.w, v.w);
+    P[i] = p;
+    M[i] = m;
+    V[i] = v;
+    const uint32_t lo = pack_bf2(p.x, p.y), hi = pack_bf2(p.z, p.w);
+    Wb[i] = make_uint2(lo, hi);
+    if (hook.wt) {
+      const int64_t e = (i - lane * s4) * 4;
+      wt_write(hook, lane, e + 0, uint16_t(lo & 0xFFFF));
+      wt_write(hook, lane, e + 1, uint16_t(lo >> 16));
+      wt_write(hook, lane, e + 2, uint16_t(hi & 0xFFFF));
+      wt_write(hook, lane, e + 3, uint16_t(hi >> 16));
+    }
+  }
+}
+
+int enqueue_optimizer(Pack& p, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n4 = int64_t(p.lanes) * p.stride / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  const int64_t cap = int64_t(sms) * 8;
+  if (blocks > cap) blocks = cap;
+  optimizer_kernel<<<int(blocks), 256, 0, st>>>(
+      p.lane_dev, p.lanes, p.stride, reinterpret_cast<float4*>(p.params),
+      reinterpret_cast<const float4*>(p.grads), reinterpret_cast<float4*>(p.mom1),
+      reinterpret_cast<float4*>(p.mom2), reinterpret_cast<uint2*>(p.wbf), wt_hook(p));
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+// ------------------------------------------------------------ end of step ---
+__global__ void end_step_kernel(LaneState* lanes, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  LaneState& s = lanes[j];
+  if (!s.active) return;
+  s.b1t *= double(s.beta1);
+  s.b2t *= double(s.beta2);
+  s.steps_done += 1;
+  s.active = s.steps_done < s.steps;
+}
+
+int enqueue_end_step(Pack& p, cudaStream_t st) {
+  end_step_kernel<<<(p.lanes + 127) / 128, 128, 0, st>>>(p.lane_dev, p.lanes);
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+}  // namespace tlk

@@ -1,0 +1,75 @@
+// Pack = K job lanes of one model co-resident on one GPU, plus the launch
+// sequence of one training step for all of them.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "models.cuh"
+#include "tlk_common.cuh"
+
+namespace tlk {
+
+struct Pack {
+  // description
+  int model = 0, batch = 0, lanes = 0, max_steps = 0, host_input = 0;
+  const ModelDef* def = nullptr;
+  int64_t pcount = 0, stride = 0;
+  // lane table
+  LaneState* lane_dev = nullptr;
+  std::vector<LaneState> lane_host;
+  // per-lane arenas [lanes, stride]
+  float *params = nullptr, *grads = nullptr, *mom1 = nullptr, *mom2 = nullptr;
+  uint16_t* wbf = nullptr;
+  float* loss = nullptr;       // [lanes, max_steps]
+  float* last_loss = nullptr;  // [lanes]
+  // inputs
+  uint8_t* pixels = nullptr;   // [lanes, batch, 784]
+  int32_t* labels = nullptr;   // [lanes, batch]
+  uint16_t* x = nullptr;       // [lanes, batch, 784] bf16 (k/256)
+  const int8_t* teacher = nullptr;  // [10, 784] (context-owned)
+  // model scratch (one allocation, carved by the model's alloc function)
+  void* scratch = nullptr;            // host-side struct of device pointers
+  void (*scratch_free)(void*) = nullptr;
+  void* acts = nullptr;          // activation scratch base (TLK_BUF_ACTS)
+  size_t acts_bytes = 0;
+  uint16_t* wt = nullptr;       // transposed bf16 weight copies (model specific)
+  int64_t wt_stride = 0;
+  // all device allocations of this pack, freed on destroy
+  std::vector<void*> allocs;
+  // CUDA graph of one step
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int launches_per_step = 0;
+};
+
+// Device allocation that records ownership; reports "out of memory" on failure.
+int pack_alloc(Pack& p, void** ptr, size_t bytes);
+
+// Model hooks.
+int mlp_setup(Pack& p);
+int mlp_enqueue_step(Pack& p, cudaStream_t st);
+int cnn_setup(Pack& p);
+int cnn_enqueue_step(Pack& p, cudaStream_t st);
+
+// Common kernels (kernels.cu).
+struct TensorTable {
+  int n;
+  int64_t off[MAX_TENSORS];
+  int64_t count[MAX_TENSORS];
+  float bound[MAX_TENSORS];
+};
+TensorTable make_tensor_table(const ModelDef& d);
+
+int enqueue_inputs(Pack& p, cudaStream_t st);  // datagen (or host-input convert)
+int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_t w_off,
+                 int64_t b_off, uint16_t* dz_prev, int64_t db_prev_off);
+int enqueue_optimizer(Pack& p, cudaStream_t st);
+int enqueue_end_step(Pack& p, cudaStream_t st);
+int enqueue_lane_init(Pack& p, int lane, cudaStream_t st);
+int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teacher, uint8_t* px,
+                        int32_t* labels, cudaStream_t st);
+int build_teacher(int8_t** dev_out);
+
+}  // namespace tlk

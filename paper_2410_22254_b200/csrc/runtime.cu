@@ -1,0 +1,393 @@
+// libtlk C ABI: contexts (one per GPU), packs of K job lanes, graph-captured
+// steps, host-buffer end-to-end steps, result readback.  See include/tlk.h.
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "pack.cuh"
+
+namespace tlk {
+
+// ------------------------------------------------------------ errors --------
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(TLK_EOOM, "out of memory: %s (%s)", what, cudaGetErrorString(e));
+  return fail(TLK_ECUDA, "CUDA error %s at %s", cudaGetErrorString(e), what);
+}
+
+int pack_alloc(Pack& p, void** ptr, size_t bytes) {
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TLK_EOOM, "out of memory: pack allocation of %zu bytes failed (%s)", bytes,
+                cudaGetErrorString(e));
+  }
+  p.allocs.push_back(*ptr);
+  return TLK_OK;
+}
+
+}  // namespace tlk
+
+using namespace tlk;
+
+struct tlk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int8_t* teacher = nullptr;
+  std::vector<std::unique_ptr<Pack>> packs;
+};
+
+namespace {
+
+void destroy_pack(Pack& p) {
+  if (p.graph_exec) cudaGraphExecDestroy(p.graph_exec);
+  if (p.graph) cudaGraphDestroy(p.graph);
+  for (void* a : p.allocs) cudaFree(a);
+  p.allocs.clear();
+  if (p.scratch && p.scratch_free) p.scratch_free(p.scratch);
+  p.scratch = nullptr;
+}
+
+int get_pack(tlk_ctx* ctx, int32_t id, Pack** out) {
+  TLK_CHECK(ctx, TLK_EINVAL, "null context");
+  TLK_CHECK(id >= 0 && id < int32_t(ctx->packs.size()) && ctx->packs[id], TLK_EINVAL,
+            "bad pack id %d", id);
+  TLK_CUDA(cudaSetDevice(ctx->device));
+  *out = ctx->packs[id].get();
+  return TLK_OK;
+}
+
+int enqueue_step(Pack& p, cudaStream_t st) {
+  switch (p.model) {
+    case TLK_MODEL_MLP: return mlp_enqueue_step(p, st);
+    case TLK_MODEL_CNN: return cnn_enqueue_step(p, st);
+  }
+  return fail(TLK_EINVAL, "unknown model %d", p.model);
+}
+
+int ensure_graph(Pack& p, cudaStream_t st) {
+  if (p.graph_exec) return TLK_OK;
+  TLK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step(p, st);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  TLK_CUDA(e);
+  p.graph = g;
+  TLK_CUDA(cudaGraphInstantiate(&p.graph_exec, g, 0));
+  return TLK_OK;
+}
+
+int upload_lane(tlk_ctx* ctx, Pack& p, int lane) {
+  TLK_CUDA(cudaMemcpyAsync(p.lane_dev + lane, &p.lane_host[lane], sizeof(LaneState),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  return TLK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tlk_abi_version(void) { return TLK_ABI_VERSION; }
+const char* tlk_last_error(void) { return g_err; }
+
+int tlk_model_query(int32_t model, int32_t batch, tlk_model_info* out) {
+  const ModelDef* d = model_def(model);
+  TLK_CHECK(d && out, TLK_EINVAL, "unknown model %d", model);
+  out->param_count = param_count(*d);
+  out->param_stride = param_stride(*d);
+  out->flops_per_sample = 6 * d->macs_per_sample;
+  out->num_tensors = d->ntensors;
+  (void)batch;
+  return TLK_OK;
+}
+
+int tlk_model_tensor(int32_t model, int32_t t, int64_t* offset, int64_t* count, int32_t* fan_in) {
+  const ModelDef* d = model_def(model);
+  TLK_CHECK(d && t >= 0 && t < d->ntensors, TLK_EINVAL, "bad model/tensor %d/%d", model, t);
+  if (offset) *offset = tensor_offset(*d, t);
+  if (count) *count = d->t[t].count;
+  if (fan_in) *fan_in = d->t[t].fan_in;
+  return TLK_OK;
+}
+
+int tlk_open(int32_t device, tlk_ctx** out) {
+  TLK_CHECK(out, TLK_EINVAL, "null out");
+  int n = 0;
+  TLK_CUDA(cudaGetDeviceCount(&n));
+  TLK_CHECK(device >= 0 && device < n, TLK_EINVAL, "device %d not visible (%d devices)", device,
+            n);
+  TLK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  TLK_CUDA(cudaGetDeviceProperties(&prop, device));
+  TLK_CHECK(prop.major == 10 && prop.minor == 0, TLK_ESTATE,
+            "libtlk is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major,
+            prop.minor);
+  auto ctx = std::make_unique<tlk_ctx>();
+  ctx->device = device;
+  TLK_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  int rc = build_teacher(&ctx->teacher);
+  if (rc) return rc;
+  *out = ctx.release();
+  return TLK_OK;
+}
+
+int tlk_close(tlk_ctx* ctx) {
+  if (!ctx) return TLK_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& p : ctx->packs)
+    if (p) destroy_pack(*p);
+  if (ctx->teacher) cudaFree(ctx->teacher);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TLK_OK;
+}
+
+int tlk_sync(tlk_ctx* ctx) {
+  TLK_CHECK(ctx, TLK_EINVAL, "null context");
+  TLK_CUDA(cudaSetDevice(ctx->device));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TLK_OK;
+}
+
+int tlk_stream(tlk_ctx* ctx, void** stream) {
+  TLK_CHECK(ctx && stream, TLK_EINVAL, "null argument");
+  *stream = ctx->stream;
+  return TLK_OK;
+}
+
+int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
+  TLK_CHECK(ctx && desc && pack_id, TLK_EINVAL, "null argument");
+  const ModelDef* d = model_def(desc->model);
+  TLK_CHECK(d, TLK_EINVAL, "unknown model %d", desc->model);
+  TLK_CHECK(desc->lanes >= 1 && desc->lanes <= 4096, TLK_EINVAL, "lanes must be 1..4096");
+  TLK_CHECK(desc->batch >= 8 && desc->batch <= 64 && desc->batch % 8 == 0, TLK_EINVAL,
+            "batch must be a multiple of 8 in [8, 64] (got %d)", desc->batch);
+  TLK_CHECK(desc->max_steps >= 1, TLK_EINVAL, "max_steps must be >= 1");
+  TLK_CUDA(cudaSetDevice(ctx->device));
+  auto p = std::make_unique<Pack>();
+  p->model = desc->model;
+  p->batch = desc->batch;
+  p->lanes = desc->lanes;
+  p->max_steps = desc->max_steps;
+  p->host_input = desc->host_input;
+  p->def = d;
+  p->pcount = param_count(*d);
+  p->stride = param_stride(*d);
+  p->teacher = ctx->teacher;
+  const size_t L = size_t(p->lanes), S = size_t(p->stride), B = size_t(p->batch);
+  int rc = 0;
+  void* v = nullptr;
+  auto grab = [&](size_t bytes) -> void* {
+    if (rc) return nullptr;
+    rc = pack_alloc(*p, &v, bytes);
+    return rc ? nullptr : v;
+  };
+  p->lane_dev = static_cast<LaneState*>(grab(L * sizeof(LaneState)));
+  p->params = static_cast<float*>(grab(L * S * 4));
+  p->grads = static_cast<float*>(grab(L * S * 4));
+  p->mom1 = static_cast<float*>(grab(L * S * 4));
+  p->mom2 = static_cast<float*>(grab(L * S * 4));
+  p->wbf = static_cast<uint16_t*>(grab(L * S * 2));
+  p->loss = static_cast<float*>(grab(L * size_t(p->max_steps) * 4));
+  p->last_loss = static_cast<float*>(grab(L * 4));
+  p->pixels = static_cast<uint8_t*>(grab(L * B * 784));
+  p->labels = static_cast<int32_t*>(grab(L * B * 4));
+  p->x = static_cast<uint16_t*>(grab(L * B * 784 * 2));
+  if (!rc) rc = (p->model == TLK_MODEL_MLP) ? mlp_setup(*p) : cnn_setup(*p);
+  if (rc) {
+    destroy_pack(*p);
+    return rc;
+  }
+  p->lane_host.assign(L, LaneState{});
+  TLK_CUDA(cudaMemsetAsync(p->lane_dev, 0, L * sizeof(LaneState), ctx->stream));
+  TLK_CUDA(cudaMemsetAsync(p->loss, 0, L * size_t(p->max_steps) * 4, ctx->stream));
+  TLK_CUDA(cudaMemsetAsync(p->params, 0, L * S * 4, ctx->stream));
+  TLK_CUDA(cudaMemsetAsync(p->grads, 0, L * S * 4, ctx->stream));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->packs.push_back(std::move(p));
+  *pack_id = int32_t(ctx->packs.size() - 1);
+  return TLK_OK;
+}
+
+int tlk_lane_load(tlk_ctx* ctx, int32_t pack, int32_t lane, const tlk_job_desc* job) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(job && lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
+  TLK_CHECK(job->steps >= 1 && job->steps <= p->max_steps, TLK_EINVAL,
+            "steps %d outside 1..max_steps=%d", job->steps, p->max_steps);
+  TLK_CHECK(job->optimizer == TLK_OPT_ADAM || job->optimizer == TLK_OPT_ADAMW ||
+                job->optimizer == TLK_OPT_SGD,
+            TLK_EINVAL, "unknown optimizer %d", job->optimizer);
+  TLK_CHECK(job->lr > 0.0f && job->eps > 0.0f, TLK_EINVAL, "lr and eps must be positive");
+  LaneState s{};
+  s.active = 1;
+  s.steps_done = 0;
+  s.steps = job->steps;
+  s.optimizer = job->optimizer;
+  s.lr = job->lr;
+  s.beta1 = job->beta1;
+  s.beta2 = job->beta2;
+  s.eps = job->eps;
+  s.wd = job->weight_decay;
+  s.momentum = job->momentum;
+  s.seed = job->seed;
+  s.b1t = 1.0;
+  s.b2t = 1.0;
+  p->lane_host[lane] = s;
+  if ((rc = enqueue_lane_init(*p, lane, ctx->stream))) return rc;
+  TLK_CUDA(cudaMemsetAsync(p->loss + size_t(lane) * p->max_steps, 0, size_t(p->max_steps) * 4,
+                           ctx->stream));
+  return upload_lane(ctx, *p, lane);
+}
+
+int tlk_lane_release(tlk_ctx* ctx, int32_t pack, int32_t lane) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
+  TLK_CUDA(cudaMemcpyAsync(&p->lane_host[lane], p->lane_dev + lane, sizeof(LaneState),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  p->lane_host[lane].active = 0;
+  return upload_lane(ctx, *p, lane);
+}
+
+int tlk_run(tlk_ctx* ctx, int32_t pack, int32_t steps) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(steps >= 0, TLK_EINVAL, "steps must be >= 0");
+  TLK_CHECK(!p->host_input, TLK_ESTATE, "host-input pack: use tlk_step_host");
+  if ((rc = ensure_graph(*p, ctx->stream))) return rc;
+  for (int i = 0; i < steps; ++i) TLK_CUDA(cudaGraphLaunch(p->graph_exec, ctx->stream));
+  return TLK_OK;
+}
+
+int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
+                  float* losses_out) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(p->host_input, TLK_ESTATE, "pack was created without host_input");
+  TLK_CHECK(pixels && labels, TLK_EINVAL, "null input buffers");
+  const size_t L = size_t(p->lanes), B = size_t(p->batch);
+  TLK_CUDA(cudaMemcpyAsync(p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, ctx->stream));
+  TLK_CUDA(cudaMemcpyAsync(p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if ((rc = ensure_graph(*p, ctx->stream))) return rc;
+  TLK_CUDA(cudaGraphLaunch(p->graph_exec, ctx->stream));
+  if (losses_out) {
+    TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, L * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return TLK_OK;
+}
+
+int tlk_lane_status_get(tlk_ctx* ctx, int32_t pack, int32_t lane, tlk_lane_status* out) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(out && lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
+  LaneState s;
+  TLK_CUDA(cudaMemcpyAsync(&s, p->lane_dev + lane, sizeof(s), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->active = s.active;
+  out->steps_done = s.steps_done;
+  out->steps = s.steps;
+  out->error = 0;
+  return TLK_OK;
+}
+
+int tlk_lane_losses(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int32_t n) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(host && lane >= 0 && lane < p->lanes && n >= 0 && n <= p->max_steps, TLK_EINVAL,
+            "bad lane/n");
+  TLK_CUDA(cudaMemcpyAsync(host, p->loss + size_t(lane) * p->max_steps, size_t(n) * 4,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TLK_OK;
+}
+
+int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64_t n) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(host && lane >= 0 && lane < p->lanes && n >= 0 && n <= p->stride, TLK_EINVAL,
+            "bad lane/n");
+  TLK_CUDA(cudaMemcpyAsync(host, p->params + size_t(lane) * p->stride, size_t(n) * 4,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TLK_OK;
+}
+
+int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, int64_t* bytes) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(dev_ptr && bytes, TLK_EINVAL, "null argument");
+  const int64_t L = p->lanes, S = p->stride, B = p->batch;
+  switch (which) {
+    case TLK_BUF_PARAMS: *dev_ptr = p->params; *bytes = L * S * 4; break;
+    case TLK_BUF_GRADS: *dev_ptr = p->grads; *bytes = L * S * 4; break;
+    case TLK_BUF_MOM1: *dev_ptr = p->mom1; *bytes = L * S * 4; break;
+    case TLK_BUF_MOM2: *dev_ptr = p->mom2; *bytes = L * S * 4; break;
+    case TLK_BUF_WBF16: *dev_ptr = p->wbf; *bytes = L * S * 2; break;
+    case TLK_BUF_LOSS: *dev_ptr = p->loss; *bytes = L * int64_t(p->max_steps) * 4; break;
+    case TLK_BUF_PIXELS: *dev_ptr = p->pixels; *bytes = L * B * 784; break;
+    case TLK_BUF_LABELS: *dev_ptr = p->labels; *bytes = L * B * 4; break;
+    case TLK_BUF_ACTS: *dev_ptr = p->acts; *bytes = int64_t(p->acts_bytes); break;
+    default: return fail(TLK_EINVAL, "unknown buffer %d", which);
+  }
+  return TLK_OK;
+}
+
+int tlk_pack_launches_per_step(tlk_ctx* ctx, int32_t pack, int32_t* n) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(n, TLK_EINVAL, "null argument");
+  *n = p->launches_per_step;
+  return TLK_OK;
+}
+
+int tlk_selftest_datagen(uint64_t seed, int32_t step, int32_t batch, uint8_t* pixels_dev,
+                         int32_t* labels_dev, void* stream) {
+  TLK_CHECK(pixels_dev && labels_dev && batch > 0, TLK_EINVAL, "bad arguments");
+  static int8_t* teacher = nullptr;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!teacher) {
+      int rc = build_teacher(&teacher);
+      if (rc) return rc;
+    }
+  }
+  return enqueue_datagen_raw(seed, step, batch, teacher, pixels_dev, labels_dev,
+                             static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -37,7 +37,9 @@ struct PlainGemm {
     if (n >= N || k >= K) return nullptr;
     return BMN ? B + (size_t(w.j) * K + k) * N + n : B + (size_t(w.j) * N + n) * K + k;
   }
-  TLK_DEV void epilogue(const Work& w, int m, int n0, const float (&v)[32]) const {
+  struct Carry {};
+  TLK_DEV void finish(const Work&, int, Carry&) const {}
+  TLK_DEV void epilogue(const Work& w, int m, int n0, const float (&v)[32], Carry&) const {
     if (m >= M) return;
     float* c = C + (size_t(w.j) * M + m) * N;
 #pragma unroll

@@ -153,13 +153,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) tc_gemm_kernel(const P p) {
   mbar_wait(&done_bar, 0);
   tc_fence_after();
   const int row = warp * 32 + lane;
+  typename P::Carry carry{};
 #pragma unroll 1
   for (int cc = 0; cc < BN / 32; ++cc) {
     float v[32];
     tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
-    p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v);
+    p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v, carry);
   }
-  // BN not a multiple of 32 (e.g. 16 or 48): handled by problems choosing BN%32==0.
+  p.finish(w, w.m0 + row, carry);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);

@@ -1,0 +1,232 @@
+"""Packed training parity: K lanes trained by libtlk vs the numpy oracle.
+
+Each lane of a pack is compared with an independent oracle run of the same
+task (same seed -> same init and data, same optimizer).  The oracle runs in
+its bf16-emulation mode (rounds exactly the tensors the GPU rounds), so the
+only differences are fp32 summation order.  Stated tolerances:
+
+* init weights and synthetic data: bit-exact;
+* teacher-forced step: layer-wise (oracle fed the GPU's own layer inputs)
+  bf16 outputs equal up to rare 1-ulp midpoint flips and grads rel-L2 <= 1e-5;
+  whole-step grads from the GPU's pre-step params rel-L2 <= 3e-2 (one flip of
+  a large activation perturbs the whole sample downstream); optimizer update
+  BIT-EXACT given the GPU's grads;
+* free-running trajectories: per-step loss |d| <= 5e-3 * max(1, |L|);
+  final weights rel-L2 per tensor <= 1e-2 for SGD and <= 6e-2 for Adam/AdamW.
+  (Adam's m/sqrt(v) maps the sign of near-zero gradients to +-lr, so
+  summation-order noise on those elements is amplified into whole-step
+  differences; SGD is near-linear and shows the arithmetic agreement.)
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import job as ojob
+from oracle import models as omodels
+from oracle import optim as ooptim
+from paper_2410_22254_b200 import runtime as rt
+
+pytestmark = pytest.mark.gpu
+
+LOSS_TOL = 5e-3
+W_TOL = {ooptim.SGD: 1e-2, ooptim.ADAM: 6e-2, ooptim.ADAMW: 6e-2}
+GRAD_TOL = 3e-2
+
+
+def _oracle(model, seed, steps, batch, opt, **kw):
+    st = ooptim.OptState(kind=opt, **kw)
+    return ojob.train(model, seed, steps, batch, st, bf16=True)
+
+
+def _rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _check_lane(model, pack, lane, seed, steps, batch, opt, **kw):
+    losses_ref, flat_ref, _ = _oracle(model, seed, steps, batch, opt, **kw)
+    got = pack.losses(lane, steps)
+    tol = LOSS_TOL * np.maximum(1.0, np.abs(losses_ref))
+    assert np.all(np.abs(got - losses_ref) <= tol), (lane, got[:5], losses_ref[:5])
+    params = pack.params(lane)
+    lay, _, _ = omodels.layout(model)
+    for t, off in lay:
+        r = _rel_l2(params[off:off + t.count], flat_ref[off:off + t.count])
+        assert r <= W_TOL[opt], (lane, t.name, r)
+
+
+@pytest.mark.parametrize("model", [omodels.MODEL_MLP])
+def test_init_bit_exact(model):
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(model, 64, 2, 4)
+        for lane, seed in enumerate((5, 2**33 + 1)):
+            pack.load(lane, seed=seed, steps=1)
+        ctx.sync()
+        for lane, seed in enumerate((5, 2**33 + 1)):
+            ref = omodels.flatten_params(model, omodels.init_params(model, seed))
+            assert np.array_equal(pack.params(lane), ref)
+
+
+def test_mlp_pack_matches_oracle():
+    steps, batch = 12, 64
+    jobs = [
+        (0, ooptim.ADAM, dict(lr=1e-3)),
+        (1, ooptim.ADAM, dict(lr=3e-3, beta1=0.8)),
+        (2, ooptim.ADAMW, dict(lr=2e-3, weight_decay=0.05)),
+        (3, ooptim.SGD, dict(lr=0.05, momentum=0.9, weight_decay=1e-4)),
+    ]
+    names = {"beta1": "beta1", "beta2": "beta2", "weight_decay": "weight_decay", "momentum": "momentum"}
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(omodels.MODEL_MLP, batch, len(jobs), steps)
+        for lane, (seed, opt, kw) in enumerate(jobs):
+            pack.load(lane, seed=seed, steps=steps, optimizer=opt, **{names.get(k, k): v for k, v in kw.items()})
+        pack.run(steps)
+        ctx.sync()
+        for lane, (seed, opt, kw) in enumerate(jobs):
+            st = pack.status(lane)
+            assert st.steps_done == steps and st.active == 0
+            _check_lane(omodels.MODEL_MLP, pack, lane, seed, steps, batch, opt, **kw)
+
+
+def test_mlp_lanes_with_different_lengths_stop_independently():
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(omodels.MODEL_MLP, 64, 3, 10)
+        for lane, steps in enumerate((3, 10, 6)):
+            pack.load(lane, seed=lane, steps=steps)
+        pack.run(10)
+        ctx.sync()
+        for lane, steps in enumerate((3, 10, 6)):
+            s = pack.status(lane)
+            assert (s.steps_done, s.active) == (steps, 0)
+            _check_lane(omodels.MODEL_MLP, pack, lane, lane, steps, 64, ooptim.ADAM, lr=1e-3)
+
+
+def test_host_input_step_matches_device_generated():
+    from oracle import rng
+
+    lanes, batch = 2, 64
+    with rt.Context(0) as ctx:
+        dev = ctx.pack(omodels.MODEL_MLP, batch, lanes, 4)
+        host = ctx.pack(omodels.MODEL_MLP, batch, lanes, 4, host_input=True)
+        for p in (dev, host):
+            for lane in range(lanes):
+                p.load(lane, seed=lane + 10, steps=4)
+        dev.run(4)
+        for t in range(4):
+            px = np.stack([rng.batch(lane + 10, t, batch)[0] for lane in range(lanes)])
+            lb = np.stack([rng.batch(lane + 10, t, batch)[1] for lane in range(lanes)])
+            out = host.step_host(px, lb)
+            assert out.shape == (lanes,)
+        ctx.sync()
+        for lane in range(lanes):
+            assert np.array_equal(dev.losses(lane, 4), host.losses(lane, 4))
+            assert np.array_equal(dev.params(lane), host.params(lane))
+
+
+def test_zero_copy_tensor_view():
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(omodels.MODEL_MLP, 64, 2, 2)
+        pack.load(0, seed=9, steps=2)
+        ctx.sync()
+        t = pack.tensor(rt.BUF_PARAMS)
+        assert t.is_cuda and t.numel() == 2 * pack.info.param_stride
+        ref = omodels.flatten_params(omodels.MODEL_MLP, omodels.init_params(omodels.MODEL_MLP, 9))
+        assert np.array_equal(t[: pack.info.param_stride].cpu().numpy(), ref)
+
+
+def _bf(u16):
+    return (u16.astype(np.uint32) << 16).view(np.float32)
+
+
+def _ulp_close(gpu, ref, what, frac=2e-3):
+    """bf16 tensors equal except for rare 1-ulp rounding flips (values that sit
+    on a rounding midpoint within fp32 summation-order noise)."""
+    diff = gpu != ref
+    n = int(diff.sum())
+    assert n <= max(2, frac * gpu.size), (what, n, gpu.size)
+    if n:
+        # one bf16 ulp, plus an absolute floor for values produced by heavy
+        # cancellation (tensor-core fp32 accumulation noise relative to the
+        # terms, not to the small result)
+        bound = 2.0**-7 * np.abs(ref[diff]) + 2.0**-12 * np.abs(ref).max()
+        excess = np.abs(gpu[diff] - ref[diff]) - bound
+        assert excess.max() <= 0, (what, excess.max())
+
+
+def _mlp_layerwise(pack, lane, seed, t, p0, g, batch):
+    """Oracle fed the GPU's own layer inputs (TLK_BUF_ACTS = h1, h2, dz1, dz2)."""
+    from oracle import rng
+    from oracle.bf16 import round_bf16 as r
+
+    L, n = pack.lanes, batch * 512
+    acts = pack.tensor(rt.BUF_ACTS).cpu().numpy().astype(np.uint16)
+    h1, h2, dz1, dz2 = [_bf(acts[(k * L + lane) * n:(k * L + lane + 1) * n]).reshape(batch, 512)
+                        for k in range(4)]
+    prm = omodels.unflatten(omodels.MODEL_MLP, p0)
+    px, y = rng.batch(seed, t, batch)
+    x = px.astype(np.float32) / np.float32(256)
+    w1, w2 = r(prm["fc1.w"]), r(prm["fc2.w"])
+    _ulp_close(h1, r(np.maximum(x @ w1.T + prm["fc1.b"], 0)), "h1")
+    _ulp_close(h2, r(np.maximum(h1 @ w2.T + prm["fc2.b"], 0)), "h2")
+    loss, g3w, g3b, dh2 = omodels.head(h2, prm["fc3.w"], prm["fc3.b"], y)
+    _ulp_close(dz2, r(dh2 * (h2 > 0)), "dz2")
+    _ulp_close(dz1, r((dz2 @ w2) * (h1 > 0)), "dz1")
+    ref = {"fc3.w": g3w, "fc3.b": g3b, "fc2.w": dz2.T @ h1, "fc2.b": dz2.sum(0),
+           "fc1.w": dz1.T @ x, "fc1.b": dz1.sum(0)}
+    for tt, off in omodels.layout(omodels.MODEL_MLP)[0]:
+        got = g[off:off + tt.count]
+        assert _rel_l2(got, ref[tt.name].reshape(-1)) <= 1e-5, (t, lane, tt.name)
+
+
+LAYERWISE = {omodels.MODEL_MLP: _mlp_layerwise}
+
+
+def _teacher_forced(model, lanes_cfg, steps, batch=64):
+    """Per step: (1) layer-wise -- the oracle fed the GPU's own inputs of each
+    layer reproduces its outputs (bf16: up to rare 1-ulp flips) and its
+    gradients (rel-L2 <= 1e-5); (2) whole-step grads from the GPU's pre-step
+    params within GRAD_TOL (flips cascade); (3) the optimizer update on the
+    GPU's grads is BIT-EXACT with oracle.optim."""
+    from oracle import rng
+
+    step_fn = omodels.STEP_FNS[model]
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(model, batch, len(lanes_cfg), steps)
+        for lane, (seed, opt, kw) in enumerate(lanes_cfg):
+            pack.load(lane, seed=seed, steps=steps, optimizer=opt, **kw)
+        P, G = pack.tensor(rt.BUF_PARAMS), pack.tensor(rt.BUF_GRADS)
+        M1, M2 = pack.tensor(rt.BUF_MOM1), pack.tensor(rt.BUF_MOM2)
+        S = pack.info.param_stride
+        states = [ooptim.OptState(kind=opt, **kw) for _, opt, kw in lanes_cfg]
+        for t in range(steps):
+            ctx.sync()
+            before = [(P[l * S:(l + 1) * S].cpu().numpy(), M1[l * S:(l + 1) * S].cpu().numpy(),
+                       M2[l * S:(l + 1) * S].cpu().numpy()) for l in range(len(lanes_cfg))]
+            pack.run(1)
+            ctx.sync()
+            for lane, (seed, opt, kw) in enumerate(lanes_cfg):
+                p0, m0, v0 = before[lane]
+                g = G[lane * S:(lane + 1) * S].cpu().numpy()
+                LAYERWISE[model](pack, lane, seed, t, p0, g, batch)
+                px, y = rng.batch(seed, t, batch)
+                _, gref = step_fn(omodels.unflatten(model, p0), px, y, bf16=True)
+                gflat = omodels.flatten_params(model, gref)
+                for tt, off in omodels.layout(model)[0]:
+                    sl = slice(off, off + tt.count)
+                    assert _rel_l2(g[sl], gflat[sl]) <= GRAD_TOL, (t, lane, tt.name)
+                st = states[lane]
+                st.m, st.v = m0.copy(), v0.copy()
+                p1 = ooptim.step(st, p0, g)
+                got = P[lane * S:(lane + 1) * S].cpu().numpy()
+                assert np.array_equal(got, p1), (t, lane, np.abs(got - p1).max())
+                assert np.array_equal(M1[lane * S:(lane + 1) * S].cpu().numpy(), st.m)
+                assert np.array_equal(M2[lane * S:(lane + 1) * S].cpu().numpy(), st.v)
+
+
+def test_mlp_teacher_forced_grads_and_bit_exact_update():
+    _teacher_forced(omodels.MODEL_MLP, [
+        (21, ooptim.ADAM, dict(lr=1e-3)),
+        (22, ooptim.ADAMW, dict(lr=2e-3, weight_decay=0.1)),
+        (23, ooptim.SGD, dict(lr=0.05, momentum=0.9, weight_decay=1e-4)),
+        (24, ooptim.ADAM, dict(lr=1e-3, weight_decay=1e-2, beta2=0.99)),
+    ], steps=4)
