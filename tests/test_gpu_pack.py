@@ -55,7 +55,7 @@ def _check_lane(model, pack, lane, seed, steps, batch, opt, **kw):
         assert r <= W_TOL[opt], (lane, t.name, r)
 
 
-@pytest.mark.parametrize("model", [omodels.MODEL_MLP])
+@pytest.mark.parametrize("model", [omodels.MODEL_MLP, omodels.MODEL_CNN])
 def test_init_bit_exact(model):
     with rt.Context(0) as ctx:
         pack = ctx.pack(model, 64, 2, 4)
@@ -178,7 +178,78 @@ def _mlp_layerwise(pack, lane, seed, t, p0, g, batch):
         assert _rel_l2(got, ref[tt.name].reshape(-1)) <= 1e-5, (t, lane, tt.name)
 
 
-LAYERWISE = {omodels.MODEL_MLP: _mlp_layerwise}
+def _cnn_acts(pack, lane, B):
+    """Split TLK_BUF_ACTS (csrc/cnn.cu layout) into this lane's tensors (fp32)."""
+    L = pack.lanes
+    raw = pack.tensor(rt.BUF_ACTS).cpu().numpy().view(np.uint8)
+    sizes = [("h1", B * 676 * 32 * 2), ("p2", B * 9216 * 2), ("idx", B * 9216), ("h3", B * 128 * 2),
+             ("dz3", B * 128 * 2), ("dz2", B * 576 * 64 * 2), ("dz1", B * 676 * 32 * 2)]
+    out, off = {}, 0
+    for name, per in sizes:
+        blob = raw[off + lane * per: off + (lane + 1) * per]
+        out[name] = blob.copy() if name == "idx" else _bf(blob.view(np.uint16))
+        off += L * per
+    out["h1"] = out["h1"].reshape(B, 26, 26, 32)
+    out["p2"] = out["p2"].reshape(B, 12, 12, 64)
+    out["idx"] = out["idx"].reshape(B, 12, 12, 64)
+    out["h3"] = out["h3"].reshape(B, 128)
+    out["dz3"] = out["dz3"].reshape(B, 128)
+    out["dz2"] = (out["dz2"].reshape(B, 12, 12, 2, 2, 64).transpose(0, 1, 3, 2, 4, 5)
+                  .reshape(B, 24, 24, 64))
+    out["dz1"] = out["dz1"].reshape(B, 26, 26, 32)
+    return out
+
+
+def _cnn_layerwise(pack, lane, seed, t, p0, g, batch):
+    from oracle import rng
+    from oracle.bf16 import round_bf16 as r
+
+    B = batch
+    a = _cnn_acts(pack, lane, B)
+    prm = omodels.unflatten(omodels.MODEL_CNN, p0)
+    px, y = rng.batch(seed, t, B)
+    x = (px.astype(np.float32) / np.float32(256)).reshape(B, 28, 28, 1)
+    cols1 = omodels._taps(x, 26)
+    _ulp_close(a["h1"], r(np.maximum(cols1 @ prm["conv1.w"].T + prm["conv1.b"], 0)), "h1")
+    w2 = r(prm["conv2.w"])
+    cols2 = omodels._taps(a["h1"], 24)
+    a2 = np.maximum(cols2 @ w2.T + prm["conv2.b"], 0)
+    win = a2.reshape(B, 12, 2, 12, 2, 64).transpose(0, 1, 3, 2, 4, 5).reshape(B, 12, 12, 4, 64)
+    _ulp_close(a["p2"], r(win.max(axis=3)), "p2")
+    srt = np.sort(win, axis=3)
+    clear = (srt[:, :, :, 3] - srt[:, :, :, 2]) > 1e-4 * np.maximum(srt[:, :, :, 3], 1e-3)
+    assert (a["idx"] == np.argmax(win, axis=3))[clear & (srt[:, :, :, 3] > 0)].all(), "argmax"
+    flat = a["p2"].reshape(B, 9216)
+    w3 = r(prm["fc1.w"])
+    _ulp_close(a["h3"], r(np.maximum(flat @ w3.T + prm["fc1.b"], 0)), "h3")
+    loss, g4w, g4b, dh3 = omodels.head(a["h3"], prm["fc2.w"], prm["fc2.b"], y)
+    _ulp_close(a["dz3"], r(dh3 * (a["h3"] > 0)), "dz3")
+    dp2 = (a["dz3"] @ w3).reshape(B, 12, 12, 64)
+    onehot = np.arange(4)[None, None, None, :, None] == a["idx"][:, :, :, None, :]
+    dwin = np.where(onehot & (a["p2"][:, :, :, None, :] > 0), dp2[:, :, :, None, :], np.float32(0))
+    ref_dz2 = r(dwin.reshape(B, 12, 12, 2, 2, 64).transpose(0, 1, 3, 2, 4, 5).reshape(B, 24, 24, 64))
+    _ulp_close(a["dz2"], ref_dz2, "dz2")
+    dz2 = a["dz2"]
+    dpad = np.pad(dz2, ((0, 0), (2, 2), (2, 2), (0, 0)))
+    w2t = w2.reshape(64, 9, 32)
+    dh1 = np.zeros((B, 26, 26, 32), np.float32)
+    for kh in range(3):
+        for kw in range(3):
+            dh1 += dpad[:, 2 - kh:2 - kh + 26, 2 - kw:2 - kw + 26, :] @ w2t[:, kh * 3 + kw, :]
+    _ulp_close(a["dz1"], r(dh1 * (a["h1"] > 0)), "dz1")
+    dz1 = a["dz1"]
+    ref = {"fc2.w": g4w, "fc2.b": g4b, "fc1.w": a["dz3"].T @ flat, "fc1.b": a["dz3"].sum(0),
+           "conv2.w": dz2.reshape(-1, 64).T @ cols2.reshape(-1, 288),
+           "conv2.b": dz2.reshape(-1, 64).sum(0),
+           "conv1.w": dz1.reshape(-1, 32).T @ cols1.reshape(-1, 9),
+           "conv1.b": dz1.reshape(-1, 32).sum(0)}
+    for tt, off in omodels.layout(omodels.MODEL_CNN)[0]:
+        got = g[off:off + tt.count]
+        assert _rel_l2(got, ref[tt.name].reshape(-1)) <= 1e-5, (t, lane, tt.name,
+                                                               _rel_l2(got, ref[tt.name].reshape(-1)))
+
+
+LAYERWISE = {omodels.MODEL_MLP: _mlp_layerwise, omodels.MODEL_CNN: _cnn_layerwise}
 
 
 def _teacher_forced(model, lanes_cfg, steps, batch=64):
@@ -230,3 +301,37 @@ def test_mlp_teacher_forced_grads_and_bit_exact_update():
         (23, ooptim.SGD, dict(lr=0.05, momentum=0.9, weight_decay=1e-4)),
         (24, ooptim.ADAM, dict(lr=1e-3, weight_decay=1e-2, beta2=0.99)),
     ], steps=4)
+
+
+def test_cnn_teacher_forced_grads_and_bit_exact_update():
+    _teacher_forced(omodels.MODEL_CNN, [
+        (31, ooptim.ADAM, dict(lr=1e-3)),
+        (32, ooptim.SGD, dict(lr=0.02, momentum=0.9)),
+        (33, ooptim.ADAMW, dict(lr=1e-3, weight_decay=0.01)),
+    ], steps=3)
+
+
+def test_cnn_pack_matches_oracle():
+    steps, batch = 8, 64
+    jobs = [(40 + i, ooptim.ADAM, dict(lr=1e-3 * (1 + i % 2))) for i in range(4)]
+    jobs.append((50, ooptim.SGD, dict(lr=0.02, momentum=0.9)))
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(omodels.MODEL_CNN, batch, len(jobs), steps)
+        for lane, (seed, opt, kw) in enumerate(jobs):
+            pack.load(lane, seed=seed, steps=steps, optimizer=opt, **kw)
+        pack.run(steps)
+        ctx.sync()
+        for lane, (seed, opt, kw) in enumerate(jobs):
+            _check_lane(omodels.MODEL_CNN, pack, lane, seed, steps, batch, opt, **kw)
+
+
+@pytest.mark.parametrize("batch", [8, 32])
+def test_cnn_small_batches(batch):
+    with rt.Context(0) as ctx:
+        pack = ctx.pack(omodels.MODEL_CNN, batch, 2, 3)
+        for lane in range(2):
+            pack.load(lane, seed=60 + lane, steps=3)
+        pack.run(3)
+        ctx.sync()
+        for lane in range(2):
+            _check_lane(omodels.MODEL_CNN, pack, lane, 60 + lane, 3, batch, ooptim.ADAM, lr=1e-3)
