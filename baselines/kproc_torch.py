@@ -1,0 +1,99 @@
+"""K-process time-sliced PyTorch baseline job (the paper's sharing mechanism).
+
+One ordinary PyTorch training process per task; K of them pinned to the same
+GPU through the slot env (CUDA_VISIBLE_DEVICES from the triples mapping) and
+time-sliced by the driver -- exactly what the reference's run_plan does with
+the paper's LeNet/ResNet jobs (executor.py:105-141).  This is
+a BASELINE, not product code: bench.py launches K copies through
+paper_2410_22254_b200.run_plan (subprocess backend == reference mechanism).
+
+Timing: every process trains until wall-clock ``--t0`` (warm-up: imports,
+CUDA context, cuDNN autotune), then counts completed steps (``loss.item()``
+per step, as a logging training loop does) during [t0, t0 + duration].  The
+aggregate is sum(steps * batch) / duration over the K processes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import time
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+
+class Net(nn.Module):
+    """pytorch/examples MNIST Net without dropout (same shapes as TLK_MODEL_CNN)."""
+
+    def __init__(self):
+        super().__init__()
+        self.conv1 = nn.Conv2d(1, 32, 3, 1)
+        self.conv2 = nn.Conv2d(32, 64, 3, 1)
+        self.fc1 = nn.Linear(9216, 128)
+        self.fc2 = nn.Linear(128, 10)
+
+    def forward(self, x):
+        x = F.relu(self.conv1(x))
+        x = F.max_pool2d(F.relu(self.conv2(x)), 2)
+        x = F.relu(self.fc1(torch.flatten(x, 1)))
+        return self.fc2(x)
+
+
+class MLP(nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.fc1, self.fc2, self.fc3 = nn.Linear(784, 512), nn.Linear(512, 512), nn.Linear(512, 10)
+
+    def forward(self, x):
+        x = torch.flatten(x, 1)
+        return self.fc3(F.relu(self.fc2(F.relu(self.fc1(x)))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="cnn", choices=("cnn", "mlp"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--t0", type=float, required=True, help="wall-clock start of the timed window")
+    ap.add_argument("--duration", type=float, default=10.0)
+    ap.add_argument("--bf16", type=int, default=0, help="1: torch.autocast(bfloat16)")
+    a = ap.parse_args()
+    torch.manual_seed(a.seed)
+    dev = torch.device("cuda")
+    model = (Net() if a.model == "cnn" else MLP()).to(dev)
+    opt = torch.optim.Adam(model.parameters(), lr=a.lr)
+    torch.backends.cudnn.benchmark = True
+
+    def step():
+        x = torch.rand(a.batch, 1, 28, 28, device=dev)
+        y = torch.randint(0, 10, (a.batch,), device=dev)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=bool(a.bf16)):
+            loss = F.cross_entropy(model(x), y)
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+        return loss.item()
+
+    warm = 0
+    while time.time() < a.t0 or warm < 3:
+        step()
+        warm += 1
+    if time.time() > a.t0 + 0.5 * a.duration:
+        print(json.dumps({"error": "warm-up overran the timed window", "warm": warm}))
+        return 3
+    start = time.time()
+    steps = 0
+    while time.time() < a.t0 + a.duration:
+        step()
+        steps += 1
+    elapsed = time.time() - start
+    print(json.dumps({"steps": steps, "elapsed_s": elapsed, "batch": a.batch, "warm_steps": warm,
+                      "samples_per_s": steps * a.batch / elapsed}))
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Aggregate training samples/s of K co-resident jobs per B200 (packed triples mode).
+
+Workload (BASELINE.json configs[1]): 8 co-resident MNIST-CNN training jobs
+per GPU (triples [1, 8*N, 1] -> 8 slots pinned to each GPU), batch 64 per
+job, Adam, synthetic on-device data.  One *step* = one optimizer step of all
+8 jobs on a GPU (512 samples per GPU).  N>1 (torchrun): every rank runs its
+own 8 jobs -- the jobs are independent, so there is no data-path collective
+(weak scaling); the only NCCL call is the MAX-reduction of the timings.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl packed|reference]
+
+Prints ONE JSON line (rank 0).  Keys beyond the driver contract:
+roofline (dominant kernel), step_roofline (whole step vs max(F/peak_tc,
+B/peak_hbm)), cpu_baseline (the oracle CPU path, run through run_plan = the
+reference's mechanism), kproc_baseline (K-process time-sliced PyTorch, the
+paper's mechanism), kernels (per-kernel device ms of one step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "aggregate samples/sec per B200 vs jobs/GPU (triples NPPN); 1/2/4/8-GPU scaling"
+UNIT = "samples/s"
+WORKLOAD = "configs[1]: 8 co-resident MNIST CNN jobs packed per B200 (triples [1,8,1] per GPU)"
+JOBS_PER_GPU = 8
+BATCH = 64
+MODEL = "cnn"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------- dist --------
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def dist_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- clocks ------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.dev = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- roofline ----
+def kernel_work(name, info, lanes, batch):
+    """(bound, algorithmic units per launch) for a CNN-pack kernel; units are
+    FLOPs for tensor-bound kernels and bytes for HBM-bound ones."""
+    B, L = batch, lanes
+    conv2_flops = 2.0 * B * 576 * 64 * 288 * L
+    fc1_flops = 2.0 * B * 9216 * 128 * L
+    act = {
+        "optimizer": ("hbm", 28.0 * info.param_count * L),
+        "conv2_fwd_pool": ("tensor", conv2_flops),
+        "conv2_wgrad_splitk": ("tensor", conv2_flops),
+        "conv2_dgrad": ("tensor", conv2_flops),
+        "fc1_fwd_splitk": ("tensor", fc1_flops),
+        "fc1_wgrad": ("tensor", fc1_flops),
+        "fc1_dgrad_unpool": ("tensor", fc1_flops),
+        # CUDA-core / bookkeeping kernels: compulsory HBM bytes
+        "inputs": ("hbm", L * B * (784 + 784 * 2 + 4)),
+        "conv1_fwd": ("hbm", L * B * (784 * 2 + 676 * 32 * 2)),
+        "conv1_wgrad": ("hbm", L * B * (784 * 2 + 676 * 32 * 2)),
+        "fc1_reduce": ("hbm", L * (18 * 128 * 64 * 4 + B * 128 * 2)),
+        "head": ("hbm", L * B * 128 * 4),
+        "grad_finalize": ("hbm", L * (24 * 288 * 64 * 4 + 9216 * 4)),
+        "end_step": ("hbm", L * 128),
+    }
+    return act.get(name, ("hbm", 0.0))
+
+
+def step_roofline(info, lanes, batch, hbm_gbs, tflops):
+    flops = 6.0 * (26 * 26 * 32 * 9 + 24 * 24 * 64 * 288 + 9216 * 128 + 128 * 10) * batch * lanes
+    bytes_ = 28.0 * info.param_count * lanes
+    return max(flops / (tflops * 1e12), bytes_ / (hbm_gbs * 1e9)), flops, bytes_
+
+
+# ---------------------------------------------------------------- baselines ---
+def run_tasks_via_run_plan(argvs, ntpp, timeout):
+    """Launch tasks as processes through run_plan (the reference mechanism)."""
+    from paper_2410_22254_b200 import NodeSpec, TaskDef, TripleSpec, build_plan, run_plan
+
+    tasks = [TaskDef(i, tuple(a)) for i, a in enumerate(argvs)]
+    cores = os.cpu_count() or 1
+    plan = build_plan(tasks, TripleSpec(1, len(tasks), ntpp), NodeSpec(cores=max(cores, 1)))
+    logdir = tempfile.mkdtemp(prefix="tlk_bench_")
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    report = run_plan(plan, 0, log_dir=logdir, timeout_s=timeout, base_env=env)
+    outs = []
+    for r in report.results:
+        try:
+            txt = open(os.path.join(logdir, f"task_{r.task_id}.out")).read().strip().splitlines()
+            outs.append(json.loads(txt[-1]))
+        except Exception:
+            outs.append({"error": f"exit {r.exit_status}"})
+    return report, outs
+
+
+def cpu_oracle_rate(steps, warmup, jobs=JOBS_PER_GPU):
+    """The numpy oracle jobs run as `jobs` concurrent processes on the host
+    cores (run_plan, OMP_NUM_THREADS = cores // jobs); returns the aggregate
+    steady-state samples/s and the thread count used."""
+    cores = os.cpu_count() or 1
+    ntpp = max(1, cores // jobs)
+    argvs = [[sys.executable, "-m", "oracle.job", "--model", MODEL, "--seed", str(i), "--batch",
+              str(BATCH), "--steps", str(steps + warmup), "--warmup", str(warmup), "--json"]
+             for i in range(jobs)]
+    report, outs = run_tasks_via_run_plan(argvs, ntpp, timeout=900)
+    rates = [o.get("samples_per_s") for o in outs]
+    if any(r is None for r in rates):
+        return None, ntpp * jobs, outs
+    return float(sum(rates)), ntpp * jobs, outs
+
+
+def kproc_rate(jobs=JOBS_PER_GPU, duration=10.0, lead=35.0):
+    t0 = time.time() + lead
+    argvs = [[sys.executable, os.path.join(ROOT, "baselines", "kproc_torch.py"), "--model", MODEL,
+              "--seed", str(i), "--batch", str(BATCH), "--t0", f"{t0:.3f}",
+              "--duration", str(duration)] for i in range(jobs)]
+    report, outs = run_tasks_via_run_plan(argvs, 1, timeout=lead + duration + 120)
+    rates = [o.get("samples_per_s") for o in outs]
+    if any(r is None for r in rates):
+        return None, outs
+    return float(sum(rates)), outs
+
+
+# ---------------------------------------------------------------- arms --------
+def reference_arm(a, world, rank):
+    """--impl reference: the oracle CPU path (the reference has no training
+    code; its CPU path for these tasks is run_plan spawning CPU jobs)."""
+    if rank != 0:
+        return 0
+    # bounded sample: each "step" is one optimizer step of all 8 jobs; cap the
+    # number actually run so the whole arm stays within a few minutes.
+    timed = max(1, min(a.steps, 4))
+    warm = max(1, min(a.warmup, 1))
+    value, cores, outs = cpu_oracle_rate(timed, warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": (JOBS_PER_GPU * BATCH / value * 1e3) if value else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter RNG, same seeds/shapes as the packed arm)",
+        "config": {"workload": WORKLOAD, "jobs": JOBS_PER_GPU, "batch_per_job": BATCH,
+                   "optimizer": "adam", "path": "oracle/ numpy jobs via run_plan (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{JOBS_PER_GPU} CNN jobs x {timed} timed steps (+{warm} warm-up), "
+                                   f"bs {BATCH}, concurrent processes via run_plan, "
+                                   f"OMP_NUM_THREADS={max(1, (os.cpu_count() or 1) // JOBS_PER_GPU)}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def packed_arm(a, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2410_22254_b200 import runtime as rt
+
+    torch.cuda.set_device(local)
+    hbm, tc, tc_sus, peak_kind = load_peaks()
+    lanes = a.jobs
+    ctx = rt.Context(local)
+    total_steps = a.warmup + a.steps + a.profile_iters + 2
+    pack = ctx.pack(rt.MODELS[MODEL], BATCH, lanes, total_steps)
+    for j in range(lanes):
+        pack.load(j, seed=rank * lanes + j, steps=total_steps, lr=1e-3, task_id=rank * lanes + j,
+                  slot_index=rank + world * j)
+    stream = torch.cuda.ExternalStream(ctx.stream_handle)
+
+    with ClockSampler(local) as clk:
+        pack.run(a.warmup)
+        ctx.sync()
+        barrier(world)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        pack.run(a.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = ev0.elapsed_time(ev1)
+    clocks = clk.summary()
+    ms_max = dist_max(ms, world)
+    samples = world * lanes * BATCH * a.steps
+    value = samples / (ms_max / 1e3)
+
+    # per-kernel device times of one step (CUDA events on the launching stream)
+    kernels = pack.profile_step(a.profile_iters)
+    step_ms = sum(t for _, t in kernels)
+    top_name, top_ms = max(kernels, key=lambda kv: kv[1])
+    bound, work = kernel_work(top_name, pack.info, lanes, BATCH)
+    if bound == "tensor":
+        achieved = work / (top_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": top_name, "achieved": achieved, "peak": tc,
+                "unit": "TFLOP/s", "frac": achieved / tc, "traffic": None,
+                "algorithmic_per_launch": work, "ms_per_launch": top_ms,
+                "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
+    else:
+        achieved = work / (top_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": top_name, "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "algorithmic_per_launch": work, "ms_per_launch": top_ms,
+                "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
+    t_roof, sflops, sbytes = step_roofline(pack.info, lanes, BATCH, hbm, tc)
+    ms_step = ms_max / a.steps
+
+    # end-to-end through the public API with HOST buffers (pinned), per step:
+    # H2D of the step's pixels+labels, one packed step, D2H of the losses.
+    e2e_steps = max(3, min(a.steps, 100))
+    hpack = ctx.pack(rt.MODELS[MODEL], BATCH, lanes, a.warmup + e2e_steps + 2, host_input=True)
+    for j in range(lanes):
+        hpack.load(j, seed=rank * lanes + j, steps=a.warmup + e2e_steps + 2)
+    rng = np.random.default_rng(rank)
+    px = torch.from_numpy(rng.integers(0, 256, (lanes, BATCH, 784), dtype=np.uint8)).pin_memory()
+    lb = torch.from_numpy(rng.integers(0, 10, (lanes, BATCH), dtype=np.int32)).pin_memory()
+    loss_out = torch.empty(lanes, dtype=torch.float32).pin_memory()
+    pxn, lbn, lon = px.numpy(), lb.numpy(), loss_out.numpy()
+    for _ in range(max(1, a.warmup)):
+        hpack.step_host(pxn, lbn, lon)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        hpack.step_host(pxn, lbn, lon)
+    e2e_s = dist_max(time.perf_counter() - t0, world)
+    e2e_value = world * lanes * BATCH * e2e_steps / e2e_s
+    h2d = lanes * BATCH * 784 + lanes * BATCH * 4
+    d2h = lanes * 4
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (on-device counter RNG MNIST-shaped batches, teacher labels; random-init weights)",
+        "config": {"workload": WORKLOAD, "triple": [1, JOBS_PER_GPU * world, 1],
+                   "jobs_per_gpu": lanes, "batch_per_job": BATCH, "samples_per_step_per_gpu": lanes * BATCH,
+                   "optimizer": "adam (fp32 master, bf16 GEMM operands)",
+                   "parallelism": f"independent jobs, {lanes}/GPU x {world} GPU(s), no collective",
+                   "l2": "no explicit flush: per-step working set "
+                         f"{(16 * pack.info.param_count * lanes + 115e6 / 8 * lanes) / 1e6:.0f} MB > 126 MB L2"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "paper_2410_22254_b200.runtime.Pack.step_host -> tlk_step_host (pinned host buffers)",
+                "steps": e2e_steps},
+        "gpu_launches": pack.launches_per_step() * a.steps,
+        "clocks": clocks,
+        "roofline": roof,
+        "step_roofline": {"t_roof_ms": t_roof * 1e3, "measured_ms": ms_step,
+                          "frac": t_roof * 1e3 / ms_step, "flops_per_step": sflops,
+                          "compulsory_bytes_per_step": sbytes,
+                          "samples_per_s_roof": lanes * BATCH / t_roof},
+        "kernels": {k: round(v, 5) for k, v in kernels},
+    }
+    if rank == 0 and world == 1 and not a.no_baselines:
+        cpu, cores, _ = cpu_oracle_rate(2, 1)
+        line["cpu_baseline"] = {
+            "value": cpu, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{JOBS_PER_GPU} CNN jobs x 2 timed steps (+1 warm-up), bs {BATCH}, numpy oracle, "
+                      f"concurrent processes via run_plan"}
+        kp, outs = kproc_rate(JOBS_PER_GPU, duration=a.kproc_seconds)
+        line["kproc_baseline"] = {
+            "value": kp, "unit": UNIT, "procs": JOBS_PER_GPU,
+            "mechanism": "8 PyTorch (fp32, cudnn) processes pinned to one GPU via run_plan, time-sliced",
+            "packed_over_kproc": (value / kp) if kp else None,
+            "packed_e2e_over_kproc": (e2e_value / kp) if kp else None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("packed", "reference"), default="packed")
+    ap.add_argument("--jobs", type=int, default=JOBS_PER_GPU, help="co-resident jobs per GPU")
+    ap.add_argument("--profile-iters", type=int, default=5)
+    ap.add_argument("--kproc-seconds", type=float, default=10.0)
+    ap.add_argument("--no-baselines", action="store_true")
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    world, rank, local = dist_setup(a.gpus)
+    try:
+        if a.impl == "reference":
+            return reference_arm(a, world, rank)
+        return packed_arm(a, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

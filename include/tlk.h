@@ -124,6 +124,12 @@ int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, i
 /* Number of kernels one tlk_run step launches for this pack. */
 int tlk_pack_launches_per_step(tlk_ctx* ctx, int32_t pack, int32_t* n);
 
+/* Per-kernel device time of one step: runs `iters` un-graphed steps with a CUDA
+ * event after every launch; ms[k] = mean duration of launch k, names =
+ * comma-separated kernel names.  Advances the lanes like tlk_run. */
+int tlk_profile_step(tlk_ctx* ctx, int32_t pack, int32_t iters, float* ms, char* names,
+                     int32_t names_len, int32_t max_n, int32_t* n_out);
+
 /* -- self-test hooks (used by tests/ only) --------------------------------- */
 /* C[b] = A[b] * B[b]^T on the tcgen05 path.  A is [M,K] (a_mn=0) or [K,M]
  * (a_mn=1); B is [N,K] (b_mn=0) or [K,N] (b_mn=1); bf16 in, fp32 C [M,N]. */

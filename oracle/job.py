@@ -33,24 +33,27 @@ def add_job_args(ap: argparse.ArgumentParser) -> None:
 
 
 def train(model: int, seed: int, steps: int, batch: int, opt: optim.OptState,
-          bf16: bool = True, timer: bool = False):
-    """Run ``steps`` steps; returns (losses [steps], final flat params, seconds/step)."""
+          bf16: bool = True, warmup: int = 1):
+    """Run ``steps`` steps; returns (losses [steps], final flat params, seconds/step).
+
+    seconds/step is measured over the steps after the first ``warmup`` ones
+    (all steps if there are not more than ``warmup``).
+    """
     params = models.init_params(model, seed)
     flat = models.flatten_params(model, params)
     step_fn = models.STEP_FNS[model]
     losses = np.zeros(steps, np.float32)
-    t_first = None
+    warmup = warmup if steps > warmup else 0
     t0 = time.perf_counter()
     for t in range(steps):
-        if t == 1:
-            t_first = time.perf_counter()
+        if t == warmup:
+            t0 = time.perf_counter()
         px, y = rng.batch(seed, t, batch)
         loss, g = step_fn(models.unflatten(model, flat), px, y, bf16=bf16)
         gflat = models.flatten_params(model, g)
         flat = optim.step(opt, flat, gflat)
         losses[t] = loss
-    t1 = time.perf_counter()
-    per_step = (t1 - (t_first if t_first is not None else t0)) / max(1, steps - (1 if t_first else 0))
+    per_step = (time.perf_counter() - t0) / max(1, steps - warmup)
     return losses, flat, per_step
 
 
@@ -63,12 +66,16 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="oracle.job")
     add_job_args(ap)
     ap.add_argument("--bf16", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=1, help="steps excluded from the timing")
     ap.add_argument("--json", action="store_true")
     a = ap.parse_args(argv)
     model = models.MODEL_NAMES[a.model]
-    losses, _, per_step = train(model, a.seed, a.steps, a.batch, opt_from_args(a), bool(a.bf16))
+    losses, _, per_step = train(model, a.seed, a.steps, a.batch, opt_from_args(a), bool(a.bf16),
+                                warmup=a.warmup)
     out = {
         "model": a.model, "seed": a.seed, "steps": a.steps, "batch": a.batch,
+        "timed_steps": a.steps - (a.warmup if a.steps > a.warmup else 0),
+        "seconds_per_step": per_step,
         "samples_per_s": a.batch / per_step if per_step > 0 else None,
         "first_loss": float(losses[0]), "last_loss": float(losses[-1]),
     }

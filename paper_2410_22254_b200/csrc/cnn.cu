@@ -486,27 +486,37 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   if ((rc = enqueue_inputs(p, st))) return rc;
   conv1_fwd_kernel<<<dim3(B, L), 256, 0, st>>>(p.lane_dev, p.x, p.params, p.stride, o_c1w, o_c1b,
                                                 b.h1, B);
+  p.mark(st, "conv1_fwd");
   TLK_CUDA(cudaGetLastError());
   Conv2Fwd c2f{p.lane_dev, b, p.wbf, p.params, p.stride, o_c2w, o_c2b};
   TLK_CUDA(launch_gemm(c2f, dim3(B * 576 / GEMM_BM, 1, L), st));
+  p.mark(st, "conv2_fwd_pool");
   Fc1Fwd f1{p.lane_dev, b, p.wbf, p.stride, o_f1w};
   TLK_CUDA(launch_gemm(f1, dim3(1, 1, L * FC1_SPLITS), st));
+  p.mark(st, "fc1_fwd_splitk");
   fc1_reduce_kernel<<<dim3(128 * 64 / 256, L), 256, 0, st>>>(p.lane_dev, b, p.params, p.stride,
                                                               o_f1b);
+  p.mark(st, "fc1_reduce");
   TLK_CUDA(cudaGetLastError());
   if ((rc = enqueue_head(p, st, b.h3, 128, o_f2w, o_f2b, b.dz3, o_f1b))) return rc;
   LinWgrad f1w{p.lane_dev, b.dz3, b.h3_st, b.p2, b.p2_st, p.grads, p.stride, o_f1w, 128, 9216, B};
   TLK_CUDA(launch_gemm(f1w, dim3(1, 9216 / LinWgrad::BN, L), st));
+  p.mark(st, "fc1_wgrad");
   Fc1Dgrad f1d{p.lane_dev, b, p.wbf, p.stride, o_f1w};
   TLK_CUDA(launch_gemm(f1d, dim3(9216 / GEMM_BM, 1, L), st));
+  p.mark(st, "fc1_dgrad_unpool");
   Conv2Wgrad c2w{p.lane_dev, b};
   TLK_CUDA(launch_gemm(c2w, dim3(3, 1, L * C2W_SPLITS), st));
+  p.mark(st, "conv2_wgrad_splitk");
   Conv2Dgrad c2d{p.lane_dev, b, p.wt, p.wt_stride};
   TLK_CUDA(launch_gemm(c2d, dim3((B * 676 + GEMM_BM - 1) / GEMM_BM, 1, L), st));
+  p.mark(st, "conv2_dgrad");
   conv1_wgrad_kernel<<<dim3(C1W_SPLITS, L), 256, 0, st>>>(p.lane_dev, b, p.x);
+  p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   cnn_finalize_kernel<<<dim3((18432 + 64 + 320 + 255) / 256, L), 256, 0, st>>>(
       p.lane_dev, b, p.grads, p.stride, o_c1w, o_c1b, o_c2w, o_c2b);
+  p.mark(st, "grad_finalize");
   TLK_CUDA(cudaGetLastError());
   if ((rc = enqueue_optimizer(p, st))) return rc;
   return enqueue_end_step(p, st);

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(128) inputs_kernel(const LaneState* __restrict
 int enqueue_inputs(Pack& p, cudaStream_t st) {
   inputs_kernel<<<dim3(p.batch, p.lanes), 128, 0, st>>>(p.lane_dev, 0, 0, p.batch, p.teacher,
                                                        p.pixels, p.labels, p.x, p.host_input);
+  p.mark(st, "inputs");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }
@@ -292,6 +293,7 @@ int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_
                                                  db_prev_off, p.loss, p.max_steps, p.last_loss);
   else
     return fail(TLK_EINVAL, "head: unsupported hidden %d", hidden);
+  p.mark(st, "head");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }
@@ -368,6 +370,7 @@ int enqueue_optimizer(Pack& p, cudaStream_t st) {
       p.lane_dev, p.lanes, p.stride, reinterpret_cast<float4*>(p.params),
       reinterpret_cast<const float4*>(p.grads), reinterpret_cast<float4*>(p.mom1),
       reinterpret_cast<float4*>(p.mom2), reinterpret_cast<uint2*>(p.wbf), wt_hook(p));
+  p.mark(st, "optimizer");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }
@@ -386,6 +389,7 @@ __global__ void end_step_kernel(LaneState* lanes, int n) {
 
 int enqueue_end_step(Pack& p, cudaStream_t st) {
   end_step_kernel<<<(p.lanes + 127) / 128, 128, 0, st>>>(p.lane_dev, p.lanes);
+  p.mark(st, "end_step");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }

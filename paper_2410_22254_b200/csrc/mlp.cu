@@ -46,19 +46,24 @@ int mlp_enqueue_step(Pack& p, cudaStream_t st) {
   LinFwd f1{p.lane_dev, p.wbf, p.params, p.stride, o_w1, o_b1, p.x, int64_t(B) * 784, s.h1, act,
             512, 784, B};
   TLK_CUDA(launch_gemm(f1, dim3(512 / GEMM_BM, (B + 63) / 64, L), st));
+  p.mark(st, "fc1_fwd");
   LinFwd f2{p.lane_dev, p.wbf, p.params, p.stride, o_w2, o_b2, s.h1, act, s.h2, act, 512, 512, B};
   TLK_CUDA(launch_gemm(f2, dim3(512 / GEMM_BM, (B + 63) / 64, L), st));
+  p.mark(st, "fc2_fwd");
 
   if ((rc = enqueue_head(p, st, s.h2, 512, o_w3, o_b3, s.dz2, o_b2))) return rc;
 
   LinWgrad g2{p.lane_dev, s.dz2, act, s.h1, act, p.grads, p.stride, o_w2, 512, 512, B};
   TLK_CUDA(launch_gemm(g2, dim3(512 / GEMM_BM, 512 / LinWgrad::BN, L), st));
+  p.mark(st, "fc2_wgrad");
   LinDgrad d2{p.lane_dev, p.wbf, p.stride, o_w2, s.dz2, act, s.h1, s.dz1, act, p.grads, o_b1,
               512, 512, B};
   TLK_CUDA(launch_gemm(d2, dim3(512 / GEMM_BM, 1, L), st));
+  p.mark(st, "fc2_dgrad");
   LinWgrad g1{p.lane_dev, s.dz1, act, p.x, int64_t(B) * 784, p.grads, p.stride, o_w1,
               512, 784, B};
   TLK_CUDA(launch_gemm(g1, dim3(512 / GEMM_BM, (784 + LinWgrad::BN - 1) / LinWgrad::BN, L), st));
+  p.mark(st, "fc1_wgrad");
 
   if ((rc = enqueue_optimizer(p, st))) return rc;
   return enqueue_end_step(p, st);

@@ -42,6 +42,17 @@ struct Pack {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int launches_per_step = 0;
+  // per-kernel profiling (tlk_profile_step): an event after every launch
+  std::vector<cudaEvent_t>* prof = nullptr;
+  std::vector<const char*>* prof_names = nullptr;
+  void mark(cudaStream_t st, const char* name) {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    prof->push_back(e);
+    prof_names->push_back(name);
+  }
 };
 
 // Device allocation that records ownership; reports "out of memory" on failure.

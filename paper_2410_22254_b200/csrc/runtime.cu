@@ -3,6 +3,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <string>
 
 #include "pack.cuh"
 
@@ -371,6 +372,57 @@ int tlk_pack_launches_per_step(tlk_ctx* ctx, int32_t pack, int32_t* n) {
   if (rc) return rc;
   TLK_CHECK(n, TLK_EINVAL, "null argument");
   *n = p->launches_per_step;
+  return TLK_OK;
+}
+
+int tlk_profile_step(tlk_ctx* ctx, int32_t pack, int32_t iters, float* ms, char* names,
+                     int32_t names_len, int32_t max_n, int32_t* n_out) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(iters >= 1 && ms && n_out && max_n > 0, TLK_EINVAL, "bad arguments");
+  TLK_CHECK(!p->host_input, TLK_ESTATE, "profile needs a device-input pack");
+  std::vector<double> acc;
+  std::vector<const char*> nm;
+  for (int it = 0; it < iters; ++it) {
+    std::vector<cudaEvent_t> ev;
+    std::vector<const char*> names_v;
+    cudaEvent_t start;
+    TLK_CUDA(cudaEventCreate(&start));
+    TLK_CUDA(cudaEventRecord(start, ctx->stream));
+    p->prof = &ev;
+    p->prof_names = &names_v;
+    rc = enqueue_step(*p, ctx->stream);
+    p->prof = nullptr;
+    p->prof_names = nullptr;
+    if (rc) return rc;
+    TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (acc.empty()) {
+      acc.assign(ev.size(), 0.0);
+      nm = names_v;
+    }
+    cudaEvent_t prev = start;
+    for (size_t k = 0; k < ev.size() && k < acc.size(); ++k) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, prev, ev[k]);
+      acc[k] += t;
+      prev = ev[k];
+    }
+    cudaEventDestroy(start);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  const int n = int(acc.size()) < max_n ? int(acc.size()) : max_n;
+  std::string joined;
+  for (int k = 0; k < n; ++k) {
+    ms[k] = float(acc[k] / iters);
+    joined += nm[k];
+    if (k + 1 < n) joined += ",";
+  }
+  if (names && names_len > 0) {
+    std::strncpy(names, joined.c_str(), size_t(names_len) - 1);
+    names[names_len - 1] = 0;
+  }
+  *n_out = n;
   return TLK_OK;
 }
 

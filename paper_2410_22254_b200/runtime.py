@@ -24,7 +24,8 @@ EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
     "tlk_close", "tlk_sync", "tlk_stream", "tlk_pack_create", "tlk_lane_load", "tlk_lane_release",
     "tlk_run", "tlk_step_host", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
-    "tlk_pack_tensor", "tlk_pack_launches_per_step", "tlk_selftest_gemm", "tlk_selftest_datagen",
+    "tlk_pack_tensor", "tlk_pack_launches_per_step", "tlk_profile_step", "tlk_selftest_gemm",
+    "tlk_selftest_datagen",
 )
 
 
@@ -210,6 +211,17 @@ class Pack:
         n = C.c_int32()
         check(lib().tlk_pack_launches_per_step(self.ctx._ctx, self.id, C.byref(n)))
         return n.value
+
+    def profile_step(self, iters: int = 5):
+        """[(kernel name, mean ms)] for one step, measured with CUDA events on
+        the context stream (un-graphed; advances the lanes by `iters` steps)."""
+        ms = (C.c_float * 64)()
+        names = C.create_string_buffer(4096)
+        n = C.c_int32()
+        check(lib().tlk_profile_step(self.ctx._ctx, self.id, int(iters), ms, names, 4096, 64,
+                                     C.byref(n)))
+        labels = names.value.decode().split(",")
+        return [(labels[k], float(ms[k])) for k in range(n.value)]
 
     def tensor(self, which: int):
         """Zero-copy torch view of a pack buffer (TLK_BUF_*)."""
