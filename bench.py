@@ -64,14 +64,9 @@ def dist_setup(n_gpus):
 
 
 def dist_max(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+    from paper_2410_22254_b200.multigpu import max_over_ranks
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return max_over_ranks(x)
 
 
 def barrier(world):
@@ -250,13 +245,24 @@ def packed_arm(a, world, rank, local):
 
     torch.cuda.set_device(local)
     hbm, tc, tc_sus, peak_kind = load_peaks()
+    from paper_2410_22254_b200 import TaskDef
+    from paper_2410_22254_b200.jobspec import JobSpec, parse_task
+    from paper_2410_22254_b200.multigpu import rank_share, weak_scaling_plan
+
     lanes = a.jobs
     ctx = rt.Context(local)
     total_steps = a.warmup + a.steps + a.profile_iters + 2
+    # the workload as a parametric task list through the triples mapping:
+    # triples [1, jobs*world, 1] on a world-GPU node; this rank trains the
+    # slots pinned to GPU `rank` (task i -> slot i -> GPU i % world).
+    plan = weak_scaling_plan(lanes, world, lambda i: TaskDef(i, tuple(
+        JobSpec(model=MODEL, seed=i, steps=total_steps, batch=BATCH, lr=1e-3).argv())))
+    share = rank_share(plan, rank)
     pack = ctx.pack(rt.MODELS[MODEL], BATCH, lanes, total_steps)
-    for j in range(lanes):
-        pack.load(j, seed=rank * lanes + j, steps=total_steps, lr=1e-3, task_id=rank * lanes + j,
-                  slot_index=rank + world * j)
+    for j, (slot, tasks) in enumerate(share):
+        spec = parse_task(tasks[0].argv)
+        pack.load(j, seed=spec.seed, steps=spec.steps, lr=spec.lr, task_id=tasks[0].task_id,
+                  slot_index=slot)
     stream = torch.cuda.ExternalStream(ctx.stream_handle)
 
     with ClockSampler(local) as clk:

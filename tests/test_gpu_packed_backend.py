@@ -1,0 +1,83 @@
+"""run_plan(..., backend="packed") on a real B200.
+
+* a parametric task list (CNN + MLP jobs, T > S so slots refill) runs through
+  the drop-in API; every task exits 0, concurrency <= NPPN, per-slot order and
+  TaskResult semantics hold;
+* packing invariance: each task's loss curve from the pack is BIT-IDENTICAL to
+  the same task trained alone (one-lane pack) -- lanes never interact;
+* the job entry point runs standalone as an ordinary process;
+* an allocation that cannot fit fails with "out of memory" (oom_flag) and the
+  context stays usable.
+"""
+
+import json
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2410_22254_b200 import NodeSpec, TaskDef, TripleSpec, build_plan, run_plan
+from paper_2410_22254_b200 import runtime as rt
+from paper_2410_22254_b200.executor import classify_failure
+from paper_2410_22254_b200.jobspec import JobSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def _alone(spec):
+    with rt.Context(0) as ctx:
+        p = ctx.pack(rt.MODELS[spec.model], spec.batch, 1, spec.steps)
+        p.load(0, seed=spec.seed, steps=spec.steps, optimizer=rt.OPTIMIZERS[spec.optim], lr=spec.lr,
+               beta1=spec.beta1, beta2=spec.beta2, eps=spec.eps, weight_decay=spec.wd,
+               momentum=spec.momentum)
+        p.run(spec.steps)
+        ctx.sync()
+        return p.losses(0, spec.steps)
+
+
+def test_packed_run_plan_refill_and_packing_invariance(tmp_path):
+    specs = [JobSpec(model="cnn" if i % 3 else "mlp", seed=100 + i, steps=4 + (i % 4),
+                     lr=1e-3 * (1 + i % 2), optim="sgd" if i == 5 else "adam",
+                     momentum=0.9 if i == 5 else 0.0) for i in range(10)]
+    tasks = [TaskDef(i, tuple(s.argv(sys.executable))) for i, s in enumerate(specs)]
+    plan = build_plan(tasks, TripleSpec(1, 4, 1), NodeSpec(cores=8, gpus=1, gpu_mem_mib=183359))
+    report = run_plan(plan, 0, log_dir=tmp_path, backend="packed", packed_options={"chunk": 3})
+    assert report.failures == 0, [(r.task_id, r.exit_status, (tmp_path / f"task_{r.task_id}.err").read_text())
+                                  for r in report.results if r.exit_status]
+    assert report.max_observed_concurrency <= 4
+    assert [r.task_id for r in report.results] == list(range(10))
+    for r in report.results:
+        assert r.slot_index == r.task_id % 4 and r.gpu_index == 0
+    by_slot = {}
+    for r in report.results:
+        by_slot.setdefault(r.slot_index, []).append(r)
+    for rs in by_slot.values():
+        for a, b in zip(rs, rs[1:]):
+            assert a.end_ms <= b.start_ms
+    assert report.to_json_dict()["packed"]["packed_slots"] == 4
+    for i, spec in enumerate(specs):
+        out = json.loads((tmp_path / f"task_{i}.out").read_text())
+        ref = _alone(spec)
+        assert out["steps"] == spec.steps
+        assert np.float32(out["first_loss"]) == ref[0] and np.float32(out["last_loss"]) == ref[-1], i
+
+
+def test_job_entry_point_runs_standalone():
+    spec = JobSpec(model="mlp", seed=7, steps=5)
+    proc = subprocess.run(spec.argv(sys.executable), capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0, proc.stderr
+    out = json.loads(proc.stdout.strip().splitlines()[-1])
+    assert np.float32(out["last_loss"]) == _alone(spec)[-1]
+
+
+def test_admission_oom_is_reported_and_context_survives():
+    with rt.Context(0) as ctx:
+        with pytest.raises(rt.TlkError) as ei:
+            ctx.pack(rt.MODEL_CNN, 64, 4096, 1 << 24)  # ~275 GB loss curves alone
+        assert ei.value.oom and classify_failure(1, str(ei.value)) == "oom"
+        p = ctx.pack(rt.MODEL_MLP, 64, 1, 2)
+        p.load(0, seed=1, steps=2)
+        p.run(2)
+        ctx.sync()
+        assert p.status(0).steps_done == 2
