@@ -26,3 +26,12 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_sessionstart(session):
+    # libtlk.so is built in-tree; build it here if the checkout has none yet
+    lib = os.path.join(ROOT, "paper_2410_22254_b200", "_lib", "libtlk.so")
+    if not os.path.exists(lib):
+        from paper_2410_22254_b200.build import build
+
+        build()
