@@ -300,6 +300,13 @@ def packed_arm(a, world, rank, local):
                 "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                 "algorithmic_per_launch": work, "ms_per_launch": top_ms,
                 "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
+    try:  # dram bytes of this kernel from the committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(top_name)
+        if tr:
+            roof["traffic"] = tr["dram_bytes"]
+            roof["traffic_source"] = tr["source"]
+    except (OSError, ValueError):
+        pass
     t_roof, sflops, sbytes = step_roofline(pack.info, lanes, BATCH, hbm, tc)
     ms_step = ms_max / a.steps
 
