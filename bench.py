@@ -136,7 +136,7 @@ def kernel_work(name, info, lanes, batch):
     act = {
         "optimizer": ("hbm", 28.0 * info.param_count * L),
         "conv2_fwd_pool": ("tensor", conv2_flops),
-        "conv2_wgrad_splitk": ("tensor", conv2_flops),
+        "conv2_wgrad": ("tensor", conv2_flops),
         "conv2_dgrad": ("tensor", conv2_flops),
         "fc1_fwd_splitk": ("tensor", fc1_flops),
         "fc1_wgrad": ("tensor", fc1_flops),

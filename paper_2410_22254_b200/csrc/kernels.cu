@@ -6,6 +6,7 @@
 #include "pack.cuh"
 #include "rng.cuh"
 #include "tlk_ptx.cuh"
+#include "conv_layout.cuh"
 
 namespace tlk {
 
@@ -109,9 +110,10 @@ int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teache
 }
 
 // ----------------------------------------------------- transposed shadows --
-// Model-specific bf16 copies in a second layout, refreshed wherever the bf16
-// shadow is written.  CNN: conv2.w (oc, tap, ic) -> wt (ic, tap, oc) so that
-// the conv2 dgrad GEMM reads its B operand K-major.
+// Model-specific bf16 copies in other layouts, refreshed wherever the bf16
+// shadow is written.  CNN: conv2.w (oc, tap, ic) -> the two K-major,
+// core-matrix-ordered operand blobs of the conv2 fwd / dgrad kernels
+// (conv_tc.cuh: wf_index, wd_index), each TMA-bulk-copied as is.
 struct WtHook {
   uint16_t* wt;
   int64_t wt_stride;
@@ -122,8 +124,10 @@ __device__ __forceinline__ void wt_write(const WtHook& h, int lane, int64_t e, u
   if (!h.wt) return;
   int64_t r = e - h.off;
   if (r < 0 || r >= h.count) return;
-  int oc = int(r / 288), t = int(r % 288), tap = t >> 5, ic = t & 31;
-  h.wt[lane * h.wt_stride + ic * 576 + tap * 64 + oc] = b;
+  const int oc = int(r / 288), t = int(r % 288), tap = t >> 5, ic = t & 31;
+  uint16_t* w = h.wt + lane * h.wt_stride;
+  w[wf_index(oc, tap, ic)] = b;  // conv2 fwd B operand
+  w[wd_index(oc, tap, ic)] = b;  // conv2 dgrad B operand
 }
 static WtHook wt_hook(const Pack& p) {
   WtHook h{nullptr, 0, 0, 0};

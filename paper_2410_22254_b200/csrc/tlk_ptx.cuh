@@ -150,6 +150,37 @@ TLK_DEV uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sb
   return d;
 }
 
+// SWIZZLE_NONE ("interleave") canonical layouts: core matrix = 8 rows x 16 B
+// stored as 128 contiguous bytes.  K-major: LBO = byte step between core
+// matrices along K, SBO = byte step between 8-row groups along M/N.
+// MN-major: SBO = step between 8-element groups along M/N, LBO = step
+// between 8-deep groups along K.  Start address only needs 16-B alignment,
+// which is what lets a convolution tap be a plain offset of the start.
+TLK_DEV uint64_t umma_desc_interleave(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version, layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+// ------------------------------------------------------------ TMA bulk ----
+// 1-D bulk copy global -> shared through the TMA engine, completing `bytes`
+// of transaction count on `bar` (armed with mbar_expect_tx).
+TLK_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+TLK_DEV void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 D.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn_major,
                                                         bool b_mn_major) {

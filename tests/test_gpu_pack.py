@@ -178,25 +178,38 @@ def _mlp_layerwise(pack, lane, seed, t, p0, g, batch):
         assert _rel_l2(got, ref[tt.name].reshape(-1)) <= 1e-5, (t, lane, tt.name)
 
 
+def _p28_to_nhwc(planes, B, size, off):
+    """P28 chunk planes [C][npos][8] -> NHWC [B, size, size, 8*C] (interior at +off)."""
+    C = planes.shape[0]
+    img = planes[:, 32:32 + B * 784, :].reshape(C, B, 28, 28, 8)
+    border = img.copy()
+    border[:, :, off:off + size, off:off + size, :] = 0
+    assert not border.any(), "P28 border/padding must stay zero"
+    x = img[:, :, off:off + size, off:off + size, :]
+    return np.ascontiguousarray(x.transpose(1, 2, 3, 0, 4).reshape(B, size, size, 8 * C))
+
+
 def _cnn_acts(pack, lane, B):
-    """Split TLK_BUF_ACTS (csrc/cnn.cu layout) into this lane's tensors (fp32)."""
+    """Split TLK_BUF_ACTS (csrc/cnn.cu layout) into this lane's NHWC fp32 tensors."""
     L = pack.lanes
+    npos = 32 + B * 784 + 64
     raw = pack.tensor(rt.BUF_ACTS).cpu().numpy().view(np.uint8)
-    sizes = [("h1", B * 676 * 32 * 2), ("p2", B * 9216 * 2), ("idx", B * 9216), ("h3", B * 128 * 2),
-             ("dz3", B * 128 * 2), ("dz2", B * 576 * 64 * 2), ("dz1", B * 676 * 32 * 2)]
+    sizes = [("h1", 4 * npos * 16), ("p2", B * 9216 * 2), ("idx", B * 9216), ("h3", B * 128 * 2),
+             ("dz3", B * 128 * 2), ("dz2", 8 * npos * 16), ("dz1", 4 * npos * 16)]
     out, off = {}, 0
     for name, per in sizes:
         blob = raw[off + lane * per: off + (lane + 1) * per]
         out[name] = blob.copy() if name == "idx" else _bf(blob.view(np.uint16))
-        off += L * per
-    out["h1"] = out["h1"].reshape(B, 26, 26, 32)
+        off += (L * per + 15) // 16 * 16
+    out["h1"] = _p28_to_nhwc(out["h1"].reshape(4, npos, 8), B, 26, 1)
     out["p2"] = out["p2"].reshape(B, 12, 12, 64)
-    out["idx"] = out["idx"].reshape(B, 12, 12, 64)
+    out["live"] = (out["idx"].reshape(B, 12, 12, 64) & 4) != 0
+    out["idx"] = out["idx"].reshape(B, 12, 12, 64) & 3
     out["h3"] = out["h3"].reshape(B, 128)
     out["dz3"] = out["dz3"].reshape(B, 128)
-    out["dz2"] = (out["dz2"].reshape(B, 12, 12, 2, 2, 64).transpose(0, 1, 3, 2, 4, 5)
-                  .reshape(B, 24, 24, 64))
-    out["dz1"] = out["dz1"].reshape(B, 26, 26, 32)
+    out["dz2"] = _p28_to_nhwc(out["dz2"].reshape(8, npos, 8), B, 24, 2)
+    dz1 = out["dz1"].reshape(4, npos, 8)[:, 32:32 + B * 784, :].reshape(4, B, 28, 28, 8)
+    out["dz1"] = np.ascontiguousarray(dz1[:, :, 1:27, 1:27, :].transpose(1, 2, 3, 0, 4).reshape(B, 26, 26, 32))
     return out
 
 
@@ -219,6 +232,7 @@ def _cnn_layerwise(pack, lane, seed, t, p0, g, batch):
     srt = np.sort(win, axis=3)
     clear = (srt[:, :, :, 3] - srt[:, :, :, 2]) > 1e-4 * np.maximum(srt[:, :, :, 3], 1e-3)
     assert (a["idx"] == np.argmax(win, axis=3))[clear & (srt[:, :, :, 3] > 0)].all(), "argmax"
+    assert np.array_equal(a["live"], a["p2"] > 0), "live bit"
     flat = a["p2"].reshape(B, 9216)
     w3 = r(prm["fc1.w"])
     _ulp_close(a["h3"], r(np.maximum(flat @ w3.T + prm["fc1.b"], 0)), "h3")

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 # ncu kernel name fragment -> bench.py kernel label
-LABELS = {"Conv2Fwd": "conv2_fwd_pool", "Conv2Dgrad": "conv2_dgrad", "Conv2Wgrad": "conv2_wgrad_splitk",
+LABELS = {"Conv2Fwd": "conv2_fwd_pool", "Conv2Dgrad": "conv2_dgrad", "conv2_wgrad_tc": "conv2_wgrad", "conv2_fwd_tc": "conv2_fwd_pool", "conv2_dgrad_tc": "conv2_dgrad",
           "Fc1Dgrad": "fc1_dgrad_unpool", "Fc1Fwd": "fc1_fwd_splitk", "LinWgrad": "fc1_wgrad",
           "optimizer_kernel": "optimizer", "conv1_wgrad": "conv1_wgrad", "conv1_fwd": "conv1_fwd",
           "head_kernel": "head", "inputs_kernel": "inputs", "cnn_finalize": "grad_finalize",
