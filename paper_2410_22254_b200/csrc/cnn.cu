@@ -354,10 +354,10 @@ int cnn_setup(Pack& p) {
   p.wt_stride = 2 * CONV2_W;
   if ((rc = pack_alloc(p, &wt, L * p.wt_stride * 2))) return rc;
   p.wt = static_cast<uint16_t*>(wt);
-  TLK_CUDA(cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FWD_SMEM));
-  TLK_CUDA(cudaFuncSetAttribute(conv2_dgrad_tc_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM));
+  TLK_CUDA(cudaFuncSetAttribute(conv2_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                ConvPolicy<true>::SMEM));
+  TLK_CUDA(cudaFuncSetAttribute(conv2_tc_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, ConvPolicy<false>::SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
   p.launches_per_step = 14;
@@ -378,7 +378,7 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   conv1_fwd_kernel<<<dim3(B, L), 256, 0, st>>>(p.lane_dev, p.x, p.params, p.stride, o_c1w, o_c1b, b);
   p.mark(st, "conv1_fwd");
   TLK_CUDA(cudaGetLastError());
-  conv2_fwd_tc_kernel<<<dim3(B * 6, L), 128, FWD_SMEM, st>>>(ca);
+  conv2_tc_kernel<true><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<true>::SMEM, st>>>(ca);
   p.mark(st, "conv2_fwd_pool");
   TLK_CUDA(cudaGetLastError());
   Fc1Fwd f1{p.lane_dev, b, p.wbf, p.stride, o_f1w};
@@ -395,10 +395,10 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   Fc1Dgrad f1d{p.lane_dev, b, p.wbf, p.stride, o_f1w};
   TLK_CUDA(launch_gemm(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
-  conv2_wgrad_tc_kernel<<<dim3(C2W_SPLITS, L), 128, WG_SMEM, st>>>(ca);
+  conv2_wgrad_tc_kernel<<<dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st>>>(ca);
   p.mark(st, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
-  conv2_dgrad_tc_kernel<<<dim3(B * 6, L), 128, DG_SMEM, st>>>(ca);
+  conv2_tc_kernel<false><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st>>>(ca);
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
   conv1_wgrad_kernel<<<dim3(B, L), 128, 0, st>>>(p.lane_dev, b, p.x);

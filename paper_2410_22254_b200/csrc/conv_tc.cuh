@@ -24,214 +24,235 @@ struct ConvArgs {
   int wgrad_splits;
 };
 
-// ------------------------------------------------------------ conv2 fwd ----
-// CTA = (4 output rows of one image, lane): M = 128 P28 positions starting at
-// row 2+4i (112 real + 16 spill), N = 64 oc, K = 9 taps x 32 ic = 18 MMAs.
-// Epilogue: bias + ReLU + 2x2 maxpool + argmax through a shared-memory tile.
-constexpr int FWD_SMEM_A = 4 * PATCH_BYTES;           // 11904
-constexpr int FWD_SMEM_B = 9 * 4 * 1024;              // 36864
-constexpr int FWD_SMEM = FWD_SMEM_A + FWD_SMEM_B + 128;
-constexpr int FWD_TILE_LD = 68;                       // floats per staged row
+TLK_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__global__ void __launch_bounds__(128) conv2_fwd_tc_kernel(ConvArgs a) {
-  const int tile = blockIdx.x, j = blockIdx.y;
+// ------------------------------------------- persistent conv2 fwd / dgrad --
+// Grid = (CTAS_PER_LANE, lanes); a CTA keeps its lane's weight operand
+// resident in shared memory (one TMA bulk load) and loops over that lane's
+// 128-position tiles.  Warp roles: warp 4 = TMA producer (double-buffered
+// patches), warp 5 = MMA issuer (double-buffered TMEM accumulators), warps
+// 0-3 = epilogue (TMEM lane quarters).  Tile i's epilogue overlaps tile i+1's
+// patch load and MMAs.
+//
+//   fwd   : A = h1 patch (4 planes), B = wf, N = 64, 9 taps x 2 K-steps,
+//           tiles = 4 output rows of an image (6 per image), epilogue =
+//           bias + ReLU + 2x2 maxpool + argmax via a shared fp32 tile.
+//   dgrad : A = dz2 patch (8 planes), B = wd, N = 32, 9 taps x 4 K-steps,
+//           tiles = 128 positions from row 1 of an image (6 per image),
+//           epilogue = ReLU mask with h1 -> dz1 (valid positions only).
+template <bool FWD>
+struct ConvPolicy {
+  static constexpr int PLANES = FWD ? 4 : 8;
+  static constexpr int N = FWD ? 64 : 32;
+  static constexpr int KSTEPS = FWD ? 2 : 4;   // K16 steps per tap
+  static constexpr int BCHUNK = N * 16;        // bytes per 8-wide K chunk of B
+  static constexpr int A_BYTES = PLANES * PATCH_BYTES;
+  static constexpr int B_BYTES = 9 * 2 * KSTEPS * BCHUNK;  // 36864 for both
+  static constexpr int TILE_BYTES = FWD ? 128 * 68 * 4 : 0;
+  static constexpr int SMEM = B_BYTES + 2 * A_BYTES + TILE_BYTES + 128;
+  static constexpr uint32_t TCOLS = 2 * N;     // two accumulators
+  TLK_DEV static int tap_off(int t) { return FWD ? tap_off_fwd(t) : tap_off_dgrad(t); }
+  TLK_DEV static int64_t tile_p0(int tile) {   // first position of the tile
+    const int b = tile / 6, k = tile % 6;
+    return P28_FRONT + int64_t(b) * P28_IMG + (FWD ? (2 + 4 * k) * P28 : P28 + 128 * k);
+  }
+};
+constexpr int CONV_CTAS_PER_LANE = 36;
+constexpr int CONV_THREADS = 192;
+
+template <bool FWD>
+__global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
+  using P = ConvPolicy<FWD>;
+  const int j = blockIdx.y;
   if (!a.lanes[j].active) return;
-  const int b = tile / 6, ti = tile % 6;
+  const int ntiles = a.B * 6;
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full_bar, done_bar;
+  __shared__ __align__(8) uint64_t wfull, afull[2], aempty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t sA = smem_u32(sm), sB = sA + FWD_SMEM_A;
-  const int64_t p0 = P28_FRONT + int64_t(b) * P28_IMG + (2 + 4 * ti) * P28;
+  const uint32_t sB = smem_u32(sm), sA0 = sB + P::B_BYTES;
+  float* tileS = reinterpret_cast<float*>(sm + P::B_BYTES + 2 * P::A_BYTES);
 
   if (tid == 0) {
-    mbar_init(&full_bar, 1);
-    mbar_init(&done_bar, 1);
+    mbar_init(&wfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<64>(&tmem_s);
+  if (warp == 0) tmem_alloc<P::TCOLS>(&tmem_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_s;
+  const uint16_t* src = FWD ? a.h1 + int64_t(j) * 4 * a.npos * 8 : a.dz2 + int64_t(j) * 8 * a.npos * 8;
 
-  if (tid == 0) {
-    mbar_expect_tx(&full_bar, FWD_SMEM_A + FWD_SMEM_B);
-    const uint16_t* h1 = a.h1 + int64_t(j) * 4 * a.npos * 8;
-    for (int c = 0; c < 4; ++c)
-      tma_bulk_g2s(sA + c * PATCH_BYTES, h1 + (c * a.npos + p0 - HALO) * 8, PATCH_BYTES, &full_bar);
-    const uint16_t* wf = a.wt + int64_t(j) * a.wt_stride;
-    for (int t = 0; t < 9; ++t)
-      tma_bulk_g2s(sB + t * 4096, wf + t * 2048, 4096, &full_bar);
-    mbar_wait(&full_bar, 0);
-    tc_fence_after();
-    constexpr uint32_t IDESC = umma_idesc_bf16(128, 64, false, false);
-#pragma unroll 1
-    for (int t = 0; t < 9; ++t)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint64_t ad = umma_desc_interleave(
-            sA + 2 * h * PATCH_BYTES + (HALO + tap_off_fwd(t)) * 16, PATCH_BYTES, 128);
-        const uint64_t bd = umma_desc_interleave(sB + (t * 4 + 2 * h) * 1024, 1024, 128);
-        mma_bf16(tmem, ad, bd, IDESC, (t | h) ? 1u : 0u);
+  if (warp == 4) {  // ---------------- TMA producer
+    if (lane == 0) {
+      const uint16_t* w = a.wt + int64_t(j) * a.wt_stride + (FWD ? 0 : CONV2_W);
+      mbar_expect_tx(&wfull, P::B_BYTES);
+      for (int t = 0; t < 9; ++t) tma_bulk_g2s(sB + t * 4096, w + t * 2048, 4096, &wfull);
+      int i = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i & 1;
+        if (i >= 2) mbar_wait(&aempty[s], ((i >> 1) - 1) & 1);
+        const int64_t p0 = P::tile_p0(tile);
+        mbar_expect_tx(&afull[s], P::A_BYTES);
+        for (int c = 0; c < P::PLANES; ++c)
+          tma_bulk_g2s(sA0 + s * P::A_BYTES + c * PATCH_BYTES, src + (c * a.npos + p0 - HALO) * 8,
+                       PATCH_BYTES, &afull[s]);
       }
-    mma_commit(&done_bar);
-  }
-  mbar_wait(&done_bar, 0);
-  tc_fence_after();
-  // TMEM -> shared tile [128][68] fp32 (the operand area is free now)
-  float* tileS = reinterpret_cast<float*>(sm);
-  const int row = warp * 32 + lane;
+    }
+  } else if (warp == 5) {  // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = umma_idesc_bf16(128, P::N, false, false);
+      const uint64_t bd0 = umma_desc_interleave(sB, P::BCHUNK, 128);
+      mbar_wait(&wfull, 0);
+      int i = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i & 1;
+        mbar_wait(&afull[s], (i >> 1) & 1);
+        if (i >= 2) mbar_wait(&tempty[s], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint64_t ad0 = umma_desc_interleave(sA0 + s * P::A_BYTES + HALO * 16, PATCH_BYTES, 128);
+        const uint32_t d = tmem + s * P::N;
 #pragma unroll 1
-  for (int cc = 0; cc < 2; ++cc) {
-    float v[32];
-    tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
+        for (int t = 0; t < 9; ++t) {
+          const int toff = P::tap_off(t);
 #pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4*>(tileS + row * FWD_TILE_LD + cc * 32 + i) =
-          make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-  }
-  tc_fence_before();
-  __syncthreads();
-  // 2 pooled rows x 12 pooled cols x 8 channel chunks = 192 items
-  const float* bias = a.params + j * a.pstride + a.b2_off;
-  for (int it = tid; it < 192; it += 128) {
-    const int ch = it & 7, pw = (it >> 3) % 12, phl = (it >> 3) / 12;
-    float mx[8], bb[8];
-    int arg[8];
+          for (int k = 0; k < P::KSTEPS; ++k) {
+            // descriptor start field is address >> 4: offsets add directly
+            const uint64_t ad = ad0 + uint64_t((2 * k * PATCH_BYTES + toff * 16) >> 4);
+            const uint64_t bd = bd0 + uint64_t(((t * 2 * P::KSTEPS + 2 * k) * P::BCHUNK) >> 4);
+            mma_bf16(d, ad, bd, IDESC, (t | k) ? 1u : 0u);
+          }
+        }
+        mma_commit(&aempty[s]);
+        mma_commit(&tfull[s]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 0..3 (TMEM lanes 32w..32w+31)
+    const int row = warp * 32 + lane;
+    int i = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      const int s = i & 1;
+      mbar_wait(&tfull[s], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + s * P::N + (uint32_t(warp * 32) << 16);
+      const int64_t p0 = P::tile_p0(tile);
+      if constexpr (FWD) {
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32];
+          tmem_ld32(taddr + cc * 32, v);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) bb[e] = bias[ch * 8 + e];
+          for (int q = 0; q < 32; q += 4)
+            *reinterpret_cast<float4*>(tileS + row * 68 + cc * 32 + q) =
+                make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+        named_bar_sync(1, 128);
+        const int b = tile / 6, ti = tile % 6;
+        const float* bias = a.params + j * a.pstride + a.b2_off;
+        for (int it = tid; it < 192; it += 128) {
+          const int ch = it & 7, pw = (it >> 3) % 12, phl = (it >> 3) / 12;
+          float mx[8], bb[8];
+          int arg[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int m = (2 * phl + (q >> 1)) * P28 + 2 + 2 * pw + (q & 1);
-      const float4 lo = *reinterpret_cast<const float4*>(tileS + m * FWD_TILE_LD + ch * 8);
-      const float4 hi = *reinterpret_cast<const float4*>(tileS + m * FWD_TILE_LD + ch * 8 + 4);
-      const float z[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          for (int e = 0; e < 8; ++e) bb[e] = bias[ch * 8 + e];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float r = fmaxf(z[e] + bb[e], 0.0f);
-        if (q == 0 || r > mx[e]) {
-          mx[e] = r;
-          arg[e] = q;
+          for (int q = 0; q < 4; ++q) {
+            const int m = (2 * phl + (q >> 1)) * P28 + 2 + 2 * pw + (q & 1);
+            const float4 lo = *reinterpret_cast<const float4*>(tileS + m * 68 + ch * 8);
+            const float4 hi = *reinterpret_cast<const float4*>(tileS + m * 68 + ch * 8 + 4);
+            const float z[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float r = fmaxf(z[e] + bb[e], 0.0f);
+              if (q == 0 || r > mx[e]) {
+                mx[e] = r;
+                arg[e] = q;
+              }
+            }
+          }
+          const int ph = 2 * ti + phl;
+          const int64_t o = ((int64_t(j) * a.B + b) * 144 + ph * 12 + pw) * 64 + ch * 8;
+          uint32_t w4[4], i0 = 0, i1 = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) w4[e] = pack_bf2(mx[2 * e], mx[2 * e + 1]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            i0 |= uint32_t(arg[e] | (mx[e] > 0.0f ? 4 : 0)) << (8 * e);
+            i1 |= uint32_t(arg[e + 4] | (mx[e + 4] > 0.0f ? 4 : 0)) << (8 * e);
+          }
+          *reinterpret_cast<uint4*>(a.p2 + o) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          *reinterpret_cast<uint2*>(a.idx + o) = make_uint2(i0, i1);
+        }
+        named_bar_sync(1, 128);  // tile buffer free for the next tile
+      } else {
+        float v[32];
+        tmem_ld32(taddr, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+        const int r = int(p0 - P28_FRONT) % P28_IMG + row;  // position within the image
+        const int pr = r / P28, pc = r % P28;
+        if (pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26) {
+          const int64_t pos = p0 + row;
+          const int64_t base = int64_t(j) * 4 * a.npos * 8;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(a.h1 + base + (c * a.npos + pos) * 8);
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+            uint32_t ow[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float lo = bf2f(uint16_t(hw[e] & 0xFFFF)) > 0.f ? v[c * 8 + 2 * e] : 0.f;
+              const float hi = bf2f(uint16_t(hw[e] >> 16)) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f;
+              ow[e] = pack_bf2(lo, hi);
+            }
+            *reinterpret_cast<uint4*>(a.dz1 + base + (c * a.npos + pos) * 8) =
+                make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          }
         }
       }
     }
-    const int ph = 2 * ti + phl;
-    const int64_t o = ((int64_t(j) * a.B + b) * 144 + ph * 12 + pw) * 64 + ch * 8;
-    uint32_t w[4];
-    uint32_t i0 = 0, i1 = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) w[e] = pack_bf2(mx[2 * e], mx[2 * e + 1]);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      i0 |= uint32_t(arg[e] | (mx[e] > 0.0f ? 4 : 0)) << (8 * e);
-      i1 |= uint32_t(arg[e + 4] | (mx[e + 4] > 0.0f ? 4 : 0)) << (8 * e);
-    }
-    *reinterpret_cast<uint4*>(a.p2 + o) = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint2*>(a.idx + o) = make_uint2(i0, i1);
-  }
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<64>(tmem);
-}
-
-// ------------------------------------------------------------ conv2 dgrad --
-// CTA = 128 consecutive P28 positions (rows 1..26 of one image, 6 tiles),
-// N = 32 ic, K = 9 taps x 64 oc (36 MMAs).  Epilogue: ReLU mask with h1,
-// write dz1 (valid 26x26 positions only; the border stays zero).
-constexpr int DG_SMEM_A = 8 * PATCH_BYTES;       // 23808
-constexpr int DG_SMEM_B = 9 * 8 * 512;           // 36864
-constexpr int DG_SMEM = DG_SMEM_A + DG_SMEM_B + 128;
-
-__global__ void __launch_bounds__(128) conv2_dgrad_tc_kernel(ConvArgs a) {
-  const int tile = blockIdx.x, j = blockIdx.y;
-  if (!a.lanes[j].active) return;
-  const int b = tile / 6, tk = tile % 6;
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full_bar, done_bar;
-  __shared__ uint32_t tmem_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t sA = smem_u32(sm), sB = sA + DG_SMEM_A;
-  const int64_t p0 = P28_FRONT + int64_t(b) * P28_IMG + P28 + 128 * tk;
-
-  if (tid == 0) {
-    mbar_init(&full_bar, 1);
-    mbar_init(&done_bar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<32>(&tmem_s);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_s;
-
-  if (tid == 0) {
-    mbar_expect_tx(&full_bar, DG_SMEM_A + DG_SMEM_B);
-    const uint16_t* dz2 = a.dz2 + int64_t(j) * 8 * a.npos * 8;
-    for (int c = 0; c < 8; ++c)
-      tma_bulk_g2s(sA + c * PATCH_BYTES, dz2 + (c * a.npos + p0 - HALO) * 8, PATCH_BYTES, &full_bar);
-    const uint16_t* wd = a.wt + int64_t(j) * a.wt_stride + CONV2_W;
-    for (int t = 0; t < 9; ++t)
-      tma_bulk_g2s(sB + t * 4096, wd + t * 2048, 4096, &full_bar);
-    mbar_wait(&full_bar, 0);
-    tc_fence_after();
-    constexpr uint32_t IDESC = umma_idesc_bf16(128, 32, false, false);
-#pragma unroll 1
-    for (int t = 0; t < 9; ++t)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const uint64_t ad = umma_desc_interleave(
-            sA + 2 * s * PATCH_BYTES + (HALO + tap_off_dgrad(t)) * 16, PATCH_BYTES, 128);
-        const uint64_t bd = umma_desc_interleave(sB + (t * 8 + 2 * s) * 512, 512, 128);
-        mma_bf16(tmem, ad, bd, IDESC, (t | s) ? 1u : 0u);
-      }
-    mma_commit(&done_bar);
-  }
-  mbar_wait(&done_bar, 0);
-  tc_fence_after();
-  float v[32];
-  tmem_ld32(tmem + (uint32_t(warp * 32) << 16), v);
-  const int r = (P28 + 128 * tk + warp * 32 + lane);  // position within image
-  const int pr = r / P28, pc = r % P28;
-  if (pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26) {
-    const int64_t pos = p0 + warp * 32 + lane;
-    const int64_t base = int64_t(j) * 4 * a.npos * 8;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 hv = *reinterpret_cast<const uint4*>(a.h1 + base + (c * a.npos + pos) * 8);
-      const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
-      uint32_t ow[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float lo = bf2f(uint16_t(hw[e] & 0xFFFF)) > 0.f ? v[c * 8 + 2 * e] : 0.f;
-        const float hi = bf2f(uint16_t(hw[e] >> 16)) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f;
-        ow[e] = pack_bf2(lo, hi);
-      }
-      *reinterpret_cast<uint4*>(a.dz1 + base + (c * a.npos + pos) * 8) =
-          make_uint4(ow[0], ow[1], ow[2], ow[3]);
-    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  if (warp == 0) tmem_dealloc<P::TCOLS>(tmem);
 }
 
 // ------------------------------------------------------------ conv2 wgrad --
 // dW2[oc][tap][ic] = sum_p dz2[p][oc] * h1[p + off(tap)][ic] over all P28
 // positions p (dz2's zero border kills invalid ones).  K = positions, both
-// operands MN-major.  M = 64 oc + 64 zero rows (UMMA M = 128), N = 32 ic per
-// tap, 9 accumulators in TMEM columns [32t, 32t+32).  CTA = (position range,
-// lane); 3-stage TMA-bulk ring of 128-position chunks.
+// operands MN-major (SWIZZLE_NONE).
+//   A = h1: for each ic chunk c, FOUR copies of the plane shifted by
+//       k = 0..3 positions are staged side by side (MN group g = 4c + k), so
+//       A's 128 rows = (ic chunk, kw shift) and ONE M=128 MMA computes the
+//       three kw taps of a kernel row (rows with k = 3 are spare).
+//   B = dz2 planes: N = 64 oc.
+//   D[kh] (TMEM cols 64kh..64kh+63) = rows (k, ic) x cols oc.
+// Per 16 positions: 3 MMAs (one per kh) instead of 9, and no zero padding.
+// Warp 4 = TMA producer (3-stage ring), warp 5 = MMA issuer, warps 0-2
+// write the partials (warp k holds tap kw = k).
 constexpr int WG_KC = 128;                        // positions per stage
-constexpr int WG_A_PLANE = WG_KC * 16;            // 2048
-constexpr int WG_A_BYTES = 16 * WG_A_PLANE;       // 8 real + 8 zero planes
-constexpr int WG_B_PLANE = 192 * 16;              // 186 used, padded to 192
-constexpr int WG_B_BYTES = 4 * WG_B_PLANE;
-constexpr int WG_STAGE = WG_A_BYTES + WG_B_BYTES; // 45056
+constexpr int WG_ACOPY = 184 * 16;                // one shifted copy: 184 positions
+constexpr int WG_ASTRIDE = 192 * 16;              // copy stride in smem (SBO)
+constexpr int WG_A_BYTES = 16 * WG_ASTRIDE;       // 49152
+constexpr int WG_B_PLANE = WG_KC * 16;            // 2048
+constexpr int WG_B_BYTES = 8 * WG_B_PLANE;        // 16384
+constexpr int WG_STAGE = WG_A_BYTES + WG_B_BYTES; // 65536
 constexpr int WG_STAGES = 3;
 constexpr int WG_SMEM = WG_STAGES * WG_STAGE + 128;
-constexpr uint32_t WG_TX = 8 * WG_A_PLANE + 4 * PATCH_BYTES;
+constexpr uint32_t WG_TX = 16 * WG_ACOPY + WG_B_BYTES;
 
-__global__ void __launch_bounds__(128) conv2_wgrad_tc_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
   const int split = blockIdx.x, j = blockIdx.y;
   if (!a.lanes[j].active) return;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -241,13 +262,8 @@ __global__ void __launch_bounds__(128) conv2_wgrad_tc_kernel(ConvArgs a) {
   const uint32_t s0 = smem_u32(sm);
   const int nch = a.B * P28_IMG / WG_KC;
   const int c_begin = split * nch / a.wgrad_splits, c_end = (split + 1) * nch / a.wgrad_splits;
+  const int n = c_end - c_begin;
 
-  // zero the padding planes (A rows 64..127) of every stage once
-  for (int s = 0; s < WG_STAGES; ++s) {
-    uint4* z = reinterpret_cast<uint4*>(sm + s * WG_STAGE + 8 * WG_A_PLANE);
-    for (int i = tid; i < 8 * WG_A_PLANE / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
-  }
-  fence_proxy_async_smem();
   if (tid == 0) {
     for (int s = 0; s < WG_STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -256,69 +272,80 @@ __global__ void __launch_bounds__(128) conv2_wgrad_tc_kernel(ConvArgs a) {
     mbar_init(&done_bar, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<512>(&tmem_s);
+  if (warp == 0) tmem_alloc<256>(&tmem_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_s;
 
-  if (tid == 0) {
-    const uint16_t* dz2 = a.dz2 + int64_t(j) * 8 * a.npos * 8;
-    const uint16_t* h1 = a.h1 + int64_t(j) * 4 * a.npos * 8;
-    auto load = [&](int c, int s) {
-      const int64_t q0 = P28_FRONT + int64_t(c) * WG_KC;
-      const uint32_t st = s0 + s * WG_STAGE;
-      mbar_expect_tx(&full_bar[s], WG_TX);
-      for (int k = 0; k < 8; ++k)
-        tma_bulk_g2s(st + k * WG_A_PLANE, dz2 + (k * a.npos + q0) * 8, WG_A_PLANE, &full_bar[s]);
-      for (int k = 0; k < 4; ++k)
-        tma_bulk_g2s(st + WG_A_BYTES + k * WG_B_PLANE, h1 + (k * a.npos + q0 - HALO) * 8,
-                     PATCH_BYTES, &full_bar[s]);
-    };
-    const int n = c_end - c_begin;
-    for (int i = 0; i < WG_STAGES - 1 && i < n; ++i) load(c_begin + i, i);
-    constexpr uint32_t IDESC = umma_idesc_bf16(128, 32, true, true);
-    for (int i = 0; i < n; ++i) {
-      const int s = i % WG_STAGES;
-      mbar_wait(&full_bar[s], (i / WG_STAGES) & 1);
-      tc_fence_after();
-      const uint32_t st = s0 + s * WG_STAGE;
-#pragma unroll 1
-      for (int k = 0; k < WG_KC / 16; ++k)
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const uint64_t ad = umma_desc_interleave(st + k * 256, 128, WG_A_PLANE);
-          const uint64_t bd = umma_desc_interleave(
-              st + WG_A_BYTES + (HALO + tap_off_fwd(t) + 16 * k) * 16, 128, WG_B_PLANE);
-          mma_bf16(tmem + 32 * t, ad, bd, IDESC, (i | k) ? 1u : 0u);
-        }
-      mma_commit(&empty_bar[s]);
-      const int nxt = i + WG_STAGES - 1;
-      if (nxt < n) {
-        const int sn = nxt % WG_STAGES;
-        if (nxt >= WG_STAGES) mbar_wait(&empty_bar[sn], ((nxt / WG_STAGES) - 1) & 1);
-        load(c_begin + nxt, sn);
+  if (warp == 4) {  // ---------------- TMA producer
+    if (lane == 0) {
+      const uint16_t* dz2 = a.dz2 + int64_t(j) * 8 * a.npos * 8;
+      const uint16_t* h1 = a.h1 + int64_t(j) * 4 * a.npos * 8;
+      for (int i = 0; i < n; ++i) {
+        const int s = i % WG_STAGES;
+        if (i >= WG_STAGES) mbar_wait(&empty_bar[s], ((i / WG_STAGES) - 1) & 1);
+        const int64_t q0 = P28_FRONT + int64_t(c_begin + i) * WG_KC;
+        const uint32_t st = s0 + s * WG_STAGE;
+        mbar_expect_tx(&full_bar[s], WG_TX);
+        for (int c = 0; c < 4; ++c)
+          for (int k = 0; k < 4; ++k)
+            tma_bulk_g2s(st + (c * 4 + k) * WG_ASTRIDE, h1 + (c * a.npos + q0 - HALO + k) * 8,
+                         WG_ACOPY, &full_bar[s]);
+        for (int c = 0; c < 8; ++c)
+          tma_bulk_g2s(st + WG_A_BYTES + c * WG_B_PLANE, dz2 + (c * a.npos + q0) * 8, WG_B_PLANE,
+                       &full_bar[s]);
       }
     }
-    mma_commit(&done_bar);
-  }
-  mbar_wait(&done_bar, 0);
-  tc_fence_after();
-  if (warp < 2) {  // rows 0..63 = oc
-    const int oc = warp * 32 + lane;
-    float* out = a.part2 + ((int64_t(j) * a.wgrad_splits + split) * 9 * 64 + oc) * 32;
-#pragma unroll 1
-    for (int t = 0; t < 9; ++t) {
-      float v[32];
-      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + 32 * t, v);
+  } else if (warp == 5) {  // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = umma_idesc_bf16(128, 64, true, true);
+      for (int i = 0; i < n; ++i) {
+        const int s = i % WG_STAGES;
+        mbar_wait(&full_bar[s], (i / WG_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = s0 + s * WG_STAGE;
+        const uint64_t ad0 = umma_desc_interleave(st, 128, WG_ASTRIDE);
+        const uint64_t bd0 = umma_desc_interleave(st + WG_A_BYTES, 128, WG_B_PLANE);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(out + t * 64 * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int k = 0; k < WG_KC / 16; ++k)
+#pragma unroll
+          for (int kh = 0; kh < 3; ++kh) {
+            // copy k' of plane c starts at position q0-29+k', so tap (kh, kw=k')
+            // of position q0+16k+r sits at index 16k + 28kh + r in every copy
+            const uint64_t ad = ad0 + uint64_t(((16 * k + 28 * kh) * 16) >> 4);
+            const uint64_t bd = bd0 + uint64_t((k * 256) >> 4);
+            mma_bf16(tmem + 64 * kh, ad, bd, IDESC, (i | k) ? 1u : 0u);
+          }
+        mma_commit(&empty_bar[s]);
+      }
+      mma_commit(&done_bar);
     }
+  }
+  if (warp < 4) mbar_wait(&done_bar, 0);
+  __syncthreads();
+  tc_fence_after();
+  if (warp < 4) {
+    // TMEM row r = 8g + e with MN group g = 4c + k': warp w holds ic chunk
+    // c = w, shift k' = lane >> 3 (k' = 3 is the spare copy), ic = 8c + e.
+    const int kp = lane >> 3, ic = warp * 8 + (lane & 7);
+    float* out = a.part2 + (int64_t(j) * a.wgrad_splits + split) * 9 * 64 * 32;
+#pragma unroll 1
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + 64 * kh + 32 * h, v);
+        if (kp < 3) {
+          float* o = out + ((kh * 3 + kp) * 64 + 32 * h) * 32 + ic;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) o[q * 32] = v[q];
+        }
+      }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace tlk
