@@ -134,12 +134,15 @@ def kernel_work(name, info, lanes, batch):
     conv2_flops = 2.0 * B * 576 * 64 * 288 * L
     fc1_flops = 2.0 * B * 9216 * 128 * L
     act = {
-        "optimizer": ("hbm", 28.0 * info.param_count * L),
+        # fc1.w (9216x128, 98% of the params) is updated inside its wgrad
+        # epilogue: p, m, v read + write and the bf16 shadow (26 B/param); the
+        # batched optimizer does the rest (28 B/param + 2 B shadow)
+        "fc1_wgrad_adam": ("hbm", 26.0 * 9216 * 128 * L),
+        "optimizer": ("hbm", 30.0 * (info.param_count - 9216 * 128) * L),
         "conv2_fwd_pool": ("tensor", conv2_flops),
         "conv2_wgrad": ("tensor", conv2_flops),
         "conv2_dgrad": ("tensor", conv2_flops),
         "fc1_fwd_splitk": ("tensor", fc1_flops),
-        "fc1_wgrad": ("tensor", fc1_flops),
         "fc1_dgrad_unpool": ("tensor", fc1_flops),
         # CUDA-core / bookkeeping kernels: compulsory HBM bytes
         "inputs": ("hbm", L * B * (784 + 784 * 2 + 4)),

@@ -74,7 +74,12 @@ typedef struct {
   int32_t lanes;      /* K co-resident jobs */
   int32_t max_steps;  /* loss-curve capacity per lane */
   int32_t host_input; /* 1: inputs come from tlk_step_host, 0: synthesised on device */
+  int32_t flags;      /* TLK_PACK_* */
 } tlk_pack_desc;
+
+/* pack flags */
+#define TLK_PACK_WRITE_ALL_GRADS 1 /* also store gradients whose optimizer update is fused
+                                      into a wgrad epilogue (tests/inspection) */
 
 typedef struct {
   int64_t param_count;   /* real parameters per job */

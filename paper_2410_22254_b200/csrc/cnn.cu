@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
 struct Fc1Fwd {
   static constexpr int BN = 64, STAGES = 4;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {};
   const LaneState* lanes;
@@ -146,6 +147,7 @@ __global__ void fc1_reduce_kernel(const LaneState* __restrict__ lanes, CnnBufs b
 struct Fc1Dgrad {
   static constexpr int BN = 64, STAGES = 4;
   static constexpr bool A_MN = true, B_MN = false;
+  static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {
     float s;
@@ -195,6 +197,83 @@ struct Fc1Dgrad {
   }
   TLK_DEV void finish(const Work& w, int f, Carry& c) const {
     buf.colsum[int64_t(w.j) * 9216 + f] = c.s;
+  }
+};
+
+// ------------------------------------------- fc1 wgrad + optimizer (TC) -----
+// dW1[o, f] = sum_b dz3[b, o] p2[b, f] (M = 128 out, N = 9216 in, K = batch,
+// both operands MN-major) with the lane's optimizer update applied in the
+// epilogue: fc1.w is 98% of the CNN's parameters, so its fp32 gradient never
+// makes the HBM round trip (grads are stored only with
+// TLK_PACK_WRITE_ALL_GRADS).  Must run after every reader of this step's fc1
+// weights (fc1 dgrad).  (Measured alternative: a separate optimizer pass in a
+// forked graph branch concurrent with the conv backward kernels was slower --
+// it crowds the SMs the conv kernels need.)
+struct Fc1WgradOpt {
+  static constexpr int BN = 64, STAGES = 2, THREADS = 256;
+  static constexpr bool A_MN = true, B_MN = true;
+  static constexpr bool TILE_EPILOGUE = true;
+  using Work = LaneWork;
+  struct Carry {};
+  const LaneState* lanes;
+  CnnBufs buf;
+  float *params, *grads, *m1, *m2;
+  uint16_t* wbf;
+  int64_t pstride, w_off;
+  int write_grads;
+
+  TLK_DEV bool work(Work& w) const {
+    w.j = blockIdx.z;
+    if (!lanes[w.j].active) return false;
+    w.m0 = 0;
+    w.n0 = blockIdx.y * BN;
+    w.kb_begin = 0;
+    w.kb_end = (buf.B + GEMM_BK - 1) / GEMM_BK;
+    w.split = 0;
+    return true;
+  }
+  TLK_DEV const void* zero_src() const { return buf.dz3; }
+  TLK_DEV const void* a_src(const Work& w, int m, int k) const {
+    return k < buf.B ? buf.dz3 + w.j * buf.h3_st + int64_t(k) * 128 + m : nullptr;
+  }
+  TLK_DEV const void* b_src(const Work& w, int n, int k) const {
+    return k < buf.B ? buf.p2 + w.j * buf.p2_st + int64_t(k) * 9216 + n : nullptr;
+  }
+  TLK_DEV void epilogue(const Work&, int, int, const float (&)[32], Carry&) const {}
+  TLK_DEV void finish(const Work&, int, Carry&) const {}
+  // tile = dW1[128 o][64 f] in smem.  256 threads: thread -> float4 column
+  // c4 = tid % 16 of rows r0 + 16k: a warp covers two 256-B row segments per
+  // access; 2 rows (6 float4 loads) in flight per thread before any math.
+  TLK_DEV void tile_epilogue(const Work& w, const float* tile, int ld) const {
+    const LaneState s = lanes[w.j];
+    const int tid = threadIdx.x, c4 = tid & 15, r0 = tid >> 4;
+    const int64_t base = w.j * pstride + w_off + w.n0 + 4 * c4;
+#pragma unroll 1
+    for (int k0 = 0; k0 < 8; k0 += 2) {
+      float4 p[2], mm[2], vv[2];
+      int64_t e[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        e[u] = base + int64_t(r0 + 16 * (k0 + u)) * 9216;
+        p[u] = *reinterpret_cast<const float4*>(params + e[u]);
+        mm[u] = *reinterpret_cast<const float4*>(m1 + e[u]);
+        vv[u] = *reinterpret_cast<const float4*>(m2 + e[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 g = *reinterpret_cast<const float4*>(tile + (r0 + 16 * (k0 + u)) * ld + 4 * c4);
+        opt_update(s, p[u].x, g.x, mm[u].x, vv[u].x);
+        opt_update(s, p[u].y, g.y, mm[u].y, vv[u].y);
+        opt_update(s, p[u].z, g.z, mm[u].z, vv[u].z);
+        opt_update(s, p[u].w, g.w, mm[u].w, vv[u].w);
+        *reinterpret_cast<float4*>(params + e[u]) = p[u];
+        *reinterpret_cast<float4*>(m1 + e[u]) = mm[u];
+        *reinterpret_cast<float4*>(m2 + e[u]) = vv[u];
+        *reinterpret_cast<uint2*>(wbf + e[u]) =
+            make_uint2(pack_bf2(p[u].x, p[u].y), pack_bf2(p[u].z, p[u].w));
+        if (write_grads) *reinterpret_cast<float4*>(grads + e[u]) = g;
+      }
+    }
   }
 };
 
@@ -361,6 +440,8 @@ int cnn_setup(Pack& p) {
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
   p.launches_per_step = 14;
+  p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
+  p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
 }
 
@@ -389,12 +470,13 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   p.mark(st, "fc1_reduce");
   TLK_CUDA(cudaGetLastError());
   if ((rc = enqueue_head(p, st, b.h3, 128, o_f2w, o_f2b, b.dz3, o_f1b))) return rc;
-  LinWgrad f1w{p.lane_dev, b.dz3, b.h3_st, b.p2, b.p2_st, p.grads, p.stride, o_f1w, 128, 9216, B};
-  TLK_CUDA(launch_gemm(f1w, dim3(1, 9216 / LinWgrad::BN, L), st));
-  p.mark(st, "fc1_wgrad");
-  Fc1Dgrad f1d{p.lane_dev, b, p.wbf, p.stride, o_f1w};
+  Fc1Dgrad f1d{p.lane_dev, b, p.wbf, p.stride, o_f1w};  // reads this step's fc1 weights
   TLK_CUDA(launch_gemm(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
+  Fc1WgradOpt f1w{p.lane_dev, b, p.params, p.grads, p.mom1, p.mom2, p.wbf, p.stride, o_f1w,
+                  (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0};
+  TLK_CUDA(launch_gemm(f1w, dim3(1, 9216 / Fc1WgradOpt::BN, L), st));
+  p.mark(st, "fc1_wgrad_adam");
   conv2_wgrad_tc_kernel<<<dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st>>>(ca);
   p.mark(st, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());

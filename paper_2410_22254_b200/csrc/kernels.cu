@@ -1,6 +1,7 @@
 // Model-independent kernels of a pack step: synthetic inputs, lane init,
 // fused classifier head (Linear + softmax-CE + its backward), batched
 // optimizer over every lane's flat parameter arena, step bookkeeping.
+#include <algorithm>
 #include <cmath>
 
 #include "pack.cuh"
@@ -307,76 +308,108 @@ int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_
 // p, g, m, v (16 B/param), writes p, m, v (12 B) + the bf16 GEMM shadow (2 B).
 // Every op is an explicit IEEE-rounded intrinsic in the same order as
 // oracle/optim.py, so the update is bit-exact given identical gradients.
-__device__ __forceinline__ void opt_one(const LaneState& s, float& p, float g, float& m, float& v) {
-  if (s.optimizer == TLK_OPT_SGD) {
-    if (s.wd != 0.0f) g = __fadd_rn(g, __fmul_rn(p, s.wd));
-    if (s.momentum != 0.0f) {
-      m = s.first_step ? g : __fadd_rn(__fmul_rn(m, s.momentum), g);
-      g = m;
-    }
-    p = __fsub_rn(p, __fmul_rn(s.lr, g));
-    return;
-  }
-  if (s.optimizer == TLK_OPT_ADAMW)
-    p = __fmul_rn(p, s.decay);
-  else if (s.wd != 0.0f)
-    g = __fadd_rn(g, __fmul_rn(p, s.wd));
-  m = __fadd_rn(m, __fmul_rn(s.w1, __fsub_rn(g, m)));
-  v = __fadd_rn(__fmul_rn(v, s.b2f), __fmul_rn(__fmul_rn(g, g), s.w2));
-  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), s.bc2s), s.eps);
-  p = __fsub_rn(p, __fmul_rn(s.step_size, __fdiv_rn(m, denom)));
-}
-
+// Grid = (blocks_per_lane, lanes): a CTA streams a contiguous range of ONE
+// lane (its LaneState read once), two float4 per thread in flight.  The
+// range processed in every lane is the union of two segments
+// [a0, a1) u [b0, b1) (float4 units) so a pack can update different tensors
+// in different graph branches (CNN: fc1.w concurrently with the conv
+// backward kernels, everything else at the end of the step).
 __global__ void __launch_bounds__(256) optimizer_kernel(const LaneState* __restrict__ lanes,
-                                                        int nlanes, int64_t stride,
+                                                        int64_t stride, int64_t a0, int64_t a1,
+                                                        int64_t b0, int64_t b1,
                                                         float4* __restrict__ P,
                                                         const float4* __restrict__ Gr,
                                                         float4* __restrict__ M,
                                                         float4* __restrict__ V,
                                                         uint2* __restrict__ Wb, WtHook hook) {
-  const int64_t n4 = int64_t(nlanes) * stride / 4;
-  const int64_t s4 = stride / 4;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int lane = int(i / s4);
-    const LaneState& s = lanes[lane];
-    if (!s.active) continue;
-    float4 p = P[i], m = M[i], v = V[i];
-    const float4 g = Gr[i];
-    opt_one(s, p.x, g.x, m.x, v.x);
-    opt_one(s, p.y, g.y, m.y, v.y);
-    opt_one(s, p.z, g.z, m.z, v.z);
-    opt_one(s, p.w, g.w, m.w, v.w);
-    P[i] = p;
-    M[i] = m;
-    V[i] = v;
-    const uint32_t lo = pack_bf2(p.x, p.y), hi = pack_bf2(p.z, p.w);
-    Wb[i] = make_uint2(lo, hi);
+  const int lane = blockIdx.y;
+  if (!lanes[lane].active) return;
+  const LaneState s = lanes[lane];
+  const int64_t na = a1 - a0, work = na + (b1 - b0);
+  const int64_t per = (work + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = blockIdx.x * per, w1 = min(work, w0 + per);
+  const int64_t base = lane * (stride / 4);
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += 2 * blockDim.x) {
+    const int64_t wb = w + blockDim.x;
+    const bool two = wb < w1;
+    const int64_t ia = base + (w < na ? a0 + w : b0 + (w - na));
+    const int64_t ib = base + (wb < na ? a0 + wb : b0 + (wb - na));
+    float4 pa = P[ia], ma = M[ia], va = V[ia];
+    const float4 ga = Gr[ia];
+    float4 pb, mb, vb, gb;
+    if (two) {
+      pb = P[ib];
+      mb = M[ib];
+      vb = V[ib];
+      gb = Gr[ib];
+    }
+    opt_update(s, pa.x, ga.x, ma.x, va.x);
+    opt_update(s, pa.y, ga.y, ma.y, va.y);
+    opt_update(s, pa.z, ga.z, ma.z, va.z);
+    opt_update(s, pa.w, ga.w, ma.w, va.w);
+    P[ia] = pa;
+    M[ia] = ma;
+    V[ia] = va;
+    const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
+    Wb[ia] = make_uint2(lo, hi);
     if (hook.wt) {
-      const int64_t e = (i - lane * s4) * 4;
+      const int64_t e = (ia - base) * 4;
       wt_write(hook, lane, e + 0, uint16_t(lo & 0xFFFF));
       wt_write(hook, lane, e + 1, uint16_t(lo >> 16));
       wt_write(hook, lane, e + 2, uint16_t(hi & 0xFFFF));
       wt_write(hook, lane, e + 3, uint16_t(hi >> 16));
     }
+    if (two) {
+      opt_update(s, pb.x, gb.x, mb.x, vb.x);
+      opt_update(s, pb.y, gb.y, mb.y, vb.y);
+      opt_update(s, pb.z, gb.z, mb.z, vb.z);
+      opt_update(s, pb.w, gb.w, mb.w, vb.w);
+      P[ib] = pb;
+      M[ib] = mb;
+      V[ib] = vb;
+      const uint32_t lo2 = pack_bf2(pb.x, pb.y), hi2 = pack_bf2(pb.z, pb.w);
+      Wb[ib] = make_uint2(lo2, hi2);
+      if (hook.wt) {
+        const int64_t e = (ib - base) * 4;
+        wt_write(hook, lane, e + 0, uint16_t(lo2 & 0xFFFF));
+        wt_write(hook, lane, e + 1, uint16_t(lo2 >> 16));
+        wt_write(hook, lane, e + 2, uint16_t(hi2 & 0xFFFF));
+        wt_write(hook, lane, e + 3, uint16_t(hi2 >> 16));
+      }
+    }
   }
 }
 
-int enqueue_optimizer(Pack& p, cudaStream_t st) {
+// Update the floats [lo, hi) of every lane (lo, hi multiples of 4), or with
+// complement=true everything else.
+int enqueue_optimizer_range(Pack& p, cudaStream_t st, int64_t lo, int64_t hi, bool complement,
+                            const char* name) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t n4 = int64_t(p.lanes) * p.stride / 4;
-  int64_t blocks = (n4 + 255) / 256;
-  const int64_t cap = int64_t(sms) * 8;
-  if (blocks > cap) blocks = cap;
-  optimizer_kernel<<<int(blocks), 256, 0, st>>>(
-      p.lane_dev, p.lanes, p.stride, reinterpret_cast<float4*>(p.params),
+  const int64_t s4 = p.stride / 4;
+  int64_t a0, a1, b0, b1;
+  if (complement) {
+    a0 = 0, a1 = lo / 4, b0 = hi / 4, b1 = s4;
+  } else {
+    a0 = lo / 4, a1 = hi / 4, b0 = b1 = 0;
+  }
+  const int64_t work = (a1 - a0) + (b1 - b0);
+  if (work <= 0) return TLK_OK;
+  int64_t per_lane = (work + 511) / 512;  // ~2 float4 per thread
+  const int64_t cap = std::max<int64_t>(1, int64_t(sms) * 8 / p.lanes);
+  per_lane = std::min(std::max<int64_t>(per_lane, 1), cap);
+  optimizer_kernel<<<dim3(unsigned(per_lane), p.lanes), 256, 0, st>>>(
+      p.lane_dev, p.stride, a0, a1, b0, b1, reinterpret_cast<float4*>(p.params),
       reinterpret_cast<const float4*>(p.grads), reinterpret_cast<float4*>(p.mom1),
       reinterpret_cast<float4*>(p.mom2), reinterpret_cast<uint2*>(p.wbf), wt_hook(p));
-  p.mark(st, "optimizer");
+  p.mark(st, name);
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
+}
+
+int enqueue_optimizer(Pack& p, cudaStream_t st) {
+  return enqueue_optimizer_range(p, st, p.fused_lo, p.fused_hi, true, "optimizer");
 }
 
 // ------------------------------------------------------------ end of step ---

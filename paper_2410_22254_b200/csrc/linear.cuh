@@ -22,6 +22,7 @@ struct LaneWork {
 struct LinFwd {
   static constexpr int BN = 64, STAGES = 4;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {};
   const LaneState* lanes;
@@ -65,6 +66,7 @@ struct LinFwd {
 struct LinWgrad {
   static constexpr int BN = 128, STAGES = 4;
   static constexpr bool A_MN = true, B_MN = true;
+  static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {};
   const LaneState* lanes;
@@ -112,6 +114,7 @@ struct LinWgrad {
 struct LinDgrad {
   static constexpr int BN = 64, STAGES = 4;
   static constexpr bool A_MN = true, B_MN = false;
+  static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {
     float db;

@@ -42,6 +42,13 @@ struct Pack {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int launches_per_step = 0;
+  // parameter range (floats, within a lane) whose update is fused into its
+  // wgrad epilogue (see cnn.cu); the end-of-step optimizer skips it
+  int64_t fused_lo = 0, fused_hi = 0;
+  // side stream + events for concurrent graph branches
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int flags = 0;  // TLK_PACK_* (e.g. write every gradient for tests)
   // per-kernel profiling (tlk_profile_step): an event after every launch
   std::vector<cudaEvent_t>* prof = nullptr;
   std::vector<const char*>* prof_names = nullptr;
@@ -77,6 +84,8 @@ int enqueue_inputs(Pack& p, cudaStream_t st);  // datagen (or host-input convert
 int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_t w_off,
                  int64_t b_off, uint16_t* dz_prev, int64_t db_prev_off);
 int enqueue_optimizer(Pack& p, cudaStream_t st);
+int enqueue_optimizer_range(Pack& p, cudaStream_t st, int64_t lo, int64_t hi, bool complement,
+                            const char* name);
 int enqueue_end_step(Pack& p, cudaStream_t st);
 int enqueue_lane_init(Pack& p, int lane, cudaStream_t st);
 int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teacher, uint8_t* px,

@@ -56,6 +56,9 @@ struct tlk_ctx {
 namespace {
 
 void destroy_pack(Pack& p) {
+  if (p.side) cudaStreamDestroy(p.side);
+  if (p.ev_fork) cudaEventDestroy(p.ev_fork);
+  if (p.ev_join) cudaEventDestroy(p.ev_join);
   if (p.graph_exec) cudaGraphExecDestroy(p.graph_exec);
   if (p.graph) cudaGraphDestroy(p.graph);
   for (void* a : p.allocs) cudaFree(a);
@@ -191,6 +194,7 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   p->lanes = desc->lanes;
   p->max_steps = desc->max_steps;
   p->host_input = desc->host_input;
+  p->flags = desc->flags;
   p->def = d;
   p->pcount = param_count(*d);
   p->stride = param_stride(*d);
@@ -219,6 +223,9 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
     destroy_pack(*p);
     return rc;
   }
+  TLK_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  TLK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  TLK_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   p->lane_host.assign(L, LaneState{});
   TLK_CUDA(cudaMemsetAsync(p->lane_dev, 0, L * sizeof(LaneState), ctx->stream));
   TLK_CUDA(cudaMemsetAsync(p->loss, 0, L * size_t(p->max_steps) * 4, ctx->stream));

@@ -11,6 +11,7 @@ template <int BN_, bool AMN, bool BMN>
 struct PlainGemm {
   static constexpr int BN = BN_;
   static constexpr bool A_MN = AMN, B_MN = BMN;
+  static constexpr bool TILE_EPILOGUE = false;
   static constexpr int STAGES = 4;
   struct Work {
     int j, m0, n0, kb_begin, kb_end;

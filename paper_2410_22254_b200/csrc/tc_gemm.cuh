@@ -68,7 +68,17 @@ TLK_DEV uint64_t stage_desc(uint32_t base, int kk) {
 }
 
 template <class P>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) tc_gemm_kernel(const P p) {
+struct GemmThreads {  // problems may ask for 256 threads (extra epilogue warps)
+  template <class Q>
+  static constexpr int get(decltype(Q::THREADS)*) { return Q::THREADS; }
+  template <class Q>
+  static constexpr int get(...) { return GEMM_THREADS; }
+  static constexpr int value = get<P>(nullptr);
+};
+
+template <class P>
+__global__ void __launch_bounds__(GemmThreads<P>::value, 1) tc_gemm_kernel(const P p) {
+  constexpr int NT = GemmThreads<P>::value;
   constexpr int BN = P::BN;
   constexpr int STAGES = P::STAGES;
   using S = GemmSmem<P>;
@@ -112,7 +122,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) tc_gemm_kernel(const P p) {
       const uint32_t a_s = sbase + s * S::STAGE_BYTES;
       const uint32_t b_s = a_s + S::A_BYTES;
 #pragma unroll 4
-      for (int i = tid; i < A_CH; i += GEMM_THREADS) {
+      for (int i = tid; i < A_CH; i += NT) {
         int mn, k;
         uint32_t off;
         chunk_coord<GEMM_BM, P::A_MN>(i, mn, k, off);
@@ -120,7 +130,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) tc_gemm_kernel(const P p) {
         cp_async16(a_s + off, src ? src : p.zero_src(), src ? 16u : 0u);
       }
 #pragma unroll 4
-      for (int i = tid; i < B_CH; i += GEMM_THREADS) {
+      for (int i = tid; i < B_CH; i += NT) {
         int mn, k;
         uint32_t off;
         chunk_coord<BN, P::B_MN>(i, mn, k, off);
@@ -153,14 +163,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) tc_gemm_kernel(const P p) {
   mbar_wait(&done_bar, 0);
   tc_fence_after();
   const int row = warp * 32 + lane;
-  typename P::Carry carry{};
+  if constexpr (P::TILE_EPILOGUE) {
+    // stage the fp32 tile in (now idle) operand smem, then let all threads
+    // run a coalesced, many-loads-in-flight epilogue over it
+    static_assert(GEMM_BM * (BN + 4) * 4 <= P::STAGES * S::STAGE_BYTES, "tile fits");
+    float* tile = reinterpret_cast<float*>(smem);
+    if (warp < 4) {
 #pragma unroll 1
-  for (int cc = 0; cc < BN / 32; ++cc) {
-    float v[32];
-    tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
-    p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v, carry);
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(tile + row * (BN + 4) + cc * 32 + i) =
+              make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+    __syncthreads();
+    p.tile_epilogue(w, tile, BN + 4);
+  } else if (warp < 4) {
+    typename P::Carry carry{};
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      float v[32];
+      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
+      p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v, carry);
+    }
+    p.finish(w, w.m0 + row, carry);
   }
-  p.finish(w, w.m0 + row, carry);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
@@ -177,7 +207,7 @@ inline cudaError_t launch_gemm(const P& p, dim3 grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  tc_gemm_kernel<P><<<grid, GEMM_THREADS, bytes, stream>>>(p);
+  tc_gemm_kernel<P><<<grid, GemmThreads<P>::value, bytes, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@ MODEL_MLP, MODEL_CNN = 1, 2
 MODELS = {"mlp": MODEL_MLP, "cnn": MODEL_CNN}
 OPT_ADAM, OPT_ADAMW, OPT_SGD = 1, 2, 3
 OPTIMIZERS = {"adam": OPT_ADAM, "adamw": OPT_ADAMW, "sgd": OPT_SGD}
+PACK_WRITE_ALL_GRADS = 1
 BUF_PARAMS, BUF_GRADS, BUF_MOM1, BUF_MOM2, BUF_WBF16, BUF_LOSS, BUF_PIXELS, BUF_LABELS, BUF_ACTS = range(9)
 
 EXPORTS = (
@@ -45,7 +46,7 @@ class JobDesc(C.Structure):
 
 class PackDesc(C.Structure):
     _fields_ = [("model", C.c_int32), ("batch", C.c_int32), ("lanes", C.c_int32),
-                ("max_steps", C.c_int32), ("host_input", C.c_int32)]
+                ("max_steps", C.c_int32), ("host_input", C.c_int32), ("flags", C.c_int32)]
 
 
 class ModelInfo(C.Structure):
@@ -144,18 +145,19 @@ class Context:
         check(lib().tlk_stream(self._ctx, C.byref(s)))
         return s.value or 0
 
-    def pack(self, model: int, batch: int, lanes: int, max_steps: int, host_input: bool = False):
-        return Pack(self, model, batch, lanes, max_steps, host_input)
+    def pack(self, model: int, batch: int, lanes: int, max_steps: int, host_input: bool = False,
+             flags: int = 0):
+        return Pack(self, model, batch, lanes, max_steps, host_input, flags)
 
 
 class Pack:
     """K co-resident training lanes of one model (tlk_pack_*)."""
 
     def __init__(self, ctx: Context, model: int, batch: int, lanes: int, max_steps: int,
-                 host_input: bool = False):
+                 host_input: bool = False, flags: int = 0):
         self.ctx, self.model, self.batch, self.lanes = ctx, model, batch, lanes
         self.max_steps, self.host_input = max_steps, host_input
-        desc = PackDesc(model, batch, lanes, max_steps, int(host_input))
+        desc = PackDesc(model, batch, lanes, max_steps, int(host_input), int(flags))
         pid = C.c_int32()
         check(lib().tlk_pack_create(ctx._ctx, C.byref(desc), C.byref(pid)))
         self.id = pid.value

@@ -276,7 +276,7 @@ def _teacher_forced(model, lanes_cfg, steps, batch=64):
 
     step_fn = omodels.STEP_FNS[model]
     with rt.Context(0) as ctx:
-        pack = ctx.pack(model, batch, len(lanes_cfg), steps)
+        pack = ctx.pack(model, batch, len(lanes_cfg), steps, flags=rt.PACK_WRITE_ALL_GRADS)
         for lane, (seed, opt, kw) in enumerate(lanes_cfg):
             pack.load(lane, seed=seed, steps=steps, optimizer=opt, **kw)
         P, G = pack.tensor(rt.BUF_PARAMS), pack.tensor(rt.BUF_GRADS)
