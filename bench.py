@@ -290,6 +290,7 @@ def packed_arm(a, world, rank, local):
     kernels = pack.profile_step(a.profile_iters)
     step_ms = sum(t for _, t in kernels)
     top_name, top_ms = max(kernels, key=lambda kv: kv[1])
+    top_ms = max(top_ms, 1e-6)
     bound, work = kernel_work(top_name, pack.info, lanes, BATCH)
     if bound == "tensor":
         achieved = work / (top_ms / 1e3) / 1e12

@@ -30,6 +30,11 @@ constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
 constexpr int C2W_SPLITS = 18;     // conv2 wgrad position splits per lane
 
 struct CnnBufs {
+  // TMA tensor maps of the plain-layout fc1 operands (lanes = dim 2)
+  CUtensorMap w1_k;   // fc1.w bf16 [9216 in][128 out]: box 64 x 128 (K-major A)
+  CUtensorMap w1_mn;  // fc1.w bf16: box 64 x 64 (MN-major A of dgrad)
+  CUtensorMap p2m;    // p2 [9216][B]: box 64 x 64
+  CUtensorMap dz3m;   // dz3 [128][B]: box 64 x 64
   int B;
   int64_t npos;
   uint16_t *h1, *p2, *h3, *dz3, *dz2, *dz1;
@@ -61,26 +66,32 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
   if (tid < 32) bs[tid] = params[j * pstride + b_off + tid];
   __syncthreads();
   uint16_t* h1 = buf.h1 + int64_t(j) * 4 * buf.npos * 8;
-  for (int i = tid; i < 676 * 4; i += 256) {
-    const int pos = i >> 2, c = i & 3, oh = pos / 26, ow = pos % 26;
+  const int c = tid & 3;  // this thread's 8-channel chunk: its 72 weights live in registers
+  float w[8][9], bsum[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    bsum[e] = bs[c * 8 + e];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) w[e][t] = ws[(c * 8 + e) * 9 + t];
+  }
+  for (int pos = tid >> 2; pos < 676; pos += 64) {
+    const int oh = pos / 26, ow = pos % 26;
+    float xv[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
     float acc[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int e = 0; e < 8; ++e) {
+      acc[e] = 0.f;
 #pragma unroll
-    for (int kh = 0; kh < 3; ++kh)
-#pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const float xv = xs[(oh + kh) * 28 + ow + kw];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += xv * ws[(c * 8 + e) * 9 + kh * 3 + kw];
-      }
-    uint32_t w[4];
+      for (int t = 0; t < 9; ++t) acc[e] += xv[t] * w[e][t];
+    }
+    uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      w[e] = pack_bf2(fmaxf(acc[2 * e] + bs[c * 8 + 2 * e], 0.f),
-                      fmaxf(acc[2 * e + 1] + bs[c * 8 + 2 * e + 1], 0.f));
+      o[e] = pack_bf2(fmaxf(acc[2 * e] + bsum[2 * e], 0.f), fmaxf(acc[2 * e + 1] + bsum[2 * e + 1], 0.f));
     *reinterpret_cast<uint4*>(h1 + (c * buf.npos + p28_pos(s, oh + 1, ow + 1)) * 8) =
-        make_uint4(w[0], w[1], w[2], w[3]);
+        make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -92,10 +103,8 @@ struct Fc1Fwd {
   static constexpr bool TILE_EPILOGUE = false;
   using Work = LaneWork;
   struct Carry {};
+  CnnBufs buf;  // first: holds the (64-B aligned) tensor maps
   const LaneState* lanes;
-  CnnBufs buf;
-  const uint16_t* wbf;
-  int64_t pstride, w_off;
 
   TLK_DEV bool work(Work& w) const {
     w.j = blockIdx.z / FC1_SPLITS;
@@ -107,12 +116,15 @@ struct Fc1Fwd {
     w.kb_end = w.kb_begin + 144 / FC1_SPLITS;
     return true;
   }
-  TLK_DEV const void* zero_src() const { return wbf; }
-  TLK_DEV const void* a_src(const Work& w, int m, int k) const {
-    return wbf + w.j * pstride + w_off + int64_t(m) * 9216 + k;
+  TLK_DEV void prefetch() const {
+    tma_prefetch_desc(&buf.w1_k);
+    tma_prefetch_desc(&buf.p2m);
   }
-  TLK_DEV const void* b_src(const Work& w, int n, int k) const {
-    return n < buf.B ? buf.p2 + w.j * buf.p2_st + int64_t(n) * 9216 + k : nullptr;
+  TLK_DEV void load_a(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.w1_k, kb * GEMM_BK, 0, w.j, bar);
+  }
+  TLK_DEV void load_b(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.p2m, kb * GEMM_BK, 0, w.j, bar);
   }
   TLK_DEV void epilogue(const Work& w, int m, int n0, const float (&v)[32], Carry&) const {
     float* o = buf.part_fc1 + ((int64_t(w.j) * FC1_SPLITS + w.split) * 128 + m) * 64 + n0;
@@ -145,17 +157,13 @@ __global__ void fc1_reduce_kernel(const LaneState* __restrict__ lanes, CnnBufs b
 // argmax (live bit = pooled value > 0) into the dz2 P28 planes and
 // accumulates the conv2 bias-gradient partial colsum[f] = sum_b dz2 value.
 struct Fc1Dgrad {
-  static constexpr int BN = 64, STAGES = 4;
+  static constexpr int BN = 64, STAGES = 2, THREADS = 256;
   static constexpr bool A_MN = true, B_MN = false;
-  static constexpr bool TILE_EPILOGUE = false;
+  static constexpr bool TILE_EPILOGUE = true;
   using Work = LaneWork;
-  struct Carry {
-    float s;
-  };
-  const LaneState* lanes;
+  struct Carry {};
   CnnBufs buf;
-  const uint16_t* wbf;
-  int64_t pstride, w_off;
+  const LaneState* lanes;
 
   TLK_DEV bool work(Work& w) const {
     w.j = blockIdx.z;
@@ -167,36 +175,63 @@ struct Fc1Dgrad {
     w.split = 0;
     return true;
   }
-  TLK_DEV const void* zero_src() const { return wbf; }
-  TLK_DEV const void* a_src(const Work& w, int m, int k) const {
-    return wbf + w.j * pstride + w_off + int64_t(k) * 9216 + m;
+  TLK_DEV void prefetch() const {
+    tma_prefetch_desc(&buf.w1_mn);
+    tma_prefetch_desc(&buf.dz3m);
   }
-  TLK_DEV const void* b_src(const Work& w, int n, int k) const {
-    return n < buf.B ? buf.dz3 + w.j * buf.h3_st + n * 128 + k : nullptr;
+  TLK_DEV void load_a(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.w1_mn, w.m0, kb * GEMM_BK, w.j, bar);
+    tma_load_3d(dst + 8192, &buf.w1_mn, w.m0 + 64, kb * GEMM_BK, w.j, bar);
   }
-  TLK_DEV void epilogue(const Work& w, int f, int n0, const float (&v)[32], Carry& c) const {
-    const int pos = f >> 6, ch = f & 63, ph = pos / 12, pw = pos % 12;
-    const uint8_t* ix = buf.idx + w.j * buf.p2_st + f;
-    uint8_t code[32];
+  TLK_DEV void load_b(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.dz3m, kb * GEMM_BK, 0, w.j, bar);
+  }
+  TLK_DEV void epilogue(const Work&, int, int, const float (&)[32], Carry&) const {}
+  TLK_DEV void finish(const Work&, int, Carry&) const {}
+  // tile = dp2^T[128 f][64 b] for f = two pooled positions x 64 channels.
+  // Phase 1, item = (b, position, 8-channel chunk): the 2x2 window of the
+  // chunk is written as four 16-B stores into the dz2 P28 plane (argmax gets
+  // bf16(value) if the pooled output was live, the rest zeros); the rounded
+  // value replaces the tile entry.  Phase 2: colsum[f] = sum_b (fixed order).
+  TLK_DEV void tile_epilogue(const Work& w, float* tile, int ld) const {
+    const int tid = threadIdx.x, B = buf.B;
+    const int pos0 = w.m0 >> 6;
+    for (int i = tid; i < 64 * 16; i += 256) {
+      const int b = i & 63, pl = (i >> 6) >> 3, ch = (i >> 6) & 7;
+      if (b >= B) continue;
+      const int pos = pos0 + pl, ph = pos / 12, pw = pos % 12, f = pl * 64 + ch * 8;
+      const uint2 code2 = *reinterpret_cast<const uint2*>(buf.idx + w.j * buf.p2_st +
+                                                          int64_t(b) * 9216 + pos * 64 + ch * 8);
+      const uint32_t cw[2] = {code2.x, code2.y};
+      uint16_t z[8];
+      int q[8];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) code[i] = (n0 + i < buf.B) ? ix[int64_t(n0 + i) * 9216] : 0;
-    uint16_t* plane = buf.dz2 + (int64_t(w.j) * 8 + (ch >> 3)) * buf.npos * 8 + (ch & 7);
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t code = (cw[e >> 2] >> (8 * (e & 3))) & 0xFF;
+        float* t = tile + (f + e) * ld + b;
+        z[e] = (code & 4) ? f2bf(*t) : uint16_t(0);
+        q[e] = code & 3;
+        *t = bf2f(z[e]);
+      }
+      uint16_t* plane = buf.dz2 + (int64_t(w.j) * 8 + ch) * buf.npos * 8;
+      const int64_t p = p28_pos(b, 2 * ph + 2, 2 * pw + 2);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int b = n0 + i;
-      if (b < buf.B) {
-        const uint16_t z = (code[i] & 4) ? f2bf(v[i]) : uint16_t(0);
-        const int q = code[i] & 3;
-        const int64_t p = p28_pos(b, 2 * ph + 2, 2 * pw + 2);
+      for (int r = 0; r < 4; ++r) {
+        uint32_t o[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          plane[(p + (r >> 1) * P28 + (r & 1)) * 8] = (r == q) ? z : uint16_t(0);
-        c.s += bf2f(z);
+        for (int e = 0; e < 4; ++e)
+          o[e] = uint32_t(q[2 * e] == r ? z[2 * e] : 0) |
+                 (uint32_t(q[2 * e + 1] == r ? z[2 * e + 1] : 0) << 16);
+        *reinterpret_cast<uint4*>(plane + (p + (r >> 1) * P28 + (r & 1)) * 8) =
+            make_uint4(o[0], o[1], o[2], o[3]);
       }
     }
-  }
-  TLK_DEV void finish(const Work& w, int f, Carry& c) const {
-    buf.colsum[int64_t(w.j) * 9216 + f] = c.s;
+    __syncthreads();
+    if (tid < 128) {
+      float s = 0.f;
+      for (int b = 0; b < B; ++b) s += tile[tid * ld + b];
+      buf.colsum[int64_t(w.j) * 9216 + w.m0 + tid] = s;
+    }
   }
 };
 
@@ -215,8 +250,8 @@ struct Fc1WgradOpt {
   static constexpr bool TILE_EPILOGUE = true;
   using Work = LaneWork;
   struct Carry {};
-  const LaneState* lanes;
   CnnBufs buf;
+  const LaneState* lanes;
   float *params, *grads, *m1, *m2;
   uint16_t* wbf;
   int64_t pstride, w_off;
@@ -232,19 +267,23 @@ struct Fc1WgradOpt {
     w.split = 0;
     return true;
   }
-  TLK_DEV const void* zero_src() const { return buf.dz3; }
-  TLK_DEV const void* a_src(const Work& w, int m, int k) const {
-    return k < buf.B ? buf.dz3 + w.j * buf.h3_st + int64_t(k) * 128 + m : nullptr;
+  TLK_DEV void prefetch() const {
+    tma_prefetch_desc(&buf.dz3m);
+    tma_prefetch_desc(&buf.p2m);
   }
-  TLK_DEV const void* b_src(const Work& w, int n, int k) const {
-    return k < buf.B ? buf.p2 + w.j * buf.p2_st + int64_t(k) * 9216 + n : nullptr;
+  TLK_DEV void load_a(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.dz3m, 0, kb * GEMM_BK, w.j, bar);
+    tma_load_3d(dst + 8192, &buf.dz3m, 64, kb * GEMM_BK, w.j, bar);
+  }
+  TLK_DEV void load_b(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
+    tma_load_3d(dst, &buf.p2m, w.n0, kb * GEMM_BK, w.j, bar);
   }
   TLK_DEV void epilogue(const Work&, int, int, const float (&)[32], Carry&) const {}
   TLK_DEV void finish(const Work&, int, Carry&) const {}
   // tile = dW1[128 o][64 f] in smem.  256 threads: thread -> float4 column
   // c4 = tid % 16 of rows r0 + 16k: a warp covers two 256-B row segments per
   // access; 2 rows (6 float4 loads) in flight per thread before any math.
-  TLK_DEV void tile_epilogue(const Work& w, const float* tile, int ld) const {
+  TLK_DEV void tile_epilogue(const Work& w, float* tile, int ld) const {
     const LaneState s = lanes[w.j];
     const int tid = threadIdx.x, c4 = tid & 15, r0 = tid >> 4;
     const int64_t base = w.j * pstride + w_off + w.n0 + 4 * c4;
@@ -298,24 +337,34 @@ __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __res
 #pragma unroll
     for (int t = 0; t < 10; ++t) acc[e][t] = 0.f;
   const uint16_t* dz = buf.dz1 + (int64_t(j) * 4 + c) * buf.npos * 8;
-  for (int q = g; q < 676; q += 32) {
-    const int oh = q / 26, ow = q % 26;
-    const uint4 dv = *reinterpret_cast<const uint4*>(dz + p28_pos(b, oh + 1, ow + 1) * 8);
-    const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
-    float d[8];
+  // 676 = 21 * 32 + 4: positions g, g+32, ...; four loads issued before the math
+  for (int q0 = g; q0 < 676; q0 += 128) {
+    uint4 dv[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      d[2 * e] = bf2f(uint16_t(dw[e] & 0xFFFF));
-      d[2 * e + 1] = bf2f(uint16_t(dw[e] >> 16));
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + 32 * u;
+      dv[u] = q < 676 ? *reinterpret_cast<const uint4*>(dz + p28_pos(b, q / 26 + 1, q % 26 + 1) * 8)
+                      : make_uint4(0, 0, 0, 0);
     }
-    float xv[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
+    for (int u = 0; u < 4; ++u) {
+      const int q = min(q0 + 32 * u, 675), oh = q / 26, ow = q % 26;
+      const uint32_t dw[4] = {dv[u].x, dv[u].y, dv[u].z, dv[u].w};
+      float d[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < 4; ++e) {
+        d[2 * e] = bf2f(uint16_t(dw[e] & 0xFFFF));
+        d[2 * e + 1] = bf2f(uint16_t(dw[e] >> 16));
+      }
+      float xv[9];
 #pragma unroll
-      for (int t = 0; t < 9; ++t) acc[e][t] += d[e] * xv[t];
-      acc[e][9] += d[e];
+      for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[e][t] += d[e] * xv[t];
+        acc[e][9] += d[e];
+      }
     }
   }
 #pragma unroll
@@ -429,6 +478,18 @@ int cnn_setup(Pack& p) {
   b->part_fc1 = reinterpret_cast<float*>(take(L * FC1_SPLITS * 128 * 64 * 4));
   b->part2 = reinterpret_cast<float*>(take(L * C2W_SPLITS * 9 * 64 * 32 * 4));
   b->part1 = reinterpret_cast<float*>(take(L * B * 320 * 4));
+  {  // TMA maps: lanes stacked as the outermost dimension
+    const int64_t o_f1w = tensor_offset(*p.def, 4);
+    const uint16_t* w1 = p.wbf + o_f1w;
+    if ((rc = make_tmap_bf16_3d(&b->w1_k, w1, 9216, 128, L, 9216 * 2, p.stride * 2, 64, 128)))
+      return rc;
+    if ((rc = make_tmap_bf16_3d(&b->w1_mn, w1, 9216, 128, L, 9216 * 2, p.stride * 2, 64, 64)))
+      return rc;
+    if ((rc = make_tmap_bf16_3d(&b->p2m, b->p2, 9216, B, L, 9216 * 2, b->p2_st * 2, 64, 64)))
+      return rc;
+    if ((rc = make_tmap_bf16_3d(&b->dz3m, b->dz3, 128, B, L, 128 * 2, b->h3_st * 2, 64, 64)))
+      return rc;
+  }
   void* wt = nullptr;
   p.wt_stride = 2 * CONV2_W;
   if ((rc = pack_alloc(p, &wt, L * p.wt_stride * 2))) return rc;
@@ -439,7 +500,7 @@ int cnn_setup(Pack& p) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ConvPolicy<false>::SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
-  p.launches_per_step = 14;
+  p.launches_per_step = 13;
   p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
   p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
@@ -462,21 +523,17 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   conv2_tc_kernel<true><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<true>::SMEM, st>>>(ca);
   p.mark(st, "conv2_fwd_pool");
   TLK_CUDA(cudaGetLastError());
-  Fc1Fwd f1{p.lane_dev, b, p.wbf, p.stride, o_f1w};
-  TLK_CUDA(launch_gemm(f1, dim3(1, 1, L * FC1_SPLITS), st));
+  Fc1Fwd f1{b, p.lane_dev};
+  TLK_CUDA(launch_gemm_tma(f1, dim3(1, 1, L * FC1_SPLITS), st));
   p.mark(st, "fc1_fwd_splitk");
   fc1_reduce_kernel<<<dim3(128 * 64 / 256, L), 256, 0, st>>>(p.lane_dev, b, p.params, p.stride,
                                                               o_f1b);
   p.mark(st, "fc1_reduce");
   TLK_CUDA(cudaGetLastError());
   if ((rc = enqueue_head(p, st, b.h3, 128, o_f2w, o_f2b, b.dz3, o_f1b))) return rc;
-  Fc1Dgrad f1d{p.lane_dev, b, p.wbf, p.stride, o_f1w};  // reads this step's fc1 weights
-  TLK_CUDA(launch_gemm(f1d, dim3(9216 / GEMM_BM, 1, L), st));
+  Fc1Dgrad f1d{b, p.lane_dev};  // reads this step's fc1 weights
+  TLK_CUDA(launch_gemm_tma(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
-  Fc1WgradOpt f1w{p.lane_dev, b, p.params, p.grads, p.mom1, p.mom2, p.wbf, p.stride, o_f1w,
-                  (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0};
-  TLK_CUDA(launch_gemm(f1w, dim3(1, 9216 / Fc1WgradOpt::BN, L), st));
-  p.mark(st, "fc1_wgrad_adam");
   conv2_wgrad_tc_kernel<<<dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st>>>(ca);
   p.mark(st, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
@@ -486,6 +543,10 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   conv1_wgrad_kernel<<<dim3(B, L), 128, 0, st>>>(p.lane_dev, b, p.x);
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
+  Fc1WgradOpt f1w{b, p.lane_dev, p.params, p.grads, p.mom1, p.mom2, p.wbf, p.stride, o_f1w,
+                  (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0};
+  TLK_CUDA(launch_gemm_tma(f1w, dim3(1, 9216 / Fc1WgradOpt::BN, L), st));
+  p.mark(st, "fc1_wgrad_adam");
   cnn_finalize_kernel<<<dim3((18432 + 64 + 320 + 255) / 256, L), 256, 0, st>>>(
       p.lane_dev, b, p.grads, p.stride, o_c1w, o_c1b, o_c2w, o_c2b);
   p.mark(st, "grad_finalize");

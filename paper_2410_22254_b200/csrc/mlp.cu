@@ -28,7 +28,7 @@ int mlp_setup(Pack& p) {
   p.acts_bytes = 4 * n;
   p.scratch = s;
   p.scratch_free = [](void* q) { delete static_cast<MlpScratch*>(q); };
-  p.launches_per_step = 9;
+  p.launches_per_step = 8;
   return TLK_OK;
 }
 

@@ -56,7 +56,7 @@ struct Pack {
     if (!prof) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
-    cudaEventRecord(e, st);
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);  // a graph node under capture
     prof->push_back(e);
     prof_names->push_back(name);
   }

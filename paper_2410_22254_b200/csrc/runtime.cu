@@ -389,35 +389,41 @@ int tlk_profile_step(tlk_ctx* ctx, int32_t pack, int32_t iters, float* ms, char*
   if (rc) return rc;
   TLK_CHECK(iters >= 1 && ms && n_out && max_n > 0, TLK_EINVAL, "bad arguments");
   TLK_CHECK(!p->host_input, TLK_ESTATE, "profile needs a device-input pack");
-  std::vector<double> acc;
+  // One step captured with an event node after every kernel, replayed
+  // `iters` times: device-side durations without host launch gaps.
+  std::vector<cudaEvent_t> ev;
   std::vector<const char*> nm;
+  cudaEvent_t start;
+  TLK_CUDA(cudaEventCreate(&start));
+  TLK_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  cudaEventRecordWithFlags(start, ctx->stream, cudaEventRecordExternal);
+  p->prof = &ev;
+  p->prof_names = &nm;
+  rc = enqueue_step(*p, ctx->stream);
+  p->prof = nullptr;
+  p->prof_names = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (rc) return rc;
+  TLK_CUDA(e);
+  cudaGraphExec_t ge = nullptr;
+  TLK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  std::vector<double> acc(ev.size(), 0.0);
   for (int it = 0; it < iters; ++it) {
-    std::vector<cudaEvent_t> ev;
-    std::vector<const char*> names_v;
-    cudaEvent_t start;
-    TLK_CUDA(cudaEventCreate(&start));
-    TLK_CUDA(cudaEventRecord(start, ctx->stream));
-    p->prof = &ev;
-    p->prof_names = &names_v;
-    rc = enqueue_step(*p, ctx->stream);
-    p->prof = nullptr;
-    p->prof_names = nullptr;
-    if (rc) return rc;
+    TLK_CUDA(cudaGraphLaunch(ge, ctx->stream));
     TLK_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (acc.empty()) {
-      acc.assign(ev.size(), 0.0);
-      nm = names_v;
-    }
     cudaEvent_t prev = start;
-    for (size_t k = 0; k < ev.size() && k < acc.size(); ++k) {
+    for (size_t k = 0; k < ev.size(); ++k) {
       float t = 0.f;
       cudaEventElapsedTime(&t, prev, ev[k]);
       acc[k] += t;
       prev = ev[k];
     }
-    cudaEventDestroy(start);
-    for (auto e : ev) cudaEventDestroy(e);
   }
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaEventDestroy(start);
+  for (auto x : ev) cudaEventDestroy(x);
   const int n = int(acc.size()) < max_n ? int(acc.size()) : max_n;
   std::string joined;
   for (int k = 0; k < n; ++k) {

@@ -20,6 +20,7 @@
 //   releases the epilogue: each warp tcgen05.ld's its 32 TMEM lanes (rows) in
 //   32-column chunks and hands them to P::epilogue.
 #pragma once
+#include "tma.cuh"
 #include "tlk_ptx.cuh"
 
 namespace tlk {
@@ -75,6 +76,41 @@ struct GemmThreads {  // problems may ask for 256 threads (extra epilogue warps)
   static constexpr int get(...) { return GEMM_THREADS; }
   static constexpr int value = get<P>(nullptr);
 };
+
+// Epilogue shared by both mainloops: TMEM -> registers -> problem functor
+// (per-row chunks), or -> shared fp32 tile -> problem tile functor.
+template <class P>
+TLK_DEV void gemm_epilogue(const P& p, const typename P::Work& w, uint32_t tmem, uint8_t* smem) {
+  constexpr int BN = P::BN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row = warp * 32 + lane;
+  if constexpr (P::TILE_EPILOGUE) {
+    static_assert(GEMM_BM * (BN + 4) * 4 <= P::STAGES * GemmSmem<P>::STAGE_BYTES, "tile fits");
+    float* tile = reinterpret_cast<float*>(smem);
+    if (warp < 4) {
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(tile + row * (BN + 4) + cc * 32 + i) =
+              make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+    __syncthreads();
+    p.tile_epilogue(w, tile, BN + 4);  // may __syncthreads(): all threads call it
+  } else if (warp < 4) {
+    typename P::Carry carry{};
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      float v[32];
+      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
+      p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v, carry);
+    }
+    p.finish(w, w.m0 + row, carry);
+  }
+}
 
 template <class P>
 __global__ void __launch_bounds__(GemmThreads<P>::value, 1) tc_gemm_kernel(const P p) {
@@ -162,38 +198,100 @@ __global__ void __launch_bounds__(GemmThreads<P>::value, 1) tc_gemm_kernel(const
 
   mbar_wait(&done_bar, 0);
   tc_fence_after();
-  const int row = warp * 32 + lane;
-  if constexpr (P::TILE_EPILOGUE) {
-    // stage the fp32 tile in (now idle) operand smem, then let all threads
-    // run a coalesced, many-loads-in-flight epilogue over it
-    static_assert(GEMM_BM * (BN + 4) * 4 <= P::STAGES * S::STAGE_BYTES, "tile fits");
-    float* tile = reinterpret_cast<float*>(smem);
-    if (warp < 4) {
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(tile + row * (BN + 4) + cc * 32 + i) =
-              make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-      }
-    }
-    __syncthreads();
-    p.tile_epilogue(w, tile, BN + 4);
-  } else if (warp < 4) {
-    typename P::Carry carry{};
-#pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
-      float v[32];
-      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
-      p.epilogue(w, w.m0 + row, w.n0 + cc * 32, v, carry);
-    }
-    p.finish(w, w.m0 + row, carry);
-  }
+  gemm_epilogue<P>(p, w, tmem, smem);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// ---------------------------------------------------------------- TMA path --
+// Same tiles, but operands arrive as TMA boxes (cp.async.bulk.tensor) into
+// the SWIZZLE_128B layouts; warp 0 lane 0 = producer, warp 1 lane 0 = MMA
+// issuer, full/empty mbarrier ring.  MN-major operands are 64-wide boxes
+// stacked 8 KB apart (LBO = 8192, SBO = 1024).
+template <int ROWS, bool MN_MAJOR>
+TLK_DEV uint64_t stage_desc_tma(uint32_t base, int kk) {
+  if (!MN_MAJOR) return umma_desc_sw128(base + kk * 32, 16, 1024);
+  return umma_desc_sw128(base + kk * 2 * 1024, 8192, 1024);
+}
+
+template <class P>
+__global__ void __launch_bounds__(GemmThreads<P>::value, 1)
+    tc_gemm_tma_kernel(const __grid_constant__ P p) {
+  constexpr int BN = P::BN;
+  constexpr int STAGES = P::STAGES;
+  using S = GemmSmem<P>;
+  constexpr uint32_t TCOLS = TmemCols<BN>::value;
+  constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, P::A_MN, P::B_MN);
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  typename P::Work w;
+  if (!p.work(w)) return;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<TCOLS>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int nk = w.kb_end - w.kb_begin;
+  if (warp == 0 && lane == 0) {  // producer
+    p.prefetch();
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+      const uint32_t a_s = sbase + s * S::STAGE_BYTES;
+      mbar_expect_tx(&full_bar[s], S::STAGE_BYTES);
+      p.load_a(w, w.kb_begin + it, a_s, &full_bar[s]);
+      p.load_b(w, w.kb_begin + it, a_s + S::A_BYTES, &full_bar[s]);
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full_bar[s], (it / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a_s = sbase + s * S::STAGE_BYTES;
+      const uint32_t b_s = a_s + S::A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < GEMM_BK / 16; ++kk)
+        mma_bf16(tmem, stage_desc_tma<GEMM_BM, P::A_MN>(a_s, kk), stage_desc_tma<BN, P::B_MN>(b_s, kk),
+                 IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+      mma_commit(&empty_bar[s]);
+      if (it == nk - 1) mma_commit(&done_bar);
+    }
+  }
+  mbar_wait(&done_bar, 0);
+  tc_fence_after();
+  gemm_epilogue<P>(p, w, tmem, smem);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+template <class P>
+inline cudaError_t launch_gemm_tma(const P& p, dim3 grid, cudaStream_t stream) {
+  constexpr int bytes = GemmSmem<P>::BYTES;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_tma_kernel<P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  tc_gemm_tma_kernel<P><<<grid, GemmThreads<P>::value, bytes, stream>>>(p);
+  return cudaGetLastError();
 }
 
 template <class P>

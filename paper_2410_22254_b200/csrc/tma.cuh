@@ -1,0 +1,33 @@
+// TMA tensor maps (host) and tiled tensor loads (device) for the plain-layout
+// GEMM operands.  Packs stack their lanes as the outermost tensor dimension,
+// so one CUtensorMap serves every lane of a grouped launch (coordinate 2 =
+// lane).  cuTensorMapEncodeTiled is resolved through the runtime's driver
+// entry point (no link-time libcuda dependency).
+#pragma once
+#include <cuda.h>
+
+#include "tlk_common.cuh"
+#include "tlk_ptx.cuh"
+
+namespace tlk {
+
+// bf16 3-D tensor [d2][d1][d0] (d0 contiguous) -> tensor map with box
+// {b0, b1, 1} and 128-byte swizzle (b0 * 2 must be 128).
+int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1);
+
+TLK_DEV void tma_prefetch_desc(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+// Box load: smem (swizzled) <- tensor[c2][c1 .. c1+b1)[c0 .. c0+b0), completing
+// the box's bytes on `bar`.  Out-of-range elements are zero-filled.
+TLK_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace tlk
