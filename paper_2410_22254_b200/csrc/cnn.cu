@@ -20,6 +20,7 @@
 //   (argmax | live<<2) | h3 bf16 [B,128] | dz3 bf16 [B,128] |
 //   dz2 P28 [8][npos][8] | dz1 P28 [4][npos][8]      (npos = 32 + 784 B + 64)
 #include "conv_tc.cuh"
+#include "tma.cuh"
 #include "linear.cuh"
 #include "pack.cuh"
 
@@ -28,6 +29,7 @@ namespace {
 
 constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
 constexpr int C2W_SPLITS = 18;     // conv2 wgrad position splits per lane
+constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
 
 struct CnnBufs {
   // TMA tensor maps of the plain-layout fc1 operands (lanes = dim 2)
@@ -60,8 +62,16 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
   __shared__ float xs[784];
   __shared__ float ws[32 * 9];
   __shared__ float bs[32];
-  const uint16_t* xr = x + (size_t(j) * buf.B + s) * 784;
-  for (int i = tid; i < 784; i += 256) xs[i] = bf2f(xr[i]);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t(j) * buf.B + s) * 784);
+  if (tid < 98) {  // 784 bf16 = 98 x 16 B
+    const uint4 v = xr[tid];
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      xs[tid * 8 + 2 * e] = bf2f(uint16_t(wv[e] & 0xFFFF));
+      xs[tid * 8 + 2 * e + 1] = bf2f(uint16_t(wv[e] >> 16));
+    }
+  }
   for (int i = tid; i < 288; i += 256) ws[i] = params[j * pstride + w_off + i];
   if (tid < 32) bs[tid] = params[j * pstride + b_off + tid];
   __syncthreads();
@@ -196,12 +206,21 @@ struct Fc1Dgrad {
   TLK_DEV void tile_epilogue(const Work& w, float* tile, int ld) const {
     const int tid = threadIdx.x, B = buf.B;
     const int pos0 = w.m0 >> 6;
-    for (int i = tid; i < 64 * 16; i += 256) {
+    uint2 codes[4];  // all four items' argmax codes in flight before any math
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = tid + 256 * u, b = i & 63, pl = (i >> 6) >> 3, ch = (i >> 6) & 7;
+      codes[u] = b < B ? *reinterpret_cast<const uint2*>(buf.idx + w.j * buf.p2_st +
+                                                          int64_t(b) * 9216 + (pos0 + pl) * 64 + ch * 8)
+                       : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = tid + 256 * u;
       const int b = i & 63, pl = (i >> 6) >> 3, ch = (i >> 6) & 7;
       if (b >= B) continue;
       const int pos = pos0 + pl, ph = pos / 12, pw = pos % 12, f = pl * 64 + ch * 8;
-      const uint2 code2 = *reinterpret_cast<const uint2*>(buf.idx + w.j * buf.p2_st +
-                                                          int64_t(b) * 9216 + pos * 64 + ch * 8);
+      const uint2 code2 = codes[u];
       const uint32_t cw[2] = {code2.x, code2.y};
       uint16_t z[8];
       int q[8];
@@ -323,59 +342,85 @@ struct Fc1WgradOpt {
 __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __restrict__ lanes,
                                                           CnnBufs buf,
                                                           const uint16_t* __restrict__ x) {
-  const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (!lanes[j].active) return;
+  extern __shared__ __align__(16) uint16_t dzs_raw[];  // this image's dz1 planes (50 KB)
+  uint16_t(*dzs)[P28_IMG * 8] = reinterpret_cast<uint16_t(*)[P28_IMG * 8]>(dzs_raw);
   __shared__ float xs[784];
-  __shared__ float red[32][4][80];
-  const uint16_t* xr = x + (size_t(j) * buf.B + b) * 784;
-  for (int i = tid; i < 784; i += 128) xs[i] = bf2f(xr[i]);
+  __shared__ float red[4][4][80];
+  __shared__ __align__(8) uint64_t bar;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-  const int c = tid & 3, g = tid >> 2;
+  if (tid == 0) {
+    mbar_expect_tx(&bar, 4 * P28_IMG * 16);
+    for (int c = 0; c < 4; ++c)
+      tma_bulk_g2s(smem_u32(dzs[c]),
+                   buf.dz1 + ((int64_t(j) * 4 + c) * buf.npos + p28_pos(b, 0, 0)) * 8,
+                   P28_IMG * 16, &bar);
+  }
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t(j) * buf.B + b) * 784);
+  if (tid < 98) {
+    const uint4 v = xr[tid];
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      xs[tid * 8 + 2 * e] = bf2f(uint16_t(wv[e] & 0xFFFF));
+      xs[tid * 8 + 2 * e + 1] = bf2f(uint16_t(wv[e] >> 16));
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int c = tid & 3, g = tid >> 2;  // chunk, position group (32 groups)
   float acc[8][10];
 #pragma unroll
   for (int e = 0; e < 8; ++e)
 #pragma unroll
     for (int t = 0; t < 10; ++t) acc[e][t] = 0.f;
-  const uint16_t* dz = buf.dz1 + (int64_t(j) * 4 + c) * buf.npos * 8;
-  // 676 = 21 * 32 + 4: positions g, g+32, ...; four loads issued before the math
-  for (int q0 = g; q0 < 676; q0 += 128) {
-    uint4 dv[4];
+  for (int q = g; q < 676; q += 32) {
+    const int oh = q / 26, ow = q % 26;
+    const uint4 dv = *reinterpret_cast<const uint4*>(&dzs[c][((oh + 1) * P28 + ow + 1) * 8]);
+    const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
+    float d[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + 32 * u;
-      dv[u] = q < 676 ? *reinterpret_cast<const uint4*>(dz + p28_pos(b, q / 26 + 1, q % 26 + 1) * 8)
-                      : make_uint4(0, 0, 0, 0);
+    for (int e = 0; e < 4; ++e) {
+      d[2 * e] = bf2f(uint16_t(dw[e] & 0xFFFF));
+      d[2 * e + 1] = bf2f(uint16_t(dw[e] >> 16));
     }
+    float xv[9];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = min(q0 + 32 * u, 675), oh = q / 26, ow = q % 26;
-      const uint32_t dw[4] = {dv[u].x, dv[u].y, dv[u].z, dv[u].w};
-      float d[8];
+    for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        d[2 * e] = bf2f(uint16_t(dw[e] & 0xFFFF));
-        d[2 * e + 1] = bf2f(uint16_t(dw[e] >> 16));
-      }
-      float xv[9];
+    for (int e = 0; e < 8; ++e) {
 #pragma unroll
-      for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-#pragma unroll
-        for (int t = 0; t < 9; ++t) acc[e][t] += d[e] * xv[t];
-        acc[e][9] += d[e];
-      }
+      for (int t = 0; t < 9; ++t) acc[e][t] += d[e] * xv[t];
+      acc[e][9] += d[e];
     }
   }
+  // reduce the 8 groups of this warp that share chunk c (lanes c, c+4, ...), fixed order
 #pragma unroll
   for (int e = 0; e < 8; ++e)
 #pragma unroll
-    for (int t = 0; t < 10; ++t) red[g][c][e * 10 + t] = acc[e][t];
+    for (int t = 0; t < 10; ++t) {
+      float v = acc[e][t];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      acc[e][t] = v;
+    }
+  if (lane < 4) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int t = 0; t < 10; ++t) red[warp][c][e * 10 + t] = acc[e][t];
+  }
   __syncthreads();
   for (int o = tid; o < 320; o += 128) {  // o = oc*10 + t
     const int oc = o / 10, t = o % 10;
-    float s = 0.f;
-    for (int gg = 0; gg < 32; ++gg) s += red[gg][oc >> 3][(oc & 7) * 10 + t];
+    const float s = red[0][oc >> 3][(oc & 7) * 10 + t] + red[1][oc >> 3][(oc & 7) * 10 + t] +
+                    red[2][oc >> 3][(oc & 7) * 10 + t] + red[3][oc >> 3][(oc & 7) * 10 + t];
     buf.part1[(int64_t(j) * buf.B + b) * 320 + o] = s;
   }
 }
@@ -498,6 +543,8 @@ int cnn_setup(Pack& p) {
                                 ConvPolicy<true>::SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_tc_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ConvPolicy<false>::SMEM));
+  TLK_CUDA(cudaFuncSetAttribute(conv1_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C1W_SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
   p.launches_per_step = 13;
@@ -540,7 +587,7 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   conv2_tc_kernel<false><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st>>>(ca);
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
-  conv1_wgrad_kernel<<<dim3(B, L), 128, 0, st>>>(p.lane_dev, b, p.x);
+  conv1_wgrad_kernel<<<dim3(B, L), 128, C1W_SMEM, st>>>(p.lane_dev, b, p.x);
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   Fc1WgradOpt f1w{b, p.lane_dev, p.params, p.grads, p.mom1, p.mom2, p.wbf, p.stride, o_f1w,

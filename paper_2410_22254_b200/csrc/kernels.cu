@@ -215,18 +215,29 @@ __global__ void __launch_bounds__(256) head_kernel(LaneState* __restrict__ lanes
   float* logit = sh;          // [B][C]
   float* d = sh + B * C;      // [B][C]
   float* lossb = d + B * C;   // [B]
+  float* hs = lossb + B;      // [B][HS] this CTA's hidden slice (fp32)
+  float* zs = hs + B * HS;    // [B][HS]
+  float* wsl = zs + B * HS;   // [C][HS]
+  float* Wf = wsl + C * HS;   // [C][H] classifier weights (fp32)
+  uint16_t* hb = reinterpret_cast<uint16_t*>(Wf + C * H);  // [B][H] activations (bf16)
   const float* W = params + j * stride + w_off;
   const float* bias = params + j * stride + b_off;
   const uint16_t* hj = h + size_t(j) * B * H;
+  // stage h and W with 16-B loads (all in flight at once)
+  for (int i = tid; i < B * H / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(hb)[i] = reinterpret_cast<const uint4*>(hj)[i];
+  for (int i = tid; i < C * H / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(Wf)[i] = reinterpret_cast<const float4*>(W)[i];
+  __syncthreads();
 
   for (int b = warp; b < B; b += 8) {
     float acc[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[c] = 0.0f;
     for (int k = lane; k < H; k += 32) {
-      const float hv = bf2f(hj[b * H + k]);
+      const float hv = bf2f(hb[b * H + k]);
 #pragma unroll
-      for (int c = 0; c < C; ++c) acc[c] += hv * W[c * H + k];
+      for (int c = 0; c < C; ++c) acc[c] += hv * Wf[c * H + k];
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -270,14 +281,11 @@ __global__ void __launch_bounds__(256) head_kernel(LaneState* __restrict__ lanes
   // backward for hidden units [k0, k0+HS), all operands staged in smem:
   //   dz_prev[b][k] = bf16(sum_c d[b][c] W[c][k] * [h[b][k] > 0])  (thread per (b, k))
   //   db_prev[k] = sum_b dz_prev[b][k], dW[c][k] = sum_b d[b][c] h[b][k]  (fixed order)
-  float* hs = lossb + B;        // [B][HS]
-  float* zs = hs + B * HS;      // [B][HS]
-  float* wsl = zs + B * HS;     // [C][HS]
   for (int i = tid; i < B * HS; i += blockDim.x) {
     const int b = i / HS, kk = i % HS;
-    hs[i] = bf2f(hj[b * H + k0 + kk]);
+    hs[i] = bf2f(hb[b * H + k0 + kk]);
   }
-  for (int i = tid; i < C * HS; i += blockDim.x) wsl[i] = W[(i / HS) * H + k0 + i % HS];
+  for (int i = tid; i < C * HS; i += blockDim.x) wsl[i] = Wf[(i / HS) * H + k0 + i % HS];
   __syncthreads();
   uint16_t* dzj = dz_prev + size_t(j) * B * H + k0;
   for (int i = tid; i < B * HS; i += blockDim.x) {
@@ -307,7 +315,16 @@ int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_
                  int64_t b_off, uint16_t* dz_prev, int64_t db_prev_off) {
   const int hs = hidden == 512 ? 32 : 16;
   const size_t smem = (size_t(p.batch) * (2 * CLASSES + 1) + 2 * size_t(p.batch) * hs +
-                       size_t(CLASSES) * hs) * sizeof(float);
+                       size_t(CLASSES) * hs + size_t(CLASSES) * hidden) * sizeof(float) +
+                      size_t(p.batch) * hidden * 2;
+  static bool configured = false;
+  if (!configured) {
+    TLK_CUDA(cudaFuncSetAttribute(head_kernel<512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  160 * 1024));
+    TLK_CUDA(cudaFuncSetAttribute(head_kernel<128, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  160 * 1024));
+    configured = true;
+  }
   if (hidden == 512)
     head_kernel<512, 32><<<dim3(512 / 32, p.lanes), 256, smem, st>>>(
         p.lane_dev, p.batch, h, p.params, p.grads, p.stride, w_off, b_off, p.labels, dz_prev,
