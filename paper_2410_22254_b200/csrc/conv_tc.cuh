@@ -139,11 +139,11 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
     int i = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
       const int s = i & 1;
-      mbar_wait(&tfull[s], (i >> 1) & 1);
-      tc_fence_after();
       const uint32_t taddr = tmem + s * P::N + (uint32_t(warp * 32) << 16);
       const int64_t p0 = P::tile_p0(tile);
       if constexpr (FWD) {
+        mbar_wait(&tfull[s], (i >> 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {
           float v[32];
@@ -195,20 +195,28 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
         }
         named_bar_sync(1, 128);  // tile buffer free for the next tile
       } else {
+        // h1 (ReLU mask) of this row: loaded before the accumulator is ready
+        const int r = int(p0 - P28_FRONT) % P28_IMG + row;  // position within the image
+        const int pr = r / P28, pc = r % P28;
+        const bool valid = pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26;
+        const int64_t pos = p0 + row;
+        const int64_t base = int64_t(j) * 4 * a.npos * 8;
+        uint4 hv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          hv[c] = valid ? *reinterpret_cast<const uint4*>(a.h1 + base + (c * a.npos + pos) * 8)
+                        : make_uint4(0, 0, 0, 0);
+        mbar_wait(&tfull[s], (i >> 1) & 1);
+        tc_fence_after();
         float v[32];
         tmem_ld32(taddr, v);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
-        const int r = int(p0 - P28_FRONT) % P28_IMG + row;  // position within the image
-        const int pr = r / P28, pc = r % P28;
-        if (pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26) {
-          const int64_t pos = p0 + row;
-          const int64_t base = int64_t(j) * 4 * a.npos * 8;
+        if (valid) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint4 hv = *reinterpret_cast<const uint4*>(a.h1 + base + (c * a.npos + pos) * 8);
-            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+            const uint32_t hw[4] = {hv[c].x, hv[c].y, hv[c].z, hv[c].w};
             uint32_t ow[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -250,7 +258,8 @@ constexpr int WG_B_BYTES = 8 * WG_B_PLANE;        // 16384
 constexpr int WG_STAGE = WG_A_BYTES + WG_B_BYTES; // 65536
 constexpr int WG_STAGES = 3;
 constexpr int WG_SMEM = WG_STAGES * WG_STAGE + 128;
-constexpr uint32_t WG_TX = 16 * WG_ACOPY + WG_B_BYTES;
+// the k' = 3 copies (spare MMA rows, never read back) are not loaded
+constexpr uint32_t WG_TX = 12 * WG_ACOPY + WG_B_BYTES;
 
 __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
   const int split = blockIdx.x, j = blockIdx.y;
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a
         const uint32_t st = s0 + s * WG_STAGE;
         mbar_expect_tx(&full_bar[s], WG_TX);
         for (int c = 0; c < 4; ++c)
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < 3; ++k)
             tma_bulk_g2s(st + (c * 4 + k) * WG_ASTRIDE, h1 + (c * a.npos + q0 - HALO + k) * 8,
                          WG_ACOPY, &full_bar[s]);
         for (int c = 0; c < 8; ++c)
