@@ -78,9 +78,10 @@ def barrier(world):
 
 # ---------------------------------------------------------------- clocks ------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+    """nvidia-smi clocks / throttle reasons sampled every 10 ms; summary() keeps
+    the samples stamped inside the timed window (mark_start / mark_end)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -88,42 +89,66 @@ class ClockSampler:
         self.path = tempfile.mktemp(suffix=".csv")
         self.dev = device_index
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms", "10"], stdout=self.f,
                 stderr=subprocess.DEVNULL)
+            time.sleep(0.5)  # let the sampler come up before the measured work
         except OSError:
             self.proc = None
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             self.proc.wait()
             self.f.close()
 
     def summary(self):
+        import datetime
+
         rows = []
         try:
             for line in open(self.path):
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
+                if len(parts) < 10:
+                    continue
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    ts = None
+                rows.append((ts, parts))
         except OSError:
             pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        win = [p for ts, p in rows if ts is not None and self.t0 and self.t1 and
+               self.t0 - 0.01 <= ts <= self.t1 + 0.01]
+        scope = "timed region"
+        if not win:  # region shorter than the sampling period: nearest samples
+            win = [p for ts, p in rows if ts is not None and self.t0 and self.t1 and
+                   self.t0 - 0.1 <= ts <= self.t1 + 0.1] or [p for _, p in rows]
+            scope = "timed region +-100 ms"
+        num = lambda s: s.replace(".", "", 1).isdigit()
+        sm = [float(r[2]) for r in win if num(r[2])]
+        mx = [float(r[3]) for r in win if num(r[3])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({names[i] for r in win for i in range(4) if r[6 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(win), "scope": scope}
 
 
 # ---------------------------------------------------------------- roofline ----
@@ -274,10 +299,12 @@ def packed_arm(a, world, rank, local):
         barrier(world)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk.mark_start()
         ev0.record(stream)
         pack.run(a.steps)
         ev1.record(stream)
         ev1.synchronize()
+        clk.mark_end()
         torch.cuda.synchronize()
         barrier(world)
         ms = ev0.elapsed_time(ev1)

@@ -12,7 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 # ncu kernel name fragment -> bench.py kernel label
-LABELS = {"Conv2Fwd": "conv2_fwd_pool", "Conv2Dgrad": "conv2_dgrad", "conv2_wgrad_tc": "conv2_wgrad", "conv2_fwd_tc": "conv2_fwd_pool", "conv2_dgrad_tc": "conv2_dgrad",
+LABELS = {"conv2_tc_kernel<1>": "conv2_fwd_pool", "conv2_tc_kernel<0>": "conv2_dgrad",
+          "Fc1WgradOpt": "fc1_wgrad_adam", "Conv2Fwd": "conv2_fwd_pool", "Conv2Dgrad": "conv2_dgrad", "conv2_wgrad_tc": "conv2_wgrad", "conv2_fwd_tc": "conv2_fwd_pool", "conv2_dgrad_tc": "conv2_dgrad",
           "Fc1Dgrad": "fc1_dgrad_unpool", "Fc1Fwd": "fc1_fwd_splitk", "LinWgrad": "fc1_wgrad",
           "optimizer_kernel": "optimizer", "conv1_wgrad": "conv1_wgrad", "conv1_fwd": "conv1_fwd",
           "head_kernel": "head", "inputs_kernel": "inputs", "cnn_finalize": "grad_finalize",
