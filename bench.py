@@ -386,6 +386,23 @@ def packed_arm(a, world, rank, local):
                           "samples_per_s_roof": lanes * BATCH / t_roof},
         "kernels": {k: round(v, 5) for k, v in kernels},
     }
+    if rank == 0 and world == 1 and a.sweep:
+        # the metric's "vs jobs/GPU" axis: packed throughput for NPPN/GPU = 1..32
+        sweep = []
+        for k in (1, 2, 4, 8, 16, 32):
+            sp = ctx.pack(rt.MODELS[MODEL], BATCH, k, 10 + 50 + 2)
+            for jj in range(k):
+                sp.load(jj, seed=1000 + jj, steps=10 + 50 + 2)
+            sp.run(10)
+            ctx.sync()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sp.run(50)
+            e1.record(stream)
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / 50
+            sweep.append({"jobs_per_gpu": k, "ms_per_step": t, "samples_per_s": k * BATCH / (t / 1e3)})
+        line["nppn_sweep"] = sweep
     if rank == 0 and world == 1 and not a.no_baselines:
         cpu, cores, _ = cpu_oracle_rate(2, 1)
         line["cpu_baseline"] = {
@@ -414,6 +431,8 @@ def main():
     ap.add_argument("--profile-iters", type=int, default=5)
     ap.add_argument("--kproc-seconds", type=float, default=10.0)
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false",
+                    help="skip the jobs/GPU sweep (1..32 packed CNN jobs)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     world, rank, local = dist_setup(a.gpus)
