@@ -15,11 +15,13 @@ import time
 
 import numpy as np
 
-from . import models, optim, rng
+from . import gpt, models, optim, rng
+
+GPT_MODELS = {"xformer": gpt.MODEL_XFORMER, "gpt": gpt.MODEL_GPT}
 
 
 def add_job_args(ap: argparse.ArgumentParser) -> None:
-    ap.add_argument("--model", choices=sorted(models.MODEL_NAMES), default="mlp")
+    ap.add_argument("--model", choices=sorted(models.MODEL_NAMES) + sorted(GPT_MODELS), default="mlp")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--batch", type=int, default=64)
@@ -57,6 +59,24 @@ def train(model: int, seed: int, steps: int, batch: int, opt: optim.OptState,
     return losses, flat, per_step
 
 
+def train_gpt(cfg, seed: int, steps: int, opt: optim.OptState, bf16: bool = True, warmup: int = 1,
+              batch: int | None = None):
+    """Transformer job (oracle/gpt.py); returns (losses, final flat params, s/step)."""
+    flat = gpt.flatten(cfg, gpt.init_params(cfg, seed))
+    losses = np.zeros(steps, np.float32)
+    warmup = warmup if steps > warmup else 0
+    t0 = time.perf_counter()
+    for t in range(steps):
+        if t == warmup:
+            t0 = time.perf_counter()
+        toks = gpt.tokens(cfg, seed, t, batch)
+        loss, g = gpt.gpt_step(cfg, gpt.unflatten(cfg, flat), toks, bf16=bf16)
+        flat = optim.step(opt, flat, gpt.flatten(cfg, g))
+        losses[t] = loss
+    per_step = (time.perf_counter() - t0) / max(1, steps - warmup)
+    return losses, flat, per_step
+
+
 def opt_from_args(a) -> optim.OptState:
     return optim.OptState(kind=optim.OPT_NAMES[a.optim], lr=a.lr, beta1=a.beta1, beta2=a.beta2,
                           eps=a.eps, weight_decay=a.wd, momentum=a.momentum)
@@ -69,9 +89,14 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=1, help="steps excluded from the timing")
     ap.add_argument("--json", action="store_true")
     a = ap.parse_args(argv)
-    model = models.MODEL_NAMES[a.model]
-    losses, _, per_step = train(model, a.seed, a.steps, a.batch, opt_from_args(a), bool(a.bf16),
-                                warmup=a.warmup)
+    if a.model in GPT_MODELS:
+        cfg = gpt.CFGS[GPT_MODELS[a.model]]
+        losses, _, per_step = train_gpt(cfg, a.seed, a.steps, opt_from_args(a), bool(a.bf16),
+                                        warmup=a.warmup, batch=a.batch)
+    else:
+        model = models.MODEL_NAMES[a.model]
+        losses, _, per_step = train(model, a.seed, a.steps, a.batch, opt_from_args(a),
+                                    bool(a.bf16), warmup=a.warmup)
     out = {
         "model": a.model, "seed": a.seed, "steps": a.steps, "batch": a.batch,
         "timed_steps": a.steps - (a.warmup if a.steps > a.warmup else 0),

@@ -24,7 +24,7 @@ import torch.nn.functional as F
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle import models, rng  # noqa: E402
+from oracle import gpt, models, rng  # noqa: E402
 
 RUNS = [
     # name, model, batch, steps, optim, kwargs
@@ -101,12 +101,66 @@ def run(name, model, batch, steps, opt, kw):
             f"{name}/sample": flat[idx], f"{name}/norms": norms}
 
 
+GPT_RUNS = [
+    # name, cfg, steps, optim, kwargs
+    ("gpt_small_adamw", gpt.GptCfg(2, 64, 2, 16, 17, 4), 3, "adamw", dict(lr=3e-3, weight_decay=0.1)),
+    ("xformer_small_adam", gpt.GptCfg(1, 32, 2, 8, 256, 2), 3, "adam", dict(lr=1e-3)),
+]
+
+
+def gpt_forward(cfg, P, toks):
+    """Independent torch implementation of oracle/gpt.py's model."""
+    B, T, d, H = toks.shape[0], cfg.T, cfg.d, cfg.heads
+    dh = d // H
+    inp = toks[:, :-1]
+    x = P["wte"][inp] + P["wpe"][:T][None]
+    mask = torch.tril(torch.ones(T, T, dtype=torch.bool))
+    for l in range(cfg.layers):
+        q_ = f"h{l}."
+        a = F.layer_norm(x, (d,), P[q_ + "ln1.g"], P[q_ + "ln1.b"], eps=1e-5)
+        qkv = F.linear(a, P[q_ + "attn.w"], P[q_ + "attn.b"]).view(B, T, 3, H, dh)
+        q, k, v = (qkv[:, :, i].transpose(1, 2) for i in range(3))
+        s = (q @ k.transpose(-1, -2)) / (dh ** 0.5)
+        s = s.masked_fill(~mask, float("-inf"))
+        y = torch.softmax(s, dim=-1) @ v
+        x = x + F.linear(y.transpose(1, 2).reshape(B, T, d), P[q_ + "proj.w"], P[q_ + "proj.b"])
+        m = F.layer_norm(x, (d,), P[q_ + "ln2.g"], P[q_ + "ln2.b"], eps=1e-5)
+        f = F.gelu(F.linear(m, P[q_ + "fc.w"], P[q_ + "fc.b"]), approximate="tanh")
+        x = x + F.linear(f, P[q_ + "fc2.w"], P[q_ + "fc2.b"])
+    x = F.layer_norm(x, (d,), P["lnf.g"], P["lnf.b"], eps=1e-5)
+    return F.linear(x, P["head.w"])
+
+
+def run_gpt(name, cfg, steps, opt, kw):
+    init = gpt.init_params(cfg, SEED)
+    P = {k: torch.tensor(v, requires_grad=True) for k, v in init.items()}
+    params = list(P.values())
+    o = (torch.optim.AdamW if opt == "adamw" else torch.optim.Adam)(params, foreach=False, **kw)
+    losses = []
+    for t in range(steps):
+        toks = torch.tensor(gpt.tokens(cfg, SEED, t), dtype=torch.long)
+        logits = gpt_forward(cfg, P, toks)
+        loss = F.cross_entropy(logits.reshape(-1, cfg.V), toks[:, 1:].reshape(-1))
+        o.zero_grad()
+        loss.backward()
+        o.step()
+        losses.append(loss.item())
+    final = {k: v.detach().numpy() for k, v in P.items()}
+    flat = gpt.flatten(cfg, final)
+    idx = np.linspace(0, flat.size - 1, SAMPLES).astype(np.int64)
+    norms = np.array([np.linalg.norm(final[n]) for n, *_ in gpt.tensors(cfg)], np.float64)
+    return {f"{name}/losses": np.array(losses, np.float64), f"{name}/idx": idx,
+            f"{name}/sample": flat[idx], f"{name}/norms": norms}
+
+
 def main():
     torch.manual_seed(0)
     torch.set_num_threads(1)
     out = {}
     for r in RUNS:
         out.update(run(*r))
+    for r in GPT_RUNS:
+        out.update(run_gpt(*r))
     path = os.path.join(HERE, "torch_golden.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, {k: v.shape for k, v in out.items()})
