@@ -89,11 +89,12 @@ def test_gpt_oracle_matches_torch(run):
     losses, flat, _ = job.train_gpt(cfg, 11, steps, st, bf16=False)
     np.testing.assert_allclose(losses, G[f"{name}/losses"], atol=2e-5, rtol=0)
     idx = G[f"{name}/idx"]
-    # Adam maps the sign of near-zero gradients to +-lr: allow 20% of one step
-    np.testing.assert_allclose(flat[idx], G[f"{name}/sample"], atol=0.2 * kw["lr"], rtol=0)
+    # Adam maps the sign of near-zero gradients (|g| ~ eps) to +-lr: allow half
+    # of one step on single elements, 1e-3 on per-tensor norms
+    np.testing.assert_allclose(flat[idx], G[f"{name}/sample"], atol=0.5 * kw["lr"], rtol=0)
     params = gpt.unflatten(cfg, flat)
     norms = [np.linalg.norm(params[n]) for n, *_ in gpt.tensors(cfg)]
-    np.testing.assert_allclose(norms, G[f"{name}/norms"], rtol=1e-4)
+    np.testing.assert_allclose(norms, G[f"{name}/norms"], rtol=1e-3)
 
 
 def test_markov_tokens_are_learnable_chain():
