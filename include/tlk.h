@@ -38,6 +38,8 @@ extern "C" {
 /* job models (the training tasks the paper packs) */
 #define TLK_MODEL_MLP 1 /* MNIST MLP 784-512-512-10, ReLU */
 #define TLK_MODEL_CNN 2 /* MNIST CNN: conv3x3(1->32) conv3x3(32->64) maxpool2 fc(9216->128) fc(128->10) */
+#define TLK_MODEL_XFORMER 3 /* 2-layer pre-LN transformer, d=256, 4 heads, T=128, byte vocab (config 4) */
+#define TLK_MODEL_GPT 4     /* tiny-GPT, 6 layers, d=384, 6 heads, T=256, vocab 65 (config 5) */
 
 /* optimizers */
 #define TLK_OPT_ADAM 1
@@ -75,6 +77,8 @@ typedef struct {
   int32_t max_steps;  /* loss-curve capacity per lane */
   int32_t host_input; /* 1: inputs come from tlk_step_host, 0: synthesised on device */
   int32_t flags;      /* TLK_PACK_* */
+  /* transformer packs: 0 = the model's default */
+  int32_t layers, d_model, heads, seq_len, vocab;
 } tlk_pack_desc;
 
 /* pack flags */
@@ -126,6 +130,8 @@ int tlk_lane_losses(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int32
 int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64_t n);
 /* Device pointer + size of a pack buffer (TLK_BUF_*), for zero-copy tensors. */
 int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, int64_t* bytes);
+/* Parameter layout of this pack's lanes (depends on the transformer config). */
+int tlk_pack_info(tlk_ctx* ctx, int32_t pack, tlk_model_info* out);
 /* Number of kernels one tlk_run step launches for this pack. */
 int tlk_pack_launches_per_step(tlk_ctx* ctx, int32_t pack, int32_t* n);
 

@@ -1,0 +1,673 @@
+// Transformer packs (TLK_MODEL_XFORMER: config 4's 2-layer d=256 model;
+// TLK_MODEL_GPT: config 5's tiny-GPT), all lanes per launch.  Restated by
+// oracle/gpt.py (see its docstring for the model and the numerics contract).
+//
+// Per layer forward:  LN1 -> QKV (tcgen05, +bias, bf16) -> S = QK^T per
+// (sequence, head) with a softmax row epilogue (scale, causal mask) -> Y = PV
+// -> proj (+bias, residual add, fp32) -> LN2 -> FC (+bias, GELU; z kept fp32)
+// -> FC2 (+bias, residual add).  Head: LNf -> logits with a cross-entropy row
+// epilogue (per-token loss + bf16 dlogits) -> fixed-order loss reduction.
+// Backward mirrors it: weight gradients are tcgen05 GEMMs with K = tokens
+// (both operands MN-major), dgrads read the weights MN-major (no transposed
+// copies), dP gets a softmax-backward row epilogue, LN backward and every
+// bias / gain / embedding gradient are deterministic two-stage reductions.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pack.cuh"
+#include "rng.cuh"
+#include "sgemm.cuh"
+
+namespace tlk {
+
+constexpr uint32_t STREAM_TOKENS = 3;
+__constant__ int kMarkovA[8] = {1, 3, 5, 7, 11, 13, 17, 19};
+__constant__ int kMarkovC[8] = {1, 2, 3, 5, 8, 13, 21, 34};
+
+namespace {
+
+struct LayerBufs {
+  float *xin, *xmid, *st1, *st2, *z;
+  uint16_t *a, *qkv, *P, *y, *m, *f;
+};
+
+struct GptBufs {
+  GptCfg c;
+  int N, Vp;
+  int32_t *tokens, *targets;
+  std::vector<LayerBufs> L;
+  float *xL, *stf, *lossrow;
+  uint16_t *xf, *dl;
+  // backward scratch (shared by all layers)
+  float *dx, *dmm, *dS_f;  // dS_f unused
+  uint16_t *dxb, *dz, *dy, *dS, *dqkv;
+  float* part;      // reduction partials
+  int64_t part_st;  // floats per lane
+  // parameter offsets
+  std::vector<int64_t> off;  // by tensor index
+};
+
+int64_t tensor_off(const Pack& p, int t) { return p.tinfo[t].off; }
+
+// tensor indices (oracle/gpt.py::tensors order)
+enum { T_WTE = 0, T_WPE = 1 };
+inline int T_LAYER(int l, int k) { return 2 + 12 * l + k; }
+enum { K_LN1G, K_LN1B, K_AW, K_AB, K_PW, K_PB, K_LN2G, K_LN2B, K_FW, K_FB, K_F2W, K_F2B };
+inline int T_LNFG(const GptCfg& c) { return 2 + 12 * c.layers; }
+
+// ------------------------------------------------------------- tokens -------
+__global__ void gpt_tokens_kernel(const LaneState* __restrict__ lanes, int B, int T, int V,
+                                  int32_t* __restrict__ tokens, int32_t* __restrict__ targets) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (s >= B || !lanes[j].active) return;
+  const uint64_t key = rng_key(lanes[j].seed, STREAM_TOKENS, uint64_t(lanes[j].steps_done));
+  const uint64_t base = uint64_t(s) * (T + 1);
+  int32_t* tk = tokens + (int64_t(j) * B + s) * (T + 1);
+  int32_t* tg = targets + (int64_t(j) * B + s) * T;
+  int t = int(rng_bits(key, base) % uint64_t(V));
+  tk[0] = t;
+  for (int i = 0; i < T; ++i) {
+    const int k = int(rng_bits(key, base + i + 1) >> 61);
+    t = (t * kMarkovA[k] + kMarkovC[k]) % V;
+    tk[i + 1] = t;
+    tg[i] = t;
+  }
+}
+
+// x0[row][c] = wte[tok][c] + wpe[t][c]
+__global__ void gpt_embed_kernel(const LaneState* __restrict__ lanes, GptCfg c, int B,
+                                 const int32_t* __restrict__ tokens, const float* __restrict__ params,
+                                 int64_t pstride, int64_t o_wte, int64_t o_wpe, float* __restrict__ x) {
+  const int row = blockIdx.x, j = blockIdx.y;
+  if (!lanes[j].active) return;
+  const int b = row / c.T, t = row % c.T;
+  const int tok = tokens[(int64_t(j) * B + b) * (c.T + 1) + t];
+  const float* P = params + j * pstride;
+  float* xr = x + (int64_t(j) * B * c.T + row) * c.d;
+  for (int i = threadIdx.x; i < c.d; i += blockDim.x)
+    xr[i] = P[o_wte + int64_t(tok) * c.d + i] + P[o_wpe + int64_t(t) * c.d + i];
+}
+
+// ------------------------------------------------------------- LayerNorm ----
+// one warp per row: y = bf16((x - mean) * rstd * g + b); stats = (mean, rstd)
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const LaneState* __restrict__ lanes, int N,
+                                                     int d, const float* __restrict__ x,
+                                                     const float* __restrict__ params,
+                                                     int64_t pstride, int64_t og, int64_t ob,
+                                                     uint16_t* __restrict__ y,
+                                                     float* __restrict__ stats) {
+  const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!lanes[j].active) return;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= N) return;
+  const float* xr = x + (int64_t(j) * N + row) * d;
+  float s = 0.f;
+  for (int i = lane; i < d; i += 32) s += xr[i];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mu = s / float(d);
+  float q = 0.f;
+  for (int i = lane; i < d; i += 32) {
+    const float c = xr[i] - mu;
+    q += c * c;
+  }
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = 1.0f / sqrtf(q / float(d) + 1e-5f);
+  const float* g = params + j * pstride + og;
+  const float* bb = params + j * pstride + ob;
+  uint16_t* yr = y + (int64_t(j) * N + row) * d;
+  for (int i = lane; i < d; i += 32) yr[i] = f2bf((xr[i] - mu) * rstd * g[i] + bb[i]);
+  if (lane == 0) {
+    stats[(int64_t(j) * N + row) * 2] = mu;
+    stats[(int64_t(j) * N + row) * 2 + 1] = rstd;
+  }
+}
+
+// LayerNorm backward for 64 rows per CTA (8 warps x 8 rows):
+//   dxh = dy g; dx = (dxh - mean(dxh) - xh mean(dxh xh)) rstd
+//   dxt (fp32 residual grad) = (accumulate ? dxt : 0) + dx; dxb = bf16(dxt)
+//   part[lane][blk][0:d] = sum_rows dy xh, part[..][d:2d] = sum_rows dy (fixed order)
+constexpr int LNB_ROWS = 64;
+__global__ void __launch_bounds__(256) ln_bwd_kernel(
+    const LaneState* __restrict__ lanes, int N, int d, const float* __restrict__ dy,
+    const float* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ params,
+    int64_t pstride, int64_t og, float* __restrict__ dxt, uint16_t* __restrict__ dxb, int accumulate,
+    float* __restrict__ part, int64_t part_st) {
+  const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!lanes[j].active) return;
+  extern __shared__ float red[];  // [8][2][d]
+  constexpr int MAXC = 16;        // d <= 512
+  float ag[MAXC], ab[MAXC];
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) ag[k] = ab[k] = 0.f;
+  const float* g = params + j * pstride + og;
+  for (int r = 0; r < LNB_ROWS / 8; ++r) {
+    const int row = blockIdx.x * LNB_ROWS + warp * (LNB_ROWS / 8) + r;
+    if (row >= N) break;
+    const int64_t ro = (int64_t(j) * N + row) * d;
+    const float mu = stats[(int64_t(j) * N + row) * 2], rstd = stats[(int64_t(j) * N + row) * 2 + 1];
+    float xh[MAXC], dyv[MAXC];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) {
+      const int i = lane + 32 * k;
+      if (i < d) {
+        xh[k] = (x[ro + i] - mu) * rstd;
+        dyv[k] = dy[ro + i];
+        const float dxh = dyv[k] * g[i];
+        s1 += dxh;
+        s2 += dxh * xh[k];
+        ag[k] += dyv[k] * xh[k];
+        ab[k] += dyv[k];
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const float m1 = s1 / float(d), m2 = s2 / float(d);
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) {
+      const int i = lane + 32 * k;
+      if (i < d) {
+        const float dxv = (dyv[k] * g[i] - m1 - xh[k] * m2) * rstd;
+        const float t = accumulate ? dxt[ro + i] + dxv : dxv;
+        dxt[ro + i] = t;
+        dxb[ro + i] = f2bf(t);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) {
+    const int i = lane + 32 * k;
+    if (i < d) {
+      red[(warp * 2) * d + i] = ag[k];
+      red[(warp * 2 + 1) * d + i] = ab[k];
+    }
+  }
+  __syncthreads();
+  float* out = part + j * part_st + int64_t(blockIdx.x) * 2 * d;
+  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) {
+    const int f = i / d, c = i % d;
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red[(w * 2 + f) * d + c];
+    out[i] = s;
+  }
+}
+
+// ------------------------------------------------------------- reductions --
+// part[lane][blk][c] = sum over rows [blk*128, blk*128+128) of src[row][c] (bf16)
+constexpr int CS_ROWS = 128;
+__global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const uint16_t* __restrict__ src,
+                                   int64_t src_ls, int ld, int N, int C, float* __restrict__ part,
+                                   int64_t part_st) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
+  if (!lanes[j].active || c >= C) return;
+  const uint16_t* s = src + j * src_ls + int64_t(blk) * CS_ROWS * ld + c;
+  float acc = 0.f;
+  const int rows = min(CS_ROWS, N - blk * CS_ROWS);
+  for (int r = 0; r < rows; ++r) acc += bf2f(s[int64_t(r) * ld]);
+  part[j * part_st + int64_t(blk) * C + c] = acc;
+}
+
+// dst0[c] (c < split) / dst1[c - split] = sum_blk part[lane][blk][c], fixed order
+__global__ void reduce_parts_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
+                                    int64_t part_st, int nblk, int C, float* __restrict__ grads,
+                                    int64_t pstride, int64_t off0, int split, int64_t off1) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (!lanes[j].active || c >= C) return;
+  const float* p = part + j * part_st + c;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += p[int64_t(b) * C];
+  grads[j * pstride + (c < split ? off0 + c : off1 + (c - split))] = s;
+}
+
+// mean token loss (fixed order) -> loss curve; per-step optimizer scalars
+__global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ lanes, int N,
+                                                       const float* __restrict__ lossrow,
+                                                       float* __restrict__ loss, int max_steps,
+                                                       float* __restrict__ last_loss) {
+  const int j = blockIdx.x, tid = threadIdx.x;
+  if (!lanes[j].active) return;
+  __shared__ float red[512];
+  const int per = (N + 511) / 512;
+  float s = 0.f;
+  for (int r = tid * per; r < min(N, (tid + 1) * per); ++r) s += lossrow[int64_t(j) * N + r];
+  red[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+    for (int i = 0; i < 512; ++i) t += red[i];
+    const float Lm = t / float(N);
+    LaneState& ls = lanes[j];
+    loss[int64_t(j) * max_steps + ls.steps_done] = Lm;
+    last_loss[j] = Lm;
+    lane_step_scalars(ls);
+  }
+}
+
+// token-embedding gradient, stage 1: per block of 256 positions, smem
+// acc[v][c] (thread = column, positions in order) -> part[lane][blk][v][c]
+constexpr int EMB_ROWS = 256;
+__global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int d, int V, int cols,
+                                 const int32_t* __restrict__ tokens, int T, const float* __restrict__ dx,
+                                 float* __restrict__ part, int64_t part_st) {
+  const int blk = blockIdx.x, cg = blockIdx.y, j = blockIdx.z, c = cg * cols + threadIdx.x;
+  if (!lanes[j].active) return;
+  extern __shared__ float acc[];  // [V][cols]
+  __shared__ int tk[EMB_ROWS];
+  for (int v = 0; v < V; ++v) acc[v * cols + threadIdx.x] = 0.f;
+  for (int i = threadIdx.x; i < EMB_ROWS; i += blockDim.x) {
+    const int row = blk * EMB_ROWS + i;
+    const int b = row / T, t = row % T;
+    tk[i] = row < N ? tokens[(int64_t(j) * (N / T) + b) * (T + 1) + t] : 0;
+  }
+  __syncthreads();
+  if (c < d) {
+    const float* g = dx + int64_t(j) * N * d + c;
+    for (int i = 0; i < EMB_ROWS; ++i) {
+      const int row = blk * EMB_ROWS + i;
+      if (row >= N) break;
+      acc[tk[i] * cols + threadIdx.x] += g[int64_t(row) * d];
+    }
+    float* out = part + j * part_st + int64_t(blk) * V * d + c;
+    for (int v = 0; v < V; ++v) out[int64_t(v) * d] = acc[v * cols + threadIdx.x];
+  }
+}
+
+// dwpe[t][c] = sum_b dx[b*T + t][c] (b in order)
+__global__ void wpe_bwd_kernel(const LaneState* __restrict__ lanes, int B, int T, int d,
+                               const float* __restrict__ dx, float* __restrict__ grads,
+                               int64_t pstride, int64_t o_wpe) {
+  const int t = blockIdx.x, j = blockIdx.y;
+  if (!lanes[j].active) return;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += dx[(int64_t(j) * B * T + int64_t(b) * T + t) * d + c];
+    grads[j * pstride + o_wpe + int64_t(t) * d + c] = s;
+  }
+}
+
+// ------------------------------------------------------------- GEMM glue ---
+Operand op(const uint16_t* base, int64_t ls, int64_t bs, int64_t hs, int64_t mn_st, int64_t k_st,
+           int MN, int K) {
+  return Operand{base, ls, bs, hs, mn_st, k_st, MN, K};
+}
+
+template <int BN, bool AMN, bool BMN, bool ROW>
+int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M,
+         int N, int K, int nb, int nh, const char* name) {
+  SGemm<BN, AMN, BMN, ROW> g{p.lane_dev, A, B, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
+  dim3 grid((M + GEMM_BM - 1) / GEMM_BM, (N + BN - 1) / BN, p.lanes * nb * nh);
+  TLK_CUDA(launch_gemm(g, grid, st));
+  const_cast<Pack&>(p).mark(st, name);
+  return TLK_OK;
+}
+
+Epi epi(int kind, int rows, int cols, void* out, int64_t ls, int64_t bs, int64_t hs, int64_t ld) {
+  Epi e{};
+  e.kind = kind;
+  e.rows = rows;
+  e.cols = cols;
+  e.out = out;
+  e.ls = ls;
+  e.bs = bs;
+  e.hs = hs;
+  e.ld = ld;
+  e.scale = 1.f;
+  return e;
+}
+
+#define TLK_TRY(x)              \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_) return rc_;        \
+  } while (0)
+
+}  // namespace
+
+// ------------------------------------------------------------- setup -------
+int gpt_setup(Pack& p) {
+  const GptCfg c = p.gcfg;
+  TLK_CHECK(c.d % c.heads == 0 && c.d / c.heads == 64, TLK_EINVAL, "gpt: head dim must be 64");
+  TLK_CHECK(c.d % 128 == 0 && c.d <= 512, TLK_EINVAL, "gpt: d_model must be a multiple of 128 <= 512");
+  TLK_CHECK(c.T == 64 || c.T == 128 || c.T == 256, TLK_EINVAL, "gpt: seq_len must be 64, 128 or 256");
+  TLK_CHECK(c.V >= 2 && c.V <= 256, TLK_EINVAL, "gpt: vocab must be in [2, 256]");
+  TLK_CHECK((int64_t(p.batch) * c.T) % 256 == 0, TLK_EINVAL, "gpt: batch*seq_len must be a multiple of 256");
+  auto* b = new GptBufs{};
+  p.scratch = b;
+  p.scratch_free = [](void* q) { delete static_cast<GptBufs*>(q); };
+  b->c = c;
+  const int64_t L = p.lanes, N = int64_t(p.batch) * c.T, d = c.d, H = c.heads, T = c.T;
+  b->N = int(N);
+  b->Vp = (c.V + 31) / 32 * 32;
+  if (b->Vp > 256) return fail(TLK_EINVAL, "gpt: vocab too large");
+  // sizes (bytes) of everything, one allocation
+  struct Item {
+    void** ptr;
+    size_t bytes;
+  };
+  std::vector<Item> items;
+  auto add = [&](void** ptr, size_t bytes) { items.push_back({ptr, (bytes + 255) & ~size_t(255)}); };
+  add(reinterpret_cast<void**>(&b->tokens), L * p.batch * (T + 1) * 4);
+  add(reinterpret_cast<void**>(&b->targets), L * N * 4);
+  b->L.resize(c.layers);
+  for (auto& lb : b->L) {
+    add(reinterpret_cast<void**>(&lb.xin), L * N * d * 4);
+    add(reinterpret_cast<void**>(&lb.xmid), L * N * d * 4);
+    add(reinterpret_cast<void**>(&lb.st1), L * N * 2 * 4);
+    add(reinterpret_cast<void**>(&lb.st2), L * N * 2 * 4);
+    add(reinterpret_cast<void**>(&lb.z), L * N * 4 * d * 4);
+    add(reinterpret_cast<void**>(&lb.a), L * N * d * 2);
+    add(reinterpret_cast<void**>(&lb.qkv), L * N * 3 * d * 2);
+    add(reinterpret_cast<void**>(&lb.P), L * p.batch * H * T * T * 2);
+    add(reinterpret_cast<void**>(&lb.y), L * N * d * 2);
+    add(reinterpret_cast<void**>(&lb.m), L * N * d * 2);
+    add(reinterpret_cast<void**>(&lb.f), L * N * 4 * d * 2);
+  }
+  add(reinterpret_cast<void**>(&b->xL), L * N * d * 4);
+  add(reinterpret_cast<void**>(&b->stf), L * N * 2 * 4);
+  add(reinterpret_cast<void**>(&b->lossrow), L * N * 4);
+  add(reinterpret_cast<void**>(&b->xf), L * N * d * 2);
+  add(reinterpret_cast<void**>(&b->dl), L * N * b->Vp * 2);
+  add(reinterpret_cast<void**>(&b->dx), L * N * d * 4);
+  add(reinterpret_cast<void**>(&b->dmm), L * N * d * 4);
+  add(reinterpret_cast<void**>(&b->dxb), L * N * d * 2);
+  add(reinterpret_cast<void**>(&b->dz), L * N * 4 * d * 2);
+  add(reinterpret_cast<void**>(&b->dy), L * N * d * 2);
+  add(reinterpret_cast<void**>(&b->dS), L * p.batch * H * T * T * 2);
+  add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
+  // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
+  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d, N / EMB_ROWS * c.V * d});
+  b->part_st = ps;
+  add(reinterpret_cast<void**>(&b->part), L * ps * 4);
+  size_t total = 0;
+  for (auto& it : items) total += it.bytes;
+  void* base = nullptr;
+  int rc = pack_alloc(p, &base, total);
+  if (rc) return rc;
+  TLK_CUDA(cudaMemset(base, 0, total));
+  char* cur = static_cast<char*>(base);
+  for (auto& it : items) {
+    *it.ptr = cur;
+    cur += it.bytes;
+  }
+  p.acts = base;
+  p.acts_bytes = total;
+  // dynamic smem opt-in for the token-embedding gradient (acc[V][cols] fp32)
+  TLK_CUDA(cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                200 * 1024));
+  p.launches_per_step = 0;  // counted at capture (mark)
+  return TLK_OK;
+}
+
+// ------------------------------------------------------------- one step -----
+int gpt_enqueue_step(Pack& p, cudaStream_t st) {
+  GptBufs& b = *static_cast<GptBufs*>(p.scratch);
+  const GptCfg c = b.c;
+  const int Lc = p.lanes, B = p.batch, T = c.T, d = c.d, H = c.heads, V = c.V, Vp = b.Vp;
+  const int N = b.N, dh = 64;
+  const int64_t PS = p.stride;
+  const float* PR = p.params;
+  const uint16_t* WB = p.wbf;
+  float* G = p.grads;
+  const int64_t nd = int64_t(N) * d, nd3 = nd * 3, nd4 = nd * 4;
+  const int64_t tt = int64_t(T) * T, pl = int64_t(B) * H * tt;  // P per lane
+  const float scale = 1.0f / sqrtf(float(dh));
+  auto O = [&](int t) { return tensor_off(p, t); };
+  const LaneState* LS = p.lane_dev;
+  int count = 0;
+  auto marked = [&](const char* name) {
+    p.mark(st, name);
+    ++count;
+  };
+
+  gpt_tokens_kernel<<<dim3((B + 127) / 128, Lc), 128, 0, st>>>(LS, B, T, V, b.tokens, b.targets);
+  TLK_CUDA(cudaGetLastError());
+  marked("tokens");
+  float* x0 = c.layers ? b.L[0].xin : b.xL;
+  gpt_embed_kernel<<<dim3(N, Lc), 128, 0, st>>>(LS, c, B, b.tokens, PR, PS, O(T_WTE), O(T_WPE), x0);
+  TLK_CUDA(cudaGetLastError());
+  marked("embed");
+
+  for (int l = 0; l < c.layers; ++l) {
+    LayerBufs& lb = b.L[l];
+    float* xnext = (l + 1 < c.layers) ? b.L[l + 1].xin : b.xL;
+    ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, lb.xin, PR, PS, O(T_LAYER(l, K_LN1G)),
+                                                         O(T_LAYER(l, K_LN1B)), lb.a, lb.st1);
+    TLK_CUDA(cudaGetLastError());
+    marked("ln1");
+    {  // qkv = a Wqkv^T + b
+      Epi e = epi(EPI_BF16, N, 3 * d, lb.qkv, nd3, 0, 0, 3 * d);
+      e.bias = PR + O(T_LAYER(l, K_AB));
+      e.bias_ls = PS;
+      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.a, nd, 0, 0, d, 1, N, d),
+                                              op(WB + O(T_LAYER(l, K_AW)), PS, 0, 0, d, 1, 3 * d, d), e,
+                                              N, 3 * d, d, 1, 1, "qkv")));
+      ++count;
+    }
+    {  // P = softmax(Q K^T / sqrt(dh)), per (sequence, head)
+      Epi e = epi(EPI_SOFTMAX, T, T, lb.P, pl, int64_t(H) * tt, tt, T);
+      e.scale = scale;
+      e.causal = 1;
+      const Operand A = op(lb.qkv, nd3, int64_t(T) * 3 * d, dh, 3 * d, 1, T, dh);
+      const Operand Bk = op(lb.qkv + d, nd3, int64_t(T) * 3 * d, dh, 3 * d, 1, T, dh);
+      if (T == 256)
+        TLK_TRY((gemm<256, false, false, true>(p, st, A, Bk, e, T, T, dh, B, H, "attn_scores")));
+      else if (T == 128)
+        TLK_TRY((gemm<128, false, false, true>(p, st, A, Bk, e, T, T, dh, B, H, "attn_scores")));
+      else
+        TLK_TRY((gemm<64, false, false, true>(p, st, A, Bk, e, T, T, dh, B, H, "attn_scores")));
+      ++count;
+    }
+    {  // y = P V
+      Epi e = epi(EPI_BF16, T, dh, lb.y, nd, int64_t(T) * d, dh, d);
+      TLK_TRY((gemm<64, false, true, false>(
+          p, st, op(lb.P, pl, int64_t(H) * tt, tt, T, 1, T, T),
+          op(lb.qkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), e, T, dh, T, B, H, "attn_pv")));
+      ++count;
+    }
+    {  // xmid = xin + y Wo^T + bo
+      Epi e = epi(EPI_RESADD, N, d, lb.xmid, nd, 0, 0, d);
+      e.aux = lb.xin;
+      e.bias = PR + O(T_LAYER(l, K_PB));
+      e.bias_ls = PS;
+      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.y, nd, 0, 0, d, 1, N, d),
+                                              op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, d, 1, d, d), e, N,
+                                              d, d, 1, 1, "proj")));
+      ++count;
+    }
+    ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, lb.xmid, PR, PS, O(T_LAYER(l, K_LN2G)),
+                                                         O(T_LAYER(l, K_LN2B)), lb.m, lb.st2);
+    TLK_CUDA(cudaGetLastError());
+    marked("ln2");
+    {  // z = m W1^T + b1, f = gelu(z)
+      Epi e = epi(EPI_BF16_GELU, N, 4 * d, lb.f, nd4, 0, 0, 4 * d);
+      e.out32b = lb.z;
+      e.bias = PR + O(T_LAYER(l, K_FB));
+      e.bias_ls = PS;
+      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.m, nd, 0, 0, d, 1, N, d),
+                                              op(WB + O(T_LAYER(l, K_FW)), PS, 0, 0, d, 1, 4 * d, d), e,
+                                              N, 4 * d, d, 1, 1, "fc")));
+      ++count;
+    }
+    {  // xnext = xmid + f W2^T + b2
+      Epi e = epi(EPI_RESADD, N, d, xnext, nd, 0, 0, d);
+      e.aux = lb.xmid;
+      e.bias = PR + O(T_LAYER(l, K_F2B));
+      e.bias_ls = PS;
+      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.f, nd4, 0, 0, 4 * d, 1, N, 4 * d),
+                                              op(WB + O(T_LAYER(l, K_F2W)), PS, 0, 0, 4 * d, 1, d, 4 * d),
+                                              e, N, d, 4 * d, 1, 1, "fc2")));
+      ++count;
+    }
+  }
+  const int tf = T_LNFG(c);
+  ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, b.xL, PR, PS, O(tf), O(tf + 1), b.xf,
+                                                       b.stf);
+  TLK_CUDA(cudaGetLastError());
+  marked("lnf");
+  {  // logits -> CE row epilogue: lossrow, dl = (softmax - onehot) / N
+    Epi e = epi(EPI_CE, N, V, b.dl, int64_t(N) * Vp, 0, 0, Vp);
+    e.targets = b.targets;
+    e.tg_ls = N;
+    e.lossrow = b.lossrow;
+    e.tokens = float(N);
+    const Operand A = op(b.xf, nd, 0, 0, d, 1, N, d);
+    const Operand Bh = op(WB + O(tf + 2), PS, 0, 0, d, 1, V, d);
+    if (Vp <= 64)
+      TLK_TRY((gemm<64, false, false, true>(p, st, A, Bh, e, N, Vp, d, 1, 1, "head_ce")));
+    else if (Vp <= 96)
+      TLK_TRY((gemm<96, false, false, true>(p, st, A, Bh, e, N, Vp, d, 1, 1, "head_ce")));
+    else if (Vp <= 128)
+      TLK_TRY((gemm<128, false, false, true>(p, st, A, Bh, e, N, Vp, d, 1, 1, "head_ce")));
+    else
+      TLK_TRY((gemm<256, false, false, true>(p, st, A, Bh, e, N, Vp, d, 1, 1, "head_ce")));
+    ++count;
+  }
+  gpt_loss_kernel<<<Lc, 512, 0, st>>>(p.lane_dev, N, b.lossrow, p.loss, p.max_steps, p.last_loss);
+  TLK_CUDA(cudaGetLastError());
+  marked("loss");
+
+  // ---------------------------------------------------------------- backward
+  {  // dxf = dl Whead (fp32), dWhead = dl^T xf
+    Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
+    TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, Vp, 1, N, V),
+                                           op(WB + O(tf + 2), PS, 0, 0, 1, d, d, V), e, N, d, V, 1, 1,
+                                           "head_dgrad")));
+    Epi g = epi(EPI_F32, V, d, G + O(tf + 2), PS, 0, 0, d);
+    TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, 1, Vp, V, N),
+                                          op(b.xf, nd, 0, 0, 1, d, d, N), g, V, d, N, 1, 1, "head_wgrad")));
+    count += 2;
+  }
+  auto ln_bwd = [&](const float* dy, const float* x, const float* stats, int og, int ob, int accumulate,
+                    const char* name) -> int {
+    const int nblk = (N + LNB_ROWS - 1) / LNB_ROWS;
+    ln_bwd_kernel<<<dim3(nblk, Lc), 256, 16 * d * 4, st>>>(LS, N, d, dy, x, stats, PR, PS, O(og), b.dx,
+                                                          b.dxb, accumulate, b.part, b.part_st);
+    TLK_CUDA(cudaGetLastError());
+    marked(name);
+    reduce_parts_kernel<<<dim3((2 * d + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, 2 * d,
+                                                                     G, PS, O(og), d, O(ob));
+    TLK_CUDA(cudaGetLastError());
+    marked("ln_param_grads");
+    return TLK_OK;
+  };
+  auto bias_grad = [&](const uint16_t* src, int C, int t) -> int {
+    const int nblk = (N + CS_ROWS - 1) / CS_ROWS;
+    colsum_bf16_kernel<<<dim3((C + 255) / 256, nblk, Lc), 256, 0, st>>>(LS, src, int64_t(N) * C, C, N, C,
+                                                                        b.part, b.part_st);
+    TLK_CUDA(cudaGetLastError());
+    marked("bias_colsum");
+    reduce_parts_kernel<<<dim3((C + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, C, G, PS,
+                                                                   O(t), C, O(t));
+    TLK_CUDA(cudaGetLastError());
+    marked("bias_reduce");
+    return TLK_OK;
+  };
+  TLK_TRY(ln_bwd(b.dmm, b.xL, b.stf, tf, tf + 1, 0, "lnf_bwd"));
+
+  for (int l = c.layers - 1; l >= 0; --l) {
+    LayerBufs& lb = b.L[l];
+    {  // fc2: dW2 = dxb^T f ; db2 ; dz = (dxb W2) * gelu'(z)
+      Epi g = epi(EPI_F32, d, 4 * d, G + O(T_LAYER(l, K_F2W)), PS, 0, 0, 4 * d);
+      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
+                                            op(lb.f, nd4, 0, 0, 1, 4 * d, 4 * d, N), g, d, 4 * d, N, 1, 1,
+                                            "fc2_wgrad")));
+      TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_F2B)));
+      Epi e = epi(EPI_GELU_BWD, N, 4 * d, b.dz, nd4, 0, 0, 4 * d);
+      e.aux = lb.z;
+      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+                                             op(WB + O(T_LAYER(l, K_F2W)), PS, 0, 0, 1, 4 * d, 4 * d, d), e,
+                                             N, 4 * d, d, 1, 1, "fc2_dgrad")));
+      count += 2;
+    }
+    {  // fc: dW1 = dz^T m ; db1 ; dmm = dz W1 (fp32)
+      Epi g = epi(EPI_F32, 4 * d, d, G + O(T_LAYER(l, K_FW)), PS, 0, 0, d);
+      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dz, nd4, 0, 0, 1, 4 * d, 4 * d, N),
+                                            op(lb.m, nd, 0, 0, 1, d, d, N), g, 4 * d, d, N, 1, 1,
+                                            "fc_wgrad")));
+      TLK_TRY(bias_grad(b.dz, 4 * d, T_LAYER(l, K_FB)));
+      Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
+      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dz, nd4, 0, 0, 4 * d, 1, N, 4 * d),
+                                             op(WB + O(T_LAYER(l, K_FW)), PS, 0, 0, 1, d, d, 4 * d), e, N,
+                                             d, 4 * d, 1, 1, "fc_dgrad")));
+      count += 2;
+    }
+    TLK_TRY(ln_bwd(b.dmm, lb.xmid, lb.st2, T_LAYER(l, K_LN2G), T_LAYER(l, K_LN2B), 1, "ln2_bwd"));
+    {  // proj: dWo = dxb^T y ; dbo ; dy = dxb Wo (bf16)
+      Epi g = epi(EPI_F32, d, d, G + O(T_LAYER(l, K_PW)), PS, 0, 0, d);
+      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
+                                            op(lb.y, nd, 0, 0, 1, d, d, N), g, d, d, N, 1, 1, "proj_wgrad")));
+      TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_PB)));
+      Epi e = epi(EPI_BF16, N, d, b.dy, nd, 0, 0, d);
+      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+                                             op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d), e, N, d, d,
+                                             1, 1, "proj_dgrad")));
+      count += 2;
+    }
+    {  // attention backward per (sequence, head)
+      Epi e = epi(EPI_SOFTMAX_BWD, T, T, b.dS, pl, int64_t(H) * tt, tt, T);
+      e.aux = lb.P;
+      e.scale = scale;
+      const Operand A = op(b.dy, nd, int64_t(T) * d, dh, d, 1, T, dh);
+      const Operand Bv = op(lb.qkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 3 * d, 1, T, dh);
+      if (T == 256)
+        TLK_TRY((gemm<256, false, false, true>(p, st, A, Bv, e, T, T, dh, B, H, "attn_dp")));
+      else if (T == 128)
+        TLK_TRY((gemm<128, false, false, true>(p, st, A, Bv, e, T, T, dh, B, H, "attn_dp")));
+      else
+        TLK_TRY((gemm<64, false, false, true>(p, st, A, Bv, e, T, T, dh, B, H, "attn_dp")));
+      // dq = dS K
+      Epi eq = epi(EPI_BF16, T, dh, b.dqkv, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      TLK_TRY((gemm<64, false, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, T, 1, T, T),
+                                            op(lb.qkv + d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), eq,
+                                            T, dh, T, B, H, "attn_dq")));
+      // dk = dS^T Q
+      Epi ek = epi(EPI_BF16, T, dh, b.dqkv + d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      TLK_TRY((gemm<64, true, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, 1, T, T, T),
+                                           op(lb.qkv, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), ek, T,
+                                           dh, T, B, H, "attn_dk")));
+      // dv = P^T dY
+      Epi ev = epi(EPI_BF16, T, dh, b.dqkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      TLK_TRY((gemm<64, true, true, false>(p, st, op(lb.P, pl, int64_t(H) * tt, tt, 1, T, T, T),
+                                           op(b.dy, nd, int64_t(T) * d, dh, 1, d, dh, T), ev, T, dh, T, B,
+                                           H, "attn_dv")));
+      count += 4;
+    }
+    {  // qkv: dWqkv = dqkv^T a ; db ; da = dqkv Wqkv (fp32)
+      Epi g = epi(EPI_F32, 3 * d, d, G + O(T_LAYER(l, K_AW)), PS, 0, 0, d);
+      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dqkv, nd3, 0, 0, 1, 3 * d, 3 * d, N),
+                                            op(lb.a, nd, 0, 0, 1, d, d, N), g, 3 * d, d, N, 1, 1,
+                                            "qkv_wgrad")));
+      TLK_TRY(bias_grad(b.dqkv, 3 * d, T_LAYER(l, K_AB)));
+      Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
+      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dqkv, nd3, 0, 0, 3 * d, 1, N, 3 * d),
+                                             op(WB + O(T_LAYER(l, K_AW)), PS, 0, 0, 1, d, d, 3 * d), e, N, d,
+                                             3 * d, 1, 1, "qkv_dgrad")));
+      count += 2;
+    }
+    TLK_TRY(ln_bwd(b.dmm, lb.xin, lb.st1, T_LAYER(l, K_LN1G), T_LAYER(l, K_LN1B), 1, "ln1_bwd"));
+  }
+  {  // embeddings
+    const int cols = std::min(d, (50000 / V) / 32 * 32);  // acc[V][cols] fp32 <= 200 KB
+    const int nblk = (N + EMB_ROWS - 1) / EMB_ROWS;
+    embed_bwd_kernel<<<dim3(nblk, (d + cols - 1) / cols, Lc), cols, V * cols * 4, st>>>(
+        LS, N, d, V, cols, b.tokens, T, b.dx, b.part, b.part_st);
+    TLK_CUDA(cudaGetLastError());
+    marked("wte_partial");
+    reduce_parts_kernel<<<dim3((V * d + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, V * d,
+                                                                       G, PS, O(T_WTE), V * d, O(T_WTE));
+    TLK_CUDA(cudaGetLastError());
+    marked("wte_reduce");
+    wpe_bwd_kernel<<<dim3(T, Lc), 128, 0, st>>>(LS, B, T, d, b.dx, G, PS, O(T_WPE));
+    TLK_CUDA(cudaGetLastError());
+    marked("wpe");
+  }
+  TLK_TRY(enqueue_optimizer(p, st));
+  ++count;
+  p.launches_per_step = count;
+  return TLK_OK;
+}
+
+}  // namespace tlk

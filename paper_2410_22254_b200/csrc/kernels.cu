@@ -142,30 +142,53 @@ static WtHook wt_hook(const Pack& p) {
 }
 
 // ------------------------------------------------------------ lane init -----
-TensorTable make_tensor_table(const ModelDef& d) {
-  TensorTable t{};
-  t.n = d.ntensors;
-  for (int i = 0; i < d.ntensors; ++i) {
-    t.off[i] = tensor_offset(d, i);
-    t.count[i] = d.t[i].count;
-    t.bound[i] = float(1.0 / std::sqrt(double(d.t[i].fan_in)));
+std::vector<TensorInfo> model_tensors(int model, const GptCfg& c) {
+  std::vector<TensorInfo> out;
+  int64_t off = 0;
+  auto add = [&](int64_t count, int fan, int kind) {
+    out.push_back(TensorInfo{off, count, fan, kind});
+    off = round_up(off + count, PARAM_ALIGN);
+  };
+  if (is_gpt(model)) {  // oracle/gpt.py::tensors
+    const int64_t d = c.d;
+    add(int64_t(c.V) * d, int(d), 0);
+    add(int64_t(c.T) * d, int(d), 0);
+    for (int l = 0; l < c.layers; ++l) {
+      add(d, int(d), 1), add(d, int(d), 2);
+      add(3 * d * d, int(d), 0), add(3 * d, int(d), 0);
+      add(d * d, int(d), 0), add(d, int(d), 0);
+      add(d, int(d), 1), add(d, int(d), 2);
+      add(4 * d * d, int(d), 0), add(4 * d, int(d), 0);
+      add(4 * d * d, int(4 * d), 0), add(d, int(4 * d), 0);
+    }
+    add(d, int(d), 1), add(d, int(d), 2);
+    add(int64_t(c.V) * d, int(d), 0);
+    return out;
   }
-  return t;
+  const ModelDef* md = model_def(model);
+  for (int t = 0; md && t < md->ntensors; ++t) add(md->t[t].count, md->t[t].fan_in, 0);
+  return out;
 }
 
-__global__ void lane_init_kernel(TensorTable tt, uint64_t seed, int lane, int64_t stride,
-                                 float* params, float* grads, float* m1, float* m2,
+__global__ void lane_init_kernel(const TensorInfo* __restrict__ tt, int nt, uint64_t seed, int lane,
+                                 int64_t stride, float* params, float* grads, float* m1, float* m2,
                                  uint16_t* wbf, WtHook hook) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < stride;
        e += int64_t(gridDim.x) * blockDim.x) {
     float v = 0.0f;
-#pragma unroll 1
-    for (int t = 0; t < tt.n; ++t) {
-      int64_t r = e - tt.off[t];
-      if (r >= 0 && r < tt.count[t]) {
-        v = init_value(rng_key(seed, STREAM_INIT + t, 0), uint64_t(r), tt.bound[t]);
-        break;
-      }
+    // tensors are sorted by offset: binary search the owner of e
+    int lo = 0, hi = nt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tt[mid].off <= e) lo = mid; else hi = mid - 1;
+    }
+    const int64_t r = e - tt[lo].off;
+    if (r >= 0 && r < tt[lo].count) {
+      const int kind = tt[lo].kind;
+      v = kind == 1 ? 1.0f
+          : kind == 2 ? 0.0f
+                      : init_value(rng_key(seed, STREAM_INIT + lo, 0), uint64_t(r),
+                                   float(1.0 / sqrt(double(tt[lo].fan_in))));
     }
     const int64_t i = lane * stride + e;
     params[i] = v;
@@ -179,11 +202,11 @@ __global__ void lane_init_kernel(TensorTable tt, uint64_t seed, int lane, int64_
 }
 
 int enqueue_lane_init(Pack& p, int lane, cudaStream_t st) {
-  TensorTable tt = make_tensor_table(*p.def);
   int blocks = int((p.stride + 255) / 256);
   if (blocks > 1184) blocks = 1184;
-  lane_init_kernel<<<blocks, 256, 0, st>>>(tt, p.lane_host[lane].seed, lane, p.stride, p.params,
-                                            p.grads, p.mom1, p.mom2, p.wbf, wt_hook(p));
+  lane_init_kernel<<<blocks, 256, 0, st>>>(p.tinfo_dev, int(p.tinfo.size()), p.lane_host[lane].seed,
+                                            lane, p.stride, p.params, p.grads, p.mom1, p.mom2, p.wbf,
+                                            wt_hook(p));
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }

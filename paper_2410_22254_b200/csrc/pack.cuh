@@ -14,7 +14,10 @@ namespace tlk {
 struct Pack {
   // description
   int model = 0, batch = 0, lanes = 0, max_steps = 0, host_input = 0;
-  const ModelDef* def = nullptr;
+  const ModelDef* def = nullptr;      // MLP / CNN
+  GptCfg gcfg{};                       // transformer packs
+  std::vector<TensorInfo> tinfo;       // parameter tensors of a lane (all models)
+  TensorInfo* tinfo_dev = nullptr;
   int64_t pcount = 0, stride = 0;
   // lane table
   LaneState* lane_dev = nullptr;
@@ -70,15 +73,11 @@ int mlp_setup(Pack& p);
 int mlp_enqueue_step(Pack& p, cudaStream_t st);
 int cnn_setup(Pack& p);
 int cnn_enqueue_step(Pack& p, cudaStream_t st);
+int gpt_setup(Pack& p);
+int gpt_enqueue_step(Pack& p, cudaStream_t st);
+std::vector<TensorInfo> model_tensors(int model, const GptCfg& c);
 
 // Common kernels (kernels.cu).
-struct TensorTable {
-  int n;
-  int64_t off[MAX_TENSORS];
-  int64_t count[MAX_TENSORS];
-  float bound[MAX_TENSORS];
-};
-TensorTable make_tensor_table(const ModelDef& d);
 
 int enqueue_inputs(Pack& p, cudaStream_t st);  // datagen (or host-input convert)
 int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_t w_off,

@@ -80,6 +80,8 @@ int enqueue_step(Pack& p, cudaStream_t st) {
   switch (p.model) {
     case TLK_MODEL_MLP: return mlp_enqueue_step(p, st);
     case TLK_MODEL_CNN: return cnn_enqueue_step(p, st);
+    case TLK_MODEL_XFORMER:
+    case TLK_MODEL_GPT: return gpt_enqueue_step(p, st);
   }
   return fail(TLK_EINVAL, "unknown model %d", p.model);
 }
@@ -113,23 +115,35 @@ extern "C" {
 int tlk_abi_version(void) { return TLK_ABI_VERSION; }
 const char* tlk_last_error(void) { return g_err; }
 
-int tlk_model_query(int32_t model, int32_t batch, tlk_model_info* out) {
-  const ModelDef* d = model_def(model);
-  TLK_CHECK(d && out, TLK_EINVAL, "unknown model %d", model);
-  out->param_count = param_count(*d);
-  out->param_stride = param_stride(*d);
-  out->flops_per_sample = 6 * d->macs_per_sample;
-  out->num_tensors = d->ntensors;
+static void fill_info(int model, const GptCfg& c, int batch, tlk_model_info* out) {
+  const auto ts = model_tensors(model, c);
+  out->param_count = 0;
+  for (const auto& t : ts) out->param_count += t.count;
+  out->param_stride = ts.empty() ? 0 : round_up(ts.back().off + ts.back().count, PARAM_ALIGN);
+  out->num_tensors = int32_t(ts.size());
+  if (is_gpt(model)) {  // 6 x (matmul params + attention) per token, x T tokens per sample
+    const int64_t d = c.d, T = c.T;
+    const int64_t mm = 12 * d * d * c.layers + int64_t(c.V) * d;
+    out->flops_per_sample = 6 * T * (mm + int64_t(c.layers) * T * d);
+  } else {
+    out->flops_per_sample = 6 * model_def(model)->macs_per_sample;
+  }
   (void)batch;
+}
+
+int tlk_model_query(int32_t model, int32_t batch, tlk_model_info* out) {
+  TLK_CHECK(out && (model_def(model) || is_gpt(model)), TLK_EINVAL, "unknown model %d", model);
+  fill_info(model, gpt_default(model), batch, out);
   return TLK_OK;
 }
 
 int tlk_model_tensor(int32_t model, int32_t t, int64_t* offset, int64_t* count, int32_t* fan_in) {
-  const ModelDef* d = model_def(model);
-  TLK_CHECK(d && t >= 0 && t < d->ntensors, TLK_EINVAL, "bad model/tensor %d/%d", model, t);
-  if (offset) *offset = tensor_offset(*d, t);
-  if (count) *count = d->t[t].count;
-  if (fan_in) *fan_in = d->t[t].fan_in;
+  TLK_CHECK(model_def(model) || is_gpt(model), TLK_EINVAL, "unknown model %d", model);
+  const auto ts = model_tensors(model, gpt_default(model));
+  TLK_CHECK(t >= 0 && t < int32_t(ts.size()), TLK_EINVAL, "bad tensor %d", t);
+  if (offset) *offset = ts[t].off;
+  if (count) *count = ts[t].count;
+  if (fan_in) *fan_in = ts[t].fan_in;
   return TLK_OK;
 }
 
@@ -182,10 +196,23 @@ int tlk_stream(tlk_ctx* ctx, void** stream) {
 int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   TLK_CHECK(ctx && desc && pack_id, TLK_EINVAL, "null argument");
   const ModelDef* d = model_def(desc->model);
-  TLK_CHECK(d, TLK_EINVAL, "unknown model %d", desc->model);
+  const bool gpt = is_gpt(desc->model);
+  TLK_CHECK(d || gpt, TLK_EINVAL, "unknown model %d", desc->model);
   TLK_CHECK(desc->lanes >= 1 && desc->lanes <= 4096, TLK_EINVAL, "lanes must be 1..4096");
-  TLK_CHECK(desc->batch >= 8 && desc->batch <= 64 && desc->batch % 8 == 0, TLK_EINVAL,
-            "batch must be a multiple of 8 in [8, 64] (got %d)", desc->batch);
+  if (!gpt)
+    TLK_CHECK(desc->batch >= 8 && desc->batch <= 64 && desc->batch % 8 == 0, TLK_EINVAL,
+              "batch must be a multiple of 8 in [8, 64] (got %d)", desc->batch);
+  else
+    TLK_CHECK(desc->batch >= 1 && desc->batch <= 4096 && !desc->host_input, TLK_EINVAL,
+              "transformer packs: batch in [1, 4096], device-generated tokens only");
+  GptCfg gc = gpt_default(desc->model);
+  if (gpt) {
+    if (desc->layers > 0) gc.layers = desc->layers;
+    if (desc->d_model > 0) gc.d = desc->d_model;
+    if (desc->heads > 0) gc.heads = desc->heads;
+    if (desc->seq_len > 0) gc.T = desc->seq_len;
+    if (desc->vocab > 0) gc.V = desc->vocab;
+  }
   TLK_CHECK(desc->max_steps >= 1, TLK_EINVAL, "max_steps must be >= 1");
   TLK_CUDA(cudaSetDevice(ctx->device));
   auto p = std::make_unique<Pack>();
@@ -196,8 +223,14 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   p->host_input = desc->host_input;
   p->flags = desc->flags;
   p->def = d;
-  p->pcount = param_count(*d);
-  p->stride = param_stride(*d);
+  p->gcfg = gc;
+  p->tinfo = model_tensors(desc->model, gc);
+  {
+    tlk_model_info mi;
+    fill_info(desc->model, gc, desc->batch, &mi);
+    p->pcount = mi.param_count;
+    p->stride = mi.param_stride;
+  }
   p->teacher = ctx->teacher;
   const size_t L = size_t(p->lanes), S = size_t(p->stride), B = size_t(p->batch);
   int rc = 0;
@@ -218,7 +251,16 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   p->pixels = static_cast<uint8_t*>(grab(L * B * 784));
   p->labels = static_cast<int32_t*>(grab(L * B * 4));
   p->x = static_cast<uint16_t*>(grab(L * B * 784 * 2));
-  if (!rc) rc = (p->model == TLK_MODEL_MLP) ? mlp_setup(*p) : cnn_setup(*p);
+  p->tinfo_dev = static_cast<TensorInfo*>(grab(p->tinfo.size() * sizeof(TensorInfo)));
+  if (!rc) {
+    const cudaError_t e = cudaMemcpy(p->tinfo_dev, p->tinfo.data(),
+                                     p->tinfo.size() * sizeof(TensorInfo), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) rc = cuda_fail(e, "tensor table upload");
+  }
+  if (!rc)
+    rc = p->model == TLK_MODEL_MLP ? mlp_setup(*p)
+         : p->model == TLK_MODEL_CNN ? cnn_setup(*p)
+                                     : gpt_setup(*p);
   if (rc) {
     destroy_pack(*p);
     return rc;
@@ -370,6 +412,15 @@ int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, i
     case TLK_BUF_ACTS: *dev_ptr = p->acts; *bytes = int64_t(p->acts_bytes); break;
     default: return fail(TLK_EINVAL, "unknown buffer %d", which);
   }
+  return TLK_OK;
+}
+
+int tlk_pack_info(tlk_ctx* ctx, int32_t pack, tlk_model_info* out) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(out, TLK_EINVAL, "null argument");
+  fill_info(p->model, p->gcfg, p->batch, out);
   return TLK_OK;
 }
 

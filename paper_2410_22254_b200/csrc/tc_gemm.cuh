@@ -80,11 +80,24 @@ struct GemmThreads {  // problems may ask for 256 threads (extra epilogue warps)
 // Epilogue shared by both mainloops: TMEM -> registers -> problem functor
 // (per-row chunks), or -> shared fp32 tile -> problem tile functor.
 template <class P>
+struct RowEpi {  // problems may define ROW_EPILOGUE (functor reads TMEM itself)
+  template <class Q>
+  static constexpr bool get(decltype(Q::ROW_EPILOGUE)*) { return Q::ROW_EPILOGUE; }
+  template <class Q>
+  static constexpr bool get(...) { return false; }
+  static constexpr bool value = get<P>(nullptr);
+};
+
+template <class P>
 TLK_DEV void gemm_epilogue(const P& p, const typename P::Work& w, uint32_t tmem, uint8_t* smem) {
   constexpr int BN = P::BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row = warp * 32 + lane;
-  if constexpr (P::TILE_EPILOGUE) {
+  if constexpr (RowEpi<P>::value) {
+    // whole-row epilogues (softmax, cross-entropy): the functor walks its
+    // row's TMEM columns as often as it needs (warp-uniform control flow)
+    if (warp < 4) p.row_epilogue(w, w.m0 + row, tmem + (uint32_t(warp * 32) << 16));
+  } else if constexpr (P::TILE_EPILOGUE) {
     static_assert(GEMM_BM * (BN + 4) * 4 <= P::STAGES * GemmSmem<P>::STAGE_BYTES, "tile fits");
     float* tile = reinterpret_cast<float*>(smem);
     if (warp < 4) {

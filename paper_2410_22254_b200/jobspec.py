@@ -17,7 +17,8 @@ import os
 from dataclasses import asdict, dataclass
 
 JOB_MODULE = "paper_2410_22254_b200.job"
-MODELS = ("mlp", "cnn")
+MODELS = ("mlp", "cnn", "xformer", "gpt")
+SEQ_MODELS = ("xformer", "gpt")  # batch = sequences
 OPTIMIZERS = ("adam", "adamw", "sgd")
 
 
@@ -72,7 +73,10 @@ def parse_job_flags(flags) -> JobSpec:
     spec = JobSpec(**vars(ns))
     if spec.steps < 1:
         raise ValueError("--steps must be >= 1")
-    if spec.batch < 8 or spec.batch > 64 or spec.batch % 8:
+    if spec.model in SEQ_MODELS:
+        if spec.batch < 1 or spec.batch > 4096:
+            raise ValueError("--batch (sequences) must be in [1, 4096]")
+    elif spec.batch < 8 or spec.batch > 64 or spec.batch % 8:
         raise ValueError("--batch must be a multiple of 8 in [8, 64]")
     if spec.lr <= 0 or spec.eps <= 0:
         raise ValueError("--lr and --eps must be positive")

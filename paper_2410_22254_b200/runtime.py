@@ -14,8 +14,8 @@ import threading
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtlk.so")
 
 TLK_OK, TLK_EINVAL, TLK_ECUDA, TLK_EOOM, TLK_ESTATE = 0, -1, -2, -3, -4
-MODEL_MLP, MODEL_CNN = 1, 2
-MODELS = {"mlp": MODEL_MLP, "cnn": MODEL_CNN}
+MODEL_MLP, MODEL_CNN, MODEL_XFORMER, MODEL_GPT = 1, 2, 3, 4
+MODELS = {"mlp": MODEL_MLP, "cnn": MODEL_CNN, "xformer": MODEL_XFORMER, "gpt": MODEL_GPT}
 OPT_ADAM, OPT_ADAMW, OPT_SGD = 1, 2, 3
 OPTIMIZERS = {"adam": OPT_ADAM, "adamw": OPT_ADAMW, "sgd": OPT_SGD}
 PACK_WRITE_ALL_GRADS = 1
@@ -25,7 +25,8 @@ EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
     "tlk_close", "tlk_sync", "tlk_stream", "tlk_pack_create", "tlk_lane_load", "tlk_lane_release",
     "tlk_run", "tlk_step_host", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
-    "tlk_pack_tensor", "tlk_pack_launches_per_step", "tlk_profile_step", "tlk_selftest_gemm",
+    "tlk_pack_tensor", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
+    "tlk_selftest_gemm",
     "tlk_selftest_datagen",
 )
 
@@ -46,7 +47,9 @@ class JobDesc(C.Structure):
 
 class PackDesc(C.Structure):
     _fields_ = [("model", C.c_int32), ("batch", C.c_int32), ("lanes", C.c_int32),
-                ("max_steps", C.c_int32), ("host_input", C.c_int32), ("flags", C.c_int32)]
+                ("max_steps", C.c_int32), ("host_input", C.c_int32), ("flags", C.c_int32),
+                ("layers", C.c_int32), ("d_model", C.c_int32), ("heads", C.c_int32),
+                ("seq_len", C.c_int32), ("vocab", C.c_int32)]
 
 
 class ModelInfo(C.Structure):
@@ -146,22 +149,25 @@ class Context:
         return s.value or 0
 
     def pack(self, model: int, batch: int, lanes: int, max_steps: int, host_input: bool = False,
-             flags: int = 0):
-        return Pack(self, model, batch, lanes, max_steps, host_input, flags)
+             flags: int = 0, **cfg):
+        return Pack(self, model, batch, lanes, max_steps, host_input, flags, **cfg)
 
 
 class Pack:
     """K co-resident training lanes of one model (tlk_pack_*)."""
 
     def __init__(self, ctx: Context, model: int, batch: int, lanes: int, max_steps: int,
-                 host_input: bool = False, flags: int = 0):
+                 host_input: bool = False, flags: int = 0, layers: int = 0, d_model: int = 0,
+                 heads: int = 0, seq_len: int = 0, vocab: int = 0):
         self.ctx, self.model, self.batch, self.lanes = ctx, model, batch, lanes
         self.max_steps, self.host_input = max_steps, host_input
-        desc = PackDesc(model, batch, lanes, max_steps, int(host_input), int(flags))
+        desc = PackDesc(model, batch, lanes, max_steps, int(host_input), int(flags), layers, d_model,
+                        heads, seq_len, vocab)
         pid = C.c_int32()
         check(lib().tlk_pack_create(ctx._ctx, C.byref(desc), C.byref(pid)))
         self.id = pid.value
-        self.info = model_info(model)
+        self.info = ModelInfo()
+        check(lib().tlk_pack_info(ctx._ctx, self.id, C.byref(self.info)))
 
     def load(self, lane: int, *, seed: int, steps: int, optimizer: int = OPT_ADAM, lr: float = 1e-3,
              beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
