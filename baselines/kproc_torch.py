@@ -51,27 +51,69 @@ class MLP(nn.Module):
         return self.fc3(F.relu(self.fc2(F.relu(self.fc1(x)))))
 
 
+class GPT(nn.Module):
+    """Pre-LN decoder (same shapes as TLK_MODEL_XFORMER / TLK_MODEL_GPT):
+    learned positions, fused qkv, tanh-GELU MLP, untied head without bias."""
+
+    def __init__(self, layers, d, heads, T, V):
+        super().__init__()
+        self.T, self.heads = T, heads
+        self.wte, self.wpe = nn.Embedding(V, d), nn.Embedding(T, d)
+        self.blocks = nn.ModuleList(nn.ModuleDict(dict(
+            ln1=nn.LayerNorm(d), attn=nn.Linear(d, 3 * d), proj=nn.Linear(d, d),
+            ln2=nn.LayerNorm(d), fc=nn.Linear(d, 4 * d), fc2=nn.Linear(4 * d, d)))
+            for _ in range(layers))
+        self.lnf, self.head = nn.LayerNorm(d), nn.Linear(d, V, bias=False)
+
+    def forward(self, idx):
+        B, T = idx.shape
+        x = self.wte(idx) + self.wpe.weight[:T][None]
+        for b in self.blocks:
+            q, k, v = b.attn(b.ln1(x)).view(B, T, 3, self.heads, -1).unbind(2)
+            y = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                               v.transpose(1, 2), is_causal=True)
+            x = x + b.proj(y.transpose(1, 2).reshape(B, T, -1))
+            x = x + b.fc2(F.gelu(b.fc(b.ln2(x)), approximate="tanh"))
+        return self.head(self.lnf(x))
+
+
+GPT_CFGS = {"xformer": (2, 256, 4, 128, 256), "gpt": (6, 384, 6, 256, 65)}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--model", default="cnn", choices=("cnn", "mlp"))
+    ap.add_argument("--model", default="cnn", choices=("cnn", "mlp", "xformer", "gpt"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--t0", type=float, required=True, help="wall-clock start of the timed window")
     ap.add_argument("--duration", type=float, default=10.0)
-    ap.add_argument("--bf16", type=int, default=0, help="1: torch.autocast(bfloat16)")
+    ap.add_argument("--bf16", type=int, default=None,
+                    help="1: torch.autocast(bfloat16); default 1 for the transformer models")
     a = ap.parse_args()
     torch.manual_seed(a.seed)
     dev = torch.device("cuda")
-    model = (Net() if a.model == "cnn" else MLP()).to(dev)
+    if a.bf16 is None:
+        a.bf16 = int(a.model in GPT_CFGS)
+    if a.model in GPT_CFGS:
+        cfg = GPT_CFGS[a.model]
+        model = GPT(*cfg).to(dev)
+    else:
+        model = (Net() if a.model == "cnn" else MLP()).to(dev)
     opt = torch.optim.Adam(model.parameters(), lr=a.lr)
     torch.backends.cudnn.benchmark = True
 
     def step():
-        x = torch.rand(a.batch, 1, 28, 28, device=dev)
-        y = torch.randint(0, 10, (a.batch,), device=dev)
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=bool(a.bf16)):
-            loss = F.cross_entropy(model(x), y)
+            if a.model in GPT_CFGS:
+                T, V = GPT_CFGS[a.model][3:]
+                toks = torch.randint(0, V, (a.batch, T + 1), device=dev)
+                logits = model(toks[:, :-1])
+                loss = F.cross_entropy(logits.reshape(-1, V).float(), toks[:, 1:].reshape(-1))
+            else:
+                x = torch.rand(a.batch, 1, 28, 28, device=dev)
+                y = torch.randint(0, 10, (a.batch,), device=dev)
+                loss = F.cross_entropy(model(x), y)
         opt.zero_grad(set_to_none=True)
         loss.backward()
         opt.step()

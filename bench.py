@@ -34,7 +34,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "aggregate samples/sec per B200 vs jobs/GPU (triples NPPN); 1/2/4/8-GPU scaling"
 UNIT = "samples/s"
-WORKLOAD = "configs[1]: 8 co-resident MNIST CNN jobs packed per B200 (triples [1,8,1] per GPU)"
+# name -> (model, batch per job, jobs per GPU, description).  The default
+# (driver) line is configs[1]; the others are the BASELINE configs' job
+# models at their per-GPU packing (a sample = one image / one sequence).
+WORKLOADS = {
+    "cnn": ("cnn", 64, 8, "configs[1]: 8 co-resident MNIST CNN jobs packed per B200 (triples [1,8,1] per GPU)"),
+    "mlp": ("mlp", 64, 4, "configs[0]: 4 MNIST-MLP jobs packed on one device (triples [1,4,1])"),
+    "xformer": ("xformer", 32, 32, "configs[3] transformer job (2 layers, d=256, T=128), 32 jobs/GPU"),
+    "gpt": ("gpt", 64, 16, "configs[4]: tiny-GPT (6 layers, d=384, T=256) sweep, 16 jobs/GPU"),
+}
+WORKLOAD = WORKLOADS["cnn"][3]
 JOBS_PER_GPU = 8
 BATCH = 64
 MODEL = "cnn"
@@ -182,9 +191,31 @@ def kernel_work(name, info, lanes, batch):
 
 
 def step_roofline(info, lanes, batch, hbm_gbs, tflops):
-    flops = 6.0 * (26 * 26 * 32 * 9 + 24 * 24 * 64 * 288 + 9216 * 128 + 128 * 10) * batch * lanes
+    """t_roof = max(F / peak_tc, B / peak_hbm) for one step of all lanes:
+    F = 3 x 2 x MACs per sample (libtlk's model table), B = 28 B/param Adam traffic."""
+    flops = float(info.flops_per_sample) * batch * lanes
     bytes_ = 28.0 * info.param_count * lanes
     return max(flops / (tflops * 1e12), bytes_ / (hbm_gbs * 1e9)), flops, bytes_
+
+
+GPT_CFG = {"xformer": (2, 256, 4, 128, 256), "gpt": (6, 384, 6, 256, 65)}
+
+
+def gpt_kernel_work(name, model, batch, lanes):
+    """Algorithmic FLOPs of one launch of a transformer-pack GEMM (per launch =
+    one layer's product for all lanes); None for non-GEMM kernels."""
+    Lr, d, H, T, V = GPT_CFG[model]
+    N = batch * T * lanes
+    attn = 2.0 * batch * lanes * H * T * T * 64
+    table = {"qkv": 2.0 * N * 3 * d * d, "proj": 2.0 * N * d * d, "fc": 2.0 * N * 4 * d * d,
+             "fc2": 2.0 * N * 4 * d * d, "attn_scores": attn, "attn_pv": attn, "attn_dp": attn,
+             "attn_dq": attn, "attn_dk": attn, "attn_dv": attn,
+             "qkv_wgrad": 2.0 * N * 3 * d * d, "qkv_dgrad": 2.0 * N * 3 * d * d,
+             "proj_wgrad": 2.0 * N * d * d, "proj_dgrad": 2.0 * N * d * d,
+             "fc_wgrad": 2.0 * N * 4 * d * d, "fc_dgrad": 2.0 * N * 4 * d * d,
+             "fc2_wgrad": 2.0 * N * 4 * d * d, "fc2_dgrad": 2.0 * N * 4 * d * d,
+             "head_ce": 2.0 * N * V * d, "head_dgrad": 2.0 * N * V * d, "head_wgrad": 2.0 * N * V * d}
+    return table.get(name)
 
 
 # ---------------------------------------------------------------- baselines ---
@@ -208,10 +239,11 @@ def run_tasks_via_run_plan(argvs, ntpp, timeout):
     return report, outs
 
 
-def cpu_oracle_rate(steps, warmup, jobs=JOBS_PER_GPU):
+def cpu_oracle_rate(steps, warmup, jobs=None):
     """The numpy oracle jobs run as `jobs` concurrent processes on the host
     cores (run_plan, OMP_NUM_THREADS = cores // jobs); returns the aggregate
     steady-state samples/s and the thread count used."""
+    jobs = JOBS_PER_GPU if jobs is None else jobs
     cores = os.cpu_count() or 1
     ntpp = max(1, cores // jobs)
     argvs = [[sys.executable, "-m", "oracle.job", "--model", MODEL, "--seed", str(i), "--batch",
@@ -224,7 +256,8 @@ def cpu_oracle_rate(steps, warmup, jobs=JOBS_PER_GPU):
     return float(sum(rates)), ntpp * jobs, outs
 
 
-def kproc_rate(jobs=JOBS_PER_GPU, duration=10.0, lead=35.0):
+def kproc_rate(jobs=None, duration=10.0, lead=35.0):
+    jobs = JOBS_PER_GPU if jobs is None else jobs
     t0 = time.time() + lead
     argvs = [[sys.executable, os.path.join(ROOT, "baselines", "kproc_torch.py"), "--model", MODEL,
               "--seed", str(i), "--batch", str(BATCH), "--t0", f"{t0:.3f}",
@@ -316,9 +349,23 @@ def packed_arm(a, world, rank, local):
     # per-kernel device times of one step (CUDA events on the launching stream)
     kernels = pack.profile_step(a.profile_iters)
     step_ms = sum(t for _, t in kernels)
-    top_name, top_ms = max(kernels, key=lambda kv: kv[1])
-    top_ms = max(top_ms, 1e-6)
-    bound, work = kernel_work(top_name, pack.info, lanes, BATCH)
+    if MODEL in GPT_CFG:
+        # one launch per layer per name: dominant = the GEMM family with the
+        # largest total time; roofline per launch of it
+        tot, cnt = {}, {}
+        for k, v in kernels:
+            tot[k] = tot.get(k, 0.0) + v
+            cnt[k] = cnt.get(k, 0) + 1
+        gem = [k for k in tot if gpt_kernel_work(k, MODEL, BATCH, lanes)]
+        top_name = max(gem, key=lambda k: tot[k])
+        top_ms = max(tot[top_name] / cnt[top_name], 1e-6)
+        bound, work = "tensor", gpt_kernel_work(top_name, MODEL, BATCH, lanes)
+        kernels_out = {k: round(v, 5) for k, v in tot.items()}
+    else:
+        top_name, top_ms = max(kernels, key=lambda kv: kv[1])
+        top_ms = max(top_ms, 1e-6)
+        bound, work = kernel_work(top_name, pack.info, lanes, BATCH)
+        kernels_out = {k: round(v, 5) for k, v in kernels}
     if bound == "tensor":
         achieved = work / (top_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": top_name, "achieved": achieved, "peak": tc,
@@ -343,6 +390,9 @@ def packed_arm(a, world, rank, local):
 
     # end-to-end through the public API with HOST buffers (pinned), per step:
     # H2D of the step's pixels+labels, one packed step, D2H of the losses.
+    if MODEL in GPT_CFG:
+        return _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_roof,
+                                sflops, sbytes, lanes, kernels_out)
     e2e_steps = max(3, min(a.steps, 100))
     hpack = ctx.pack(rt.MODELS[MODEL], BATCH, lanes, a.warmup + e2e_steps + 2, host_input=True)
     for j in range(lanes):
@@ -384,9 +434,9 @@ def packed_arm(a, world, rank, local):
                           "frac": t_roof * 1e3 / ms_step, "flops_per_step": sflops,
                           "compulsory_bytes_per_step": sbytes,
                           "samples_per_s_roof": lanes * BATCH / t_roof},
-        "kernels": {k: round(v, 5) for k, v in kernels},
+        "kernels": kernels_out,
     }
-    if rank == 0 and world == 1 and a.sweep:
+    if rank == 0 and world == 1 and a.sweep and MODEL == "cnn":
         # the metric's "vs jobs/GPU" axis: packed throughput for NPPN/GPU = 1..32
         sweep = []
         for k in (1, 2, 4, 8, 16, 32):
@@ -421,13 +471,43 @@ def packed_arm(a, world, rank, local):
     return 0
 
 
+def _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_roof, sflops,
+                     sbytes, lanes, kernels_out):
+    T = GPT_CFG[MODEL][3]
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s (sequences)", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (on-device order-1 Markov-chain tokens; random-init weights)",
+        "config": {"workload": WORKLOAD, "jobs_per_gpu": lanes, "batch_per_job": BATCH,
+                   "tokens_per_s": value * T, "optimizer": "adam"},
+        "e2e": None, "gpu_launches": pack.launches_per_step() * a.steps, "clocks": clocks,
+        "roofline": roof,
+        "step_roofline": {"t_roof_ms": t_roof * 1e3, "measured_ms": ms_step,
+                          "frac": t_roof * 1e3 / ms_step, "flops_per_step": sflops,
+                          "compulsory_bytes_per_step": sbytes},
+        "kernels": kernels_out,
+    }
+    if rank == 0 and world == 1 and not a.no_baselines:
+        kp, outs = kproc_rate(min(lanes, 8), duration=a.kproc_seconds, lead=60.0)
+        line["kproc_baseline"] = {"value": kp, "unit": "samples/s", "procs": min(lanes, 8),
+                                  "mechanism": "PyTorch processes pinned to one GPU via run_plan",
+                                  "packed_over_kproc": (value / kp) if kp else None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("packed", "reference"), default="packed")
-    ap.add_argument("--jobs", type=int, default=JOBS_PER_GPU, help="co-resident jobs per GPU")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cnn",
+                    help="default cnn = configs[1] (the driver's line)")
+    ap.add_argument("--jobs", type=int, default=None, help="co-resident jobs per GPU")
     ap.add_argument("--profile-iters", type=int, default=5)
     ap.add_argument("--kproc-seconds", type=float, default=10.0)
     ap.add_argument("--no-baselines", action="store_true")
@@ -435,6 +515,11 @@ def main():
                     help="skip the jobs/GPU sweep (1..32 packed CNN jobs)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
+    global MODEL, BATCH, JOBS_PER_GPU, WORKLOAD
+    MODEL, BATCH, JOBS_PER_GPU, WORKLOAD = WORKLOADS[a.workload]
+    if a.jobs is None:
+        a.jobs = JOBS_PER_GPU
+    JOBS_PER_GPU = a.jobs
     world, rank, local = dist_setup(a.gpus)
     try:
         if a.impl == "reference":

@@ -18,6 +18,7 @@
 #include "pack.cuh"
 #include "rng.cuh"
 #include "sgemm.cuh"
+#include "tgemm.cuh"
 
 namespace tlk {
 
@@ -34,7 +35,7 @@ struct LayerBufs {
 
 struct GptBufs {
   GptCfg c;
-  int N, Vp;
+  int N, Vp, sms;
   int32_t *tokens, *targets;
   std::vector<LayerBufs> L;
   float *xL, *stf, *lossrow;
@@ -297,9 +298,17 @@ Operand op(const uint16_t* base, int64_t ls, int64_t bs, int64_t hs, int64_t mn_
 template <int BN, bool AMN, bool BMN, bool ROW>
 int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M,
          int N, int K, int nb, int nh, const char* name) {
-  SGemm<BN, AMN, BMN, ROW> g{p.lane_dev, A, B, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
-  dim3 grid((M + GEMM_BM - 1) / GEMM_BM, (N + BN - 1) / BN, p.lanes * nb * nh);
-  TLK_CUDA(launch_gemm(g, grid, st));
+  using G = TGemm<BN, AMN, BMN, ROW>;
+  G g{};
+  g.g = SGemm<BN, AMN, BMN, ROW>{p.lane_dev, A, B, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
+  int rc = make_operand_map(&g.ta, A, AMN, GEMM_BM, p.lanes, nb, nh);
+  if (!rc) rc = make_operand_map(&g.tb, B, BMN, BN, p.lanes, nb, nh);
+  if (rc) return rc;
+  g.mt = (M + GEMM_BM - 1) / GEMM_BM;
+  g.nt = (N + BN - 1) / BN;
+  g.ntiles = g.mt * g.nt * p.lanes * nb * nh;
+  const int sms = static_cast<const GptBufs*>(p.scratch)->sms;
+  TLK_CUDA(launch_tgemm(g, sms, st));
   const_cast<Pack&>(p).mark(st, name);
   return TLK_OK;
 }
@@ -338,6 +347,12 @@ int gpt_setup(Pack& p) {
   p.scratch = b;
   p.scratch_free = [](void* q) { delete static_cast<GptBufs*>(q); };
   b->c = c;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    b->sms = 148;
+    cudaDeviceGetAttribute(&b->sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const int64_t L = p.lanes, N = int64_t(p.batch) * c.T, d = c.d, H = c.heads, T = c.T;
   b->N = int(N);
   b->Vp = (c.V + 31) / 32 * 32;

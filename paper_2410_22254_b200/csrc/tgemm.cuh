@@ -1,0 +1,243 @@
+// Persistent, warp-specialised grouped GEMM for the transformer packs.
+//
+//   D[z][m, n] = sum_k A[z][m, k] * B[z][n, k]      z = (lane, b, h)
+//
+// Every operand of the transformer step is a strided 5-D view of a pack
+// buffer (k or mn contiguous, then mn/k, head, sequence, lane), so one TMA
+// tensor map per operand covers all z of a launch.  The launch is persistent
+// (one CTA per SM) and walks the flattened (z, m-tile, n-tile) list:
+//
+//   warp EW     lane 0: TMA producer -> STAGES-deep smem ring (full/empty)
+//   warp EW+1   lane 0: tcgen05.mma issuer, accumulator double-buffered in
+//                       TMEM (2 x BN columns): tile i+1's mainloop runs while
+//                       the epilogue warps drain tile i
+//   warps 0..EW-1     : epilogue in two groups of 4 (one per TMEM buffer):
+//                       TMEM -> registers -> smem transpose -> coalesced
+//                       stores, or whole-row softmax / CE epilogues.
+//
+// The epilogue arithmetic is SGemm's (sgemm.cuh): the same Epi descriptor and
+// the same per-element code, so the numerics do not depend on the mainloop.
+#pragma once
+#include "sgemm.cuh"
+#include "tma.cuh"
+
+namespace tlk {
+
+template <int BN_, bool AMN, bool BMN, bool ROW>
+struct TGemm {
+  static constexpr int BN = BN_;
+  static constexpr int STAGES = BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : 3;
+  static constexpr int EW = 8;  // epilogue warps (two groups of 4 lane quarters)
+  static constexpr int THREADS = (EW + 2) * 32;
+  static constexpr bool A_MN = AMN, B_MN = BMN, ROW_EPI = ROW;
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr int B_BYTES = BN_ * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGING_BYTES = EW * 32 * 33 * 4;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024;
+  static constexpr uint32_t TCOLS = BN_ <= 64 ? 128 : BN_ <= 128 ? 256 : 512;  // 2 accumulators
+  static_assert(2 * BN_ <= 512, "two accumulators must fit TMEM");
+  static_assert(!BMN || BN_ % 64 == 0, "MN-major B is loaded in 64-wide boxes");
+
+  CUtensorMap ta, tb;
+  SGemm<BN_, AMN, BMN, ROW> g;  // epilogue functor (g.e, g.lanes)
+  int mt, nt, ntiles;
+
+  TLK_DEV bool tile(int t, ZWork& w) const {
+    const int n_t = t % nt;
+    const int r = t / nt;
+    const int m_t = r % mt;
+    const int z = r / mt, per = g.nb * g.nh;
+    w.j = z / per;
+    const int rr = z % per;
+    w.zb = rr / g.nh;
+    w.zh = rr % g.nh;
+    if (!g.lanes[w.j].active) return false;
+    w.m0 = m_t * GEMM_BM;
+    w.n0 = n_t * BN_;
+    w.kb_begin = 0;
+    w.kb_end = g.kblocks;
+    w.split = 0;
+    return true;
+  }
+  TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
+    const int k0 = kb * GEMM_BK;
+    if (!AMN) {
+      tma_load_5d(a_s, &ta, k0, w.m0, w.zh, w.zb, w.j, bar);
+    } else {
+      tma_load_5d(a_s, &ta, w.m0, k0, w.zh, w.zb, w.j, bar);
+      tma_load_5d(a_s + 8192, &ta, w.m0 + 64, k0, w.zh, w.zb, w.j, bar);
+    }
+    const uint32_t b_s = a_s + A_BYTES;
+    if (!BMN) {
+      tma_load_5d(b_s, &tb, k0, w.n0, w.zh, w.zb, w.j, bar);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BN_ / 64; ++i) tma_load_5d(b_s + i * 8192, &tb, w.n0 + 64 * i, k0, w.zh, w.zb, w.j, bar);
+    }
+  }
+};
+
+template <class P>
+__global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_constant__ P p) {
+  constexpr int BN = P::BN, STAGES = P::STAGES, EW = P::EW;
+  constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, P::A_MN, P::B_MN);
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  float* staging = reinterpret_cast<float*>(smem + STAGES * P::STAGE_BYTES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == EW) tmem_alloc<P::TCOLS>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == EW) {
+    if (lane == 0) {  // TMA producer
+      tma_prefetch_desc(&p.ta);
+      tma_prefetch_desc(&p.tb);
+      int it = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        ZWork w;
+        if (!p.tile(t, w)) continue;
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
+          mbar_expect_tx(&full_bar[s], P::STAGE_BYTES);
+          p.load(w, kb, sbase + s * P::STAGE_BYTES, &full_bar[s]);
+        }
+      }
+    }
+  } else if (warp == EW + 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        ZWork w;
+        if (!p.tile(t, w)) continue;
+        const int buf = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN;
+        for (int kb = w.kb_begin; kb < w.kb_end; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full_bar[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_s = sbase + s * P::STAGE_BYTES, b_s = a_s + P::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk)
+            mma_bf16(d, stage_desc_tma<GEMM_BM, P::A_MN>(a_s, kk), stage_desc_tma<BN, P::B_MN>(b_s, kk),
+                     IDESC, (kb > w.kb_begin || kk > 0) ? 1u : 0u);
+          mma_commit(&empty_bar[s]);
+        }
+        mma_commit(&tfull[buf]);
+        ++lt;
+      }
+    }
+  } else {  // epilogue warps: group (warp >> 2) drains TMEM buffer `group`,
+           // i.e. the CTA's even / odd local tiles, so two tiles' epilogues
+           // run concurrently (4 warps = the 4 TMEM lane quarters each)
+    const int q = warp & 3, group = warp >> 2;
+    float* buf = staging + warp * (32 * 33);
+    const int rsub = lane >> 3, c4 = (lane & 7) * 4;
+    int lt = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      ZWork w;
+      if (!p.tile(t, w)) continue;
+      const int b = lt & 1;
+      if (b != group) {
+        ++lt;
+        continue;
+      }
+      mbar_wait(&tfull[b], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tq = tmem + b * BN + (uint32_t(q * 32) << 16);
+      if constexpr (P::ROW_EPI) {
+        p.g.row_epilogue(w, w.m0 + q * 32 + lane, tq, buf, lane);
+      } else {
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          const int row0 = w.m0 + q * 32, n = w.n0 + cc * 32 + c4;
+          float4 ax[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ax[k] = p.g.aux4(w, row0 + 4 * k + rsub, n);
+          float v[32];
+          tmem_ld32(tq + cc * 32, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float* x = buf + (4 * k + rsub) * 33 + c4;
+            p.g.epilogue4(w, row0 + 4 * k + rsub, n, x[0], x[1], x[2], x[3], ax[k]);
+          }
+          __syncwarp();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      ++lt;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == EW) tmem_dealloc<P::TCOLS>(tmem);
+}
+
+// Host: 5-D tensor map of a strided operand.  K-major: dims {K, MN, h, b,
+// lane}, box {64, rows}; MN-major: dims {MN, K, h, b, lane}, box {64, 64}.
+inline int make_operand_map(CUtensorMap* m, const Operand& o, bool mn_major, int box_rows, int lanes,
+                            int nb, int nh) {
+  uint64_t dims[5], st[4];
+  if (!mn_major) {
+    TLK_CHECK(o.k_st == 1, TLK_EINVAL, "K-major operand must have unit k stride");
+    dims[0] = uint64_t(o.K);
+    dims[1] = uint64_t(o.MN);
+    st[0] = uint64_t(o.mn_st) * 2;
+  } else {
+    TLK_CHECK(o.mn_st == 1, TLK_EINVAL, "MN-major operand must have unit mn stride");
+    dims[0] = uint64_t(o.MN);
+    dims[1] = uint64_t(o.K);
+    st[0] = uint64_t(o.k_st) * 2;
+    box_rows = 64;
+  }
+  dims[2] = uint64_t(nh);
+  dims[3] = uint64_t(nb);
+  dims[4] = uint64_t(lanes);
+  st[1] = uint64_t(o.hs) * 2;
+  st[2] = uint64_t(o.bs) * 2;
+  st[3] = uint64_t(o.ls) * 2;
+  return make_tmap_bf16_5d(m, o.base, dims, st, 64, uint32_t(box_rows));
+}
+
+template <class P>
+inline cudaError_t launch_tgemm(const P& p, int sms, cudaStream_t stream) {
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tgemm_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         P::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int grid = std::max(1, std::min(p.ntiles, sms));
+  tgemm_kernel<P><<<grid, P::THREADS, P::SMEM_BYTES, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tlk

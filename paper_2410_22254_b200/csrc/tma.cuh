@@ -16,6 +16,12 @@ namespace tlk {
 int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1);
 
+// bf16 5-D tensor (dims[0] contiguous, byte strides of dims 1..4) -> tensor
+// map with box {b0, b1, 1, 1, 1}, 128-byte swizzle.  Size-1 dims may pass
+// any stride (it is replaced by a valid one).
+int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5],
+                      const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1);
+
 TLK_DEV void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -27,6 +33,16 @@ TLK_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+TLK_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
+                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
       : "memory");
 }
 

@@ -223,10 +223,11 @@ class Pack:
     def profile_step(self, iters: int = 5):
         """[(kernel name, mean ms)] for one step, measured with CUDA events on
         the context stream (un-graphed; advances the lanes by `iters` steps)."""
-        ms = (C.c_float * 64)()
-        names = C.create_string_buffer(4096)
+        cap, nlen = 1024, 32768
+        ms = (C.c_float * cap)()
+        names = C.create_string_buffer(nlen)
         n = C.c_int32()
-        check(lib().tlk_profile_step(self.ctx._ctx, self.id, int(iters), ms, names, 4096, 64,
+        check(lib().tlk_profile_step(self.ctx._ctx, self.id, int(iters), ms, names, nlen, cap,
                                      C.byref(n)))
         labels = names.value.decode().split(",")
         return [(labels[k], float(ms[k])) for k in range(n.value)]
