@@ -25,7 +25,8 @@ shadow), LayerNorm outputs, q/k/v, attention probabilities, attention
 outputs, GELU outputs, and every gradient fed to a GEMM; the residual stream
 and its gradient, softmax / LayerNorm statistics, the logits and the GEMM
 outputs consumed by LayerNorm backward stay fp32.  The attention backward
-uses the stored bf16 probabilities (ds = P (dP - rowsum(P dP)) / sqrt(dh)).
+uses the stored bf16 probabilities (ds = P (dP - D) / sqrt(dh), with
+D = rowsum(dY o Y), equal to rowsum(P o dP) in exact arithmetic).
 """
 
 from __future__ import annotations
@@ -242,7 +243,12 @@ def gpt_step(cfg: GptCfg, p: dict, toks: np.ndarray, bf16: bool = True):
         dy = _r(dxb @ wo, bf16).reshape(B, T, H, dh).transpose(0, 2, 1, 3)
         dp = dy @ v.transpose(0, 1, 3, 2)                               # [B,H,T,T]
         dv = _r(pb.transpose(0, 1, 3, 2) @ dy, bf16)
-        rowdot = (dp * pb).sum(axis=-1, keepdims=True)
+        # D = rowsum(P o dP) = rowsum(dY o Y) (the FlashAttention identity,
+        # exact in real arithmetic); formed from the stored bf16 dY and Y, a
+        # 64-wide dot product instead of a T-wide one (csrc/gpt.cu
+        # attn_rowdot_kernel)
+        yb = yf.reshape(B, T, H, dh).transpose(0, 2, 1, 3)
+        rowdot = (dy * yb).sum(axis=-1, keepdims=True)
         ds = _r(pb * (dp - rowdot) * scale, bf16)
         dq = _r(ds @ k, bf16)
         dk = _r(ds.transpose(0, 1, 3, 2) @ q, bf16)

@@ -41,7 +41,7 @@ struct GptBufs {
   float *xL, *stf, *lossrow;
   uint16_t *xf, *dl;
   // backward scratch (shared by all layers)
-  float *dx, *dmm, *dS_f;  // dS_f unused
+  float *dx, *dmm, *D;  // D: softmax-backward row terms [lane][b][h][t]
   uint16_t *dxb, *dz, *dy, *dS, *dqkv;
   float* part;      // reduction partials
   int64_t part_st;  // floats per lane
@@ -128,39 +128,75 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LaneState* __restrict
 //   dxh = dy g; dx = (dxh - mean(dxh) - xh mean(dxh xh)) rstd
 //   dxt (fp32 residual grad) = (accumulate ? dxt : 0) + dx; dxb = bf16(dxt)
 //   part[lane][blk][0:d] = sum_rows dy xh, part[..][d:2d] = sum_rows dy (fixed order)
+// Lane l of a warp owns the float4 columns 4*(l + 32k), k < KV (d = 128 KV);
+// the next row's x / dy / dxt are fetched before the current row is reduced,
+// so every warp keeps two rows of loads in flight.
 constexpr int LNB_ROWS = 64;
+template <int KV>
+struct LnRow {
+  float4 x[KV], dy[KV], acc[KV];
+  float mu, rstd;
+};
+template <int KV>
+TLK_DEV void ln_row_load(LnRow<KV>& r, const float* x, const float* dy, const float* dxt, const float* stats,
+                         int64_t ro, int64_t so, int lane, bool acc) {
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int i = 4 * (lane + 32 * k);
+    r.x[k] = *reinterpret_cast<const float4*>(x + ro + i);
+    r.dy[k] = *reinterpret_cast<const float4*>(dy + ro + i);
+    r.acc[k] = acc ? *reinterpret_cast<const float4*>(dxt + ro + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  r.mu = stats[so];
+  r.rstd = stats[so + 1];
+}
+template <int KV>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(
-    const LaneState* __restrict__ lanes, int N, int d, const float* __restrict__ dy,
+    const LaneState* __restrict__ lanes, int N, const float* __restrict__ dy,
     const float* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ params,
     int64_t pstride, int64_t og, float* __restrict__ dxt, uint16_t* __restrict__ dxb, int accumulate,
     float* __restrict__ part, int64_t part_st) {
+  constexpr int d = 128 * KV;
   const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
   extern __shared__ float red[];  // [8][2][d]
-  constexpr int MAXC = 16;        // d <= 512
-  float ag[MAXC], ab[MAXC];
+  float4 g[KV], ag[KV], ab[KV];
+  const float* gp = params + j * pstride + og;
 #pragma unroll
-  for (int k = 0; k < MAXC; ++k) ag[k] = ab[k] = 0.f;
-  const float* g = params + j * pstride + og;
-  for (int r = 0; r < LNB_ROWS / 8; ++r) {
-    const int row = blockIdx.x * LNB_ROWS + warp * (LNB_ROWS / 8) + r;
-    if (row >= N) break;
+  for (int k = 0; k < KV; ++k) {
+    const int i = 4 * (lane + 32 * k);
+    g[k] = make_float4(gp[i], gp[i + 1], gp[i + 2], gp[i + 3]);
+    ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int row0 = blockIdx.x * LNB_ROWS + warp * (LNB_ROWS / 8);
+  const int nrows = max(0, min(LNB_ROWS / 8, N - row0));
+  LnRow<KV> cur, nxt;
+  if (nrows > 0)
+    ln_row_load(cur, x, dy, dxt, stats, (int64_t(j) * N + row0) * d, (int64_t(j) * N + row0) * 2, lane,
+                accumulate);
+  for (int r = 0; r < nrows; ++r) {
+    const int row = row0 + r;
     const int64_t ro = (int64_t(j) * N + row) * d;
-    const float mu = stats[(int64_t(j) * N + row) * 2], rstd = stats[(int64_t(j) * N + row) * 2 + 1];
-    float xh[MAXC], dyv[MAXC];
+    if (r + 1 < nrows)
+      ln_row_load(nxt, x, dy, dxt, stats, ro + d, (int64_t(j) * N + row + 1) * 2, lane, accumulate);
+    float4 xh[KV];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < MAXC; ++k) {
-      const int i = lane + 32 * k;
-      if (i < d) {
-        xh[k] = (x[ro + i] - mu) * rstd;
-        dyv[k] = dy[ro + i];
-        const float dxh = dyv[k] * g[i];
-        s1 += dxh;
-        s2 += dxh * xh[k];
-        ag[k] += dyv[k] * xh[k];
-        ab[k] += dyv[k];
-      }
+    for (int k = 0; k < KV; ++k) {
+      xh[k] = make_float4((cur.x[k].x - cur.mu) * cur.rstd, (cur.x[k].y - cur.mu) * cur.rstd,
+                          (cur.x[k].z - cur.mu) * cur.rstd, (cur.x[k].w - cur.mu) * cur.rstd);
+      const float4 dv = cur.dy[k];
+      const float h0 = dv.x * g[k].x, h1 = dv.y * g[k].y, h2 = dv.z * g[k].z, h3 = dv.w * g[k].w;
+      s1 += h0 + h1 + h2 + h3;
+      s2 += h0 * xh[k].x + h1 * xh[k].y + h2 * xh[k].z + h3 * xh[k].w;
+      ag[k].x += dv.x * xh[k].x;
+      ag[k].y += dv.y * xh[k].y;
+      ag[k].z += dv.z * xh[k].z;
+      ag[k].w += dv.w * xh[k].w;
+      ab[k].x += dv.x;
+      ab[k].y += dv.y;
+      ab[k].z += dv.z;
+      ab[k].w += dv.w;
     }
     for (int o = 16; o; o >>= 1) {
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -168,23 +204,23 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     }
     const float m1 = s1 / float(d), m2 = s2 / float(d);
 #pragma unroll
-    for (int k = 0; k < MAXC; ++k) {
-      const int i = lane + 32 * k;
-      if (i < d) {
-        const float dxv = (dyv[k] * g[i] - m1 - xh[k] * m2) * rstd;
-        const float t = accumulate ? dxt[ro + i] + dxv : dxv;
-        dxt[ro + i] = t;
-        dxb[ro + i] = f2bf(t);
-      }
+    for (int k = 0; k < KV; ++k) {
+      const int i = 4 * (lane + 32 * k);
+      const float4 dv = cur.dy[k], a = cur.acc[k];
+      const float t0 = a.x + (dv.x * g[k].x - m1 - xh[k].x * m2) * cur.rstd;
+      const float t1 = a.y + (dv.y * g[k].y - m1 - xh[k].y * m2) * cur.rstd;
+      const float t2 = a.z + (dv.z * g[k].z - m1 - xh[k].z * m2) * cur.rstd;
+      const float t3 = a.w + (dv.w * g[k].w - m1 - xh[k].w * m2) * cur.rstd;
+      *reinterpret_cast<float4*>(dxt + ro + i) = make_float4(t0, t1, t2, t3);
+      *reinterpret_cast<uint2*>(dxb + ro + i) = make_uint2(pack_bf2(t0, t1), pack_bf2(t2, t3));
     }
+    cur = nxt;
   }
 #pragma unroll
-  for (int k = 0; k < MAXC; ++k) {
-    const int i = lane + 32 * k;
-    if (i < d) {
-      red[(warp * 2) * d + i] = ag[k];
-      red[(warp * 2 + 1) * d + i] = ab[k];
-    }
+  for (int k = 0; k < KV; ++k) {
+    const int i = 4 * (lane + 32 * k);
+    *reinterpret_cast<float4*>(red + (warp * 2) * d + i) = ag[k];
+    *reinterpret_cast<float4*>(red + (warp * 2 + 1) * d + i) = ab[k];
   }
   __syncthreads();
   float* out = part + j * part_st + int64_t(blockIdx.x) * 2 * d;
@@ -196,19 +232,60 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   }
 }
 
+// D[lane][b][h][t] = sum_c dY[t][h*64 + c] Y[t][h*64 + c] (bf16 inputs, fp32,
+// c in order): the softmax-backward row term rowsum(P o dP) via the identity
+// rowsum(P o dP) = rowsum(dY o Y).  One thread per (token, head).
+__global__ void attn_rowdot_kernel(const LaneState* __restrict__ lanes, int N, int T, int H,
+                                   const uint16_t* __restrict__ dy, const uint16_t* __restrict__ y,
+                                   float* __restrict__ D) {
+  const int j = blockIdx.y;
+  if (!lanes[j].active) return;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // token * H + h
+  if (idx >= N * H) return;
+  const int n = idx / H, h = idx % H, d = H * 64;
+  const int64_t o = (int64_t(j) * N + n) * d + h * 64;
+  const uint4* a = reinterpret_cast<const uint4*>(dy + o);
+  const uint4* b = reinterpret_cast<const uint4*>(y + o);
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 u = a[q], v = b[q];
+    const uint32_t uu[4] = {u.x, u.y, u.z, u.w}, vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s += __uint_as_float(uu[e] << 16) * __uint_as_float(vv[e] << 16);
+      s += __uint_as_float(uu[e] & 0xffff0000u) * __uint_as_float(vv[e] & 0xffff0000u);
+    }
+  }
+  const int bi = n / T, t = n % T;
+  D[((int64_t(j) * (N / T) + bi) * H + h) * T + t] = s;
+}
+
 // ------------------------------------------------------------- reductions --
-// part[lane][blk][c] = sum over rows [blk*128, blk*128+128) of src[row][c] (bf16)
-constexpr int CS_ROWS = 128;
+// part[lane][blk][c] = sum over rows [blk*64, blk*64+64) of src[row][c] (bf16);
+// a thread owns 8 consecutive columns (one 16-byte load per row)
+constexpr int CS_ROWS = 64;
 __global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const uint16_t* __restrict__ src,
                                    int64_t src_ls, int ld, int N, int C, float* __restrict__ part,
                                    int64_t part_st) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
-  if (!lanes[j].active || c >= C) return;
-  const uint16_t* s = src + j * src_ls + int64_t(blk) * CS_ROWS * ld + c;
-  float acc = 0.f;
+  const int cg = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
+  if (!lanes[j].active || cg * 8 >= C) return;
+  const uint16_t* s = src + j * src_ls + int64_t(blk) * CS_ROWS * ld + cg * 8;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int rows = min(CS_ROWS, N - blk * CS_ROWS);
-  for (int r = 0; r < rows; ++r) acc += bf2f(s[int64_t(r) * ld]);
-  part[j * part_st + int64_t(blk) * C + c] = acc;
+#pragma unroll 8
+  for (int r = 0; r < rows; ++r) {
+    const uint4 u = *reinterpret_cast<const uint4*>(s + int64_t(r) * ld);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc[2 * e] += __uint_as_float(w[e] << 16);
+      acc[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+    }
+  }
+  float* o = part + j * part_st + int64_t(blk) * C + cg * 8;
+  *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
 }
 
 // dst0[c] (c < split) / dst1[c - split] = sum_blk part[lane][blk][c], fixed order
@@ -300,7 +377,12 @@ int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, con
          int N, int K, int nb, int nh, const char* name) {
   using G = TGemm<BN, AMN, BMN, ROW>;
   G g{};
-  g.g = SGemm<BN, AMN, BMN, ROW>{p.lane_dev, A, B, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
+  g.g = EpiOps{p.lane_dev, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
+  // vector-epilogue contract (sgemm.cuh): 4-element aligned rows and z strides
+  TLK_CHECK(e.ld % 4 == 0 && e.ls % 4 == 0 && e.bs % 4 == 0 && e.hs % 4 == 0 &&
+                (ROW || e.cols % 4 == 0) && (reinterpret_cast<uintptr_t>(e.out) & 15) == 0,
+            TLK_EINVAL, "%s: epilogue layout not 4-element aligned", name);
+  TLK_CHECK(!ROW || N <= BN, TLK_EINVAL, "%s: row epilogue needs the whole row in one tile", name);
   int rc = make_operand_map(&g.ta, A, AMN, GEMM_BM, p.lanes, nb, nh);
   if (!rc) rc = make_operand_map(&g.tb, B, BMN, BN, p.lanes, nb, nh);
   if (rc) return rc;
@@ -392,6 +474,7 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dy), L * N * d * 2);
   add(reinterpret_cast<void**>(&b->dS), L * p.batch * H * T * T * 2);
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
+  add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
   // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
   const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d, N / EMB_ROWS * c.V * d});
   b->part_st = ps;
@@ -558,8 +641,26 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   auto ln_bwd = [&](const float* dy, const float* x, const float* stats, int og, int ob, int accumulate,
                     const char* name) -> int {
     const int nblk = (N + LNB_ROWS - 1) / LNB_ROWS;
-    ln_bwd_kernel<<<dim3(nblk, Lc), 256, 16 * d * 4, st>>>(LS, N, d, dy, x, stats, PR, PS, O(og), b.dx,
-                                                          b.dxb, accumulate, b.part, b.part_st);
+    const dim3 grid(nblk, Lc);
+    const size_t sm = 16 * size_t(d) * 4;
+    switch (d / 128) {
+      case 1:
+        ln_bwd_kernel<1><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st);
+        break;
+      case 2:
+        ln_bwd_kernel<2><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st);
+        break;
+      case 3:
+        ln_bwd_kernel<3><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st);
+        break;
+      default:
+        ln_bwd_kernel<4><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st);
+        break;
+    }
     TLK_CUDA(cudaGetLastError());
     marked(name);
     reduce_parts_kernel<<<dim3((2 * d + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, 2 * d,
@@ -570,8 +671,9 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   };
   auto bias_grad = [&](const uint16_t* src, int C, int t) -> int {
     const int nblk = (N + CS_ROWS - 1) / CS_ROWS;
-    colsum_bf16_kernel<<<dim3((C + 255) / 256, nblk, Lc), 256, 0, st>>>(LS, src, int64_t(N) * C, C, N, C,
-                                                                        b.part, b.part_st);
+    const int cgs = C / 8, th = std::min(128, (cgs + 31) / 32 * 32);
+    colsum_bf16_kernel<<<dim3((cgs + th - 1) / th, nblk, Lc), th, 0, st>>>(LS, src, int64_t(N) * C, C, N, C,
+                                                                          b.part, b.part_st);
     TLK_CUDA(cudaGetLastError());
     marked("bias_colsum");
     reduce_parts_kernel<<<dim3((C + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, C, G, PS,
@@ -622,9 +724,16 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       count += 2;
     }
     {  // attention backward per (sequence, head)
+      attn_rowdot_kernel<<<dim3((N * H + 255) / 256, Lc), 256, 0, st>>>(LS, N, T, H, b.dy, lb.y, b.D);
+      TLK_CUDA(cudaGetLastError());
+      marked("attn_rowdot");
       Epi e = epi(EPI_SOFTMAX_BWD, T, T, b.dS, pl, int64_t(H) * tt, tt, T);
       e.aux = lb.P;
       e.scale = scale;
+      e.rowvec = b.D;
+      e.rv_ls = int64_t(N) * H;
+      e.rv_bs = int64_t(H) * T;
+      e.rv_hs = T;
       const Operand A = op(b.dy, nd, int64_t(T) * d, dh, d, 1, T, dh);
       const Operand Bv = op(lb.qkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 3 * d, 1, T, dh);
       if (T == 256)

@@ -80,59 +80,11 @@ struct GemmThreads {  // problems may ask for 256 threads (extra epilogue warps)
 // Epilogue shared by both mainloops: TMEM -> registers -> problem functor
 // (per-row chunks), or -> shared fp32 tile -> problem tile functor.
 template <class P>
-struct RowEpi {  // problems may define ROW_EPILOGUE (functor reads TMEM itself)
-  template <class Q>
-  static constexpr bool get(decltype(Q::ROW_EPILOGUE)*) { return Q::ROW_EPILOGUE; }
-  template <class Q>
-  static constexpr bool get(...) { return false; }
-  static constexpr bool value = get<P>(nullptr);
-};
-
-template <class P>
-struct Epi4 {  // problems may define EPILOGUE4 (coalesced 4-column callbacks)
-  template <class Q>
-  static constexpr bool get(decltype(Q::EPILOGUE4)*) { return Q::EPILOGUE4; }
-  template <class Q>
-  static constexpr bool get(...) { return false; }
-  static constexpr bool value = get<P>(nullptr);
-};
-
-template <class P>
 TLK_DEV void gemm_epilogue(const P& p, const typename P::Work& w, uint32_t tmem, uint8_t* smem) {
   constexpr int BN = P::BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row = warp * 32 + lane;
-  if constexpr (RowEpi<P>::value) {
-    // whole-row epilogues (softmax, cross-entropy): the functor walks its
-    // row's TMEM columns as often as it needs (warp-uniform control flow)
-    if (warp < 4)
-      p.row_epilogue(w, w.m0 + row, tmem + (uint32_t(warp * 32) << 16),
-                     reinterpret_cast<float*>(smem) + warp * (32 * 33), lane);
-  } else if constexpr (Epi4<P>::value) {
-    // TMEM hands each thread one ROW; global stores want a warp to cover whole
-    // rows.  Transpose every 32x32 chunk through a per-warp smem buffer (row
-    // pitch 33: conflict-free both ways) and call the problem with 4
-    // consecutive columns per lane -> a warp stores 4 full row segments.
-    if (warp < 4) {
-      float* buf = reinterpret_cast<float*>(smem) + warp * (32 * 33);
-      const int rsub = lane >> 3, c4 = (lane & 7) * 4;
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + cc * 32, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
-        __syncwarp();
-#pragma unroll 2
-        for (int r0 = 0; r0 < 32; r0 += 4) {
-          const float* q = buf + (r0 + rsub) * 33 + c4;
-          const int m = w.m0 + warp * 32 + r0 + rsub, n = w.n0 + cc * 32 + c4;
-          p.epilogue4(w, m, n, q[0], q[1], q[2], q[3], p.aux4(w, m, n));
-        }
-        __syncwarp();
-      }
-    }
-  } else if constexpr (P::TILE_EPILOGUE) {
+  if constexpr (P::TILE_EPILOGUE) {
     static_assert(GEMM_BM * (BN + 4) * 4 <= P::STAGES * GemmSmem<P>::STAGE_BYTES, "tile fits");
     float* tile = reinterpret_cast<float*>(smem);
     if (warp < 4) {

@@ -15,8 +15,8 @@
 //                       TMEM -> registers -> smem transpose -> coalesced
 //                       stores, or whole-row softmax / CE epilogues.
 //
-// The epilogue arithmetic is SGemm's (sgemm.cuh): the same Epi descriptor and
-// the same per-element code, so the numerics do not depend on the mainloop.
+// The epilogues (bias / GELU / residual / softmax / softmax-backward / CE)
+// are EpiOps (sgemm.cuh), resolved once per tile from the launch's Epi kind.
 #pragma once
 #include "sgemm.cuh"
 #include "tma.cuh"
@@ -40,7 +40,7 @@ struct TGemm {
   static_assert(!BMN || BN_ % 64 == 0, "MN-major B is loaded in 64-wide boxes");
 
   CUtensorMap ta, tb;
-  SGemm<BN_, AMN, BMN, ROW> g;  // epilogue functor (g.e, g.lanes)
+  EpiOps g;  // epilogue state (g.e, g.lanes, z decomposition)
   int mt, nt, ntiles;
 
   TLK_DEV bool tile(int t, ZWork& w) const {
@@ -154,7 +154,6 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
            // run concurrently (4 warps = the 4 TMEM lane quarters each)
     const int q = warp & 3, group = warp >> 2;
     float* buf = staging + warp * (32 * 33);
-    const int rsub = lane >> 3, c4 = (lane & 7) * 4;
     int lt = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       ZWork w;
@@ -167,28 +166,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       mbar_wait(&tfull[b], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t tq = tmem + b * BN + (uint32_t(q * 32) << 16);
-      if constexpr (P::ROW_EPI) {
-        p.g.row_epilogue(w, w.m0 + q * 32 + lane, tq, buf, lane);
-      } else {
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          const int row0 = w.m0 + q * 32, n = w.n0 + cc * 32 + c4;
-          float4 ax[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) ax[k] = p.g.aux4(w, row0 + 4 * k + rsub, n);
-          float v[32];
-          tmem_ld32(tq + cc * 32, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
-          __syncwarp();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float* x = buf + (4 * k + rsub) * 33 + c4;
-            p.g.epilogue4(w, row0 + 4 * k + rsub, n, x[0], x[1], x[2], x[3], ax[k]);
-          }
-          __syncwarp();
-        }
-      }
+      p.g.template tile<BN>(w, tq, w.m0 + q * 32, buf, lane, P::ROW_EPI);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
