@@ -7,10 +7,13 @@ the paper's LeNet/ResNet jobs (executor.py:105-141).  This is
 a BASELINE, not product code: bench.py launches K copies through
 paper_2410_22254_b200.run_plan (subprocess backend == reference mechanism).
 
-Timing: every process trains until wall-clock ``--t0`` (warm-up: imports,
-CUDA context, cuDNN autotune), then counts completed steps (``loss.item()``
-per step, as a logging training loop does) during [t0, t0 + duration].  The
-aggregate is sum(steps * batch) / duration over the K processes.
+Timing: every process warms up (imports, CUDA context, cuDNN autotune, at
+least 3 steps), then announces itself in ``--sync-dir`` and keeps stepping
+until all ``--procs`` processes are ready; the common window starts 1 s after
+the last announcement (or at wall-clock ``--t0`` without a sync dir).  Each
+process counts completed steps (``loss.item()`` per step, as a logging
+training loop does) during [start, start + duration].  The aggregate is
+sum(steps * batch) / duration over the K processes.
 """
 
 from __future__ import annotations
@@ -86,7 +89,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--lr", type=float, default=1e-3)
-    ap.add_argument("--t0", type=float, required=True, help="wall-clock start of the timed window")
+    ap.add_argument("--t0", type=float, default=0.0, help="wall-clock start of the timed window")
+    ap.add_argument("--sync-dir", default="", help="rendezvous directory (start when all are warm)")
+    ap.add_argument("--procs", type=int, default=1)
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--bf16", type=int, default=None,
                     help="1: torch.autocast(bfloat16); default 1 for the transformer models")
@@ -120,10 +125,29 @@ def main():
         return loss.item()
 
     warm = 0
-    while time.time() < a.t0 or warm < 3:
+    while warm < 3 or (not a.sync_dir and time.time() < a.t0):
         step()
         warm += 1
-    if time.time() > a.t0 + 0.5 * a.duration:
+    if a.sync_dir:
+        import glob
+        import os
+        open(os.path.join(a.sync_dir, f"ready_{a.seed}"), "w").close()
+        deadline = time.time() + 900
+        while True:
+            ready = glob.glob(os.path.join(a.sync_dir, "ready_*"))
+            if len(ready) >= a.procs:
+                t0 = max(os.path.getmtime(p) for p in ready) + 1.0
+                break
+            if time.time() > deadline:
+                print(json.dumps({"error": "rendezvous timed out", "ready": len(ready)}))
+                return 3
+            step()
+            warm += 1
+        while time.time() < t0:
+            step()
+            warm += 1
+        a.t0 = t0
+    elif time.time() > a.t0 + 0.5 * a.duration:
         print(json.dumps({"error": "warm-up overran the timed window", "warm": warm}))
         return 3
     start = time.time()

@@ -162,9 +162,20 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- roofline ----
 def kernel_work(name, info, lanes, batch):
-    """(bound, algorithmic units per launch) for a CNN-pack kernel; units are
-    FLOPs for tensor-bound kernels and bytes for HBM-bound ones."""
+    """(bound, algorithmic units per launch) for an MLP/CNN-pack kernel; units
+    are FLOPs for tensor-bound kernels and bytes for HBM-bound ones."""
     B, L = batch, lanes
+    if MODEL == "mlp":
+        return {
+            "fc1_fwd": ("tensor", 2.0 * B * 784 * 512 * L),
+            "fc2_fwd": ("tensor", 2.0 * B * 512 * 512 * L),
+            "fc2_wgrad": ("tensor", 2.0 * B * 512 * 512 * L),
+            "fc2_dgrad": ("tensor", 2.0 * B * 512 * 512 * L),
+            "fc1_wgrad": ("tensor", 2.0 * B * 784 * 512 * L),
+            "optimizer": ("hbm", 30.0 * info.param_count * L),
+            "inputs": ("hbm", L * B * (784 + 784 * 2 + 4)),
+            "head": ("hbm", L * B * 512 * 2),
+        }.get(name, ("hbm", 0.0))
     conv2_flops = 2.0 * B * 576 * 64 * 288 * L
     fc1_flops = 2.0 * B * 9216 * 128 * L
     act = {
@@ -258,11 +269,11 @@ def cpu_oracle_rate(steps, warmup, jobs=None):
 
 def kproc_rate(jobs=None, duration=10.0, lead=35.0):
     jobs = JOBS_PER_GPU if jobs is None else jobs
-    t0 = time.time() + lead
+    sync = tempfile.mkdtemp(prefix="tlk_kproc_")
     argvs = [[sys.executable, os.path.join(ROOT, "baselines", "kproc_torch.py"), "--model", MODEL,
-              "--seed", str(i), "--batch", str(BATCH), "--t0", f"{t0:.3f}",
+              "--seed", str(i), "--batch", str(BATCH), "--sync-dir", sync, "--procs", str(jobs),
               "--duration", str(duration)] for i in range(jobs)]
-    report, outs = run_tasks_via_run_plan(argvs, 1, timeout=lead + duration + 120)
+    report, outs = run_tasks_via_run_plan(argvs, 1, timeout=lead + duration + 600)
     rates = [o.get("samples_per_s") for o in outs]
     if any(r is None for r in rates):
         return None, outs
@@ -289,7 +300,7 @@ def reference_arm(a, world, rank):
         "config": {"workload": WORKLOAD, "jobs": JOBS_PER_GPU, "batch_per_job": BATCH,
                    "optimizer": "adam", "path": "oracle/ numpy jobs via run_plan (CPU)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{JOBS_PER_GPU} CNN jobs x {timed} timed steps (+{warm} warm-up), "
+                         "sample": f"{JOBS_PER_GPU} {MODEL.upper()} jobs x {timed} timed steps (+{warm} warm-up), "
                                    f"bs {BATCH}, concurrent processes via run_plan, "
                                    f"OMP_NUM_THREADS={max(1, (os.cpu_count() or 1) // JOBS_PER_GPU)}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -379,7 +390,7 @@ def packed_arm(a, world, rank, local):
                 "algorithmic_per_launch": work, "ms_per_launch": top_ms,
                 "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
     try:  # dram bytes of this kernel from the committed ncu --set full capture
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(top_name)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(MODEL, {}).get(top_name)
         if tr:
             roof["traffic"] = tr["dram_bytes"]
             roof["traffic_source"] = tr["source"]
@@ -457,14 +468,16 @@ def packed_arm(a, world, rank, local):
         cpu, cores, _ = cpu_oracle_rate(2, 1)
         line["cpu_baseline"] = {
             "value": cpu, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{JOBS_PER_GPU} CNN jobs x 2 timed steps (+1 warm-up), bs {BATCH}, numpy oracle, "
+            "sample": f"{JOBS_PER_GPU} {MODEL.upper()} jobs x 2 timed steps (+1 warm-up), bs {BATCH}, numpy oracle, "
                       f"concurrent processes via run_plan"}
         kp, outs = kproc_rate(JOBS_PER_GPU, duration=a.kproc_seconds)
         line["kproc_baseline"] = {
             "value": kp, "unit": UNIT, "procs": JOBS_PER_GPU,
-            "mechanism": "8 PyTorch (fp32, cudnn) processes pinned to one GPU via run_plan, time-sliced",
+            "mechanism": f"{JOBS_PER_GPU} PyTorch (fp32, cudnn) processes pinned to one GPU via run_plan, "
+                         "time-sliced",
             "packed_over_kproc": (value / kp) if kp else None,
-            "packed_e2e_over_kproc": (e2e_value / kp) if kp else None}
+            "packed_e2e_over_kproc": (e2e_value / kp) if kp else None,
+            "errors": [o for o in outs if "error" in o][:2]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -492,7 +505,8 @@ def _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_
         kp, outs = kproc_rate(min(lanes, 8), duration=a.kproc_seconds, lead=60.0)
         line["kproc_baseline"] = {"value": kp, "unit": "samples/s", "procs": min(lanes, 8),
                                   "mechanism": "PyTorch processes pinned to one GPU via run_plan",
-                                  "packed_over_kproc": (value / kp) if kp else None}
+                                  "packed_over_kproc": (value / kp) if kp else None,
+                                  "errors": [o for o in outs if "error" in o][:2]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

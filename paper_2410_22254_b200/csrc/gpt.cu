@@ -342,11 +342,18 @@ __global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int
   }
   __syncthreads();
   if (c < d) {
+    // 16 independent row loads in flight, then the 16 smem accumulations in
+    // position order (same order as one-at-a-time)
     const float* g = dx + int64_t(j) * N * d + c;
-    for (int i = 0; i < EMB_ROWS; ++i) {
-      const int row = blk * EMB_ROWS + i;
-      if (row >= N) break;
-      acc[tk[i] * cols + threadIdx.x] += g[int64_t(row) * d];
+    const int rows = min(EMB_ROWS, N - blk * EMB_ROWS);
+    for (int i0 = 0; i0 < rows; i0 += 16) {
+      float vals[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        vals[u] = (i0 + u < rows) ? g[int64_t(blk * EMB_ROWS + i0 + u) * d] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (i0 + u < rows) acc[tk[i0 + u] * cols + threadIdx.x] += vals[u];
     }
     float* out = part + j * part_st + int64_t(blk) * V * d + c;
     for (int v = 0; v < V; ++v) out[int64_t(v) * d] = acc[v * cols + threadIdx.x];

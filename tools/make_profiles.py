@@ -1,6 +1,6 @@
 """Turn gpurun_out/ ncu artefacts into the tracked summaries under profiles/.
 
-usage: python tools/make_profiles.py <tag>   (e.g. r1)
+usage: python tools/make_profiles.py <tag> [model]   (e.g. r1 cnn)
 writes profiles/<tag>_launches.txt, profiles/<tag>_ncu.txt, profiles/traffic.json
 """
 import collections, csv, json, os, re, sys
@@ -46,9 +46,10 @@ def launches(tag):
     print("\n".join(out))
 
 
-def full(tag):
+def full(tag, model="cnn"):
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    per_model = traffic.setdefault(model, {})
     lines = ["# ncu --set full --clock-control none, one launch per kernel (bench CNN pack, 8 lanes)"]
     for f in sorted(os.listdir(OUT)):
         if not f.endswith(".ncu-rep"):
@@ -59,7 +60,7 @@ def full(tag):
                 v, u = s.split()
                 return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             if "dram_rd" in d and "dram_wr" in d:
-                traffic[label(d["kernel"])] = {"dram_bytes": mb(d["dram_rd"]) + mb(d["dram_wr"]),
+                per_model[label(d["kernel"])] = {"dram_bytes": mb(d["dram_rd"]) + mb(d["dram_wr"]),
                                                "source": f"profiles/{tag}_ncu.txt"}
     open(os.path.join(PROF, f"{tag}_ncu.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
@@ -70,4 +71,4 @@ if __name__ == "__main__":
     tag = sys.argv[1]
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
-    full(tag)
+    full(tag, sys.argv[2] if len(sys.argv) > 2 else "cnn")
