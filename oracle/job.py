@@ -15,13 +15,15 @@ import time
 
 import numpy as np
 
-from . import gpt, models, optim, rng
+from . import gpt, models, optim, resnet, rng
 
 GPT_MODELS = {"xformer": gpt.MODEL_XFORMER, "gpt": gpt.MODEL_GPT}
+RESNET_MODELS = {"resnet18": resnet.MODEL_RESNET18}
 
 
 def add_job_args(ap: argparse.ArgumentParser) -> None:
-    ap.add_argument("--model", choices=sorted(models.MODEL_NAMES) + sorted(GPT_MODELS), default="mlp")
+    ap.add_argument("--model", choices=sorted(models.MODEL_NAMES) + sorted(GPT_MODELS) + sorted(RESNET_MODELS),
+                    default="mlp")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--batch", type=int, default=64)
@@ -77,6 +79,24 @@ def train_gpt(cfg, seed: int, steps: int, opt: optim.OptState, bf16: bool = True
     return losses, flat, per_step
 
 
+def train_resnet(seed: int, steps: int, batch: int, opt: optim.OptState, bf16: bool = True,
+                 warmup: int = 1):
+    """ResNet-18 job (oracle/resnet.py); returns (losses, final flat params, s/step)."""
+    flat = resnet.flatten(resnet.init_params(seed))
+    losses = np.zeros(steps, np.float32)
+    warmup = warmup if steps > warmup else 0
+    t0 = time.perf_counter()
+    for t in range(steps):
+        if t == warmup:
+            t0 = time.perf_counter()
+        x, y = resnet.batch(seed, t, batch)
+        loss, g = resnet.resnet_step(resnet.unflatten(flat), x, y, bf16=bf16)
+        flat = optim.step(opt, flat, resnet.flatten(g))
+        losses[t] = loss
+    per_step = (time.perf_counter() - t0) / max(1, steps - warmup)
+    return losses, flat, per_step
+
+
 def opt_from_args(a) -> optim.OptState:
     return optim.OptState(kind=optim.OPT_NAMES[a.optim], lr=a.lr, beta1=a.beta1, beta2=a.beta2,
                           eps=a.eps, weight_decay=a.wd, momentum=a.momentum)
@@ -89,7 +109,10 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=1, help="steps excluded from the timing")
     ap.add_argument("--json", action="store_true")
     a = ap.parse_args(argv)
-    if a.model in GPT_MODELS:
+    if a.model in RESNET_MODELS:
+        losses, _, per_step = train_resnet(a.seed, a.steps, a.batch, opt_from_args(a), bool(a.bf16),
+                                           warmup=a.warmup)
+    elif a.model in GPT_MODELS:
         cfg = gpt.CFGS[GPT_MODELS[a.model]]
         losses, _, per_step = train_gpt(cfg, a.seed, a.steps, opt_from_args(a), bool(a.bf16),
                                         warmup=a.warmup, batch=a.batch)

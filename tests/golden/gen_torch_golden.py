@@ -24,7 +24,7 @@ import torch.nn.functional as F
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle import gpt, models, rng  # noqa: E402
+from oracle import gpt, models, resnet, rng  # noqa: E402
 
 RUNS = [
     # name, model, batch, steps, optim, kwargs
@@ -153,6 +153,58 @@ def run_gpt(name, cfg, steps, opt, kw):
             f"{name}/sample": flat[idx], f"{name}/norms": norms}
 
 
+RESNET_RUNS = [
+    # name, batch, steps, optim, kwargs
+    ("resnet18_sgd", 16, 2, "sgd", dict(lr=0.01, momentum=0.0)),
+]
+
+
+def resnet_forward(P, x):
+    """Independent torch implementation of oracle/resnet.py's model (NCHW)."""
+    def conv(h, w, stride):
+        w = w.permute(0, 3, 1, 2)  # (co, kh, kw, ci) -> (co, ci, kh, kw)
+        return F.conv2d(h, w, stride=stride, padding=(w.shape[-1] - 1) // 2)
+
+    def bn(h, g, b):
+        return F.batch_norm(h, None, None, g, b, training=True, eps=1e-5)
+
+    h = x.permute(0, 3, 1, 2)
+    h = F.relu(bn(conv(h, P["stem.w"], 1), P["bn0.g"], P["bn0.b"]))
+    for s, (C, stride) in enumerate(resnet.STAGES):
+        for b in range(2):
+            q = f"l{s + 1}.{b}."
+            st = stride if b == 0 else 1
+            o = F.relu(bn(conv(h, P[q + "conv1.w"], st), P[q + "bn1.g"], P[q + "bn1.b"]))
+            o = bn(conv(o, P[q + "conv2.w"], 1), P[q + "bn2.g"], P[q + "bn2.b"])
+            short = bn(conv(h, P[q + "ds.w"], st), P[q + "dsbn.g"], P[q + "dsbn.b"]) if q + "ds.w" in P else h
+            h = F.relu(o + short)
+    return F.linear(h.mean(dim=(2, 3)), P["fc.w"], P["fc.b"])
+
+
+def run_resnet(name, batch, steps, opt, kw):
+    """float64: batch-statistics BN at batch 8 is ill-conditioned enough that
+    torch's own fp32 CPU path differs from fp64 by up to ~35% on some
+    gradients; the oracle (fp32, centred variance) is pinned to fp64."""
+    init = resnet.init_params(SEED)
+    P = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in init.items()}
+    o = torch.optim.SGD(list(P.values()), foreach=False, **kw)
+    losses = []
+    for t in range(steps):
+        x, y = resnet.batch(SEED, t, batch)
+        loss = F.cross_entropy(resnet_forward(P, torch.tensor(x, dtype=torch.float64)),
+                               torch.tensor(y, dtype=torch.long))
+        o.zero_grad()
+        loss.backward()
+        o.step()
+        losses.append(loss.item())
+    final = {k: v.detach().numpy().astype(np.float32) for k, v in P.items()}
+    flat = resnet.flatten(final)
+    idx = np.linspace(0, flat.size - 1, SAMPLES).astype(np.int64)
+    norms = np.array([np.linalg.norm(final[n]) for n, *_ in resnet.tensors()], np.float64)
+    return {f"{name}/losses": np.array(losses, np.float64), f"{name}/idx": idx,
+            f"{name}/sample": flat[idx], f"{name}/norms": norms}
+
+
 def main():
     torch.manual_seed(0)
     torch.set_num_threads(1)
@@ -161,6 +213,8 @@ def main():
         out.update(run(*r))
     for r in GPT_RUNS:
         out.update(run_gpt(*r))
+    for r in RESNET_RUNS:
+        out.update(run_resnet(*r))
     path = os.path.join(HERE, "torch_golden.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, {k: v.shape for k, v in out.items()})

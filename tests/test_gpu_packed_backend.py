@@ -81,3 +81,24 @@ def test_admission_oom_is_reported_and_context_survives():
         p.run(2)
         ctx.sync()
         assert p.status(0).steps_done == 2
+
+
+def test_heterogeneous_mix_config4(tmp_path):
+    """BASELINE configs[3]: MLP + CNN + 2-layer transformer jobs interleaved in
+    one task list on one GPU (here NPPN = 6, T = 12 so slots refill).  The
+    packed worker keeps one pack per (model, batch); every task succeeds and
+    each loss curve equals the same job trained alone, bit for bit."""
+    kinds = ["mlp", "cnn", "xformer"]
+    specs = [JobSpec(model=kinds[i % 3], seed=300 + i, steps=3 + (i % 3),
+                     batch=8 if kinds[i % 3] == "xformer" else 32, lr=1e-3) for i in range(12)]
+    tasks = [TaskDef(i, tuple(s.argv(sys.executable))) for i, s in enumerate(specs)]
+    plan = build_plan(tasks, TripleSpec(1, 6, 1), NodeSpec(cores=8, gpus=1, gpu_mem_mib=183359))
+    report = run_plan(plan, 0, log_dir=tmp_path, backend="packed")
+    assert report.failures == 0, [(r.task_id, r.exit_status, (tmp_path / f"task_{r.task_id}.err").read_text())
+                                  for r in report.results if r.exit_status]
+    assert report.max_observed_concurrency <= 6
+    for i, spec in enumerate(specs):
+        out = json.loads((tmp_path / f"task_{i}.out").read_text())
+        ref = _alone(spec)
+        assert out["steps"] == spec.steps
+        assert np.float32(out["first_loss"]) == ref[0] and np.float32(out["last_loss"]) == ref[-1], i

@@ -15,7 +15,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle import gpt, job, models, optim, rng
+from oracle import resnet, gpt, job, models, optim, rng
 from oracle.bf16 import round_bf16, to_bf16_bits
 
 G = np.load(os.path.join(os.path.dirname(__file__), "golden", "torch_golden.npz"))
@@ -114,3 +114,31 @@ def test_gpt_param_layout():
     # slightly different head/bias choices; this model is defined by oracle/gpt.py)
     assert gpt.layout(gpt.CFGS[gpt.MODEL_GPT])[1] == 10_795_776
     assert gpt.layout(gpt.CFGS[gpt.MODEL_XFORMER])[1] == 1_743_872
+
+
+RESNET_RUNS = [("resnet18_sgd", 16, 2, "sgd", dict(lr=0.01, momentum=0.0))]
+
+
+@pytest.mark.parametrize("run", RESNET_RUNS, ids=[r[0] for r in RESNET_RUNS])
+def test_resnet_oracle_matches_torch(run):
+    """oracle/resnet.py (fp32 mode) vs torch float64 autograd: conv / BN /
+    residual / pool / fc forward and every backward rule, 2 SGD steps."""
+    name, batch, steps, opt, kw = run
+    st = optim.OptState(kind=optim.OPT_NAMES[opt], lr=kw["lr"], momentum=kw["momentum"])
+    losses, flat, _ = job.train_resnet(11, steps, batch, st, bf16=False)
+    # reference = torch float64 (see gen_torch_golden.run_resnet); fp32 noise
+    # through batch-8 BatchNorm is amplified, hence 5e-4 on the step-2 loss
+    np.testing.assert_allclose(losses, G[f"{name}/losses"], atol=5e-4, rtol=0)
+    idx = G[f"{name}/idx"]
+    np.testing.assert_allclose(flat[idx], G[f"{name}/sample"], atol=2e-4, rtol=0)
+    params = resnet.unflatten(flat)
+    norms = [np.linalg.norm(params[n]) for n, *_ in resnet.tensors()]
+    np.testing.assert_allclose(norms, G[f"{name}/norms"], rtol=1e-4, atol=1e-4)
+
+
+def test_resnet_layout_and_data():
+    lay, count, stride = resnet.layout()
+    assert count == 11_173_962 and all(off % 64 == 0 for _, _, off in lay)   # SURVEY Appendix B
+    x, y = resnet.batch(5, 0, 16)
+    assert x.shape == (16, 32, 32, 3) and abs(float(x.mean())) < 0.05 and abs(float(x.std()) - 1) < 0.05
+    assert np.array_equal(resnet.round_bf16(x), x) and y.min() >= 0 and y.max() < 10
