@@ -40,6 +40,7 @@ extern "C" {
 #define TLK_MODEL_CNN 2 /* MNIST CNN: conv3x3(1->32) conv3x3(32->64) maxpool2 fc(9216->128) fc(128->10) */
 #define TLK_MODEL_XFORMER 3 /* 2-layer pre-LN transformer, d=256, 4 heads, T=128, byte vocab (config 4) */
 #define TLK_MODEL_GPT 4     /* tiny-GPT, 6 layers, d=384, 6 heads, T=256, vocab 65 (config 5) */
+#define TLK_MODEL_RESNET18 5 /* ResNet-18 CIFAR variant, 3x32x32 inputs, batch-stat BN (config 3) */
 
 /* optimizers */
 #define TLK_OPT_ADAM 1
@@ -84,6 +85,8 @@ typedef struct {
 /* pack flags */
 #define TLK_PACK_WRITE_ALL_GRADS 1 /* also store gradients whose optimizer update is fused
                                       into a wgrad epilogue (tests/inspection) */
+#define TLK_PACK_SNAPSHOTS 2       /* keep per-layer copies of intermediate gradients
+                                      (layer-local parity tests; ResNet packs) */
 
 typedef struct {
   int64_t param_count;   /* real parameters per job */
@@ -130,6 +133,10 @@ int tlk_lane_losses(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int32
 int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64_t n);
 /* Device pointer + size of a pack buffer (TLK_BUF_*), for zero-copy tensors. */
 int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, int64_t* bytes);
+/* Device pointer + size of a named model-internal buffer (activations, BN
+   statistics, gradient snapshots; names per model, e.g. "conv3.y"), all
+   lanes [lanes, ...].  TLK_EINVAL for unknown names. */
+int tlk_pack_named(tlk_ctx* ctx, int32_t pack, const char* name, void** dev_ptr, int64_t* bytes);
 /* Parameter layout of this pack's lanes (depends on the transformer config). */
 int tlk_pack_info(tlk_ctx* ctx, int32_t pack, tlk_model_info* out);
 /* Number of kernels one tlk_run step launches for this pack. */

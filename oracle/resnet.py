@@ -203,40 +203,40 @@ def bn_bwd(gy, y, st, gamma):
     return dy.reshape(y.shape).astype(np.float32), sgx, sg
 
 
-# --------------------------------------------------------------- the step --
-def resnet_step(params: dict, x, labels, bf16: bool = True):
-    """One forward + backward. Returns (mean CE loss, grads dict)."""
-    p = params
-    B = x.shape[0]
-    W = {n: _r(p[n], bf16) for n, _, _, _ in tensors() if n.endswith(".w") and n != "fc.w"}
-    cache = {}
+# ------------------------------------------------------------ the pieces --
+def conv_weights(p, bf16=True):
+    return {n: _r(p[n], bf16) for n, _, _, _ in tensors() if n.endswith(".w") and n != "fc.w"}
+
+
+def stem_forward(p, W, x, bf16=True):
     y0 = _r(conv_fwd(x, W["stem.w"], 1), bf16)
     st0 = bn_stats(y0)
-    a = _r(np.maximum(bn_apply(y0, st0, p["bn0.g"], p["bn0.b"]), 0), bf16)
-    cache["stem"] = (y0, st0, a)
-    cin = 64
-    for s, (C, stride) in enumerate(STAGES):
-        for b in range(2):
-            q = f"l{s + 1}.{b}."
-            st_ = stride if b == 0 else 1
-            xin = a
-            y1 = _r(conv_fwd(xin, W[q + "conv1.w"], st_), bf16)
-            s1 = bn_stats(y1)
-            a1 = _r(np.maximum(bn_apply(y1, s1, p[q + "bn1.g"], p[q + "bn1.b"]), 0), bf16)
-            y2 = _r(conv_fwd(a1, W[q + "conv2.w"], 1), bf16)
-            s2 = bn_stats(y2)
-            if b == 0 and s > 0:
-                yd = _r(conv_fwd(xin, W[q + "ds.w"], st_), bf16)
-                sd = bn_stats(yd)
-                short = bn_apply(yd, sd, p[q + "dsbn.g"], p[q + "dsbn.b"])
-            else:
-                yd = sd = None
-                short = xin
-            o = _r(np.maximum(bn_apply(y2, s2, p[q + "bn2.g"], p[q + "bn2.b"]) + short, 0), bf16)
-            cache[q] = (xin, y1, s1, a1, y2, s2, yd, sd, o)
-            a = o
-        cin = C
-    h = a.reshape(B, 16, 512).mean(axis=1, dtype=np.float32)                  # [B, 512]
+    a0 = _r(np.maximum(bn_apply(y0, st0, p["bn0.g"], p["bn0.b"]), 0), bf16)
+    return y0, st0, a0
+
+
+def block_forward(p, W, q, xin, stride, bf16=True):
+    """BasicBlock q ('l<s>.<b>.'); returns its cache (xin, y1, s1, a1, y2, s2, yd, sd, o)."""
+    y1 = _r(conv_fwd(xin, W[q + "conv1.w"], stride), bf16)
+    s1 = bn_stats(y1)
+    a1 = _r(np.maximum(bn_apply(y1, s1, p[q + "bn1.g"], p[q + "bn1.b"]), 0), bf16)
+    y2 = _r(conv_fwd(a1, W[q + "conv2.w"], 1), bf16)
+    s2 = bn_stats(y2)
+    if q + "ds.w" in W:
+        yd = _r(conv_fwd(xin, W[q + "ds.w"], stride), bf16)
+        sd = bn_stats(yd)
+        short = bn_apply(yd, sd, p[q + "dsbn.g"], p[q + "dsbn.b"])
+    else:
+        yd = sd = None
+        short = xin
+    o = _r(np.maximum(bn_apply(y2, s2, p[q + "bn2.g"], p[q + "bn2.b"]) + short, 0), bf16)
+    return (xin, y1, s1, a1, y2, s2, yd, sd, o)
+
+
+def head(p, o, labels):
+    """avg-pool + fc + mean CE -> (loss, G = dL/do fp32, {fc.w, fc.b} grads)."""
+    B = o.shape[0]
+    h = o.reshape(B, 16, 512).mean(axis=1, dtype=np.float32)
     logits = h @ p["fc.w"].T + p["fc.b"]
     lm = logits.max(axis=1, keepdims=True)
     le = np.exp(logits - lm)
@@ -245,36 +245,62 @@ def resnet_step(params: dict, x, labels, bf16: bool = True):
     dl = le / ls
     dl[np.arange(B), labels] -= np.float32(1.0)
     dl = (dl / np.float32(B)).astype(np.float32)
-    g = {"fc.w": dl.T @ h, "fc.b": dl.sum(axis=0)}
     dh = dl @ p["fc.w"]
     G = np.broadcast_to((dh / np.float32(16.0))[:, None, None, :], (B, 4, 4, 512)).astype(np.float32)
-    for s in reversed(range(len(STAGES))):
-        C, stride = STAGES[s]
-        for b in reversed(range(2)):
-            q = f"l{s + 1}.{b}."
-            st_ = stride if b == 0 else 1
-            xin, y1, s1, a1, y2, s2, yd, sd, o = cache[q]
-            go = G * (o > 0)
-            dy2, g[q + "bn2.g"], g[q + "bn2.b"] = bn_bwd(go, y2, s2, p[q + "bn2.g"])
-            dy2 = _r(dy2, bf16)
-            g[q + "conv2.w"] = conv_wgrad(dy2, a1, 3, 1)
-            da1 = conv_dgrad(dy2, W[q + "conv2.w"], 1, a1.shape[1], a1.shape[2])
-            ga1 = da1 * (a1 > 0)
-            dy1, g[q + "bn1.g"], g[q + "bn1.b"] = bn_bwd(ga1, y1, s1, p[q + "bn1.g"])
-            dy1 = _r(dy1, bf16)
-            g[q + "conv1.w"] = conv_wgrad(dy1, xin, 3, st_)
-            Gx = conv_dgrad(dy1, W[q + "conv1.w"], st_, xin.shape[1], xin.shape[2])
-            if yd is not None:
-                dyd, g[q + "dsbn.g"], g[q + "dsbn.b"] = bn_bwd(go, yd, sd, p[q + "dsbn.g"])
-                dyd = _r(dyd, bf16)
-                g[q + "ds.w"] = conv_wgrad(dyd, xin, 1, st_)
-                Gx = Gx + conv_dgrad(dyd, W[q + "ds.w"], st_, xin.shape[1], xin.shape[2])
-            else:
-                Gx = Gx + go
-            G = Gx
-    y0, st0, a0 = cache["stem"]
+    return loss, G, {"fc.w": dl.T @ h, "fc.b": dl.sum(axis=0)}
+
+
+def block_backward(p, W, q, cache, G, stride, bf16=True):
+    """G = dL/d(block output) fp32 -> (dL/d(block input) fp32, grads of the block)."""
+    xin, y1, s1, a1, y2, s2, yd, sd, o = cache
+    g = {}
+    go = G * (o > 0)
+    dy2, g[q + "bn2.g"], g[q + "bn2.b"] = bn_bwd(go, y2, s2, p[q + "bn2.g"])
+    dy2 = _r(dy2, bf16)
+    g[q + "conv2.w"] = conv_wgrad(dy2, a1, 3, 1)
+    da1 = conv_dgrad(dy2, W[q + "conv2.w"], 1, a1.shape[1], a1.shape[2])
+    ga1 = da1 * (a1 > 0)
+    dy1, g[q + "bn1.g"], g[q + "bn1.b"] = bn_bwd(ga1, y1, s1, p[q + "bn1.g"])
+    dy1 = _r(dy1, bf16)
+    g[q + "conv1.w"] = conv_wgrad(dy1, xin, 3, stride)
+    Gx = conv_dgrad(dy1, W[q + "conv1.w"], stride, xin.shape[1], xin.shape[2])
+    if yd is not None:
+        dyd, g[q + "dsbn.g"], g[q + "dsbn.b"] = bn_bwd(go, yd, sd, p[q + "dsbn.g"])
+        dyd = _r(dyd, bf16)
+        g[q + "ds.w"] = conv_wgrad(dyd, xin, 1, stride)
+        Gx = Gx + conv_dgrad(dyd, W[q + "ds.w"], stride, xin.shape[1], xin.shape[2])
+    else:
+        Gx = Gx + go
+    return Gx, g
+
+
+def stem_backward(p, x, y0, st0, a0, G, bf16=True):
+    g = {}
     g0 = G * (a0 > 0)
     dy0, g["bn0.g"], g["bn0.b"] = bn_bwd(g0, y0, st0, p["bn0.g"])
     dy0 = _r(dy0, bf16)
     g["stem.w"] = conv_wgrad(dy0, x, 3, 1)
+    return g
+
+
+def blocks():
+    """[(prefix, stride)] in forward order."""
+    return [(f"l{s + 1}.{b}.", stride if b == 0 else 1) for s, (C, stride) in enumerate(STAGES) for b in range(2)]
+
+
+# --------------------------------------------------------------- the step --
+def resnet_step(params: dict, x, labels, bf16: bool = True):
+    """One forward + backward. Returns (mean CE loss, grads dict)."""
+    p = params
+    W = conv_weights(p, bf16)
+    y0, st0, a0 = stem_forward(p, W, x, bf16)
+    caches, a = [], a0
+    for q, stride in blocks():
+        caches.append(block_forward(p, W, q, a, stride, bf16))
+        a = caches[-1][-1]
+    loss, G, g = head(p, a, labels)
+    for (q, stride), cache in reversed(list(zip(blocks(), caches))):
+        G, gb = block_backward(p, W, q, cache, G, stride, bf16)
+        g.update(gb)
+    g.update(stem_backward(p, x, y0, st0, a0, G, bf16))
     return loss, g

@@ -165,6 +165,13 @@ std::vector<TensorInfo> model_tensors(int model, const GptCfg& c) {
     add(int64_t(c.V) * d, int(d), 0);
     return out;
   }
+  if (model == TLK_MODEL_RESNET18) {
+    std::vector<std::pair<int64_t, int>> cf;
+    std::vector<int> kinds;
+    resnet_tensor_list(cf, kinds);
+    for (size_t i = 0; i < cf.size(); ++i) add(cf[i].first, cf[i].second, kinds[i]);
+    return out;
+  }
   const ModelDef* md = model_def(model);
   for (int t = 0; md && t < md->ntensors; ++t) add(md->t[t].count, md->t[t].fan_in, 0);
   return out;

@@ -2,6 +2,7 @@
 // sequence of one training step for all of them.
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -52,6 +53,14 @@ struct Pack {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int flags = 0;  // TLK_PACK_* (e.g. write every gradient for tests)
+  // named internal buffers (tlk_pack_named): activations, statistics, snapshots
+  struct Named {
+    std::string name;
+    void* ptr;
+    size_t bytes;
+  };
+  std::vector<Named> named;
+  void name_buf(const std::string& n, void* ptr, size_t bytes) { named.push_back({n, ptr, bytes}); }
   // per-kernel profiling (tlk_profile_step): an event after every launch
   std::vector<cudaEvent_t>* prof = nullptr;
   std::vector<const char*>* prof_names = nullptr;
@@ -75,6 +84,10 @@ int cnn_setup(Pack& p);
 int cnn_enqueue_step(Pack& p, cudaStream_t st);
 int gpt_setup(Pack& p);
 int gpt_enqueue_step(Pack& p, cudaStream_t st);
+int resnet_setup(Pack& p);
+int resnet_enqueue_step(Pack& p, cudaStream_t st);
+// (count, fan_in) and init kind of every ResNet-18 tensor (oracle/resnet.py order)
+void resnet_tensor_list(std::vector<std::pair<int64_t, int>>& cnt_fan, std::vector<int>& kinds);
 std::vector<TensorInfo> model_tensors(int model, const GptCfg& c);
 
 // Common kernels (kernels.cu).

@@ -82,6 +82,7 @@ int enqueue_step(Pack& p, cudaStream_t st) {
     case TLK_MODEL_CNN: return cnn_enqueue_step(p, st);
     case TLK_MODEL_XFORMER:
     case TLK_MODEL_GPT: return gpt_enqueue_step(p, st);
+    case TLK_MODEL_RESNET18: return resnet_enqueue_step(p, st);
   }
   return fail(TLK_EINVAL, "unknown model %d", p.model);
 }
@@ -125,6 +126,19 @@ static void fill_info(int model, const GptCfg& c, int batch, tlk_model_info* out
     const int64_t d = c.d, T = c.T;
     const int64_t mm = 12 * d * d * c.layers + int64_t(c.V) * d;
     out->flops_per_sample = 6 * T * (mm + int64_t(c.layers) * T * d);
+  } else if (model == TLK_MODEL_RESNET18) {  // 6 x conv/fc MACs per sample
+    int64_t macs = 32LL * 32 * 64 * 27 + 5120;
+    const int C[4] = {64, 128, 256, 512};
+    int cin = 64, res = 32;
+    for (int s = 0; s < 4; ++s)
+      for (int b = 0; b < 2; ++b) {
+        const int ci = b == 0 ? cin : C[s], ho = (b == 0 && s > 0) ? res / 2 : res;
+        macs += int64_t(ho) * ho * C[s] * 9 * ci + int64_t(ho) * ho * C[s] * 9 * C[s];
+        if (b == 0 && s > 0) macs += int64_t(ho) * ho * C[s] * ci;
+        res = ho;
+        if (b == 1) cin = C[s];
+      }
+    out->flops_per_sample = 6 * macs;
   } else {
     out->flops_per_sample = 6 * model_def(model)->macs_per_sample;
   }
@@ -132,13 +146,15 @@ static void fill_info(int model, const GptCfg& c, int batch, tlk_model_info* out
 }
 
 int tlk_model_query(int32_t model, int32_t batch, tlk_model_info* out) {
-  TLK_CHECK(out && (model_def(model) || is_gpt(model)), TLK_EINVAL, "unknown model %d", model);
+  TLK_CHECK(out && (model_def(model) || is_gpt(model) || model == TLK_MODEL_RESNET18), TLK_EINVAL,
+            "unknown model %d", model);
   fill_info(model, gpt_default(model), batch, out);
   return TLK_OK;
 }
 
 int tlk_model_tensor(int32_t model, int32_t t, int64_t* offset, int64_t* count, int32_t* fan_in) {
-  TLK_CHECK(model_def(model) || is_gpt(model), TLK_EINVAL, "unknown model %d", model);
+  TLK_CHECK(model_def(model) || is_gpt(model) || model == TLK_MODEL_RESNET18, TLK_EINVAL,
+            "unknown model %d", model);
   const auto ts = model_tensors(model, gpt_default(model));
   TLK_CHECK(t >= 0 && t < int32_t(ts.size()), TLK_EINVAL, "bad tensor %d", t);
   if (offset) *offset = ts[t].off;
@@ -196,10 +212,13 @@ int tlk_stream(tlk_ctx* ctx, void** stream) {
 int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   TLK_CHECK(ctx && desc && pack_id, TLK_EINVAL, "null argument");
   const ModelDef* d = model_def(desc->model);
-  const bool gpt = is_gpt(desc->model);
-  TLK_CHECK(d || gpt, TLK_EINVAL, "unknown model %d", desc->model);
+  const bool gpt = is_gpt(desc->model), rn = desc->model == TLK_MODEL_RESNET18;
+  TLK_CHECK(d || gpt || rn, TLK_EINVAL, "unknown model %d", desc->model);
   TLK_CHECK(desc->lanes >= 1 && desc->lanes <= 4096, TLK_EINVAL, "lanes must be 1..4096");
-  if (!gpt)
+  if (rn)
+    TLK_CHECK(desc->batch >= 8 && desc->batch <= 512 && desc->batch % 8 == 0 && !desc->host_input, TLK_EINVAL,
+              "resnet18 packs: batch a multiple of 8 in [8, 512], device-generated inputs only");
+  else if (!gpt)
     TLK_CHECK(desc->batch >= 8 && desc->batch <= 64 && desc->batch % 8 == 0, TLK_EINVAL,
               "batch must be a multiple of 8 in [8, 64] (got %d)", desc->batch);
   else
@@ -258,9 +277,10 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
     if (e != cudaSuccess) rc = cuda_fail(e, "tensor table upload");
   }
   if (!rc)
-    rc = p->model == TLK_MODEL_MLP ? mlp_setup(*p)
-         : p->model == TLK_MODEL_CNN ? cnn_setup(*p)
-                                     : gpt_setup(*p);
+    rc = p->model == TLK_MODEL_MLP        ? mlp_setup(*p)
+         : p->model == TLK_MODEL_CNN      ? cnn_setup(*p)
+         : p->model == TLK_MODEL_RESNET18 ? resnet_setup(*p)
+                                          : gpt_setup(*p);
   if (rc) {
     destroy_pack(*p);
     return rc;
@@ -413,6 +433,20 @@ int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, i
     default: return fail(TLK_EINVAL, "unknown buffer %d", which);
   }
   return TLK_OK;
+}
+
+int tlk_pack_named(tlk_ctx* ctx, int32_t pack, const char* name, void** dev_ptr, int64_t* bytes) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(name && dev_ptr && bytes, TLK_EINVAL, "null argument");
+  for (const auto& nb : p->named)
+    if (nb.name == name) {
+      *dev_ptr = nb.ptr;
+      *bytes = int64_t(nb.bytes);
+      return TLK_OK;
+    }
+  return fail(TLK_EINVAL, "pack has no buffer named '%s'", name);
 }
 
 int tlk_pack_info(tlk_ctx* ctx, int32_t pack, tlk_model_info* out) {

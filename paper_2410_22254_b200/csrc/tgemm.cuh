@@ -1,4 +1,6 @@
-// Persistent, warp-specialised grouped GEMM for the transformer packs.
+// Persistent, warp-specialised grouped GEMM (transformer packs; the ResNet
+// implicit-GEMM convolutions in conv.cuh reuse the kernel with their own
+// tile / load / epilogue hooks).
 //
 //   D[z][m, n] = sum_k A[z][m, k] * B[z][n, k]      z = (lane, b, h)
 //
@@ -30,6 +32,7 @@ struct TGemm {
   static constexpr int EW = 8;  // epilogue warps (two groups of 4 lane quarters)
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = AMN, B_MN = BMN, ROW_EPI = ROW;
+  using Work = ZWork;
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN_ * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -59,6 +62,13 @@ struct TGemm {
     w.kb_end = g.kblocks;
     w.split = 0;
     return true;
+  }
+  TLK_DEV void prefetch() const {
+    tma_prefetch_desc(&ta);
+    tma_prefetch_desc(&tb);
+  }
+  TLK_DEV void epilogue(const ZWork& w, uint32_t tq, int row0, float* buf, int lane) const {
+    g.template tile<BN_>(w, tq, row0, buf, lane, ROW);
   }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
@@ -110,11 +120,10 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
 
   if (warp == EW) {
     if (lane == 0) {  // TMA producer
-      tma_prefetch_desc(&p.ta);
-      tma_prefetch_desc(&p.tb);
+      p.prefetch();
       int it = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        ZWork w;
+        typename P::Work w;
         if (!p.tile(t, w)) continue;
         for (int kb = w.kb_begin; kb < w.kb_end; ++kb, ++it) {
           const int s = it % STAGES;
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
     if (lane == 0) {  // MMA issuer
       int it = 0, lt = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        ZWork w;
+        typename P::Work w;
         if (!p.tile(t, w)) continue;
         const int buf = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
@@ -156,7 +165,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
     float* buf = staging + warp * (32 * 33);
     int lt = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-      ZWork w;
+      typename P::Work w;
       if (!p.tile(t, w)) continue;
       const int b = lt & 1;
       if (b != group) {
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       mbar_wait(&tfull[b], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t tq = tmem + b * BN + (uint32_t(q * 32) << 16);
-      p.g.template tile<BN>(w, tq, w.m0 + q * 32, buf, lane, P::ROW_EPI);
+      p.epilogue(w, tq, w.m0 + q * 32, buf, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);

@@ -20,7 +20,8 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t 
 // map with box {b0, b1, 1, 1, 1}, 128-byte swizzle.  Size-1 dims may pass
 // any stride (it is replaced by a valid one).
 int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5],
-                      const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1);
+                      const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1, uint32_t b2 = 1,
+                      uint32_t b3 = 1);
 
 TLK_DEV void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -40,7 +40,8 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t 
 }
 
 int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5],
-                      const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1) {
+                      const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1, uint32_t b2,
+                      uint32_t b3) {
   EncodeTiledFn fn = encode_fn();
   TLK_CHECK(fn, TLK_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   cuuint64_t d[5], st[4];
@@ -53,7 +54,7 @@ int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5]
               (unsigned long long)st[i], i + 1);
   }
   TLK_CHECK(reinterpret_cast<uintptr_t>(base) % 16 == 0, TLK_EINVAL, "tensor map base not 16-byte aligned");
-  const cuuint32_t box[5] = {b0, b1, 1, 1, 1};
+  const cuuint32_t box[5] = {b0, b1, b2, b3, 1};
   const cuuint32_t estride[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), d, st, box,
                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

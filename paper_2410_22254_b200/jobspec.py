@@ -17,7 +17,7 @@ import os
 from dataclasses import asdict, dataclass
 
 JOB_MODULE = "paper_2410_22254_b200.job"
-MODELS = ("mlp", "cnn", "xformer", "gpt")
+MODELS = ("mlp", "cnn", "xformer", "gpt", "resnet18")
 SEQ_MODELS = ("xformer", "gpt")  # batch = sequences
 OPTIMIZERS = ("adam", "adamw", "sgd")
 
@@ -76,6 +76,9 @@ def parse_job_flags(flags) -> JobSpec:
     if spec.model in SEQ_MODELS:
         if spec.batch < 1 or spec.batch > 4096:
             raise ValueError("--batch (sequences) must be in [1, 4096]")
+    elif spec.model == "resnet18":
+        if spec.batch < 8 or spec.batch > 512 or spec.batch % 8:
+            raise ValueError("--batch must be a multiple of 8 in [8, 512] for resnet18")
     elif spec.batch < 8 or spec.batch > 64 or spec.batch % 8:
         raise ValueError("--batch must be a multiple of 8 in [8, 64]")
     if spec.lr <= 0 or spec.eps <= 0:

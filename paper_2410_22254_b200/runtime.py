@@ -14,18 +14,20 @@ import threading
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtlk.so")
 
 TLK_OK, TLK_EINVAL, TLK_ECUDA, TLK_EOOM, TLK_ESTATE = 0, -1, -2, -3, -4
-MODEL_MLP, MODEL_CNN, MODEL_XFORMER, MODEL_GPT = 1, 2, 3, 4
-MODELS = {"mlp": MODEL_MLP, "cnn": MODEL_CNN, "xformer": MODEL_XFORMER, "gpt": MODEL_GPT}
+MODEL_MLP, MODEL_CNN, MODEL_XFORMER, MODEL_GPT, MODEL_RESNET18 = 1, 2, 3, 4, 5
+MODELS = {"mlp": MODEL_MLP, "cnn": MODEL_CNN, "xformer": MODEL_XFORMER, "gpt": MODEL_GPT,
+          "resnet18": MODEL_RESNET18}
 OPT_ADAM, OPT_ADAMW, OPT_SGD = 1, 2, 3
 OPTIMIZERS = {"adam": OPT_ADAM, "adamw": OPT_ADAMW, "sgd": OPT_SGD}
 PACK_WRITE_ALL_GRADS = 1
+PACK_SNAPSHOTS = 2
 BUF_PARAMS, BUF_GRADS, BUF_MOM1, BUF_MOM2, BUF_WBF16, BUF_LOSS, BUF_PIXELS, BUF_LABELS, BUF_ACTS = range(9)
 
 EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
     "tlk_close", "tlk_sync", "tlk_stream", "tlk_pack_create", "tlk_lane_load", "tlk_lane_release",
     "tlk_run", "tlk_step_host", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
-    "tlk_pack_tensor", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
+    "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
     "tlk_selftest_datagen",
 )
@@ -231,6 +233,16 @@ class Pack:
                                      C.byref(n)))
         labels = names.value.decode().split(",")
         return [(labels[k], float(ms[k])) for k in range(n.value)]
+
+    def named(self, name: str, dtype: str = "f4"):
+        """Zero-copy torch view of a named model buffer (tlk_pack_named)."""
+        import torch
+
+        ptr, nbytes = C.c_void_p(), C.c_int64()
+        check(lib().tlk_pack_named(self.ctx._ctx, self.id, name.encode(), C.byref(ptr), C.byref(nbytes)))
+        itemsize = {"f4": 4, "u2": 2, "i4": 4}[dtype]
+        return torch.as_tensor(_CudaArray(ptr.value, (nbytes.value // itemsize,), "<" + dtype, self),
+                               device=f"cuda:{self.ctx.device}")
 
     def tensor(self, which: int):
         """Zero-copy torch view of a pack buffer (TLK_BUF_*)."""
