@@ -83,9 +83,43 @@ class GPT(nn.Module):
 GPT_CFGS = {"xformer": (2, 256, 4, 128, 256), "gpt": (6, 384, 6, 256, 65)}
 
 
+class BasicBlock(nn.Module):
+    def __init__(self, cin, c, stride):
+        super().__init__()
+        self.conv1 = nn.Conv2d(cin, c, 3, stride, 1, bias=False)
+        self.bn1 = nn.BatchNorm2d(c)
+        self.conv2 = nn.Conv2d(c, c, 3, 1, 1, bias=False)
+        self.bn2 = nn.BatchNorm2d(c)
+        self.ds = None
+        if stride != 1 or cin != c:
+            self.ds = nn.Sequential(nn.Conv2d(cin, c, 1, stride, bias=False), nn.BatchNorm2d(c))
+
+    def forward(self, x):
+        o = F.relu(self.bn1(self.conv1(x)))
+        o = self.bn2(self.conv2(o))
+        return F.relu(o + (self.ds(x) if self.ds is not None else x))
+
+
+class ResNet18(nn.Module):
+    """CIFAR ResNet-18 (3x3 stem, no max-pool) -- same shapes as TLK_MODEL_RESNET18."""
+
+    def __init__(self):
+        super().__init__()
+        self.stem = nn.Sequential(nn.Conv2d(3, 64, 3, 1, 1, bias=False), nn.BatchNorm2d(64), nn.ReLU())
+        layers, cin = [], 64
+        for c, s in ((64, 1), (128, 2), (256, 2), (512, 2)):
+            layers += [BasicBlock(cin, c, s), BasicBlock(c, c, 1)]
+            cin = c
+        self.layers = nn.Sequential(*layers)
+        self.fc = nn.Linear(512, 10)
+
+    def forward(self, x):
+        return self.fc(self.layers(self.stem(x)).mean(dim=(2, 3)))
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--model", default="cnn", choices=("cnn", "mlp", "xformer", "gpt"))
+    ap.add_argument("--model", default="cnn", choices=("cnn", "mlp", "xformer", "gpt", "resnet18"))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--lr", type=float, default=1e-3)
@@ -94,18 +128,23 @@ def main():
     ap.add_argument("--procs", type=int, default=1)
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--bf16", type=int, default=None,
-                    help="1: torch.autocast(bfloat16); default 1 for the transformer models")
+                    help="1: torch.autocast(bfloat16); default 1 for the transformer / ResNet models")
     a = ap.parse_args()
     torch.manual_seed(a.seed)
     dev = torch.device("cuda")
     if a.bf16 is None:
-        a.bf16 = int(a.model in GPT_CFGS)
+        a.bf16 = int(a.model in GPT_CFGS or a.model == "resnet18")
     if a.model in GPT_CFGS:
         cfg = GPT_CFGS[a.model]
         model = GPT(*cfg).to(dev)
+    elif a.model == "resnet18":
+        model = ResNet18().to(dev).to(memory_format=torch.channels_last)
     else:
         model = (Net() if a.model == "cnn" else MLP()).to(dev)
-    opt = torch.optim.Adam(model.parameters(), lr=a.lr)
+    if a.model == "resnet18":
+        opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
+    else:
+        opt = torch.optim.Adam(model.parameters(), lr=a.lr)
     torch.backends.cudnn.benchmark = True
 
     def step():
@@ -115,6 +154,10 @@ def main():
                 toks = torch.randint(0, V, (a.batch, T + 1), device=dev)
                 logits = model(toks[:, :-1])
                 loss = F.cross_entropy(logits.reshape(-1, V).float(), toks[:, 1:].reshape(-1))
+            elif a.model == "resnet18":
+                x = torch.randn(a.batch, 3, 32, 32, device=dev).to(memory_format=torch.channels_last)
+                y = torch.randint(0, 10, (a.batch,), device=dev)
+                loss = F.cross_entropy(model(x).float(), y)
             else:
                 x = torch.rand(a.batch, 1, 28, 28, device=dev)
                 y = torch.randint(0, 10, (a.batch,), device=dev)

@@ -42,7 +42,31 @@ WORKLOADS = {
     "mlp": ("mlp", 64, 4, "configs[0]: 4 MNIST-MLP jobs packed on one device (triples [1,4,1])"),
     "xformer": ("xformer", 32, 32, "configs[3] transformer job (2 layers, d=256, T=128), 32 jobs/GPU"),
     "gpt": ("gpt", 64, 16, "configs[4]: tiny-GPT (6 layers, d=384, T=256) sweep, 16 jobs/GPU"),
+    "resnet18": ("resnet18", 128, 8, "configs[2]: ResNet-18/CIFAR-shape sweep, 64 jobs over 8 GPUs = 8 jobs/GPU, "
+                                     "bs 128, SGD momentum"),
 }
+# per-workload optimizer of the synthetic task list
+WORKLOAD_OPT = {"resnet18": dict(optim="sgd", lr=0.05, momentum=0.9)}
+
+
+def rn_kernel_work(name, batch, lanes):
+    """FLOPs of all launches of a ResNet conv kernel family in one step."""
+    C = (64, 128, 256, 512)
+    main = ds = 0
+    cin, res = 64, 32
+    for s in range(4):
+        for b in range(2):
+            ci = cin if b == 0 else C[s]
+            ho = res // 2 if (b == 0 and s > 0) else res
+            main += ho * ho * C[s] * 9 * (ci + C[s])
+            if b == 0 and s > 0:
+                ds += ho * ho * C[s] * ci
+            res = ho
+            if b == 1:
+                cin = C[s]
+    fam = {"conv_fwd": main, "conv_dgrad": main, "conv_wgrad": main,
+           "conv_fwd_ds": ds, "conv_dgrad_ds": ds, "conv_wgrad_ds": ds}
+    return 2.0 * batch * lanes * fam[name] if name in fam else None
 WORKLOAD = WORKLOADS["cnn"][3]
 JOBS_PER_GPU = 8
 BATCH = 64
@@ -327,14 +351,16 @@ def packed_arm(a, world, rank, local):
     # the workload as a parametric task list through the triples mapping:
     # triples [1, jobs*world, 1] on a world-GPU node; this rank trains the
     # slots pinned to GPU `rank` (task i -> slot i -> GPU i % world).
+    opt = WORKLOAD_OPT.get(MODEL, dict(lr=1e-3))
     plan = weak_scaling_plan(lanes, world, lambda i: TaskDef(i, tuple(
-        JobSpec(model=MODEL, seed=i, steps=total_steps, batch=BATCH, lr=1e-3).argv())))
+        JobSpec(model=MODEL, seed=i, steps=total_steps, batch=BATCH, **opt).argv())))
     share = rank_share(plan, rank)
     pack = ctx.pack(rt.MODELS[MODEL], BATCH, lanes, total_steps)
     for j, (slot, tasks) in enumerate(share):
         spec = parse_task(tasks[0].argv)
-        pack.load(j, seed=spec.seed, steps=spec.steps, lr=spec.lr, task_id=tasks[0].task_id,
-                  slot_index=slot)
+        pack.load(j, seed=spec.seed, steps=spec.steps, optimizer=rt.OPTIMIZERS[spec.optim], lr=spec.lr,
+                  beta1=spec.beta1, beta2=spec.beta2, eps=spec.eps, weight_decay=spec.wd,
+                  momentum=spec.momentum, task_id=tasks[0].task_id, slot_index=slot)
     stream = torch.cuda.ExternalStream(ctx.stream_handle)
 
     with ClockSampler(local) as clk:
@@ -372,6 +398,17 @@ def packed_arm(a, world, rank, local):
         top_ms = max(tot[top_name] / cnt[top_name], 1e-6)
         bound, work = "tensor", gpt_kernel_work(top_name, MODEL, BATCH, lanes)
         kernels_out = {k: round(v, 5) for k, v in tot.items()}
+    elif MODEL == "resnet18":
+        # conv families (20 launches each per step, different shapes): the
+        # dominant family's total FLOPs over its total device time
+        tot = {}
+        for k, v in kernels:
+            tot[k] = tot.get(k, 0.0) + v
+        fams = [k for k in tot if rn_kernel_work(k, BATCH, lanes)]
+        top_name = max(fams, key=lambda k: tot[k])
+        top_ms = max(tot[top_name], 1e-6)
+        bound, work = "tensor", rn_kernel_work(top_name, BATCH, lanes)
+        kernels_out = {k: round(v, 5) for k, v in tot.items()}
     else:
         top_name, top_ms = max(kernels, key=lambda kv: kv[1])
         top_ms = max(top_ms, 1e-6)
@@ -401,7 +438,7 @@ def packed_arm(a, world, rank, local):
 
     # end-to-end through the public API with HOST buffers (pinned), per step:
     # H2D of the step's pixels+labels, one packed step, D2H of the losses.
-    if MODEL in GPT_CFG:
+    if MODEL in GPT_CFG or MODEL == "resnet18":
         return _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_roof,
                                 sflops, sbytes, lanes, kernels_out)
     e2e_steps = max(3, min(a.steps, 100))
@@ -486,14 +523,17 @@ def packed_arm(a, world, rank, local):
 
 def _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_roof, sflops,
                      sbytes, lanes, kernels_out):
-    T = GPT_CFG[MODEL][3]
+    T = GPT_CFG[MODEL][3] if MODEL in GPT_CFG else None
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s (sequences)", "n_gpus": world,
+        "metric": METRIC, "value": value, "n_gpus": world,
+        "unit": "samples/s (sequences)" if T else "samples/s (images)",
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (on-device order-1 Markov-chain tokens; random-init weights)",
+        "data": ("synthetic (on-device order-1 Markov-chain tokens; random-init weights)" if T else
+                 "synthetic (on-device ~N(0,1) 3x32x32 images, int4-teacher labels; random-init weights)"),
         "config": {"workload": WORKLOAD, "jobs_per_gpu": lanes, "batch_per_job": BATCH,
-                   "tokens_per_s": value * T, "optimizer": "adam"},
+                   "optimizer": "sgd momentum 0.9" if MODEL == "resnet18" else "adam",
+                   **({"tokens_per_s": value * T} if T else {})},
         "e2e": None, "gpu_launches": pack.launches_per_step() * a.steps, "clocks": clocks,
         "roofline": roof,
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "measured_ms": ms_step,

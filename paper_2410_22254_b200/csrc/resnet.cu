@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) rn_stem_fwd_kernel(const LaneState* __res
 // -------------------------------------------------------------- BN stats ----
 // (mean, M2) partials of 32 rows each [P][2][C] -> stats[lane][2][C] = mean,
 // rstd via Chan's pairwise combination in a fixed order: thread (c, g)
-// folds partials g, g+8, ... ; then group results 0..7 in order.
+// folds partials g, g+32, ... ; then group results 0..31 in order.
 __device__ __forceinline__ void chan_combine(float& n, float& mean, float& m2, float nb, float meanb,
                                              float m2b) {
   const float nn = n + nb;
@@ -212,24 +212,36 @@ __device__ __forceinline__ void chan_combine(float& n, float& mean, float& m2, f
   m2 = m2 + m2b + d * d * (n * nb / nn);
   n = nn;
 }
-__global__ void __launch_bounds__(256) rn_bn_stats_kernel(const LaneState* __restrict__ lanes,
-                                                          const float* __restrict__ part, int64_t part_ls, int P,
-                                                          int C, float* __restrict__ stats) {
+constexpr int STAT_GROUPS = 32;
+__global__ void __launch_bounds__(1024) rn_bn_stats_kernel(const LaneState* __restrict__ lanes,
+                                                           const float* __restrict__ part, int64_t part_ls, int P,
+                                                           int C, float* __restrict__ stats) {
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
-  __shared__ float sh[3][8][32];
+  __shared__ float sh[3][STAT_GROUPS][32];
   float n = 0.f, mean = 0.f, m2 = 0.f;
   if (c < C) {
     const float* pp = part + j * part_ls + c;
-    for (int p = g; p < P; p += 8) {
-      const float mb = pp[int64_t(p) * 2 * C], m2b = pp[int64_t(p) * 2 * C + C];
-      if (n == 0.f) {
-        n = 32.f;
-        mean = mb;
-        m2 = m2b;
-      } else {
-        chan_combine(n, mean, m2, 32.f, mb, m2b);
+    // partials g, g + 32, ... in order; four loads in flight per round
+    for (int p0 = g; p0 < P; p0 += 4 * STAT_GROUPS) {
+      float mb[4], qb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = p0 + u * STAT_GROUPS;
+        mb[u] = p < P ? pp[int64_t(p) * 2 * C] : 0.f;
+        qb[u] = p < P ? pp[int64_t(p) * 2 * C + C] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (p0 + u * STAT_GROUPS >= P) break;
+        if (n == 0.f) {
+          n = 32.f;
+          mean = mb[u];
+          m2 = qb[u];
+        } else {
+          chan_combine(n, mean, m2, 32.f, mb[u], qb[u]);
+        }
       }
     }
   }
@@ -239,7 +251,7 @@ __global__ void __launch_bounds__(256) rn_bn_stats_kernel(const LaneState* __res
   __syncthreads();
   if (g == 0 && c < C) {
     float N = sh[0][0][cl], M = sh[1][0][cl], Q = sh[2][0][cl];
-    for (int k = 1; k < 8; ++k)
+    for (int k = 1; k < STAT_GROUPS; ++k)
       if (sh[0][k][cl] > 0.f) chan_combine(N, M, Q, sh[0][k][cl], sh[1][k][cl], sh[2][k][cl]);
     stats[(int64_t(j) * 2) * C + c] = M;
     stats[(int64_t(j) * 2 + 1) * C + c] = 1.0f / sqrtf(Q / N + BN_EPS);
@@ -395,80 +407,109 @@ __global__ void __launch_bounds__(512) rn_loss_kernel(LaneState* __restrict__ la
 }
 
 // ----------------------------------------------------------- BN backward ----
-// g = G [mask > 0]; partials per 256-row block: sum g, sum g xh [, sum g xhd]
-constexpr int BNB_ROWS = 256;
-__global__ void __launch_bounds__(128) rn_bn_bwd_reduce_kernel(
+// g = G [mask > 0]; partials per 512-row block: sum g, sum g xh [, sum g xhd].
+// CTA = 256 threads = (C/8 channel groups) x (256 / (C/8) row sub-lanes); a
+// thread owns 8 channels (16-byte bf16 / 2 x 16-byte fp32 loads), strides
+// over the block's rows, and the row sub-lanes are summed in order via smem.
+constexpr int BNB_ROWS = 512;
+__global__ void __launch_bounds__(256) rn_bn_bwd_reduce_kernel(
     const LaneState* __restrict__ lanes, int64_t M, int C, const float* __restrict__ G,
     const uint16_t* __restrict__ mask, const uint16_t* __restrict__ y, const float* __restrict__ st,
     const uint16_t* __restrict__ yd, const float* __restrict__ std_, float* __restrict__ part, int64_t part_ls) {
-  const int cg = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
-  if (!lanes[j].active || cg * 8 >= C) return;
+  const int blk = blockIdx.x, j = blockIdx.y;
+  if (!lanes[j].active) return;
+  const int CG = C / 8, R = 256 / CG;
+  const int cg = threadIdx.x % CG, sub = threadIdx.x / CG;
   const int c0 = cg * 8;
   const int K = yd ? 3 : 2;
-  float mu[8], rs[8], mud[8], rsd[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    mu[i] = st[(int64_t(j) * 2) * C + c0 + i];
-    rs[i] = st[(int64_t(j) * 2 + 1) * C + c0 + i];
-    mud[i] = yd ? std_[(int64_t(j) * 2) * C + c0 + i] : 0.f;
-    rsd[i] = yd ? std_[(int64_t(j) * 2 + 1) * C + c0 + i] : 0.f;
-  }
+  __shared__ float red[3 * 2048];  // [K][R][C] (R * C = 2048)
   float sg[8], sx[8], sd[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) sg[i] = sx[i] = sd[i] = 0.f;
-  const int64_t base = int64_t(j) * M * C;
-  const int64_t r0 = int64_t(blk) * BNB_ROWS, r1 = min(M, r0 + BNB_ROWS);
-  for (int64_t r = r0; r < r1; ++r) {
-    const int64_t e = base + r * C + c0;
-    const float4 g0 = *reinterpret_cast<const float4*>(G + e), g1 = *reinterpret_cast<const float4*>(G + e + 4);
-    const uint4 mk = *reinterpret_cast<const uint4*>(mask + e), yy = *reinterpret_cast<const uint4*>(y + e);
-    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w}, yw[4] = {yy.x, yy.y, yy.z, yy.w};
-    uint4 dd = make_uint4(0, 0, 0, 0);
-    if (yd) dd = *reinterpret_cast<const uint4*>(yd + e);
-    const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w};
+  if (sub < R) {
+    float mu[8], rs[8], mud[8], rsd[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint32_t sh = (i & 1) ? 0u : 16u;
-      const float mv = __uint_as_float((mw[i >> 1] << sh) & 0xffff0000u);
-      const float g = mv > 0.f ? gg[i] : 0.f;
-      const float yv = __uint_as_float((yw[i >> 1] << sh) & 0xffff0000u);
-      sg[i] += g;
-      sx[i] += g * ((yv - mu[i]) * rs[i]);
-      if (K == 3) {
-        const float dv = __uint_as_float((dw[i >> 1] << sh) & 0xffff0000u);
-        sd[i] += g * ((dv - mud[i]) * rsd[i]);
+      mu[i] = st[(int64_t(j) * 2) * C + c0 + i];
+      rs[i] = st[(int64_t(j) * 2 + 1) * C + c0 + i];
+      mud[i] = yd ? std_[(int64_t(j) * 2) * C + c0 + i] : 0.f;
+      rsd[i] = yd ? std_[(int64_t(j) * 2 + 1) * C + c0 + i] : 0.f;
+    }
+    const int64_t base = int64_t(j) * M * C;
+    const int64_t r1 = min(M, int64_t(blk + 1) * BNB_ROWS);
+#pragma unroll 2
+    for (int64_t r = int64_t(blk) * BNB_ROWS + sub; r < r1; r += R) {
+      const int64_t e = base + r * C + c0;
+      const float4 g0 = *reinterpret_cast<const float4*>(G + e), g1 = *reinterpret_cast<const float4*>(G + e + 4);
+      const uint4 mk = *reinterpret_cast<const uint4*>(mask + e), yy = *reinterpret_cast<const uint4*>(y + e);
+      uint4 dd = make_uint4(0, 0, 0, 0);
+      if (yd) dd = *reinterpret_cast<const uint4*>(yd + e);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w}, yw[4] = {yy.x, yy.y, yy.z, yy.w};
+      const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t sh = (i & 1) ? 0u : 16u;
+        const float mv = __uint_as_float((mw[i >> 1] << sh) & 0xffff0000u);
+        const float g = mv > 0.f ? gg[i] : 0.f;
+        const float yv = __uint_as_float((yw[i >> 1] << sh) & 0xffff0000u);
+        sg[i] += g;
+        sx[i] += g * ((yv - mu[i]) * rs[i]);
+        if (K == 3) {
+          const float dv = __uint_as_float((dw[i >> 1] << sh) & 0xffff0000u);
+          sd[i] += g * ((dv - mud[i]) * rsd[i]);
+        }
       }
     }
-  }
-  float* pp = part + j * part_ls + int64_t(blk) * K * C + c0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    pp[i] = sg[i];
-    pp[C + i] = sx[i];
-    if (K == 3) pp[2 * C + i] = sd[i];
+    for (int i = 0; i < 8; ++i) {
+      red[(0 * R + sub) * C + c0 + i] = sg[i];
+      red[(1 * R + sub) * C + c0 + i] = sx[i];
+      if (K == 3) red[(2 * R + sub) * C + c0 + i] = sd[i];
+    }
+  }
+  __syncthreads();
+  float* pp = part + j * part_ls + int64_t(blk) * K * C;
+  for (int i = threadIdx.x; i < K * C; i += 256) {
+    const int k = i / C, c = i % C;
+    float s = 0.f;
+    for (int r = 0; r < R; ++r) s += red[(k * R + r) * C + c];
+    pp[i] = s;
   }
 }
 
-// sums[lane][k][C] = sum_blk partials (fixed order); grads: dbeta = sum g,
-// dgamma = sum g xh (and the shortcut BN's from k = 2, dbeta_d = sum g)
-__global__ void rn_bn_bwd_finish_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
-                                        int64_t part_ls, int nblk, int K, int C, float* __restrict__ sums,
-                                        float* __restrict__ grads, int64_t pstride, int64_t og, int64_t ob,
-                                        int64_t ogd, int64_t obd) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  if (!lanes[j].active || c >= C) return;
-  const float* p = part + j * part_ls + c;
+// sums[lane][k][C] = sum_blk partials (8 groups of strided blocks, then the
+// groups in order); grads: dbeta = sum g, dgamma = sum g xh (and the
+// shortcut BN's from k = 2, dbeta_d = sum g)
+__global__ void __launch_bounds__(256) rn_bn_bwd_finish_kernel(
+    const LaneState* __restrict__ lanes, const float* __restrict__ part, int64_t part_ls, int nblk, int K, int C,
+    float* __restrict__ sums, float* __restrict__ grads, int64_t pstride, int64_t og, int64_t ob, int64_t ogd,
+    int64_t obd) {
+  const int j = blockIdx.y;
+  if (!lanes[j].active) return;
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
+  __shared__ float sh[3][8][32];
   float s[3] = {0.f, 0.f, 0.f};
-  for (int b = 0; b < nblk; ++b)
-    for (int k = 0; k < K; ++k) s[k] += p[(int64_t(b) * K + k) * C];
-  for (int k = 0; k < K; ++k) sums[(int64_t(j) * 3 + k) * 512 + c] = s[k];
-  float* g = grads + j * pstride;
-  g[ob + c] = s[0];
-  g[og + c] = s[1];
-  if (K == 3) {
-    g[obd + c] = s[0];
-    g[ogd + c] = s[2];
+  if (c < C) {
+    const float* p = part + j * part_ls + c;
+#pragma unroll 4
+    for (int b = g; b < nblk; b += 8)
+      for (int k = 0; k < K; ++k) s[k] += p[(int64_t(b) * K + k) * C];
+  }
+  for (int k = 0; k < 3; ++k) sh[k][g][cl] = s[k];
+  __syncthreads();
+  if (g == 0 && c < C) {
+    float t[3] = {0.f, 0.f, 0.f};
+    for (int q = 0; q < 8; ++q)
+      for (int k = 0; k < K; ++k) t[k] += sh[k][q][cl];
+    for (int k = 0; k < K; ++k) sums[(int64_t(j) * 3 + k) * 512 + c] = t[k];
+    float* gr = grads + j * pstride;
+    gr[ob + c] = t[0];
+    gr[og + c] = t[1];
+    if (K == 3) {
+      gr[obd + c] = t[0];
+      gr[ogd + c] = t[2];
+    }
   }
 }
 
@@ -637,7 +678,7 @@ int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, c
   p.mark(st, name);
   // statistics of this conv's output
   const int P = g.mt * 4;
-  rn_bn_stats_kernel<<<dim3((L.cout + 31) / 32, p.lanes), 256, 0, st>>>(p.lane_dev, R.part, R.part_ls, P, L.cout,
+  rn_bn_stats_kernel<<<dim3((L.cout + 31) / 32, p.lanes), 1024, 0, st>>>(p.lane_dev, R.part, R.part_ls, P, L.cout,
                                                                        L.stats);
   TLK_CUDA(cudaGetLastError());
   p.mark(st, "bn_stats");
@@ -961,7 +1002,7 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
   rn_stem_fwd_kernel<<<dim3(B * 8, Lc), 256, 0, st>>>(LS, B, R.xin, p.wbf, PS, O(S0.t_w), S0.y, R.part, R.part_ls);
   TLK_CUDA(cudaGetLastError());
   marked("stem_fwd");
-  rn_bn_stats_kernel<<<dim3(2, Lc), 256, 0, st>>>(LS, R.part, R.part_ls, B * 8 * 4, 64, S0.stats);
+  rn_bn_stats_kernel<<<dim3(2, Lc), 1024, 0, st>>>(LS, R.part, R.part_ls, B * 8 * 4, 64, S0.stats);
   TLK_CUDA(cudaGetLastError());
   marked("bn_stats");
   {
@@ -1020,12 +1061,12 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
     const int64_t M = int64_t(B) * c.Ho * c.Wo;
     const int nblk = int((M + BNB_ROWS - 1) / BNB_ROWS);
     const int K = cd ? 3 : 2;
-    const int cgs = c.cout / 8, th = std::min(128, (cgs + 31) / 32 * 32);
-    rn_bn_bwd_reduce_kernel<<<dim3((cgs + th - 1) / th, nblk, Lc), th, 0, st>>>(
-        LS, M, c.cout, Gin, mask, c.y, c.stats, cd ? cd->y : nullptr, cd ? cd->stats : nullptr, R.part, R.part_ls);
+    rn_bn_bwd_reduce_kernel<<<dim3(nblk, Lc), 256, 0, st>>>(LS, M, c.cout, Gin, mask, c.y, c.stats,
+                                                              cd ? cd->y : nullptr, cd ? cd->stats : nullptr,
+                                                              R.part, R.part_ls);
     TLK_CUDA(cudaGetLastError());
     marked("bn_bwd_reduce");
-    rn_bn_bwd_finish_kernel<<<dim3((c.cout + 127) / 128, Lc), 128, 0, st>>>(
+    rn_bn_bwd_finish_kernel<<<dim3((c.cout + 31) / 32, Lc), 256, 0, st>>>(
         LS, R.part, R.part_ls, nblk, K, c.cout, R.sums, p.grads, PS, O(c.t_g), O(c.t_b), cd ? O(cd->t_g) : 0,
         cd ? O(cd->t_b) : 0);
     TLK_CUDA(cudaGetLastError());
