@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(1024) rn_bn_stats_kernel(const LaneState* __re
 
 // ------------------------------------------------------ BN apply (forward) --
 // out = bf16(relu((y - mu) rstd g + b  [+ res]))  res: 0 none, 1 bf16 x,
-// 2 (yd - mud) rstdd gd + bd.  8 channels per thread.
+// 2 (yd - mud) rstdd gd + bd.  Per-channel (mu, rstd * g, b) staged in smem;
+// 8 channels (16 bytes of bf16) per thread.
 __global__ void __launch_bounds__(256) rn_bn_act_kernel(const LaneState* __restrict__ lanes, int64_t n8, int C,
                                                         const uint16_t* __restrict__ y, const float* __restrict__ st,
                                                         const float* __restrict__ params, int64_t pstride,
@@ -270,10 +271,21 @@ __global__ void __launch_bounds__(256) rn_bn_act_kernel(const LaneState* __restr
                                                         uint16_t* __restrict__ out) {
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
-  const int64_t lane_off = int64_t(j) * n8 * 8;
+  __shared__ float cf[6][512];  // mu, rstd*g, b, mud, rstdd*gd, bd
   const float* P = params + j * pstride;
-  const float* S = st + int64_t(j) * 2 * C;
-  const float* Sd = mode == 2 ? std_ + int64_t(j) * 2 * C : nullptr;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float rs = st[(int64_t(j) * 2 + 1) * C + c];
+    cf[0][c] = st[(int64_t(j) * 2) * C + c];
+    cf[1][c] = rs * P[og + c];
+    cf[2][c] = P[ob + c];
+    if (mode == 2) {
+      cf[3][c] = std_[(int64_t(j) * 2) * C + c];
+      cf[4][c] = std_[(int64_t(j) * 2 + 1) * C + c] * P[ogd + c];
+      cf[5][c] = P[obd + c];
+    }
+  }
+  __syncthreads();
+  const int64_t lane_off = int64_t(j) * n8 * 8;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t e = lane_off + i * 8;
     const int c0 = int((i * 8) % C);
@@ -290,10 +302,10 @@ __global__ void __launch_bounds__(256) rn_bn_act_kernel(const LaneState* __restr
       for (int h = 0; h < 2; ++h) {
         const int c = c0 + 2 * q + h;
         const float yv = h ? __uint_as_float(uw[q] & 0xffff0000u) : __uint_as_float(uw[q] << 16);
-        float v = (yv - S[c]) * S[C + c] * P[og + c] + P[ob + c];
+        float v = (yv - cf[0][c]) * cf[1][c] + cf[2][c];
         const float rr = h ? __uint_as_float(rw[q] & 0xffff0000u) : __uint_as_float(rw[q] << 16);
         if (mode == 1) v += rr;
-        if (mode == 2) v += (rr - Sd[c]) * Sd[C + c] * P[ogd + c] + P[obd + c];
+        if (mode == 2) v += (rr - cf[3][c]) * cf[4][c] + cf[5][c];
         o2[h] = fmaxf(v, 0.f);
       }
       ow[q] = pack_bf2(o2[0], o2[1]);
@@ -514,6 +526,8 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_finish_kernel(
 }
 
 // dy = bf16(gamma rstd ((g - sg/M) - xh (sgx/M))) [, dyd likewise] [, gx = g]
+// computed as  a g + b (y - mu) + c  with per-channel a = gamma rstd,
+// b = -gamma rstd^2 sgx/M, c = -gamma rstd sg/M staged in smem.
 __global__ void __launch_bounds__(256) rn_bn_bwd_apply_kernel(
     const LaneState* __restrict__ lanes, int64_t M, int C, const float* __restrict__ G,
     const uint16_t* __restrict__ mask, const uint16_t* __restrict__ y, const float* __restrict__ st,
@@ -522,10 +536,28 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_apply_kernel(
     uint16_t* __restrict__ dyd, float* __restrict__ gx) {
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
-  const int64_t n8 = M * C / 8;
+  __shared__ float cf[8][512];  // mu, a, b, c, mud, ad, bd, cd
   const float invM = 1.0f / float(M);
   const float* S = sums + int64_t(j) * 3 * 512;
   const float* P = params + j * pstride;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float mu = st[(int64_t(j) * 2) * C + c], rs = st[(int64_t(j) * 2 + 1) * C + c];
+    const float a = P[og + c] * rs;
+    cf[0][c] = mu;
+    cf[1][c] = a;
+    cf[2][c] = -a * rs * (S[512 + c] * invM);
+    cf[3][c] = -a * (S[c] * invM);
+    if (yd) {
+      const float mud = std_[(int64_t(j) * 2) * C + c], rsd = std_[(int64_t(j) * 2 + 1) * C + c];
+      const float ad = P[ogd + c] * rsd;
+      cf[4][c] = mud;
+      cf[5][c] = ad;
+      cf[6][c] = -ad * rsd * (S[1024 + c] * invM);
+      cf[7][c] = -ad * (S[c] * invM);
+    }
+  }
+  __syncthreads();
+  const int64_t n8 = M * C / 8;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t e = int64_t(j) * M * C + i * 8;
     const int c0 = int((i * 8) % C);
@@ -543,15 +575,11 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_apply_kernel(
       const uint32_t sh = (k & 1) ? 0u : 16u;
       const float mv = __uint_as_float((mw[k >> 1] << sh) & 0xffff0000u);
       g[k] = mv > 0.f ? gg[k] : 0.f;
-      const float mu = st[(int64_t(j) * 2) * C + c], rs = st[(int64_t(j) * 2 + 1) * C + c];
       const float yv = __uint_as_float((yw[k >> 1] << sh) & 0xffff0000u);
-      const float xh = (yv - mu) * rs;
-      o1[k] = (P[og + c] * rs) * ((g[k] - S[c] * invM) - xh * (S[512 + c] * invM));
+      o1[k] = cf[1][c] * g[k] + cf[2][c] * (yv - cf[0][c]) + cf[3][c];
       if (yd) {
-        const float mud = std_[(int64_t(j) * 2) * C + c], rsd = std_[(int64_t(j) * 2 + 1) * C + c];
         const float dv = __uint_as_float((dw[k >> 1] << sh) & 0xffff0000u);
-        const float xd = (dv - mud) * rsd;
-        o2[k] = (P[ogd + c] * rsd) * ((g[k] - S[c] * invM) - xd * (S[1024 + c] * invM));
+        o2[k] = cf[5][c] * g[k] + cf[6][c] * (dv - cf[4][c]) + cf[7][c];
       }
     }
     *reinterpret_cast<uint4*>(dy + e) = make_uint4(pack_bf2(o1[0], o1[1]), pack_bf2(o1[2], o1[3]),

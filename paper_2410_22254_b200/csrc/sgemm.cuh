@@ -99,19 +99,26 @@ struct EpiOps {
     constexpr bool BIAS = KIND == EPI_BF16 || KIND == EPI_BF16_GELU || KIND == EPI_RESADD;
     constexpr bool AUX = KIND == EPI_RESADD || KIND == EPI_GELU_BWD;
     const float* bias = (BIAS && e.bias) ? e.bias + w.j * e.bias_ls : nullptr;
+    // aux rows of chunk cc + 1 are fetched while chunk cc is processed
+    float4 ax[8], nx[8];
+    auto fetch = [&](int cc, float4 (&dst)[8]) {
+      const int n = w.n0 + cc * 32 + c4;
+      const float* a = static_cast<const float*>(e.aux) + o0 + cc * 32;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        dst[k] = (n < e.cols && row0 + 4 * k + rsub < e.rows) ? *reinterpret_cast<const float4*>(a + k * step)
+                                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    if constexpr (AUX) fetch(0, nx);
 #pragma unroll 1
     for (int cc = 0; cc < BN / 32; ++cc) {
       const int n = w.n0 + cc * 32 + c4;
       const bool col_ok = n < e.cols;
       const int64_t o = o0 + cc * 32;
-      float4 ax[8];
       if constexpr (AUX) {
-        const float* a = static_cast<const float*>(e.aux) + o;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          ax[k] = (col_ok && row0 + 4 * k + rsub < e.rows)
-                      ? *reinterpret_cast<const float4*>(a + k * step)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < 8; ++k) ax[k] = nx[k];
+        if (cc + 1 < BN / 32) fetch(cc + 1, nx);
       }
       float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
       if (bias && col_ok) bb = make_float4(bias[n], bias[n + 1], bias[n + 2], bias[n + 3]);

@@ -95,8 +95,9 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
-  uint8_t* smem =
-      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting smem_raw (not via an integer cast) so that pointers
+  // derived from it stay in the shared window (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   float* staging = reinterpret_cast<float*>(smem + STAGES * P::STAGE_BYTES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -1,4 +1,4 @@
-"""Run a few steps of a transformer pack (for ncu captures): python tools/gpt_step.py gpt 16 64 2"""
+"""Run a few steps of a pack (ncu captures): python tools/pack_step.py <model> <lanes> <batch> <steps> [opt]"""
 import os
 import sys
 
@@ -11,8 +11,9 @@ batch = int(sys.argv[3]) if len(sys.argv) > 3 else 64
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 ctx = rt.Context(0)
 pack = ctx.pack(rt.MODELS[model], batch, lanes, steps + 1)
+opt = dict(optimizer=rt.OPT_SGD, lr=0.05, momentum=0.9) if model == "resnet18" else {}
 for j in range(lanes):
-    pack.load(j, seed=j, steps=steps + 1)
+    pack.load(j, seed=j, steps=steps + 1, **opt)
 pack.run(steps)
 ctx.sync()
-print("ok", [pack.losses(j, steps).tolist() for j in range(2)])
+print("ok", [pack.losses(j, steps).tolist() for j in range(min(2, lanes))])
