@@ -207,19 +207,19 @@ def kernel_work(name, info, lanes, batch):
         # epilogue: p, m, v read + write and the bf16 shadow (26 B/param); the
         # batched optimizer does the rest (28 B/param + 2 B shadow)
         "fc1_wgrad_adam": ("hbm", 26.0 * 9216 * 128 * L),
-        "optimizer": ("hbm", 30.0 * (info.param_count - 9216 * 128) * L),
+        # the other 2%: partial-sum finalisation + update (30 B/param)
+        "grad_finalize_opt": ("hbm", L * (30.0 * (info.param_count - 9216 * 128)
+                                          + 4.0 * (18 * 288 * 64 + 9216 + B * 320))),
         "conv2_fwd_pool": ("tensor", conv2_flops),
         "conv2_wgrad": ("tensor", conv2_flops),
         "conv2_dgrad": ("tensor", conv2_flops),
         "fc1_fwd_splitk": ("tensor", fc1_flops),
         "fc1_dgrad_unpool": ("tensor", fc1_flops),
         # CUDA-core / bookkeeping kernels: compulsory HBM bytes
-        "inputs": ("hbm", L * B * (784 + 784 * 2 + 4)),
-        "conv1_fwd": ("hbm", L * B * (784 * 2 + 676 * 32 * 2)),
+        "inputs_conv1_fwd": ("hbm", L * B * (784 + 784 * 2 + 4 + 676 * 32 * 2)),
         "conv1_wgrad": ("hbm", L * B * (784 * 2 + 676 * 32 * 2)),
         "fc1_reduce": ("hbm", L * (18 * 128 * 64 * 4 + B * 128 * 2)),
         "head": ("hbm", L * B * 128 * 4),
-        "grad_finalize": ("hbm", L * (24 * 288 * 64 * 4 + 9216 * 4)),
         "end_step": ("hbm", L * 128),
     }
     return act.get(name, ("hbm", 0.0))

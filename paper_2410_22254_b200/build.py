@@ -15,11 +15,11 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-OUT_DIR = os.path.join(PKG, "_lib")
+OUT_DIR = os.environ.get("TLK_BUILD_DIR") or os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libtlk.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v"]
+         "-Xptxas", "-v", *os.environ.get("TLK_NVCC_FLAGS", "").split()]
 
 
 def _nvcc() -> str:

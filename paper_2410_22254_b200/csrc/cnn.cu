@@ -3,15 +3,16 @@
 //   x[28,28] -conv1 3x3 (1->32)+ReLU-> h1[26,26,32] -conv2 3x3 (32->64)+ReLU+maxpool2->
 //   p2[12,12,64] -flatten (h,w,c)-> fc1 (9216->128)+ReLU -> h3 -> fc2 (128->10) + CE
 //
-// Launch sequence of one step (14 kernels, graph-captured):
-//   inputs | conv1 fwd (CUDA cores, writes h1 in P28 planes) | conv2 fwd
+// Launch sequence of one step (11 kernels, graph-captured):
+//   inputs + conv1 fwd (CUDA cores, writes h1 in P28 planes) | conv2 fwd
 //   (tcgen05, TMA-bulk patch + tap-shifted descriptors; epilogue bias+ReLU+
 //   2x2 maxpool+argmax) | fc1 fwd (tcgen05 split-K) | fc1 reduce (+bias+ReLU)
 //   | head (fc2+CE+bwd) | fc1 wgrad (tcgen05) | fc1 dgrad (tcgen05; epilogue
 //   = maxpool/ReLU backward scatter into dz2 P28 planes + conv2 bias partials)
 //   | conv2 wgrad (tcgen05, 9 tap accumulators in TMEM) | conv2 dgrad
-//   (tcgen05; epilogue ReLU mask -> dz1) | conv1 wgrad (CUDA cores) | grad
-//   finalize (fixed-order reductions) | optimizer | end_step
+//   (tcgen05; epilogue ReLU mask -> dz1) | conv1 wgrad (CUDA cores) | fc1
+//   wgrad + Adam | grad finalize (fixed-order reductions) + optimizer of the
+//   remaining parameters + end of step
 //
 // The P28 layout and the conv2 kernels are described in conv_tc.cuh.
 //
@@ -23,6 +24,7 @@
 #include "tma.cuh"
 #include "linear.cuh"
 #include "pack.cuh"
+#include "inputs.cuh"
 
 namespace tlk {
 namespace {
@@ -30,6 +32,7 @@ namespace {
 constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
 constexpr int C2W_SPLITS = 18;     // conv2 wgrad position splits per lane
 constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
+constexpr int CNN_OPT_CTAS = 16;  // per lane: ~5.4k float4 of non-fc1.w parameters
 
 struct CnnBufs {
   // TMA tensor maps of the plain-layout fc1 operands (lanes = dim 2)
@@ -37,6 +40,7 @@ struct CnnBufs {
   CUtensorMap w1_mn;  // fc1.w bf16: box 64 x 64 (MN-major A of dgrad)
   CUtensorMap p2m;    // p2 [9216][B]: box 64 x 64
   CUtensorMap dz3m;   // dz3 [128][B]: box 64 x 64
+  CUtensorMap fa_p, fa_m, fa_v;  // fc1.w optimizer state tiles (fc1 wgrad + Adam)
   int B;
   int64_t npos;
   uint16_t *h1, *p2, *h3, *dz3, *dz2, *dz1;
@@ -49,31 +53,32 @@ __host__ __device__ inline int64_t p28_pos(int b, int r, int c) {
   return P28_FRONT + int64_t(b) * P28_IMG + r * P28 + c;
 }
 
-// ---------------------------------------------------------------- conv1 -----
-// One CTA per (sample, lane); fp32 math on fp32 master weights; writes the
-// 26x26 interior of h1's P28 planes (16 B = 8 channels per store).
+// ------------------------------------------------------- inputs + conv1 -----
+// One CTA per (sample, lane): the sample's inputs (inputs.cuh: pixel codes,
+// bf16 x for conv1 wgrad, teacher label) straight into shared memory, then
+// conv1 in fp32 on the fp32 master weights, writing the 26x26 interior of
+// h1's P28 planes (16 B = 8 channels per store).
 __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restrict__ lanes,
-                                                        const uint16_t* __restrict__ x,
+                                                        const int8_t* __restrict__ teacher,
+                                                        uint8_t* __restrict__ px, int32_t* __restrict__ labels,
+                                                        uint16_t* __restrict__ x, int host_input,
                                                         const float* __restrict__ params,
                                                         int64_t pstride, int64_t w_off,
                                                         int64_t b_off, CnnBufs buf) {
+  pdl_begin();
   const int s = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (!lanes[j].active) return;
+  __shared__ __align__(16) uint8_t pix[PIXELS];
+  __shared__ int part[8][CLASSES];
   __shared__ float xs[784];
   __shared__ float ws[32 * 9];
   __shared__ float bs[32];
-  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t(j) * buf.B + s) * 784);
-  if (tid < 98) {  // 784 bf16 = 98 x 16 B
-    const uint4 v = xr[tid];
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      xs[tid * 8 + 2 * e] = bf2f(uint16_t(wv[e] & 0xFFFF));
-      xs[tid * 8 + 2 * e + 1] = bf2f(uint16_t(wv[e] >> 16));
-    }
-  }
   for (int i = tid; i < 288; i += 256) ws[i] = params[j * pstride + w_off + i];
   if (tid < 32) bs[tid] = params[j * pstride + b_off + tid];
+  sample_inputs<256>(lanes[j].seed, lanes[j].steps_done, s, size_t(j) * buf.B + s, host_input, teacher, px,
+                     labels, x, pix, part);
+  __syncthreads();
+  for (int i = tid; i < 784; i += 256) xs[i] = float(pix[i]) * (1.0f / 256.0f);  // = bf16 x exactly
   __syncthreads();
   uint16_t* h1 = buf.h1 + int64_t(j) * 4 * buf.npos * 8;
   const int c = tid & 3;  // this thread's 8-channel chunk: its 72 weights live in registers
@@ -149,6 +154,7 @@ struct Fc1Fwd {
 __global__ void fc1_reduce_kernel(const LaneState* __restrict__ lanes, CnnBufs buf,
                                   const float* __restrict__ params, int64_t pstride,
                                   int64_t b_off) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // e = o*64 + b
@@ -255,85 +261,176 @@ struct Fc1Dgrad {
 };
 
 // ------------------------------------------- fc1 wgrad + optimizer (TC) -----
-// dW1[o, f] = sum_b dz3[b, o] p2[b, f] (M = 128 out, N = 9216 in, K = batch,
-// both operands MN-major) with the lane's optimizer update applied in the
-// epilogue: fc1.w is 98% of the CNN's parameters, so its fp32 gradient never
-// makes the HBM round trip (grads are stored only with
-// TLK_PACK_WRITE_ALL_GRADS).  Must run after every reader of this step's fc1
-// weights (fc1 dgrad).  (Measured alternative: a separate optimizer pass in a
-// forked graph branch concurrent with the conv backward kernels was slower --
-// it crowds the SMs the conv kernels need.)
-struct Fc1WgradOpt {
-  static constexpr int BN = 64, STAGES = 2, THREADS = 256;
-  static constexpr bool A_MN = true, B_MN = true;
-  static constexpr bool TILE_EPILOGUE = true;
-  using Work = LaneWork;
-  struct Carry {};
-  CnnBufs buf;
+// dW1^T[f, o] = sum_b p2[b, f] dz3[b, o] (M = 128 input features f, N = all
+// 128 outputs o, K = batch; both operands MN-major) with the lane's optimizer
+// update applied as the epilogue: fc1.w is 98% of the CNN's parameters, so
+// its fp32 gradient never makes the HBM round trip (stored only with
+// TLK_PACK_WRITE_ALL_GRADS) and the kernel is an HBM stream of p, m, v (read
+// + write) + the bf16 shadow.  Transposed on purpose: TMEM lane = f, so a warp
+// holds 32 consecutive f of one output row and every global store is a full
+// 128-B line.  Persistent (one CTA per SM), warp-specialised so the stream
+// never waits on the GEMM:
+//   warp 0   TMA producer: per tile the p2 / dz3 operand boxes, then the
+//            tile's p, m, v in four 32-output chunks (3 x 16 KB each,
+//            [32 o][128 f] fp32) into a 4-slot ring
+//   warp 1   tcgen05.mma issuer, accumulator double-buffered in TMEM
+//   warps 2-17  update: thread = (f = its TMEM lane, 8 outputs of the chunk):
+//            p, m, v from the slot into registers (the slot is released at
+//            once, so 3 slots stay in flight), opt_update (IEEE-exact Adam
+//            is ~50 instructions per element, hence 16 warps), coalesced
+//            stores of p, m, v and the bf16 shadow.
+// Must run after every reader of this step's fc1 weights (fc1 dgrad).
+constexpr int FWA_SLOTS = 4, FWA_UPD_WARPS = 16;
+constexpr int FWA_STAGE_BYTES = 2 * 128 * 64 * 2;  // p2^T and dz3^T tiles (two 64-wide boxes each)
+constexpr int FWA_CHUNK = 32 * 128 * 4;            // one tensor's [32 o][128 f] chunk
+constexpr int FWA_SLOT_BYTES = 3 * FWA_CHUNK;
+constexpr int FWA_SMEM = FWA_STAGE_BYTES + FWA_SLOTS * FWA_SLOT_BYTES + 1024;
+constexpr int FWA_THREADS = (2 + FWA_UPD_WARPS) * 32;
+constexpr int FWA_FT = 9216 / 128;  // f tiles per lane
+struct Fc1WgradAdam {
+  CUtensorMap dz3m, p2m;      // operands (bf16, SWIZZLE_128B boxes 64 x 64)
+  CUtensorMap tp, tm, tv;     // fc1.w params / m / v: fp32 [lane][128 o][9216 f], box 128 f x 32 o
   const LaneState* lanes;
-  float *params, *grads, *m1, *m2;
+  float *params, *m1, *m2, *grads;
   uint16_t* wbf;
   int64_t pstride, w_off;
-  int write_grads;
+  int write_grads, kblocks, ntiles;
+};
 
-  TLK_DEV bool work(Work& w) const {
-    w.j = blockIdx.z;
-    if (!lanes[w.j].active) return false;
-    w.m0 = 0;
-    w.n0 = blockIdx.y * BN;
-    w.kb_begin = 0;
-    w.kb_end = (buf.B + GEMM_BK - 1) / GEMM_BK;
-    w.split = 0;
-    return true;
+__global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __grid_constant__ Fc1WgradAdam p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t gfull, gempty, tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t sfull[FWA_SLOTS], sempty[FWA_SLOTS];
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t slot_base = sbase + FWA_STAGE_BYTES;
+  const uint8_t* slot_ptr = smem + FWA_STAGE_BYTES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&gfull, 1);
+    mbar_init(&gempty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], FWA_UPD_WARPS);
+    }
+    for (int s = 0; s < FWA_SLOTS; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], FWA_UPD_WARPS);
+    }
+    fence_mbar_init();
   }
-  TLK_DEV void prefetch() const {
-    tma_prefetch_desc(&buf.dz3m);
-    tma_prefetch_desc(&buf.p2m);
-  }
-  TLK_DEV void load_a(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
-    tma_load_3d(dst, &buf.dz3m, 0, kb * GEMM_BK, w.j, bar);
-    tma_load_3d(dst + 8192, &buf.dz3m, 64, kb * GEMM_BK, w.j, bar);
-  }
-  TLK_DEV void load_b(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
-    tma_load_3d(dst, &buf.p2m, w.n0, kb * GEMM_BK, w.j, bar);
-  }
-  TLK_DEV void epilogue(const Work&, int, int, const float (&)[32], Carry&) const {}
-  TLK_DEV void finish(const Work&, int, Carry&) const {}
-  // tile = dW1[128 o][64 f] in smem.  256 threads: thread -> float4 column
-  // c4 = tid % 16 of rows r0 + 16k: a warp covers two 256-B row segments per
-  // access; 2 rows (6 float4 loads) in flight per thread before any math.
-  TLK_DEV void tile_epilogue(const Work& w, float* tile, int ld) const {
-    const LaneState s = lanes[w.j];
-    const int tid = threadIdx.x, c4 = tid & 15, r0 = tid >> 4;
-    const int64_t base = w.j * pstride + w_off + w.n0 + 4 * c4;
-#pragma unroll 1
-    for (int k0 = 0; k0 < 8; k0 += 2) {
-      float4 p[2], mm[2], vv[2];
-      int64_t e[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        e[u] = base + int64_t(r0 + 16 * (k0 + u)) * 9216;
-        p[u] = *reinterpret_cast<const float4*>(params + e[u]);
-        mm[u] = *reinterpret_cast<const float4*>(m1 + e[u]);
-        vv[u] = *reinterpret_cast<const float4*>(m2 + e[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const float4 g = *reinterpret_cast<const float4*>(tile + (r0 + 16 * (k0 + u)) * ld + 4 * c4);
-        opt_update(s, p[u].x, g.x, mm[u].x, vv[u].x);
-        opt_update(s, p[u].y, g.y, mm[u].y, vv[u].y);
-        opt_update(s, p[u].z, g.z, mm[u].z, vv[u].z);
-        opt_update(s, p[u].w, g.w, mm[u].w, vv[u].w);
-        *reinterpret_cast<float4*>(params + e[u]) = p[u];
-        *reinterpret_cast<float4*>(m1 + e[u]) = mm[u];
-        *reinterpret_cast<float4*>(m2 + e[u]) = vv[u];
-        *reinterpret_cast<uint2*>(wbf + e[u]) =
-            make_uint2(pack_bf2(p[u].x, p[u].y), pack_bf2(p[u].z, p[u].w));
-        if (write_grads) *reinterpret_cast<float4*>(grads + e[u]) = g;
+  if (warp == 1) tmem_alloc<256>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_begin();
+  const uint32_t tmem = tmem_base_s;
+  constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, 128, true, true);
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      tma_prefetch_desc(&p.dz3m);
+      tma_prefetch_desc(&p.p2m);
+      tma_prefetch_desc(&p.tp);
+      tma_prefetch_desc(&p.tm);
+      tma_prefetch_desc(&p.tv);
+      int it = 0, cs = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const int j = t / FWA_FT, f0 = (t % FWA_FT) * 128;
+        if (!p.lanes[j].active) continue;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          if (it >= 1) mbar_wait(&gempty, (it - 1) & 1);
+          mbar_expect_tx(&gfull, FWA_STAGE_BYTES);
+          tma_load_3d(sbase, &p.p2m, f0, kb * GEMM_BK, j, &gfull);
+          tma_load_3d(sbase + 8192, &p.p2m, f0 + 64, kb * GEMM_BK, j, &gfull);
+          tma_load_3d(sbase + 16384, &p.dz3m, 0, kb * GEMM_BK, j, &gfull);
+          tma_load_3d(sbase + 24576, &p.dz3m, 64, kb * GEMM_BK, j, &gfull);
+        }
+        for (int c = 0; c < 4; ++c, ++cs) {
+          const int sl = cs % FWA_SLOTS;
+          if (cs >= FWA_SLOTS) mbar_wait(&sempty[sl], ((cs / FWA_SLOTS) - 1) & 1);
+          const uint32_t d = slot_base + sl * FWA_SLOT_BYTES;
+          mbar_expect_tx(&sfull[sl], FWA_SLOT_BYTES);
+          tma_load_3d(d, &p.tp, f0, 32 * c, j, &sfull[sl]);
+          tma_load_3d(d + FWA_CHUNK, &p.tm, f0, 32 * c, j, &sfull[sl]);
+          tma_load_3d(d + 2 * FWA_CHUNK, &p.tv, f0, 32 * c, j, &sfull[sl]);
+        }
       }
     }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        if (!p.lanes[t / FWA_FT].active) continue;
+        const int acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 128;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          mbar_wait(&gfull, it & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk)
+            mma_bf16(d, stage_desc_tma<GEMM_BM, true>(sbase, kk), stage_desc_tma<128, true>(sbase + 16384, kk),
+                     IDESC, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&gempty);
+        }
+        mma_commit(&tfull[acc]);
+        ++lt;
+      }
+    }
+  } else {  // update warps: TMEM lane quarter q = warp & 3 (hardware rule) -> f; og = 8-output group
+    const int q = warp & 3, og = (warp - 2) >> 2, fl = q * 32 + lane;
+    int lt = 0, cs = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const int j = t / FWA_FT, f0 = (t % FWA_FT) * 128;
+      if (!p.lanes[j].active) continue;
+      const LaneState s = p.lanes[j];
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < 4; ++c, ++cs) {
+        const int o0 = 32 * c + 8 * og;  // this thread's outputs o0 .. o0+7
+        float g[8];
+        tmem_ld8(tmem + acc * 128 + o0 + (uint32_t(q * 32) << 16), g);
+        if (c == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int sl = cs % FWA_SLOTS;
+        mbar_wait(&sfull[sl], (cs / FWA_SLOTS) & 1);
+        const float* P = reinterpret_cast<const float*>(slot_ptr + sl * FWA_SLOT_BYTES);
+        float pv[8], mv[8], vv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int off = (8 * og + i) * 128 + fl;  // [32 o][128 f]
+          pv[i] = P[off];
+          mv[i] = P[FWA_CHUNK / 4 + off];
+          vv[i] = P[FWA_CHUNK / 2 + off];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sl]);  // slot refillable as soon as it is read
+#pragma unroll
+        for (int i = 0; i < 8; ++i) opt_update(s, pv[i], g[i], mv[i], vv[i]);
+        const int64_t e = j * p.pstride + p.w_off + int64_t(o0) * 9216 + f0 + fl;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          p.params[e + int64_t(i) * 9216] = pv[i];
+          p.m1[e + int64_t(i) * 9216] = mv[i];
+          p.m2[e + int64_t(i) * 9216] = vv[i];
+          p.wbf[e + int64_t(i) * 9216] = f2bf(pv[i]);
+          if (p.write_grads) p.grads[e + int64_t(i) * 9216] = g[i];
+        }
+      }
+      ++lt;
+    }
   }
-};
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
 
 // ------------------------------------------------ conv1 wgrad (SIMT) --------
 // One CTA per (image, lane).  Thread = (8-channel chunk c, position group g):
@@ -342,6 +439,7 @@ struct Fc1WgradOpt {
 __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __restrict__ lanes,
                                                           CnnBufs buf,
                                                           const uint16_t* __restrict__ x) {
+  pdl_begin();
   const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (!lanes[j].active) return;
   extern __shared__ __align__(16) uint16_t dzs_raw[];  // this image's dz1 planes (50 KB)
@@ -425,41 +523,128 @@ __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __res
   }
 }
 
-// ------------------------------------------------ grad finalize -------------
-// Deterministic fixed-order reductions of the split partials into grads:
-// conv2.w (sum over position splits), conv2.b (sum over 144 pooled
-// positions), conv1.w / conv1.b (sum over images).
-__global__ void __launch_bounds__(256) cnn_finalize_kernel(const LaneState* __restrict__ lanes,
-                                                           CnnBufs buf, float* __restrict__ grads,
-                                                           int64_t pstride, int64_t o_c1w,
-                                                           int64_t o_c1b, int64_t o_c2w,
-                                                           int64_t o_c2b) {
+// ------------------------------------- grad finalize + optimizer ----------
+// Every parameter except fc1.w (updated in its wgrad epilogue), one float4 per
+// thread-iteration: the gradient is finalised on the fly with the fixed-order
+// reductions of the split partials -- conv2.w (sum over the position splits),
+// conv2.b (sum over the 144 pooled positions), conv1.w / conv1.b (sum over
+// images) -- or read from the arena (fc1.b, fc2 written by the head), stored
+// to the arena, and the lane's optimizer update applied (models.cuh
+// opt_update; bf16 shadow + transposed conv2.w copies).  The last CTA of a
+// lane ends the lane's step.  Replaces a finalize launch + the batched
+// optimizer launch.
+struct CnnOffs {
+  int64_t c1w, c1b, c2w, c2b;
+};
+struct CnnOpt {
+  LaneState* lanes;
+  int64_t stride, a1, b0;  // float4 units: [0, a1) u [b0, stride/4) of every lane
+  CnnOffs o;
+  float4 *P, *Gr, *M, *V;
+  uint2* Wb;
+  WtHook hook;
+};
+__device__ __forceinline__ void cnn_opt_apply(const CnnOpt& a, const LaneState& s, int j, int64_t idx,
+                                              const float (&g)[4]) {
+  const int64_t i = j * (a.stride / 4) + idx, e = idx * 4;
+  a.Gr[i] = make_float4(g[0], g[1], g[2], g[3]);
+  float4 pa = a.P[i], ma = a.M[i], va = a.V[i];
+  opt_update(s, pa.x, g[0], ma.x, va.x);
+  opt_update(s, pa.y, g[1], ma.y, va.y);
+  opt_update(s, pa.z, g[2], ma.z, va.z);
+  opt_update(s, pa.w, g[3], ma.w, va.w);
+  a.P[i] = pa;
+  a.M[i] = ma;
+  a.V[i] = va;
+  const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
+  a.Wb[i] = make_uint2(lo, hi);
+  if (e >= a.hook.off && e < a.hook.off + a.hook.count) {
+    wt_write(a.hook, j, e + 0, uint16_t(lo & 0xFFFF));
+    wt_write(a.hook, j, e + 1, uint16_t(lo >> 16));
+    wt_write(a.hook, j, e + 2, uint16_t(hi & 0xFFFF));
+    wt_write(a.hook, j, e + 3, uint16_t(hi >> 16));
+  }
+}
+// CTAs 0..11 of a lane: the 96 float4 whose gradients are long reductions
+// (conv1.w / conv1.b over the batch's images, conv2.b over the 144 pooled
+// positions), one warp per float4: lane l sums terms l, l+32, ... in order,
+// then a fixed xor-shuffle tree.  CTAs 12..: everything else, one float4 per
+// thread.
+constexpr int CNN_OPT_HEAVY = 12;
+__global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ CnnOpt a, CnnBufs buf) {
+  pdl_begin();
   const int j = blockIdx.y;
-  if (!lanes[j].active) return;
-  float* G = grads + j * pstride;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < 18432) {  // e = oc*288 + tap*32 + ic
-    const int oc = e / 288, r = e % 288, tap = r >> 5, ic = r & 31;
-    const float* pp = buf.part2 + ((int64_t(j) * C2W_SPLITS * 9 + tap) * 64 + oc) * 32 + ic;
-    float s = 0.f;
-#pragma unroll 6
-    for (int k = 0; k < C2W_SPLITS; ++k) s += pp[int64_t(k) * 9 * 64 * 32];
-    G[o_c2w + e] = s;
-  } else if (e < 18432 + 64) {
-    const int c = e - 18432;
-    const float* cs = buf.colsum + int64_t(j) * 9216 + c;
-    float s = 0.f;
-    for (int pos = 0; pos < 144; ++pos) s += cs[pos * 64];
-    G[o_c2b + c] = s;
-  } else if (e < 18432 + 64 + 320) {
-    const int r = e - 18432 - 64, o = r / 10, t = r % 10;
-    const float* pp = buf.part1 + int64_t(j) * buf.B * 320 + r;
-    float s = 0.f;
-    for (int k = 0; k < buf.B; ++k) s += pp[int64_t(k) * 320];
-    if (t < 9)
-      G[o_c1w + o * 9 + t] = s;
-    else
-      G[o_c1b + o] = s;
+  if (!a.lanes[j].active) return;
+  const LaneState s = a.lanes[j];
+  const CnnOffs& o = a.o;
+  if (blockIdx.x < CNN_OPT_HEAVY) {
+    const int l = threadIdx.x & 31;
+    const int h = blockIdx.x * 8 + (threadIdx.x >> 5);  // 0..71 conv1.w, 72..79 conv1.b, 80..95 conv2.b
+    {
+      float g[4] = {0.f, 0.f, 0.f, 0.f};
+      int64_t e;
+      if (h < 80) {
+        const bool wt = h < 72;
+        e = wt ? o.c1w + 4 * h : o.c1b + 4 * (h - 72);
+        const float* pp = buf.part1 + int64_t(j) * buf.B * 320;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = wt ? 4 * h + q : 4 * (h - 72) + q;
+          const int col = wt ? (r / 9) * 10 + r % 9 : r * 10 + 9;
+          for (int k = l; k < buf.B; k += 32) g[q] += pp[int64_t(k) * 320 + col];
+        }
+      } else {
+        const int c = 4 * (h - 80);
+        e = o.c2b + c;
+        const float* cs = buf.colsum + int64_t(j) * 9216 + c;
+        for (int pos = l; pos < 144; pos += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(cs + pos * 64);
+          g[0] += v.x, g[1] += v.y, g[2] += v.z, g[3] += v.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int m = 16; m; m >>= 1) g[q] += __shfl_xor_sync(0xffffffffu, g[q], m);
+      if (l == 0) cnn_opt_apply(a, s, j, e / 4, g);
+    }
+  } else {
+    const int64_t s4 = a.stride / 4, work = a.a1 + (s4 - a.b0);
+    const int nl = gridDim.x - CNN_OPT_HEAVY;
+    const int64_t per = (work + nl - 1) / nl;
+    const int64_t w0 = (blockIdx.x - CNN_OPT_HEAVY) * per, w1 = min(work, w0 + per);
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+      const int64_t idx = w < a.a1 ? w : a.b0 + (w - a.a1);
+      const int64_t e = idx * 4;
+      if ((e >= o.c1w && e < o.c1w + 288) || (e >= o.c1b && e < o.c1b + 32) || (e >= o.c2b && e < o.c2b + 64))
+        continue;  // heavy CTAs
+      float g[4];
+      if (e >= o.c2w && e < o.c2w + CONV2_W) {
+        const int r = int(e - o.c2w), oc = r / 288, t = r % 288, tap = t >> 5, ic = t & 31;
+        const float* pp = buf.part2 + ((int64_t(j) * C2W_SPLITS * 9 + tap) * 64 + oc) * 32 + ic;
+        float4 v[C2W_SPLITS];
+#pragma unroll
+        for (int k = 0; k < C2W_SPLITS; ++k) v[k] = *reinterpret_cast<const float4*>(pp + int64_t(k) * 9 * 64 * 32);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < C2W_SPLITS; ++k) acc.x += v[k].x, acc.y += v[k].y, acc.z += v[k].z, acc.w += v[k].w;
+        g[0] = acc.x, g[1] = acc.y, g[2] = acc.z, g[3] = acc.w;
+      } else {
+        const float4 v = a.Gr[j * s4 + idx];
+        g[0] = v.x, g[1] = v.y, g[2] = v.z, g[3] = v.w;
+      }
+      cnn_opt_apply(a, s, j, idx, g);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&a.lanes[j].done_ctas, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      a.lanes[j].done_ctas = 0;
+      lane_end_step(a.lanes[j]);
+    }
   }
 }
 
@@ -534,6 +719,15 @@ int cnn_setup(Pack& p) {
       return rc;
     if ((rc = make_tmap_bf16_3d(&b->dz3m, b->dz3, 128, B, L, 128 * 2, b->h3_st * 2, 64, 64)))
       return rc;
+    const int64_t ws = 9216;  // fc1.w row (one output unit) in floats
+    const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    if ((rc = make_tmap_3d(&b->fa_p, F32, p.params + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 32,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)) ||
+        (rc = make_tmap_3d(&b->fa_m, F32, p.mom1 + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 32,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)) ||
+        (rc = make_tmap_3d(&b->fa_v, F32, p.mom2 + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 32,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)))
+      return rc;
   }
   void* wt = nullptr;
   p.wt_stride = 2 * CONV2_W;
@@ -545,9 +739,10 @@ int cnn_setup(Pack& p) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ConvPolicy<false>::SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv1_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C1W_SMEM));
+  TLK_CUDA(cudaFuncSetAttribute(fc1_wgrad_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWA_SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
-  p.launches_per_step = 13;
+  p.launches_per_step = 11;
   p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
   p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
@@ -563,42 +758,51 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   const int64_t o_f2w = tensor_offset(d, 6), o_f2b = tensor_offset(d, 7);
   const ConvArgs ca = conv_args(p, b);
   int rc;
-  if ((rc = enqueue_inputs(p, st))) return rc;
-  conv1_fwd_kernel<<<dim3(B, L), 256, 0, st>>>(p.lane_dev, p.x, p.params, p.stride, o_c1w, o_c1b, b);
-  p.mark(st, "conv1_fwd");
+  TLK_CUDA(launch(conv1_fwd_kernel, dim3(B, L), 256, 0, st, p.lane_dev, p.teacher, p.pixels, p.labels, p.x,
+                  p.host_input, p.params, p.stride, o_c1w, o_c1b, b));
+  p.mark(st, "inputs_conv1_fwd");
   TLK_CUDA(cudaGetLastError());
-  conv2_tc_kernel<true><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<true>::SMEM, st>>>(ca);
+  TLK_CUDA(launch(conv2_tc_kernel<true>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<true>::SMEM, st, ca));
   p.mark(st, "conv2_fwd_pool");
   TLK_CUDA(cudaGetLastError());
   Fc1Fwd f1{b, p.lane_dev};
   TLK_CUDA(launch_gemm_tma(f1, dim3(1, 1, L * FC1_SPLITS), st));
   p.mark(st, "fc1_fwd_splitk");
-  fc1_reduce_kernel<<<dim3(128 * 64 / 256, L), 256, 0, st>>>(p.lane_dev, b, p.params, p.stride,
-                                                              o_f1b);
+  TLK_CUDA(launch(fc1_reduce_kernel, dim3(128 * 64 / 256, L), 256, 0, st, p.lane_dev, b, p.params, p.stride,
+                                                              o_f1b));
   p.mark(st, "fc1_reduce");
   TLK_CUDA(cudaGetLastError());
   if ((rc = enqueue_head(p, st, b.h3, 128, o_f2w, o_f2b, b.dz3, o_f1b))) return rc;
   Fc1Dgrad f1d{b, p.lane_dev};  // reads this step's fc1 weights
   TLK_CUDA(launch_gemm_tma(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
-  conv2_wgrad_tc_kernel<<<dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st>>>(ca);
+  TLK_CUDA(launch(conv2_wgrad_tc_kernel, dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st, ca));
   p.mark(st, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
-  conv2_tc_kernel<false><<<dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st>>>(ca);
+  TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
-  conv1_wgrad_kernel<<<dim3(B, L), 128, C1W_SMEM, st>>>(p.lane_dev, b, p.x);
+  TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), 128, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
-  Fc1WgradOpt f1w{b, p.lane_dev, p.params, p.grads, p.mom1, p.mom2, p.wbf, p.stride, o_f1w,
-                  (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0};
-  TLK_CUDA(launch_gemm_tma(f1w, dim3(1, 9216 / Fc1WgradOpt::BN, L), st));
+  {
+    Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, p.lane_dev, p.params, p.mom1, p.mom2, p.grads, p.wbf,
+                   p.stride, o_f1w,
+                   (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0, (B + GEMM_BK - 1) / GEMM_BK, L * FWA_FT};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(std::min(sms, L * FWA_FT)), FWA_THREADS, FWA_SMEM, st, f));
+  }
   p.mark(st, "fc1_wgrad_adam");
-  cnn_finalize_kernel<<<dim3((18432 + 64 + 320 + 255) / 256, L), 256, 0, st>>>(
-      p.lane_dev, b, p.grads, p.stride, o_c1w, o_c1b, o_c2w, o_c2b);
-  p.mark(st, "grad_finalize");
-  TLK_CUDA(cudaGetLastError());
-  if ((rc = enqueue_optimizer(p, st))) return rc;
+  {
+    const CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
+                   reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),
+                   reinterpret_cast<float4*>(p.mom1), reinterpret_cast<float4*>(p.mom2),
+                   reinterpret_cast<uint2*>(p.wbf), WtHook{p.wt, p.wt_stride, o_c2w, CONV2_W}};
+    TLK_CUDA(launch(cnn_opt_kernel, dim3(CNN_OPT_HEAVY + CNN_OPT_CTAS, L), 256, 0, st, a, b));
+    p.mark(st, "grad_finalize_opt");
+  }
   return enqueue_end_step(p, st);
 }
 

@@ -49,4 +49,21 @@ __host__ __device__ constexpr int wd_index(int oc, int tap, int ic) {
 }
 
 
+// Optimizer hook: refresh the transposed conv2.w copies wherever the bf16
+// shadow of an element is written (kernels.cu optimizer, cnn.cu cnn_opt).
+struct WtHook {
+  uint16_t* wt;
+  int64_t wt_stride;
+  int64_t off;    // start of the source tensor in the arena
+  int64_t count;  // its element count
+};
+__device__ __forceinline__ void wt_write(const WtHook& h, int lane, int64_t e, uint16_t b) {
+  if (!h.wt) return;
+  int64_t r = e - h.off;
+  if (r < 0 || r >= h.count) return;
+  const int oc = int(r / 288), t = int(r % 288), tap = t >> 5, ic = t & 31;
+  uint16_t* w = h.wt + lane * h.wt_stride;
+  w[wf_index(oc, tap, ic)] = b;  // conv2 fwd B operand
+  w[wd_index(oc, tap, ic)] = b;  // conv2 dgrad B operand
+}
 }  // namespace tlk

@@ -24,7 +24,6 @@ struct ConvArgs {
   int wgrad_splits;
 };
 
-TLK_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // ------------------------------------------- persistent conv2 fwd / dgrad --
 // Grid = (CTAS_PER_LANE, lanes); a CTA keeps its lane's weight operand
@@ -62,6 +61,7 @@ constexpr int CONV_THREADS = 192;
 
 template <bool FWD>
 __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
+  pdl_begin();
   using P = ConvPolicy<FWD>;
   const int j = blockIdx.y;
   if (!a.lanes[j].active) return;
@@ -262,6 +262,7 @@ constexpr int WG_SMEM = WG_STAGES * WG_STAGE + 128;
 constexpr uint32_t WG_TX = 12 * WG_ACOPY + WG_B_BYTES;
 
 __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
+  pdl_begin();
   const int split = blockIdx.x, j = blockIdx.y;
   if (!a.lanes[j].active) return;
   extern __shared__ __align__(128) uint8_t sm[];

@@ -60,6 +60,7 @@ inline int T_LNFG(const GptCfg& c) { return 2 + 12 * c.layers; }
 // ------------------------------------------------------------- tokens -------
 __global__ void gpt_tokens_kernel(const LaneState* __restrict__ lanes, int B, int T, int V,
                                   int32_t* __restrict__ tokens, int32_t* __restrict__ targets) {
+  pdl_begin();
   const int s = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (s >= B || !lanes[j].active) return;
   const uint64_t key = rng_key(lanes[j].seed, STREAM_TOKENS, uint64_t(lanes[j].steps_done));
@@ -80,6 +81,7 @@ __global__ void gpt_tokens_kernel(const LaneState* __restrict__ lanes, int B, in
 __global__ void gpt_embed_kernel(const LaneState* __restrict__ lanes, GptCfg c, int B,
                                  const int32_t* __restrict__ tokens, const float* __restrict__ params,
                                  int64_t pstride, int64_t o_wte, int64_t o_wpe, float* __restrict__ x) {
+  pdl_begin();
   const int row = blockIdx.x, j = blockIdx.y;
   if (!lanes[j].active) return;
   const int b = row / c.T, t = row % c.T;
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LaneState* __restrict
                                                      int64_t pstride, int64_t og, int64_t ob,
                                                      uint16_t* __restrict__ y,
                                                      float* __restrict__ stats) {
+  pdl_begin();
   const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
   const int row = blockIdx.x * 8 + warp;
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     const float* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ params,
     int64_t pstride, int64_t og, float* __restrict__ dxt, uint16_t* __restrict__ dxb, int accumulate,
     float* __restrict__ part, int64_t part_st) {
+  pdl_begin();
   constexpr int d = 128 * KV;
   const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
@@ -238,6 +242,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
 __global__ void attn_rowdot_kernel(const LaneState* __restrict__ lanes, int N, int T, int H,
                                    const uint16_t* __restrict__ dy, const uint16_t* __restrict__ y,
                                    float* __restrict__ D) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // token * H + h
@@ -268,6 +273,7 @@ constexpr int CS_ROWS = 64;
 __global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const uint16_t* __restrict__ src,
                                    int64_t src_ls, int ld, int N, int C, float* __restrict__ part,
                                    int64_t part_st) {
+  pdl_begin();
   const int cg = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
   if (!lanes[j].active || cg * 8 >= C) return;
   const uint16_t* s = src + j * src_ls + int64_t(blk) * CS_ROWS * ld + cg * 8;
@@ -292,6 +298,7 @@ __global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const ui
 __global__ void reduce_parts_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
                                     int64_t part_st, int nblk, int C, float* __restrict__ grads,
                                     int64_t pstride, int64_t off0, int split, int64_t off1) {
+  pdl_begin();
   const int c = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (!lanes[j].active || c >= C) return;
   const float* p = part + j * part_st + c;
@@ -305,6 +312,7 @@ __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ l
                                                        const float* __restrict__ lossrow,
                                                        float* __restrict__ loss, int max_steps,
                                                        float* __restrict__ last_loss) {
+  pdl_begin();
   const int j = blockIdx.x, tid = threadIdx.x;
   if (!lanes[j].active) return;
   __shared__ float red[512];
@@ -330,6 +338,7 @@ constexpr int EMB_ROWS = 256;
 __global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int d, int V, int cols,
                                  const int32_t* __restrict__ tokens, int T, const float* __restrict__ dx,
                                  float* __restrict__ part, int64_t part_st) {
+  pdl_begin();
   const int blk = blockIdx.x, cg = blockIdx.y, j = blockIdx.z, c = cg * cols + threadIdx.x;
   if (!lanes[j].active) return;
   extern __shared__ float acc[];  // [V][cols]
@@ -364,6 +373,7 @@ __global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int
 __global__ void wpe_bwd_kernel(const LaneState* __restrict__ lanes, int B, int T, int d,
                                const float* __restrict__ dx, float* __restrict__ grads,
                                int64_t pstride, int64_t o_wpe) {
+  pdl_begin();
   const int t = blockIdx.x, j = blockIdx.y;
   if (!lanes[j].active) return;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
@@ -527,19 +537,19 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     ++count;
   };
 
-  gpt_tokens_kernel<<<dim3((B + 127) / 128, Lc), 128, 0, st>>>(LS, B, T, V, b.tokens, b.targets);
+  TLK_CUDA(launch(gpt_tokens_kernel, dim3((B + 127) / 128, Lc), 128, 0, st, LS, B, T, V, b.tokens, b.targets));
   TLK_CUDA(cudaGetLastError());
   marked("tokens");
   float* x0 = c.layers ? b.L[0].xin : b.xL;
-  gpt_embed_kernel<<<dim3(N, Lc), 128, 0, st>>>(LS, c, B, b.tokens, PR, PS, O(T_WTE), O(T_WPE), x0);
+  TLK_CUDA(launch(gpt_embed_kernel, dim3(N, Lc), 128, 0, st, LS, c, B, b.tokens, PR, PS, O(T_WTE), O(T_WPE), x0));
   TLK_CUDA(cudaGetLastError());
   marked("embed");
 
   for (int l = 0; l < c.layers; ++l) {
     LayerBufs& lb = b.L[l];
     float* xnext = (l + 1 < c.layers) ? b.L[l + 1].xin : b.xL;
-    ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, lb.xin, PR, PS, O(T_LAYER(l, K_LN1G)),
-                                                         O(T_LAYER(l, K_LN1B)), lb.a, lb.st1);
+    TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, lb.xin, PR, PS, O(T_LAYER(l, K_LN1G)),
+                                                         O(T_LAYER(l, K_LN1B)), lb.a, lb.st1));
     TLK_CUDA(cudaGetLastError());
     marked("ln1");
     {  // qkv = a Wqkv^T + b
@@ -582,8 +592,8 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                               d, d, 1, 1, "proj")));
       ++count;
     }
-    ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, lb.xmid, PR, PS, O(T_LAYER(l, K_LN2G)),
-                                                         O(T_LAYER(l, K_LN2B)), lb.m, lb.st2);
+    TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, lb.xmid, PR, PS, O(T_LAYER(l, K_LN2G)),
+                                                         O(T_LAYER(l, K_LN2B)), lb.m, lb.st2));
     TLK_CUDA(cudaGetLastError());
     marked("ln2");
     {  // z = m W1^T + b1, f = gelu(z)
@@ -608,8 +618,8 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     }
   }
   const int tf = T_LNFG(c);
-  ln_fwd_kernel<<<dim3((N + 7) / 8, Lc), 256, 0, st>>>(LS, N, d, b.xL, PR, PS, O(tf), O(tf + 1), b.xf,
-                                                       b.stf);
+  TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, b.xL, PR, PS, O(tf), O(tf + 1), b.xf,
+                                                       b.stf));
   TLK_CUDA(cudaGetLastError());
   marked("lnf");
   {  // logits -> CE row epilogue: lossrow, dl = (softmax - onehot) / N
@@ -630,7 +640,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_TRY((gemm<256, false, false, true>(p, st, A, Bh, e, N, Vp, d, 1, 1, "head_ce")));
     ++count;
   }
-  gpt_loss_kernel<<<Lc, 512, 0, st>>>(p.lane_dev, N, b.lossrow, p.loss, p.max_steps, p.last_loss);
+  TLK_CUDA(launch(gpt_loss_kernel, Lc, 512, 0, st, p.lane_dev, N, b.lossrow, p.loss, p.max_steps, p.last_loss));
   TLK_CUDA(cudaGetLastError());
   marked("loss");
 
@@ -652,26 +662,26 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     const size_t sm = 16 * size_t(d) * 4;
     switch (d / 128) {
       case 1:
-        ln_bwd_kernel<1><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
-                                                b.part, b.part_st);
+        TLK_CUDA(launch(ln_bwd_kernel<1>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st));
         break;
       case 2:
-        ln_bwd_kernel<2><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
-                                                b.part, b.part_st);
+        TLK_CUDA(launch(ln_bwd_kernel<2>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st));
         break;
       case 3:
-        ln_bwd_kernel<3><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
-                                                b.part, b.part_st);
+        TLK_CUDA(launch(ln_bwd_kernel<3>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st));
         break;
       default:
-        ln_bwd_kernel<4><<<grid, 256, sm, st>>>(LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
-                                                b.part, b.part_st);
+        TLK_CUDA(launch(ln_bwd_kernel<4>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+                                                b.part, b.part_st));
         break;
     }
     TLK_CUDA(cudaGetLastError());
     marked(name);
-    reduce_parts_kernel<<<dim3((2 * d + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, 2 * d,
-                                                                     G, PS, O(og), d, O(ob));
+    TLK_CUDA(launch(reduce_parts_kernel, dim3((2 * d + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, 2 * d,
+                                                                     G, PS, O(og), d, O(ob)));
     TLK_CUDA(cudaGetLastError());
     marked("ln_param_grads");
     return TLK_OK;
@@ -679,12 +689,12 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   auto bias_grad = [&](const uint16_t* src, int C, int t) -> int {
     const int nblk = (N + CS_ROWS - 1) / CS_ROWS;
     const int cgs = C / 8, th = std::min(128, (cgs + 31) / 32 * 32);
-    colsum_bf16_kernel<<<dim3((cgs + th - 1) / th, nblk, Lc), th, 0, st>>>(LS, src, int64_t(N) * C, C, N, C,
-                                                                          b.part, b.part_st);
+    TLK_CUDA(launch(colsum_bf16_kernel, dim3((cgs + th - 1) / th, nblk, Lc), th, 0, st, LS, src, int64_t(N) * C, C, N, C,
+                                                                          b.part, b.part_st));
     TLK_CUDA(cudaGetLastError());
     marked("bias_colsum");
-    reduce_parts_kernel<<<dim3((C + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, C, G, PS,
-                                                                   O(t), C, O(t));
+    TLK_CUDA(launch(reduce_parts_kernel, dim3((C + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, C, G, PS,
+                                                                   O(t), C, O(t)));
     TLK_CUDA(cudaGetLastError());
     marked("bias_reduce");
     return TLK_OK;
@@ -731,7 +741,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       count += 2;
     }
     {  // attention backward per (sequence, head)
-      attn_rowdot_kernel<<<dim3((N * H + 255) / 256, Lc), 256, 0, st>>>(LS, N, T, H, b.dy, lb.y, b.D);
+      TLK_CUDA(launch(attn_rowdot_kernel, dim3((N * H + 255) / 256, Lc), 256, 0, st, LS, N, T, H, b.dy, lb.y, b.D));
       TLK_CUDA(cudaGetLastError());
       marked("attn_rowdot");
       Epi e = epi(EPI_SOFTMAX_BWD, T, T, b.dS, pl, int64_t(H) * tt, tt, T);
@@ -783,15 +793,14 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   {  // embeddings
     const int cols = std::min(d, (50000 / V) / 32 * 32);  // acc[V][cols] fp32 <= 200 KB
     const int nblk = (N + EMB_ROWS - 1) / EMB_ROWS;
-    embed_bwd_kernel<<<dim3(nblk, (d + cols - 1) / cols, Lc), cols, V * cols * 4, st>>>(
-        LS, N, d, V, cols, b.tokens, T, b.dx, b.part, b.part_st);
+    TLK_CUDA(launch(embed_bwd_kernel, dim3(nblk, (d + cols - 1) / cols, Lc), cols, V * cols * 4, st, LS, N, d, V, cols, b.tokens, T, b.dx, b.part, b.part_st));
     TLK_CUDA(cudaGetLastError());
     marked("wte_partial");
-    reduce_parts_kernel<<<dim3((V * d + 255) / 256, Lc), 256, 0, st>>>(LS, b.part, b.part_st, nblk, V * d,
-                                                                       G, PS, O(T_WTE), V * d, O(T_WTE));
+    TLK_CUDA(launch(reduce_parts_kernel, dim3((V * d + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, V * d,
+                                                                       G, PS, O(T_WTE), V * d, O(T_WTE)));
     TLK_CUDA(cudaGetLastError());
     marked("wte_reduce");
-    wpe_bwd_kernel<<<dim3(T, Lc), 128, 0, st>>>(LS, B, T, d, b.dx, G, PS, O(T_WPE));
+    TLK_CUDA(launch(wpe_bwd_kernel, dim3(T, Lc), 128, 0, st, LS, B, T, d, b.dx, G, PS, O(T_WPE)));
     TLK_CUDA(cudaGetLastError());
     marked("wpe");
   }

@@ -1,0 +1,72 @@
+// One MNIST-shaped sample of a lane's step, produced by a whole CTA: the 784
+// pixel codes (counter RNG, or the host-input buffer), their bf16 k/256 copy
+// and the exact int32 teacher label (oracle/rng.py: data + teacher_label).
+// Shared by the generic inputs kernel (kernels.cu) and the CNN's fused
+// inputs + conv1 kernel (cnn.cu).  pix: CTA shared buffer of PIXELS bytes
+// (16-byte aligned); part: NW x CLASSES ints of shared scratch.
+#pragma once
+#include "pack.cuh"
+#include "rng.cuh"
+#include "tlk_ptx.cuh"
+
+namespace tlk {
+
+template <int NT>
+__device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, size_t row, int host_input,
+                                              const int8_t* __restrict__ teacher, uint8_t* __restrict__ px,
+                                              int32_t* __restrict__ labels, uint16_t* __restrict__ x,
+                                              uint8_t* pix, int (*part)[CLASSES]) {
+  const int tid = threadIdx.x;
+  uint64_t* px_row = reinterpret_cast<uint64_t*>(px + row * PIXELS);
+  if (!host_input) {
+    const uint64_t key = rng_key(seed, STREAM_DATA, uint64_t(step));
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += NT) {
+      uint64_t h = rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
+      reinterpret_cast<uint64_t*>(pix)[q] = h;
+      px_row[q] = h;
+    }
+  } else {
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += NT) reinterpret_cast<uint64_t*>(pix)[q] = px_row[q];
+  }
+  __syncthreads();
+  if (x) {
+    uint4* xr = reinterpret_cast<uint4*>(x + row * PIXELS);
+    for (int q = tid; q < WORDS_PER_SAMPLE; q += NT) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[i] = pack_bf2(float(pix[q * 8 + 2 * i]) * (1.0f / 256.0f), float(pix[q * 8 + 2 * i + 1]) * (1.0f / 256.0f));
+      xr[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  if (host_input) return;
+  int acc[CLASSES];
+#pragma unroll
+  for (int c = 0; c < CLASSES; ++c) acc[c] = 0;
+  for (int i = tid; i < PIXELS; i += NT) {
+    const int v = 2 * int(pix[i]) - 255;
+#pragma unroll
+    for (int c = 0; c < CLASSES; ++c) acc[c] += int(teacher[c * PIXELS + i]) * v;
+  }
+#pragma unroll
+  for (int c = 0; c < CLASSES; ++c) {
+    int a = acc[c];
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((tid & 31) == 0) part[tid >> 5][c] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int best = 0, bestv = 0;
+    for (int c = 0; c < CLASSES; ++c) {
+      int v = 0;
+      for (int w = 0; w < NT / 32; ++w) v += part[w][c];
+      if (c == 0 || v > bestv) {
+        best = c;
+        bestv = v;
+      }
+    }
+    labels[row] = best;
+  }
+}
+
+}  // namespace tlk

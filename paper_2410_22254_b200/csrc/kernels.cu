@@ -8,6 +8,7 @@
 #include "rng.cuh"
 #include "tlk_ptx.cuh"
 #include "conv_layout.cuh"
+#include "inputs.cuh"
 
 namespace tlk {
 
@@ -32,6 +33,7 @@ __global__ void __launch_bounds__(128) inputs_kernel(const LaneState* __restrict
                                                      uint8_t* __restrict__ px,
                                                      int32_t* __restrict__ labels,
                                                      uint16_t* __restrict__ x, int host_input) {
+  pdl_begin();
   const int s = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (lanes) {
     if (!lanes[j].active) return;
@@ -40,63 +42,12 @@ __global__ void __launch_bounds__(128) inputs_kernel(const LaneState* __restrict
   }
   __shared__ __align__(16) uint8_t pix[PIXELS];
   __shared__ int part[4][CLASSES];
-  const size_t row = size_t(j) * batch + s;
-  uint64_t* px_row = reinterpret_cast<uint64_t*>(px + row * PIXELS);
-  if (!host_input) {
-    const uint64_t key = rng_key(seed, STREAM_DATA, uint64_t(step));
-    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x) {
-      uint64_t h = rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
-      reinterpret_cast<uint64_t*>(pix)[q] = h;
-      px_row[q] = h;
-    }
-  } else {
-    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x)
-      reinterpret_cast<uint64_t*>(pix)[q] = px_row[q];
-  }
-  __syncthreads();
-  if (x) {
-    uint4* xr = reinterpret_cast<uint4*>(x + row * PIXELS);
-    for (int q = tid; q < WORDS_PER_SAMPLE; q += blockDim.x) {
-      uint32_t w[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        w[i] = pack_bf2(float(pix[q * 8 + 2 * i]) * (1.0f / 256.0f),
-                        float(pix[q * 8 + 2 * i + 1]) * (1.0f / 256.0f));
-      xr[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-  }
-  if (host_input) return;
-  int acc[CLASSES];
-#pragma unroll
-  for (int c = 0; c < CLASSES; ++c) acc[c] = 0;
-  for (int i = tid; i < PIXELS; i += blockDim.x) {
-    const int v = 2 * int(pix[i]) - 255;
-#pragma unroll
-    for (int c = 0; c < CLASSES; ++c) acc[c] += int(teacher[c * PIXELS + i]) * v;
-  }
-#pragma unroll
-  for (int c = 0; c < CLASSES; ++c) {
-    int a = acc[c];
-    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if ((tid & 31) == 0) part[tid >> 5][c] = a;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int best = 0, bestv = 0;
-    for (int c = 0; c < CLASSES; ++c) {
-      int v = part[0][c] + part[1][c] + part[2][c] + part[3][c];
-      if (c == 0 || v > bestv) {
-        best = c;
-        bestv = v;
-      }
-    }
-    labels[row] = best;
-  }
+  sample_inputs<128>(seed, step, s, size_t(j) * batch + s, host_input, teacher, px, labels, x, pix, part);
 }
 
 int enqueue_inputs(Pack& p, cudaStream_t st) {
-  inputs_kernel<<<dim3(p.batch, p.lanes), 128, 0, st>>>(p.lane_dev, 0, 0, p.batch, p.teacher,
-                                                       p.pixels, p.labels, p.x, p.host_input);
+  TLK_CUDA(launch(inputs_kernel, dim3(p.batch, p.lanes), 128, 0, st, p.lane_dev, 0, 0, p.batch, p.teacher,
+                                                       p.pixels, p.labels, p.x, p.host_input));
   p.mark(st, "inputs");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
@@ -104,8 +55,8 @@ int enqueue_inputs(Pack& p, cudaStream_t st) {
 
 int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teacher, uint8_t* px,
                         int32_t* labels, cudaStream_t st) {
-  inputs_kernel<<<dim3(batch, 1), 128, 0, st>>>(nullptr, seed, step, batch, teacher, px, labels,
-                                                nullptr, 0);
+  TLK_CUDA(launch(inputs_kernel, dim3(batch, 1), 128, 0, st, nullptr, seed, step, batch, teacher, px, labels,
+                                                nullptr, 0));
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }
@@ -115,22 +66,7 @@ int enqueue_datagen_raw(uint64_t seed, int step, int batch, const int8_t* teache
 // shadow is written.  CNN: conv2.w (oc, tap, ic) -> the two K-major,
 // core-matrix-ordered operand blobs of the conv2 fwd / dgrad kernels
 // (conv_tc.cuh: wf_index, wd_index), each TMA-bulk-copied as is.
-struct WtHook {
-  uint16_t* wt;
-  int64_t wt_stride;
-  int64_t off;    // start of the source tensor in the arena
-  int64_t count;  // its element count
-};
-__device__ __forceinline__ void wt_write(const WtHook& h, int lane, int64_t e, uint16_t b) {
-  if (!h.wt) return;
-  int64_t r = e - h.off;
-  if (r < 0 || r >= h.count) return;
-  const int oc = int(r / 288), t = int(r % 288), tap = t >> 5, ic = t & 31;
-  uint16_t* w = h.wt + lane * h.wt_stride;
-  w[wf_index(oc, tap, ic)] = b;  // conv2 fwd B operand
-  w[wd_index(oc, tap, ic)] = b;  // conv2 dgrad B operand
-}
-static WtHook wt_hook(const Pack& p) {
+WtHook wt_hook(const Pack& p) {
   WtHook h{nullptr, 0, 0, 0};
   if (p.model == TLK_MODEL_CNN && p.wt) {
     h.wt = p.wt;
@@ -180,6 +116,7 @@ std::vector<TensorInfo> model_tensors(int model, const GptCfg& c) {
 __global__ void lane_init_kernel(const TensorInfo* __restrict__ tt, int nt, uint64_t seed, int lane,
                                  int64_t stride, float* params, float* grads, float* m1, float* m2,
                                  uint16_t* wbf, WtHook hook) {
+  pdl_begin();
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < stride;
        e += int64_t(gridDim.x) * blockDim.x) {
     float v = 0.0f;
@@ -211,9 +148,9 @@ __global__ void lane_init_kernel(const TensorInfo* __restrict__ tt, int nt, uint
 int enqueue_lane_init(Pack& p, int lane, cudaStream_t st) {
   int blocks = int((p.stride + 255) / 256);
   if (blocks > 1184) blocks = 1184;
-  lane_init_kernel<<<blocks, 256, 0, st>>>(p.tinfo_dev, int(p.tinfo.size()), p.lane_host[lane].seed,
+  TLK_CUDA(launch(lane_init_kernel, blocks, 256, 0, st, p.tinfo_dev, int(p.tinfo.size()), p.lane_host[lane].seed,
                                             lane, p.stride, p.params, p.grads, p.mom1, p.mom2, p.wbf,
-                                            wt_hook(p));
+                                            wt_hook(p)));
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
 }
@@ -234,6 +171,7 @@ __global__ void __launch_bounds__(256) head_kernel(LaneState* __restrict__ lanes
                                                    uint16_t* __restrict__ dz_prev,
                                                    int64_t db_prev_off, float* __restrict__ loss,
                                                    int max_steps, float* __restrict__ last_loss) {
+  pdl_begin();
   // grid = (H / HS, lanes): every CTA recomputes the lane's logits + CE (a few
   // 10k MACs) and owns hidden units [k0, k0 + HS) of the backward; CTA 0
   // also writes the loss, the classifier bias grad and the step scalars.
@@ -356,13 +294,11 @@ int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_
     configured = true;
   }
   if (hidden == 512)
-    head_kernel<512, 32><<<dim3(512 / 32, p.lanes), 256, smem, st>>>(
-        p.lane_dev, p.batch, h, p.params, p.grads, p.stride, w_off, b_off, p.labels, dz_prev,
-        db_prev_off, p.loss, p.max_steps, p.last_loss);
+    TLK_CUDA(launch(head_kernel<512, 32>, dim3(512 / 32, p.lanes), 256, smem, st, p.lane_dev, p.batch, h, p.params, p.grads, p.stride, w_off, b_off, p.labels, dz_prev,
+        db_prev_off, p.loss, p.max_steps, p.last_loss));
   else if (hidden == 128)
-    head_kernel<128, 16><<<dim3(128 / 16, p.lanes), 256, smem, st>>>(
-        p.lane_dev, p.batch, h, p.params, p.grads, p.stride, w_off, b_off, p.labels, dz_prev,
-        db_prev_off, p.loss, p.max_steps, p.last_loss);
+    TLK_CUDA(launch(head_kernel<128, 16>, dim3(128 / 16, p.lanes), 256, smem, st, p.lane_dev, p.batch, h, p.params, p.grads, p.stride, w_off, b_off, p.labels, dz_prev,
+        db_prev_off, p.loss, p.max_steps, p.last_loss));
   else
     return fail(TLK_EINVAL, "head: unsupported hidden %d", hidden);
   p.mark(st, "head");
@@ -389,6 +325,7 @@ __global__ void __launch_bounds__(256) optimizer_kernel(LaneState* __restrict__ 
                                                         float4* __restrict__ M,
                                                         float4* __restrict__ V,
                                                         uint2* __restrict__ Wb, WtHook hook) {
+  pdl_begin();
   const int lane = blockIdx.y;
   if (!lanes[lane].active) return;
   const LaneState s = lanes[lane];
@@ -477,10 +414,9 @@ int enqueue_optimizer_range(Pack& p, cudaStream_t st, int64_t lo, int64_t hi, bo
   int64_t per_lane = (work + 511) / 512;  // ~2 float4 per thread
   const int64_t cap = std::max<int64_t>(1, int64_t(sms) * 8 / p.lanes);
   per_lane = std::min(std::max<int64_t>(per_lane, 1), cap);
-  optimizer_kernel<<<dim3(unsigned(per_lane), p.lanes), 256, 0, st>>>(
-      p.lane_dev, p.stride, a0, a1, b0, b1, reinterpret_cast<float4*>(p.params),
+  TLK_CUDA(launch(optimizer_kernel, dim3(unsigned(per_lane), p.lanes), 256, 0, st, p.lane_dev, p.stride, a0, a1, b0, b1, reinterpret_cast<float4*>(p.params),
       reinterpret_cast<const float4*>(p.grads), reinterpret_cast<float4*>(p.mom1),
-      reinterpret_cast<float4*>(p.mom2), reinterpret_cast<uint2*>(p.wbf), wt_hook(p));
+      reinterpret_cast<float4*>(p.mom2), reinterpret_cast<uint2*>(p.wbf), wt_hook(p)));
   p.mark(st, name);
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;

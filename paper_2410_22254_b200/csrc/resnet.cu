@@ -60,6 +60,9 @@ struct RnBufs {
   int64_t wpart_ls;
   float* lossrow;        // [lane][B]
   float* snap_stem;      // TLK_PACK_SNAPSHOTS: gradient w.r.t. a0
+  float* stat2;          // BN statistics level-2 records [lane][S][3][C]
+  int64_t stat2_ls;
+  unsigned* stat_cnt;    // [lane][STAT_MAX_CBLK] arrival counters (zero between launches)
   int sms;
   int64_t act_ls(int H, int W, int C) const { return int64_t(B) * H * W * C; }
 };
@@ -68,6 +71,7 @@ struct RnBufs {
 __global__ void __launch_bounds__(256) rn_inputs_kernel(const LaneState* __restrict__ lanes, int B,
                                                         const int8_t* __restrict__ teacher,
                                                         uint16_t* __restrict__ x, int32_t* __restrict__ labels) {
+  pdl_begin();
   const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (!lanes[j].active) return;
   const LaneState& s = lanes[j];
@@ -116,33 +120,46 @@ struct WtTable {
   WtEntry e[24];
   int n, tiles;
 };
-// WT[tap][ci][co] = W[co][tap][ci] (bf16), 32x32 tiles through smem
-__global__ void rn_wt_transpose_kernel(const LaneState* __restrict__ lanes, const __grid_constant__ WtTable tab,
-                                       const uint16_t* __restrict__ wbf, int64_t wstride, uint16_t* __restrict__ wt,
-                                       int64_t wt_stride) {
+// WT[tap][ci][co] = W[co][tap][ci] (bf16), 64x64 tiles through smem (every
+// transposed conv has cin, cout multiples of 64): 16-byte loads along ci,
+// 16-byte stores along co.
+__global__ void __launch_bounds__(256) rn_wt_transpose_kernel(const LaneState* __restrict__ lanes,
+                                                              const __grid_constant__ WtTable tab,
+                                                              const uint16_t* __restrict__ wbf, int64_t wstride,
+                                                              uint16_t* __restrict__ wt, int64_t wt_stride) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
-  __shared__ uint16_t t[32][33];
+  __shared__ uint16_t t[64][72];  // [co][ci], rows padded to 144 B
   int c = 0;
   while (c + 1 < tab.n && tab.e[c + 1].tiles0 <= int(blockIdx.x)) ++c;
   const WtEntry& E = tab.e[c];
   int r = blockIdx.x - E.tiles0;
-  const int nci = (E.cin + 31) / 32, nco = (E.cout + 31) / 32;
+  const int nci = E.cin / 64, nco = E.cout / 64;
   const int ci_t = r % nci;
   r /= nci;
   const int co_t = r % nco;
   const int tap = r / nco;
   const uint16_t* src = wbf + j * wstride + E.src;
   uint16_t* dst = wt + j * wt_stride + E.dst;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int co = co_t * 32 + yy, ci = ci_t * 32 + tx;
-    t[yy][tx] = (co < E.cout && ci < E.cin) ? src[(int64_t(co) * E.taps + tap) * E.cin + ci] : 0;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {  // 64 rows x 8 chunks of 8 ci
+    const int i = threadIdx.x + 256 * u, row = i >> 3, ch = i & 7;
+    const int co = co_t * 64 + row;
+    *reinterpret_cast<uint4*>(&t[row][ch * 8]) =
+        *reinterpret_cast<const uint4*>(src + (int64_t(co) * E.taps + tap) * E.cin + ci_t * 64 + ch * 8);
   }
   __syncthreads();
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int ci = ci_t * 32 + yy, co = co_t * 32 + tx;
-    if (ci < E.cin && co < E.cout) dst[(int64_t(tap) * E.cin + ci) * E.cout + co] = t[tx][yy];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {  // 64 ci rows x 8 chunks of 8 co
+    const int i = threadIdx.x + 256 * u, row = i >> 3, ch = i & 7;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = uint32_t(t[ch * 8 + 2 * k][row]) | (uint32_t(t[ch * 8 + 2 * k + 1][row]) << 16);
+    const int ci = ci_t * 64 + row;
+    *reinterpret_cast<uint4*>(dst + (int64_t(tap) * E.cin + ci) * E.cout + co_t * 64 + ch * 8) =
+        make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -155,6 +172,7 @@ __global__ void __launch_bounds__(256) rn_stem_fwd_kernel(const LaneState* __res
                                                           const uint16_t* __restrict__ wbf, int64_t wstride,
                                                           int64_t w_off, uint16_t* __restrict__ y,
                                                           float* __restrict__ part, int64_t part_ls) {
+  pdl_begin();
   const int tile = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (!lanes[j].active) return;
   __shared__ float xs[6][34][3];
@@ -202,8 +220,12 @@ __global__ void __launch_bounds__(256) rn_stem_fwd_kernel(const LaneState* __res
 
 // -------------------------------------------------------------- BN stats ----
 // (mean, M2) partials of 32 rows each [P][2][C] -> stats[lane][2][C] = mean,
-// rstd via Chan's pairwise combination in a fixed order: thread (c, g)
-// folds partials g, g+32, ... ; then group results 0..31 in order.
+// rstd via Chan's pairwise combination in a fixed order.  Grid (C/32, S,
+// lanes): CTA s folds partials [s*128, s*128+128) (group g of 8 takes
+// g, g+8, ... in order, then the groups in order) into a level-2 record
+// (n, mean, M2); the last CTA of a (lane, channel block) to arrive -- a
+// counter, not a reduction, so the result does not depend on arrival order
+// -- combines the S records in order and writes the statistics.
 __device__ __forceinline__ void chan_combine(float& n, float& mean, float& m2, float nb, float meanb,
                                              float m2b) {
   const float nn = n + nb;
@@ -212,29 +234,34 @@ __device__ __forceinline__ void chan_combine(float& n, float& mean, float& m2, f
   m2 = m2 + m2b + d * d * (n * nb / nn);
   n = nn;
 }
-constexpr int STAT_GROUPS = 32;
-__global__ void __launch_bounds__(1024) rn_bn_stats_kernel(const LaneState* __restrict__ lanes,
-                                                           const float* __restrict__ part, int64_t part_ls, int P,
-                                                           int C, float* __restrict__ stats) {
-  const int j = blockIdx.y;
+constexpr int STAT_GROUPS = 8;
+constexpr int STAT_PER_CTA = 128;  // partials per CTA (16 per group)
+constexpr int STAT_MAX_CBLK = 16;  // channel blocks of 32 (C <= 512)
+__global__ void __launch_bounds__(256) rn_bn_stats_kernel(const LaneState* __restrict__ lanes,
+                                                          const float* __restrict__ part, int64_t part_ls, int P,
+                                                          int C, float* __restrict__ l2, int64_t l2_ls,
+                                                          unsigned* __restrict__ cnt, float* __restrict__ stats) {
+  pdl_begin();
+  const int j = blockIdx.z, sblk = blockIdx.y, S = gridDim.y;
   if (!lanes[j].active) return;
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
   __shared__ float sh[3][STAT_GROUPS][32];
+  __shared__ int last;
   float n = 0.f, mean = 0.f, m2 = 0.f;
+  const int p_lo = sblk * STAT_PER_CTA, p_hi = min(P, p_lo + STAT_PER_CTA);
   if (c < C) {
     const float* pp = part + j * part_ls + c;
-    // partials g, g + 32, ... in order; four loads in flight per round
-    for (int p0 = g; p0 < P; p0 += 4 * STAT_GROUPS) {
+    for (int p0 = p_lo + g; p0 < p_hi; p0 += 4 * STAT_GROUPS) {
       float mb[4], qb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int p = p0 + u * STAT_GROUPS;
-        mb[u] = p < P ? pp[int64_t(p) * 2 * C] : 0.f;
-        qb[u] = p < P ? pp[int64_t(p) * 2 * C + C] : 0.f;
+        const int q = p0 + u * STAT_GROUPS;
+        mb[u] = q < p_hi ? pp[int64_t(q) * 2 * C] : 0.f;
+        qb[u] = q < p_hi ? pp[int64_t(q) * 2 * C + C] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (p0 + u * STAT_GROUPS >= P) break;
+        if (p0 + u * STAT_GROUPS >= p_hi) break;
         if (n == 0.f) {
           n = 32.f;
           mean = mb[u];
@@ -242,6 +269,46 @@ __global__ void __launch_bounds__(1024) rn_bn_stats_kernel(const LaneState* __re
         } else {
           chan_combine(n, mean, m2, 32.f, mb[u], qb[u]);
         }
+      }
+    }
+  }
+  sh[0][g][cl] = n;
+  sh[1][g][cl] = mean;
+  sh[2][g][cl] = m2;
+  __syncthreads();
+  float* rec = l2 + j * l2_ls;  // [S][3][C]
+  if (g == 0 && c < C) {
+    float N = sh[0][0][cl], M = sh[1][0][cl], Q = sh[2][0][cl];
+    for (int k = 1; k < STAT_GROUPS; ++k)
+      if (sh[0][k][cl] > 0.f) chan_combine(N, M, Q, sh[0][k][cl], sh[1][k][cl], sh[2][k][cl]);
+    rec[(int64_t(sblk) * 3 + 0) * C + c] = N;
+    rec[(int64_t(sblk) * 3 + 1) * C + c] = M;
+    rec[(int64_t(sblk) * 3 + 2) * C + c] = Q;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* ctr = cnt + j * STAT_MAX_CBLK + blockIdx.x;
+    last = atomicAdd(ctr, 1u) == unsigned(S - 1);
+    if (last) *ctr = 0u;  // re-armed for the next launch (stream-ordered)
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // groups fold records g, g+8, ... in order; then groups 0..7 in order
+  n = 0.f, mean = 0.f, m2 = 0.f;
+  if (c < C) {
+    for (int r = g; r < S; r += STAT_GROUPS) {
+      const float nb = __ldcg(rec + (int64_t(r) * 3 + 0) * C + c);
+      const float mb = __ldcg(rec + (int64_t(r) * 3 + 1) * C + c);
+      const float qb = __ldcg(rec + (int64_t(r) * 3 + 2) * C + c);
+      if (nb <= 0.f) continue;
+      if (n == 0.f) {
+        n = nb;
+        mean = mb;
+        m2 = qb;
+      } else {
+        chan_combine(n, mean, m2, nb, mb, qb);
       }
     }
   }
@@ -269,6 +336,7 @@ __global__ void __launch_bounds__(256) rn_bn_act_kernel(const LaneState* __restr
                                                         const uint16_t* __restrict__ res,
                                                         const float* __restrict__ std_, int64_t ogd, int64_t obd,
                                                         uint16_t* __restrict__ out) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   __shared__ float cf[6][512];  // mu, rstd*g, b, mud, rstdd*gd, bd
@@ -286,31 +354,44 @@ __global__ void __launch_bounds__(256) rn_bn_act_kernel(const LaneState* __restr
   }
   __syncthreads();
   const int64_t lane_off = int64_t(j) * n8 * 8;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e = lane_off + i * 8;
-    const int c0 = int((i * 8) % C);
-    const uint4 u = *reinterpret_cast<const uint4*>(y + e);
-    const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
-    uint4 rv = make_uint4(0, 0, 0, 0);
-    if (mode >= 1) rv = *reinterpret_cast<const uint4*>(res + e);
-    const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
-    uint32_t ow[4];
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  // two 16-byte vectors per thread in flight; C is a power of two
+  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * step) {
+    uint4 u[2], rv[2];
+    int64_t ii[2] = {i0, i0 + step};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float o2[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = c0 + 2 * q + h;
-        const float yv = h ? __uint_as_float(uw[q] & 0xffff0000u) : __uint_as_float(uw[q] << 16);
-        float v = (yv - cf[0][c]) * cf[1][c] + cf[2][c];
-        const float rr = h ? __uint_as_float(rw[q] & 0xffff0000u) : __uint_as_float(rw[q] << 16);
-        if (mode == 1) v += rr;
-        if (mode == 2) v += (rr - cf[3][c]) * cf[4][c] + cf[5][c];
-        o2[h] = fmaxf(v, 0.f);
+    for (int h = 0; h < 2; ++h) {
+      u[h] = make_uint4(0, 0, 0, 0);
+      rv[h] = make_uint4(0, 0, 0, 0);
+      if (ii[h] < n8) {
+        u[h] = *reinterpret_cast<const uint4*>(y + lane_off + ii[h] * 8);
+        if (mode >= 1) rv[h] = *reinterpret_cast<const uint4*>(res + lane_off + ii[h] * 8);
       }
-      ow[q] = pack_bf2(o2[0], o2[1]);
     }
-    *reinterpret_cast<uint4*>(out + e) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (ii[h] >= n8) break;
+      const int c0 = int((ii[h] * 8) & (C - 1));
+      const uint32_t uw[4] = {u[h].x, u[h].y, u[h].z, u[h].w};
+      const uint32_t rw[4] = {rv[h].x, rv[h].y, rv[h].z, rv[h].w};
+      uint32_t ow[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float o2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = c0 + 2 * q + e;
+          const float yv = e ? __uint_as_float(uw[q] & 0xffff0000u) : __uint_as_float(uw[q] << 16);
+          float v = (yv - cf[0][c]) * cf[1][c] + cf[2][c];
+          const float rr = e ? __uint_as_float(rw[q] & 0xffff0000u) : __uint_as_float(rw[q] << 16);
+          if (mode == 1) v += rr;
+          if (mode == 2) v += (rr - cf[3][c]) * cf[4][c] + cf[5][c];
+          o2[e] = fmaxf(v, 0.f);
+        }
+        ow[q] = pack_bf2(o2[0], o2[1]);
+      }
+      *reinterpret_cast<uint4*>(out + lane_off + ii[h] * 8) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
   }
 }
 
@@ -323,6 +404,7 @@ __global__ void __launch_bounds__(256) rn_head_kernel(const LaneState* __restric
                                                       int64_t ow, int64_t ob, float* __restrict__ G,
                                                       float* __restrict__ lossrow, float* __restrict__ fpart,
                                                       int64_t fpart_ls) {
+  pdl_begin();
   const int j = blockIdx.x, blk = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
   __shared__ float hs[8][512];
@@ -396,6 +478,7 @@ __global__ void __launch_bounds__(256) rn_head_kernel(const LaneState* __restric
 __global__ void rn_reduce_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
                                  int64_t part_ls, int64_t blk_st, int nblk, int C, float* __restrict__ grads,
                                  int64_t pstride, int64_t off0, int split, int64_t off1) {
+  pdl_begin();
   const int c = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (!lanes[j].active || c >= C) return;
   const float* p = part + j * part_ls + c;
@@ -407,6 +490,7 @@ __global__ void rn_reduce_kernel(const LaneState* __restrict__ lanes, const floa
 __global__ void __launch_bounds__(512) rn_loss_kernel(LaneState* __restrict__ lanes, int B,
                                                       const float* __restrict__ lossrow, float* __restrict__ loss,
                                                       int max_steps, float* __restrict__ last_loss) {
+  pdl_begin();
   const int j = blockIdx.x;
   if (!lanes[j].active || threadIdx.x) return;
   float t = 0.f;
@@ -428,6 +512,7 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_reduce_kernel(
     const LaneState* __restrict__ lanes, int64_t M, int C, const float* __restrict__ G,
     const uint16_t* __restrict__ mask, const uint16_t* __restrict__ y, const float* __restrict__ st,
     const uint16_t* __restrict__ yd, const float* __restrict__ std_, float* __restrict__ part, int64_t part_ls) {
+  pdl_begin();
   const int blk = blockIdx.x, j = blockIdx.y;
   if (!lanes[j].active) return;
   const int CG = C / 8, R = 256 / CG;
@@ -497,6 +582,7 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_finish_kernel(
     const LaneState* __restrict__ lanes, const float* __restrict__ part, int64_t part_ls, int nblk, int K, int C,
     float* __restrict__ sums, float* __restrict__ grads, int64_t pstride, int64_t og, int64_t ob, int64_t ogd,
     int64_t obd) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
@@ -534,6 +620,7 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_apply_kernel(
     const uint16_t* __restrict__ yd, const float* __restrict__ std_, const float* __restrict__ sums,
     const float* __restrict__ params, int64_t pstride, int64_t og, int64_t ogd, uint16_t* __restrict__ dy,
     uint16_t* __restrict__ dyd, float* __restrict__ gx) {
+  pdl_begin();
   const int j = blockIdx.y;
   if (!lanes[j].active) return;
   __shared__ float cf[8][512];  // mu, a, b, c, mud, ad, bd, cd
@@ -558,38 +645,54 @@ __global__ void __launch_bounds__(256) rn_bn_bwd_apply_kernel(
   }
   __syncthreads();
   const int64_t n8 = M * C / 8;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e = int64_t(j) * M * C + i * 8;
-    const int c0 = int((i * 8) % C);
-    const float4 g0 = *reinterpret_cast<const float4*>(G + e), g1 = *reinterpret_cast<const float4*>(G + e + 4);
-    const uint4 mk = *reinterpret_cast<const uint4*>(mask + e), yy = *reinterpret_cast<const uint4*>(y + e);
-    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w}, yw[4] = {yy.x, yy.y, yy.z, yy.w};
-    uint4 dd = make_uint4(0, 0, 0, 0);
-    if (yd) dd = *reinterpret_cast<const uint4*>(yd + e);
-    const uint32_t dw[4] = {dd.x, dd.y, dd.z, dd.w};
-    float g[8], o1[8], o2[8];
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * step) {
+    const int64_t ii[2] = {i0, i0 + step};
+    float4 g0[2], g1[2];
+    uint4 mk[2], yy[2], dd[2];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int c = c0 + k;
-      const uint32_t sh = (k & 1) ? 0u : 16u;
-      const float mv = __uint_as_float((mw[k >> 1] << sh) & 0xffff0000u);
-      g[k] = mv > 0.f ? gg[k] : 0.f;
-      const float yv = __uint_as_float((yw[k >> 1] << sh) & 0xffff0000u);
-      o1[k] = cf[1][c] * g[k] + cf[2][c] * (yv - cf[0][c]) + cf[3][c];
-      if (yd) {
-        const float dv = __uint_as_float((dw[k >> 1] << sh) & 0xffff0000u);
-        o2[k] = cf[5][c] * g[k] + cf[6][c] * (dv - cf[4][c]) + cf[7][c];
+    for (int h = 0; h < 2; ++h) {
+      dd[h] = make_uint4(0, 0, 0, 0);
+      if (ii[h] < n8) {
+        const int64_t e = int64_t(j) * M * C + ii[h] * 8;
+        g0[h] = *reinterpret_cast<const float4*>(G + e);
+        g1[h] = *reinterpret_cast<const float4*>(G + e + 4);
+        mk[h] = *reinterpret_cast<const uint4*>(mask + e);
+        yy[h] = *reinterpret_cast<const uint4*>(y + e);
+        if (yd) dd[h] = *reinterpret_cast<const uint4*>(yd + e);
       }
     }
-    *reinterpret_cast<uint4*>(dy + e) = make_uint4(pack_bf2(o1[0], o1[1]), pack_bf2(o1[2], o1[3]),
-                                                   pack_bf2(o1[4], o1[5]), pack_bf2(o1[6], o1[7]));
-    if (yd)
-      *reinterpret_cast<uint4*>(dyd + e) = make_uint4(pack_bf2(o2[0], o2[1]), pack_bf2(o2[2], o2[3]),
-                                                      pack_bf2(o2[4], o2[5]), pack_bf2(o2[6], o2[7]));
-    if (gx) {
-      *reinterpret_cast<float4*>(gx + e) = make_float4(g[0], g[1], g[2], g[3]);
-      *reinterpret_cast<float4*>(gx + e + 4) = make_float4(g[4], g[5], g[6], g[7]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (ii[h] >= n8) break;
+      const int64_t e = int64_t(j) * M * C + ii[h] * 8;
+      const int c0 = int((ii[h] * 8) & (C - 1));
+      const float gg[8] = {g0[h].x, g0[h].y, g0[h].z, g0[h].w, g1[h].x, g1[h].y, g1[h].z, g1[h].w};
+      const uint32_t mw[4] = {mk[h].x, mk[h].y, mk[h].z, mk[h].w}, yw[4] = {yy[h].x, yy[h].y, yy[h].z, yy[h].w};
+      const uint32_t dw[4] = {dd[h].x, dd[h].y, dd[h].z, dd[h].w};
+      float g[8], o1[8], o2[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = c0 + k;
+        const uint32_t sh = (k & 1) ? 0u : 16u;
+        const float mv = __uint_as_float((mw[k >> 1] << sh) & 0xffff0000u);
+        g[k] = mv > 0.f ? gg[k] : 0.f;
+        const float yv = __uint_as_float((yw[k >> 1] << sh) & 0xffff0000u);
+        o1[k] = cf[1][c] * g[k] + cf[2][c] * (yv - cf[0][c]) + cf[3][c];
+        if (yd) {
+          const float dv = __uint_as_float((dw[k >> 1] << sh) & 0xffff0000u);
+          o2[k] = cf[5][c] * g[k] + cf[6][c] * (dv - cf[4][c]) + cf[7][c];
+        }
+      }
+      *reinterpret_cast<uint4*>(dy + e) = make_uint4(pack_bf2(o1[0], o1[1]), pack_bf2(o1[2], o1[3]),
+                                                     pack_bf2(o1[4], o1[5]), pack_bf2(o1[6], o1[7]));
+      if (yd)
+        *reinterpret_cast<uint4*>(dyd + e) = make_uint4(pack_bf2(o2[0], o2[1]), pack_bf2(o2[2], o2[3]),
+                                                        pack_bf2(o2[4], o2[5]), pack_bf2(o2[6], o2[7]));
+      if (gx) {
+        *reinterpret_cast<float4*>(gx + e) = make_float4(g[0], g[1], g[2], g[3]);
+        *reinterpret_cast<float4*>(gx + e + 4) = make_float4(g[4], g[5], g[6], g[7]);
+      }
     }
   }
 }
@@ -600,6 +703,7 @@ __global__ void __launch_bounds__(256) rn_stem_wgrad_kernel(const LaneState* __r
                                                             const uint16_t* __restrict__ x,
                                                             const uint16_t* __restrict__ dy,
                                                             float* __restrict__ part, int64_t part_ls) {
+  pdl_begin();
   const int img = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (!lanes[j].active) return;
   __shared__ float xs[34][34][3];
@@ -664,6 +768,21 @@ static int act_map_l(CUtensorMap* m, const uint16_t* base, int64_t ls, int lanes
 
 namespace {
 
+#ifndef TLK_TRY
+#define TLK_TRY(x)              \
+  do {                          \
+    if (int rc_ = (x)) return rc_; \
+  } while (0)
+#endif
+
+int enqueue_bn_stats(Pack& p, cudaStream_t st, RnBufs& R, int P, int C, float* stats) {
+  const int S = (P + STAT_PER_CTA - 1) / STAT_PER_CTA;
+  TLK_CHECK(C <= 32 * STAT_MAX_CBLK && int64_t(S) * 3 * C <= R.stat2_ls, TLK_EINVAL, "bn stats: %d x %d", P, C);
+  TLK_CUDA(launch(rn_bn_stats_kernel, dim3((C + 31) / 32, S, p.lanes), 256, 0, st, p.lane_dev, R.part, R.part_ls, P, C,
+                  R.stat2, R.stat2_ls, R.stat_cnt, stats));
+  return TLK_OK;
+}
+
 template <int BN>
 int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, const char* name) {
   using G = ConvGemm<BN, CONV_FWD>;
@@ -706,8 +825,7 @@ int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, c
   p.mark(st, name);
   // statistics of this conv's output
   const int P = g.mt * 4;
-  rn_bn_stats_kernel<<<dim3((L.cout + 31) / 32, p.lanes), 1024, 0, st>>>(p.lane_dev, R.part, R.part_ls, P, L.cout,
-                                                                       L.stats);
+  TLK_TRY(enqueue_bn_stats(p, st, R, P, L.cout, L.stats));
   TLK_CUDA(cudaGetLastError());
   p.mark(st, "bn_stats");
   return TLK_OK;
@@ -807,8 +925,7 @@ int conv_wgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
   TLK_CUDA(launch_tgemm(g, R.sms, st));
   p.mark(st, name);
   if (splits > 1) {
-    rn_reduce_kernel<<<dim3(int((wsize + 255) / 256), p.lanes), 256, 0, st>>>(
-        p.lane_dev, R.wpart, R.wpart_ls, wsize, splits, int(wsize), p.grads, p.stride, goff, int(wsize), goff);
+    TLK_CUDA(launch(rn_reduce_kernel, dim3(int((wsize + 255) / 256), p.lanes), 256, 0, st, p.lane_dev, R.wpart, R.wpart_ls, wsize, splits, int(wsize), p.grads, p.stride, goff, int(wsize), goff));
     TLK_CUDA(cudaGetLastError());
     p.mark(st, "wgrad_reduce");
   }
@@ -934,6 +1051,16 @@ int resnet_setup(Pack& p) {
   R->part_ls = round_up(pl, 64);
   add(reinterpret_cast<void**>(&R->part), size_t(L) * R->part_ls * 4);
   add(reinterpret_cast<void**>(&R->sums), size_t(L) * 3 * 512 * 4);
+  {
+    int64_t smax = 1;
+    for (auto& c : R->conv) {
+      const int64_t P = int64_t(B) * c.Ho * c.Wo / 32;
+      smax = std::max(smax, (P + STAT_PER_CTA - 1) / STAT_PER_CTA * 3 * c.cout);
+    }
+    R->stat2_ls = round_up(smax, 64);
+    add(reinterpret_cast<void**>(&R->stat2), size_t(L) * R->stat2_ls * 4);
+    add(reinterpret_cast<void**>(&R->stat_cnt), size_t(L) * STAT_MAX_CBLK * 4);
+  }
   R->wpart_ls = int64_t(8) * 64 * 9 * 128;  // split-K partials: up to 8 x (128 x 9 x 64) or fewer splits
   add(reinterpret_cast<void**>(&R->wpart), size_t(L) * R->wpart_ls * 4);
   add(reinterpret_cast<void**>(&R->lossrow), size_t(L) * B * 4);
@@ -1001,9 +1128,15 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
     p.mark(st, name);
     ++count;
   };
-  auto ew_grid = [&](int64_t n8) { return dim3(unsigned(std::min<int64_t>((n8 + 255) / 256, 2048)), Lc); };
+  // elementwise BN kernels: ~one full wave over all lanes (8 CTAs of 256 per
+  // SM), >= 4 vectors per thread, so the per-CTA channel-coefficient setup
+  // is amortised
+  auto ew_grid = [&](int64_t n8) {
+    const int64_t cap = std::max<int64_t>(1, int64_t(R.sms) * 8 / Lc);
+    return dim3(unsigned(std::clamp<int64_t>((n8 + 1023) / 1024, 1, cap)), Lc);
+  };
 
-  rn_inputs_kernel<<<dim3(B, Lc), 256, 0, st>>>(LS, B, R.teacher, R.xin, p.labels);
+  TLK_CUDA(launch(rn_inputs_kernel, dim3(B, Lc), 256, 0, st, LS, B, R.teacher, R.xin, p.labels));
   TLK_CUDA(cudaGetLastError());
   marked("inputs");
   {  // dgrad weight layouts from this step's bf16 shadow
@@ -1018,25 +1151,26 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
       e.taps = c.k * c.k;
       e.cin = c.cin;
       e.tiles0 = tiles;
-      tiles += e.taps * ((c.cout + 31) / 32) * ((c.cin + 31) / 32);
+      if (c.cin % 64 || c.cout % 64) return fail(TLK_EINVAL, "resnet: conv %zu channels not multiples of 64", i);
+      tiles += e.taps * (c.cout / 64) * (c.cin / 64);
     }
     tab.tiles = tiles;
-    rn_wt_transpose_kernel<<<dim3(tiles, Lc), 256, 0, st>>>(LS, tab, p.wbf, PS, p.wt, p.wt_stride);
+    TLK_CUDA(launch(rn_wt_transpose_kernel, dim3(tiles, Lc), 256, 0, st, LS, tab, p.wbf, PS, p.wt, p.wt_stride));
     TLK_CUDA(cudaGetLastError());
     marked("wt_transpose");
   }
   // ---- forward
   ConvL& S0 = R.conv[0];
-  rn_stem_fwd_kernel<<<dim3(B * 8, Lc), 256, 0, st>>>(LS, B, R.xin, p.wbf, PS, O(S0.t_w), S0.y, R.part, R.part_ls);
+  TLK_CUDA(launch(rn_stem_fwd_kernel, dim3(B * 8, Lc), 256, 0, st, LS, B, R.xin, p.wbf, PS, O(S0.t_w), S0.y, R.part, R.part_ls));
   TLK_CUDA(cudaGetLastError());
   marked("stem_fwd");
-  rn_bn_stats_kernel<<<dim3(2, Lc), 1024, 0, st>>>(LS, R.part, R.part_ls, B * 8 * 4, 64, S0.stats);
+  TLK_TRY(enqueue_bn_stats(p, st, R, B * 8 * 4, 64, S0.stats));
   TLK_CUDA(cudaGetLastError());
   marked("bn_stats");
   {
     const int64_t n8 = R.act_ls(32, 32, 64) / 8;
-    rn_bn_act_kernel<<<ew_grid(n8), 256, 0, st>>>(LS, n8, 64, S0.y, S0.stats, PR, PS, O(S0.t_g), O(S0.t_b), 0,
-                                                  nullptr, nullptr, 0, 0, R.a0);
+    TLK_CUDA(launch(rn_bn_act_kernel, ew_grid(n8), 256, 0, st, LS, n8, 64, S0.y, S0.stats, PR, PS, O(S0.t_g), O(S0.t_b), 0,
+                                                  nullptr, nullptr, 0, 0, R.a0));
     TLK_CUDA(cudaGetLastError());
     marked("bn_act");
   }
@@ -1046,8 +1180,8 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
     if (rc) return rc;
     count += 2;
     const int64_t n8a = R.act_ls(c1.Ho, c1.Wo, c1.cout) / 8;
-    rn_bn_act_kernel<<<ew_grid(n8a), 256, 0, st>>>(LS, n8a, c1.cout, c1.y, c1.stats, PR, PS, O(c1.t_g), O(c1.t_b),
-                                                   0, nullptr, nullptr, 0, 0, bk.a1);
+    TLK_CUDA(launch(rn_bn_act_kernel, ew_grid(n8a), 256, 0, st, LS, n8a, c1.cout, c1.y, c1.stats, PR, PS, O(c1.t_g), O(c1.t_b),
+                                                   0, nullptr, nullptr, 0, 0, bk.a1));
     TLK_CUDA(cudaGetLastError());
     marked("bn_act");
     rc = conv_fwd_any(p, st, R, c2, bk.a1, "conv_fwd");
@@ -1058,11 +1192,11 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
       rc = conv_fwd_any(p, st, R, cd, bk.xin, "conv_fwd_ds");
       if (rc) return rc;
       count += 2;
-      rn_bn_act_kernel<<<ew_grid(n8a), 256, 0, st>>>(LS, n8a, c2.cout, c2.y, c2.stats, PR, PS, O(c2.t_g),
-                                                     O(c2.t_b), 2, cd.y, cd.stats, O(cd.t_g), O(cd.t_b), bk.o);
+      TLK_CUDA(launch(rn_bn_act_kernel, ew_grid(n8a), 256, 0, st, LS, n8a, c2.cout, c2.y, c2.stats, PR, PS, O(c2.t_g),
+                                                     O(c2.t_b), 2, cd.y, cd.stats, O(cd.t_g), O(cd.t_b), bk.o));
     } else {
-      rn_bn_act_kernel<<<ew_grid(n8a), 256, 0, st>>>(LS, n8a, c2.cout, c2.y, c2.stats, PR, PS, O(c2.t_g),
-                                                     O(c2.t_b), 1, bk.xin, nullptr, 0, 0, bk.o);
+      TLK_CUDA(launch(rn_bn_act_kernel, ew_grid(n8a), 256, 0, st, LS, n8a, c2.cout, c2.y, c2.stats, PR, PS, O(c2.t_g),
+                                                     O(c2.t_b), 1, bk.xin, nullptr, 0, 0, bk.o));
     }
     TLK_CUDA(cudaGetLastError());
     marked("bn_act_res");
@@ -1071,15 +1205,15 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
   const int t_fcw = int(p.tinfo.size()) - 2, t_fcb = t_fcw + 1;
   float* G = R.G0;
   float* Gx = R.G1;
-  rn_head_kernel<<<dim3(Lc, B / 8), 256, 0, st>>>(LS, B, R.blk.back().o, p.labels, PR, PS, O(t_fcw), O(t_fcb), G,
-                                                  R.lossrow, R.part, R.part_ls);
+  TLK_CUDA(launch(rn_head_kernel, dim3(Lc, B / 8), 256, 0, st, LS, B, R.blk.back().o, p.labels, PR, PS, O(t_fcw), O(t_fcb), G,
+                                                  R.lossrow, R.part, R.part_ls));
   TLK_CUDA(cudaGetLastError());
   marked("head");
-  rn_reduce_kernel<<<dim3((5130 + 255) / 256, Lc), 256, 0, st>>>(LS, R.part, R.part_ls, 5136, B / 8, 5130, p.grads,
-                                                                  PS, O(t_fcw), 5120, O(t_fcb));
+  TLK_CUDA(launch(rn_reduce_kernel, dim3((5130 + 255) / 256, Lc), 256, 0, st, LS, R.part, R.part_ls, 5136, B / 8, 5130, p.grads,
+                                                                  PS, O(t_fcw), 5120, O(t_fcb)));
   TLK_CUDA(cudaGetLastError());
   marked("fc_reduce");
-  rn_loss_kernel<<<Lc, 32, 0, st>>>(p.lane_dev, B, R.lossrow, p.loss, p.max_steps, p.last_loss);
+  TLK_CUDA(launch(rn_loss_kernel, Lc, 32, 0, st, p.lane_dev, B, R.lossrow, p.loss, p.max_steps, p.last_loss));
   TLK_CUDA(cudaGetLastError());
   marked("loss");
 
@@ -1089,20 +1223,19 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
     const int64_t M = int64_t(B) * c.Ho * c.Wo;
     const int nblk = int((M + BNB_ROWS - 1) / BNB_ROWS);
     const int K = cd ? 3 : 2;
-    rn_bn_bwd_reduce_kernel<<<dim3(nblk, Lc), 256, 0, st>>>(LS, M, c.cout, Gin, mask, c.y, c.stats,
+    TLK_CUDA(launch(rn_bn_bwd_reduce_kernel, dim3(nblk, Lc), 256, 0, st, LS, M, c.cout, Gin, mask, c.y, c.stats,
                                                               cd ? cd->y : nullptr, cd ? cd->stats : nullptr,
-                                                              R.part, R.part_ls);
+                                                              R.part, R.part_ls));
     TLK_CUDA(cudaGetLastError());
     marked("bn_bwd_reduce");
-    rn_bn_bwd_finish_kernel<<<dim3((c.cout + 31) / 32, Lc), 256, 0, st>>>(
-        LS, R.part, R.part_ls, nblk, K, c.cout, R.sums, p.grads, PS, O(c.t_g), O(c.t_b), cd ? O(cd->t_g) : 0,
-        cd ? O(cd->t_b) : 0);
+    TLK_CUDA(launch(rn_bn_bwd_finish_kernel, dim3((c.cout + 31) / 32, Lc), 256, 0, st, LS, R.part, R.part_ls, nblk, K, c.cout, R.sums, p.grads, PS, O(c.t_g), O(c.t_b), cd ? O(cd->t_g) : 0,
+        cd ? O(cd->t_b) : 0));
     TLK_CUDA(cudaGetLastError());
     marked("bn_bwd_finish");
     const int64_t n8 = M * c.cout / 8;
-    rn_bn_bwd_apply_kernel<<<ew_grid(n8), 256, 0, st>>>(LS, M, c.cout, Gin, mask, c.y, c.stats,
+    TLK_CUDA(launch(rn_bn_bwd_apply_kernel, ew_grid(n8), 256, 0, st, LS, M, c.cout, Gin, mask, c.y, c.stats,
                                                         cd ? cd->y : nullptr, cd ? cd->stats : nullptr, R.sums, PR,
-                                                        PS, O(c.t_g), cd ? O(cd->t_g) : 0, dy, dyd, gx);
+                                                        PS, O(c.t_g), cd ? O(cd->t_g) : 0, dy, dyd, gx));
     TLK_CUDA(cudaGetLastError());
     marked("bn_bwd_apply");
     return TLK_OK;
@@ -1150,11 +1283,11 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_CUDA(cudaMemcpyAsync(R.snap_stem, G, size_t(Lc) * R.act_ls(32, 32, 64) * 4, cudaMemcpyDeviceToDevice, st));
     int rc = bn_bwd(G, R.a0, S0, nullptr, R.dy, nullptr, nullptr);
     if (rc) return rc;
-    rn_stem_wgrad_kernel<<<dim3(B, Lc), 256, 0, st>>>(LS, B, R.xin, R.dy, R.part, R.part_ls);
+    TLK_CUDA(launch(rn_stem_wgrad_kernel, dim3(B, Lc), 256, 0, st, LS, B, R.xin, R.dy, R.part, R.part_ls));
     TLK_CUDA(cudaGetLastError());
     marked("stem_wgrad");
-    rn_reduce_kernel<<<dim3((1728 + 255) / 256, Lc), 256, 0, st>>>(LS, R.part, R.part_ls, 1728, B, 1728, p.grads,
-                                                                    PS, O(S0.t_w), 1728, O(S0.t_w));
+    TLK_CUDA(launch(rn_reduce_kernel, dim3((1728 + 255) / 256, Lc), 256, 0, st, LS, R.part, R.part_ls, 1728, B, 1728, p.grads,
+                                                                    PS, O(S0.t_w), 1728, O(S0.t_w)));
     TLK_CUDA(cudaGetLastError());
     marked("stem_wgrad_reduce");
   }

@@ -1,5 +1,6 @@
 // libtlk C ABI: contexts (one per GPU), packs of K job lanes, graph-captured
 // steps, host-buffer end-to-end steps, result readback.  See include/tlk.h.
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -29,6 +30,14 @@ int cuda_fail(cudaError_t e, const char* what) {
   if (e == cudaErrorMemoryAllocation)
     return fail(TLK_EOOM, "out of memory: %s (%s)", what, cudaGetErrorString(e));
   return fail(TLK_ECUDA, "CUDA error %s at %s", cudaGetErrorString(e), what);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("TLK_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 int pack_alloc(Pack& p, void** ptr, size_t bytes) {

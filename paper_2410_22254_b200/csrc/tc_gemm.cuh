@@ -114,6 +114,7 @@ TLK_DEV void gemm_epilogue(const P& p, const typename P::Work& w, uint32_t tmem,
 
 template <class P>
 __global__ void __launch_bounds__(GemmThreads<P>::value, 1) tc_gemm_kernel(const P p) {
+  pdl_begin();
   constexpr int NT = GemmThreads<P>::value;
   constexpr int BN = P::BN;
   constexpr int STAGES = P::STAGES;
@@ -218,6 +219,7 @@ TLK_DEV uint64_t stage_desc_tma(uint32_t base, int kk) {
 template <class P>
 __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
     tc_gemm_tma_kernel(const __grid_constant__ P p) {
+  pdl_begin();
   constexpr int BN = P::BN;
   constexpr int STAGES = P::STAGES;
   using S = GemmSmem<P>;
@@ -290,7 +292,7 @@ inline cudaError_t launch_gemm_tma(const P& p, dim3 grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  tc_gemm_tma_kernel<P><<<grid, GemmThreads<P>::value, bytes, stream>>>(p);
+  if (cudaError_t le = launch(tc_gemm_tma_kernel<P>, grid, GemmThreads<P>::value, bytes, stream, p); le != cudaSuccess) return le;
   return cudaGetLastError();
 }
 
@@ -305,7 +307,7 @@ inline cudaError_t launch_gemm(const P& p, dim3 grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  tc_gemm_kernel<P><<<grid, GemmThreads<P>::value, bytes, stream>>>(p);
+  if (cudaError_t le = launch(tc_gemm_kernel<P>, grid, GemmThreads<P>::value, bytes, stream, p); le != cudaSuccess) return le;
   return cudaGetLastError();
 }
 

@@ -90,6 +90,7 @@ struct TGemm {
 
 template <class P>
 __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_constant__ P p) {
+  pdl_begin();
   constexpr int BN = P::BN, STAGES = P::STAGES, EW = P::EW;
   constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, P::A_MN, P::B_MN);
   extern __shared__ uint8_t smem_raw[];
@@ -224,7 +225,7 @@ inline cudaError_t launch_tgemm(const P& p, int sms, cudaStream_t stream) {
     configured = true;
   }
   const int grid = std::max(1, std::min(p.ntiles, sms));
-  tgemm_kernel<P><<<grid, P::THREADS, P::SMEM_BYTES, stream>>>(p);
+  if (cudaError_t le = launch(tgemm_kernel<P>, grid, P::THREADS, P::SMEM_BYTES, stream, p); le != cudaSuccess) return le;
   return cudaGetLastError();
 }
 

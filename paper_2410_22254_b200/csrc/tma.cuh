@@ -47,4 +47,30 @@ TLK_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int
       : "memory");
 }
 
+// Generic 3-D tensor map (dims[0] contiguous), box {b0, b1, 1}, given element
+// type and swizzle; used for the fp32 optimizer-state tiles and the bf16
+// shadow tile of the CNN's fused fc1 wgrad + Adam kernel.
+int make_tmap_3d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+                 uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                 CUtensorMapSwizzle sw);
+
+// Box store: tensor[c2][c1 ..][c0 ..] <- smem (same layout/swizzle as a load),
+// tracked by the issuing thread's bulk async-group.
+TLK_DEV void tma_store_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+TLK_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N bulk groups still READ their shared-memory source
+template <int N>
+TLK_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+TLK_DEV void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 }  // namespace tlk

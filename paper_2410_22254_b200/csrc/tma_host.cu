@@ -63,4 +63,21 @@ int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5]
   return TLK_OK;
 }
 
+int make_tmap_3d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+                 uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                 CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  TLK_CHECK(fn, TLK_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  TLK_CHECK(reinterpret_cast<uintptr_t>(base) % 16 == 0 && stride1_bytes % 16 == 0 && stride2_bytes % 16 == 0,
+            TLK_EINVAL, "tensor map base/strides not 16-byte aligned");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(out, dt, 3, const_cast<void*>(base), dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TLK_CHECK(r == CUDA_SUCCESS, TLK_ECUDA, "cuTensorMapEncodeTiled (3d) failed (%d)", int(r));
+  return TLK_OK;
+}
+
 }  // namespace tlk

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtlk.so")
+LIB_PATH = os.environ.get("TLK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtlk.so")
 
 TLK_OK, TLK_EINVAL, TLK_ECUDA, TLK_EOOM, TLK_ESTATE = 0, -1, -2, -3, -4
 MODEL_MLP, MODEL_CNN, MODEL_XFORMER, MODEL_GPT, MODEL_RESNET18 = 1, 2, 3, 4, 5

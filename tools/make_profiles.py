@@ -15,8 +15,8 @@ PROF = os.path.join(ROOT, "profiles")
 LABELS = {"conv2_tc_kernel<1>": "conv2_fwd_pool", "conv2_tc_kernel<0>": "conv2_dgrad",
           "Fc1WgradOpt": "fc1_wgrad_adam", "Conv2Fwd": "conv2_fwd_pool", "Conv2Dgrad": "conv2_dgrad", "conv2_wgrad_tc": "conv2_wgrad", "conv2_fwd_tc": "conv2_fwd_pool", "conv2_dgrad_tc": "conv2_dgrad",
           "Fc1Dgrad": "fc1_dgrad_unpool", "Fc1Fwd": "fc1_fwd_splitk", "LinWgrad": "fc1_wgrad",
-          "optimizer_kernel": "optimizer", "conv1_wgrad": "conv1_wgrad", "conv1_fwd": "conv1_fwd",
-          "head_kernel": "head", "inputs_kernel": "inputs", "cnn_finalize": "grad_finalize",
+          "optimizer_kernel": "optimizer", "conv1_wgrad": "conv1_wgrad", "conv1_fwd": "inputs_conv1_fwd",
+          "head_kernel": "head", "inputs_kernel": "inputs", "cnn_opt": "grad_finalize_opt",
           "fc1_reduce": "fc1_reduce", "end_step": "end_step"}
 
 
