@@ -276,9 +276,10 @@ struct Fc1Dgrad {
 //   warp 1   tcgen05.mma issuer, accumulator double-buffered in TMEM
 //   warps 2-17  update: thread = (f = its TMEM lane, 8 outputs of the chunk):
 //            p, m, v from the slot into registers (the slot is released at
-//            once, so 3 slots stay in flight), opt_update (IEEE-exact Adam
-//            is ~50 instructions per element, hence 16 warps), coalesced
-//            stores of p, m, v and the bf16 shadow.
+//            once, so 3 slots stay in flight), the update with the optimizer
+//            kind resolved once per chunk (IEEE-exact Adam is ~50 issued
+//            instructions per element: the kernel is issue-bound), coalesced
+//            128-B stores of p, m, v and the bf16 shadow.
 // Must run after every reader of this step's fc1 weights (fc1 dgrad).
 constexpr int FWA_SLOTS = 4, FWA_UPD_WARPS = 16;
 constexpr int FWA_STAGE_BYTES = 2 * 128 * 64 * 2;  // p2^T and dz3^T tiles (two 64-wide boxes each)
@@ -412,8 +413,16 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sl]);  // slot refillable as soon as it is read
+        if (s.optimizer == TLK_OPT_SGD) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) opt_update(s, pv[i], g[i], mv[i], vv[i]);
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_SGD>(s, pv[i], g[i], mv[i], vv[i]);
+        } else if (s.optimizer == TLK_OPT_ADAMW) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_ADAMW>(s, pv[i], g[i], mv[i], vv[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_ADAM>(s, pv[i], g[i], mv[i], vv[i]);
+        }
         const int64_t e = j * p.pstride + p.w_off + int64_t(o0) * 9216 + f0 + fl;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -421,7 +430,10 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
           p.m1[e + int64_t(i) * 9216] = mv[i];
           p.m2[e + int64_t(i) * 9216] = vv[i];
           p.wbf[e + int64_t(i) * 9216] = f2bf(pv[i]);
-          if (p.write_grads) p.grads[e + int64_t(i) * 9216] = g[i];
+        }
+        if (p.write_grads) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) p.grads[e + int64_t(i) * 9216] = g[i];
         }
       }
       ++lt;

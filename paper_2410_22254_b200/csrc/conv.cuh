@@ -31,16 +31,29 @@ struct ConvWork {
   int mt;     // m-tile index (FWD stats partials)
 };
 
-template <int BN_, int MODE>
+// HALO (stride-1 3x3 FWD / DGRAD on 16- or 32-wide grids, 128 % W == 0):
+// a 128-pixel tile is 128/W whole image rows, so one TMA box of those rows
+// plus a one-row halo above and below -- (64 ch, W px, 128/W + 2 rows) at x
+// shift dx -- holds the A operand of all three taps (dh = -1, 0, 1) of that
+// dx: tap dh is the same smem image with the UMMA start moved by (1 + dh) * W
+// rows (a multiple of the 8-row SW128 atom for W = 16, 32).  A stage = that
+// box + the three taps' B tiles, 12 MMAs; A traffic drops from 9 to 3 boxes
+// per 64 channels (L2 -> SM bytes per MMA from 96 to ~60 B/clk at BN 64).
+// TG = 3 (WGRAD, 64 input channels): one tile computes the three taps of a
+// kernel row at once, N = 3 x 64 -- the dY operand (A) is loaded once for
+// three taps and each MMA does 3x the work of a single-tap tile.
+template <int BN_, int MODE, bool HALO = false, int TG = 1>
 struct ConvGemm {
   static constexpr int BN = BN_;
-  static constexpr int STAGES = BN_ <= 64 ? 6 : BN_ <= 128 ? 4 : 3;
+  static_assert(TG == 1 || (MODE == CONV_WGRAD && BN_ == 64 * TG), "tap groups: WGRAD, 64 channels per tap");
+  static constexpr int A_BYTES = HALO ? 6 * 32 * 128 : GEMM_BM * GEMM_BK * 2;  // halo: <= (128/W + 2) W rows
+  static constexpr int B_BYTES = (HALO ? 3 : 1) * BN_ * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = HALO ? (BN_ <= 64 ? 3 : 2) : (BN_ <= 64 ? 6 : BN_ <= 128 ? 4 : BN_ <= 192 ? 4 : 3);
   static constexpr int EW = 8;
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = MODE == CONV_WGRAD, B_MN = MODE == CONV_WGRAD, ROW_EPI = false;
-  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr int B_BYTES = BN_ * GEMM_BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static_assert(!HALO || MODE != CONV_WGRAD, "halo mode is FWD / DGRAD only");
   static constexpr int STAGING_BYTES = EW * 32 * 33 * 4;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024;
   static constexpr uint32_t TCOLS = BN_ <= 64 ? 128 : BN_ <= 128 ? 256 : 512;
@@ -70,6 +83,23 @@ struct ConvGemm {
   TLK_DEV void prefetch() const {
     tma_prefetch_desc(&ta[0]);
     tma_prefetch_desc(&tb[0]);
+  }
+  TLK_DEV uint32_t tx_bytes() const {
+    return HALO ? uint32_t((GEMM_BM / Wr + 2) * Wr * 128 + B_BYTES) : uint32_t(STAGE_BYTES);
+  }
+  // halo k-block kb = (dx index, channel block): taps kh = 0..2 at kw = dx
+  template <uint32_t IDESC>
+  TLK_DEV void issue_mma(uint32_t d, uint32_t a_s, bool acc) const {
+    if constexpr (!HALO) {
+      gemm_stage_mma<BN_, A_MN, B_MN, IDESC>(d, a_s, a_s + A_BYTES, acc);
+    } else {
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int r = MODE == CONV_FWD ? kh : 2 - kh;  // 1 + dh (fwd) or 1 - dh (dgrad)
+        gemm_stage_mma<BN_, false, false, IDESC>(d, a_s + uint32_t(r * Wr * 128),
+                                                 a_s + A_BYTES + uint32_t(kh * BN_ * 128), acc || kh > 0);
+      }
+    }
   }
   // taps of stride-2 dgrad phase p (parity of d = k - pad must equal p)
   TLK_DEV int ntap1(int parity) const {
@@ -119,6 +149,22 @@ struct ConvGemm {
 
   TLK_DEV void load(const ConvWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const uint32_t b_s = a_s + A_BYTES;
+    if constexpr (HALO) {
+      int b0, y0;
+      pix_origin(w.m0, Hr, Wr, b0, y0);
+      const int cblk = MODE == CONV_FWD ? cin_blk : cout_blk;
+      const int kw = kb / cblk, c0 = (kb % cblk) * 64, dw = kw - 1;
+      tma_load_5d(a_s, &ta[0], c0, MODE == CONV_FWD ? dw : -dw, y0 - 1, b0, w.j, bar);
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int tap = kh * 3 + kw;
+        if (MODE == CONV_FWD)
+          tma_load_5d(b_s + kh * BN_ * 128, &tb[0], tap * cin_blk * 64 + c0, w.n0, w.j, 0, 0, bar);
+        else
+          tma_load_5d(b_s + kh * BN_ * 128, &tb[0], c0, w.n0, tap, w.j, 0, bar);
+      }
+      return;
+    }
     if (MODE == CONV_FWD) {
       const int tap = kb / cin_blk, c0 = (kb % cin_blk) * 64;
       const int dh = tap / ksz - pad, dw = tap % ksz - pad;
@@ -157,6 +203,14 @@ struct ConvGemm {
       const int dh = w.z / ksz - pad, dw = w.z % ksz - pad;
       tma_load_5d(a_s, &ta[0], w.m0, 0, y0, b0, w.j, bar);
       tma_load_5d(a_s + 8192, &ta[0], w.m0 + 64, 0, y0, b0, w.j, bar);
+      if constexpr (TG > 1) {  // stride 1, taps TG*z .. TG*z+TG-1 (one kernel row)
+#pragma unroll
+        for (int i = 0; i < TG; ++i) {
+          const int tap = w.z * TG + i;
+          tma_load_5d(b_s + i * 8192, &tb[0], 0, tap % ksz - pad, y0 + tap / ksz - pad, b0, w.j, bar);
+        }
+        return;
+      }
 #pragma unroll
       for (int i = 0; i < BN_ / 64; ++i) {
         if (stride == 1) {
@@ -173,7 +227,8 @@ struct ConvGemm {
   // element offset of D row m (within lane w.j), column 0
   TLK_DEV int64_t row_off(const ConvWork& w, int m) const {
     if (MODE == CONV_FWD) return int64_t(m) * cols;
-    if (MODE == CONV_WGRAD) return int64_t(w.split) * split_st + int64_t(m) * taps * cols + int64_t(w.z) * cols;
+    if (MODE == CONV_WGRAD)  // (tap group z, column n) -> tap TG z + n / cols, channel n % cols
+      return int64_t(w.split) * split_st + int64_t(m) * taps * cols + int64_t(w.z) * TG * cols;
     if (stride == 1) return int64_t(m) * cols;
     const int py = w.z >> 1, px = w.z & 1;
     const int v = m % Wr, u = (m / Wr) % Hr, b = m / (Wr * Hr);
@@ -190,7 +245,7 @@ struct ConvGemm {
 #pragma unroll
       for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
       __syncwarp();
-      const bool col_ok = n < cols;
+      const bool col_ok = n < cols * TG;
       if (MODE == CONV_FWD) {
         // y = bf16(D); BN statistics of the stored values as (mean, M2) of
         // this warp's 32 rows (centred: combined with Chan's formula later)
@@ -234,18 +289,24 @@ struct ConvGemm {
         }
       } else {
         float* o = static_cast<float*>(out) + w.j * out_ls;
+        float4 prev[8];  // accumulate: all eight row loads in flight before any add
+        if (MODE == CONV_DGRAD && accumulate) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int m = row0 + 4 * k + rsub;
+            prev[k] = (col_ok && m < rows) ? *reinterpret_cast<const float4*>(o + row_off(w, m) + n)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int m = row0 + 4 * k + rsub;
           if (!col_ok || m >= rows) continue;
           const float* x = buf + (4 * k + rsub) * 33 + c4;
-          float4* dst = reinterpret_cast<float4*>(o + row_off(w, m) + n);
           float4 val = make_float4(x[0], x[1], x[2], x[3]);
-          if (MODE == CONV_DGRAD && accumulate) {
-            const float4 a = *dst;
-            val = make_float4(a.x + val.x, a.y + val.y, a.z + val.z, a.w + val.w);
-          }
-          *dst = val;
+          if (MODE == CONV_DGRAD && accumulate)
+            val = make_float4(prev[k].x + val.x, prev[k].y + val.y, prev[k].z + val.z, prev[k].w + val.w);
+          *reinterpret_cast<float4*>(o + row_off(w, m) + n) = val;
         }
       }
       __syncwarp();

@@ -317,6 +317,64 @@ int enqueue_head(Pack& p, cudaStream_t st, const uint16_t* h, int hidden, int64_
 // [a0, a1) u [b0, b1) (float4 units) so a pack can update different tensors
 // in different graph branches (CNN: fc1.w concurrently with the conv
 // backward kernels, everything else at the end of the step).
+// The element loop of the batched optimizer with the optimizer kind fixed
+// at compile time (the kernel branches on the lane's kind once).
+template <int KIND>
+__device__ __forceinline__ void optimizer_loop(const LaneState& s, int lane, int64_t w0, int64_t w1, int64_t na,
+                                               int64_t a0, int64_t b0, int64_t base, float4* __restrict__ P,
+                                               const float4* __restrict__ Gr, float4* __restrict__ M,
+                                               float4* __restrict__ V, uint2* __restrict__ Wb, const WtHook& hook) {
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += 2 * blockDim.x) {
+    const int64_t wb = w + blockDim.x;
+    const bool two = wb < w1;
+    const int64_t ia = base + (w < na ? a0 + w : b0 + (w - na));
+    const int64_t ib = base + (wb < na ? a0 + wb : b0 + (wb - na));
+    float4 pa = P[ia], ma = M[ia], va = V[ia];
+    const float4 ga = Gr[ia];
+    float4 pb, mb, vb, gb;
+    if (two) {
+      pb = P[ib];
+      mb = M[ib];
+      vb = V[ib];
+      gb = Gr[ib];
+    }
+    opt_update_k<KIND>(s, pa.x, ga.x, ma.x, va.x);
+    opt_update_k<KIND>(s, pa.y, ga.y, ma.y, va.y);
+    opt_update_k<KIND>(s, pa.z, ga.z, ma.z, va.z);
+    opt_update_k<KIND>(s, pa.w, ga.w, ma.w, va.w);
+    P[ia] = pa;
+    M[ia] = ma;
+    V[ia] = va;
+    const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
+    Wb[ia] = make_uint2(lo, hi);
+    if (hook.wt) {
+      const int64_t e = (ia - base) * 4;
+      wt_write(hook, lane, e + 0, uint16_t(lo & 0xFFFF));
+      wt_write(hook, lane, e + 1, uint16_t(lo >> 16));
+      wt_write(hook, lane, e + 2, uint16_t(hi & 0xFFFF));
+      wt_write(hook, lane, e + 3, uint16_t(hi >> 16));
+    }
+    if (two) {
+      opt_update_k<KIND>(s, pb.x, gb.x, mb.x, vb.x);
+      opt_update_k<KIND>(s, pb.y, gb.y, mb.y, vb.y);
+      opt_update_k<KIND>(s, pb.z, gb.z, mb.z, vb.z);
+      opt_update_k<KIND>(s, pb.w, gb.w, mb.w, vb.w);
+      P[ib] = pb;
+      M[ib] = mb;
+      V[ib] = vb;
+      const uint32_t lo2 = pack_bf2(pb.x, pb.y), hi2 = pack_bf2(pb.z, pb.w);
+      Wb[ib] = make_uint2(lo2, hi2);
+      if (hook.wt) {
+        const int64_t e = (ib - base) * 4;
+        wt_write(hook, lane, e + 0, uint16_t(lo2 & 0xFFFF));
+        wt_write(hook, lane, e + 1, uint16_t(lo2 >> 16));
+        wt_write(hook, lane, e + 2, uint16_t(hi2 & 0xFFFF));
+        wt_write(hook, lane, e + 3, uint16_t(hi2 >> 16));
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) optimizer_kernel(LaneState* __restrict__ lanes,
                                                         int64_t stride, int64_t a0, int64_t a1,
                                                         int64_t b0, int64_t b1,
@@ -333,55 +391,12 @@ __global__ void __launch_bounds__(256) optimizer_kernel(LaneState* __restrict__ 
   const int64_t per = (work + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = blockIdx.x * per, w1 = min(work, w0 + per);
   const int64_t base = lane * (stride / 4);
-  for (int64_t w = w0 + threadIdx.x; w < w1; w += 2 * blockDim.x) {
-    const int64_t wb = w + blockDim.x;
-    const bool two = wb < w1;
-    const int64_t ia = base + (w < na ? a0 + w : b0 + (w - na));
-    const int64_t ib = base + (wb < na ? a0 + wb : b0 + (wb - na));
-    float4 pa = P[ia], ma = M[ia], va = V[ia];
-    const float4 ga = Gr[ia];
-    float4 pb, mb, vb, gb;
-    if (two) {
-      pb = P[ib];
-      mb = M[ib];
-      vb = V[ib];
-      gb = Gr[ib];
-    }
-    opt_update(s, pa.x, ga.x, ma.x, va.x);
-    opt_update(s, pa.y, ga.y, ma.y, va.y);
-    opt_update(s, pa.z, ga.z, ma.z, va.z);
-    opt_update(s, pa.w, ga.w, ma.w, va.w);
-    P[ia] = pa;
-    M[ia] = ma;
-    V[ia] = va;
-    const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
-    Wb[ia] = make_uint2(lo, hi);
-    if (hook.wt) {
-      const int64_t e = (ia - base) * 4;
-      wt_write(hook, lane, e + 0, uint16_t(lo & 0xFFFF));
-      wt_write(hook, lane, e + 1, uint16_t(lo >> 16));
-      wt_write(hook, lane, e + 2, uint16_t(hi & 0xFFFF));
-      wt_write(hook, lane, e + 3, uint16_t(hi >> 16));
-    }
-    if (two) {
-      opt_update(s, pb.x, gb.x, mb.x, vb.x);
-      opt_update(s, pb.y, gb.y, mb.y, vb.y);
-      opt_update(s, pb.z, gb.z, mb.z, vb.z);
-      opt_update(s, pb.w, gb.w, mb.w, vb.w);
-      P[ib] = pb;
-      M[ib] = mb;
-      V[ib] = vb;
-      const uint32_t lo2 = pack_bf2(pb.x, pb.y), hi2 = pack_bf2(pb.z, pb.w);
-      Wb[ib] = make_uint2(lo2, hi2);
-      if (hook.wt) {
-        const int64_t e = (ib - base) * 4;
-        wt_write(hook, lane, e + 0, uint16_t(lo2 & 0xFFFF));
-        wt_write(hook, lane, e + 1, uint16_t(lo2 >> 16));
-        wt_write(hook, lane, e + 2, uint16_t(hi2 & 0xFFFF));
-        wt_write(hook, lane, e + 3, uint16_t(hi2 >> 16));
-      }
-    }
-  }
+  if (s.optimizer == TLK_OPT_SGD)
+    optimizer_loop<TLK_OPT_SGD>(s, lane, w0, w1, na, a0, b0, base, P, Gr, M, V, Wb, hook);
+  else if (s.optimizer == TLK_OPT_ADAMW)
+    optimizer_loop<TLK_OPT_ADAMW>(s, lane, w0, w1, na, a0, b0, base, P, Gr, M, V, Wb, hook);
+  else
+    optimizer_loop<TLK_OPT_ADAM>(s, lane, w0, w1, na, a0, b0, base, P, Gr, M, V, Wb, hook);
   // the last CTA of this lane to finish ends the lane's step (replaces a
   // separate end-of-step launch)
   __syncthreads();

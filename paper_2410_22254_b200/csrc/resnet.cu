@@ -15,6 +15,7 @@
 //                   block-input gradient
 //   stem BN backward + stem wgrad (SIMT) -> optimizer
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -738,6 +739,11 @@ __global__ void __launch_bounds__(256) rn_stem_wgrad_kernel(const LaneState* __r
 }
 
 // ------------------------------------------------------------- GEMM glue ----
+inline bool getenv_flag(const char* n) {
+  const char* v = getenv(n);
+  return v && v[0] && v[0] != '0';
+}
+
 inline void pix_box(int H, int W, int npix, int& bx, int& by, int& bb) {
   bx = W;
   by = std::min(H, npix / W);
@@ -783,9 +789,15 @@ int enqueue_bn_stats(Pack& p, cudaStream_t st, RnBufs& R, int P, int C, float* s
   return TLK_OK;
 }
 
-template <int BN>
+// stride-1 3x3 conv on a grid whose 128-pixel tiles are whole rows of one
+// image with 8-row-aligned tap shifts: the halo mode of ConvGemm applies
+inline bool halo_ok(const ConvL& L) {
+  return L.stride == 1 && L.k == 3 && (L.W == 16 || L.W == 32) && 128 / L.W <= L.H && !getenv_flag("TLK_NO_HALO");
+}
+
+template <int BN, bool HALO = false>
 int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, const char* name) {
-  using G = ConvGemm<BN, CONV_FWD>;
+  using G = ConvGemm<BN, CONV_FWD, HALO>;
   G g{};
   g.lanes = p.lane_dev;
   g.Hr = L.Ho, g.Wr = L.Wo;
@@ -795,7 +807,9 @@ int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, c
   pix_box(L.Ho, L.Wo, 128, bx, by, bb);
   const int64_t xls = R.act_ls(L.H, L.W, L.cin);
   int rc = 0;
-  if (L.stride == 1) {
+  if (HALO) {
+    rc = act_map_l(&g.ta[0], x, xls, p.lanes, R.B, L.H, L.W, L.cin, -1, L.W, 128 / L.W + 2, 1);
+  } else if (L.stride == 1) {
     rc = act_map_l(&g.ta[0], x, xls, p.lanes, R.B, L.H, L.W, L.cin, -1, bx, by, bb);
   } else {
     for (int ph = 0; ph < 4 && !rc; ++ph)
@@ -814,7 +828,7 @@ int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, c
   g.nt = L.cout / BN;
   g.nz = 1;
   g.ntiles = g.mt * g.nt * p.lanes;
-  g.kblocks = L.k * L.k * g.cin_blk;
+  g.kblocks = (HALO ? 3 : L.k * L.k) * g.cin_blk;
   g.out = L.y;
   g.out_ls = M * L.cout;
   g.rows = int(M);
@@ -832,10 +846,10 @@ int conv_fwd(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, c
 }
 
 // dgrad: out[pix(H x W)][cin] (=|+=) sum dY[..][cout] WT ; fp32
-template <int BN>
+template <int BN, bool HALO = false>
 int conv_dgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, float* out, int accumulate,
                const char* name) {
-  using G = ConvGemm<BN, CONV_DGRAD>;
+  using G = ConvGemm<BN, CONV_DGRAD, HALO>;
   G g{};
   g.lanes = p.lane_dev;
   g.ksz = L.k, g.pad = (L.k - 1) / 2, g.stride = L.stride;
@@ -845,7 +859,9 @@ int conv_dgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
   g.Wr = L.stride == 1 ? L.W : L.Wo;
   int bx, by, bb;
   pix_box(g.Hr, g.Wr, 128, bx, by, bb);
-  int rc = act_map_l(&g.ta[0], dY, R.act_ls(L.Ho, L.Wo, L.cout), p.lanes, R.B, L.Ho, L.Wo, L.cout, -1, bx, by, bb);
+  int rc = HALO ? act_map_l(&g.ta[0], dY, R.act_ls(L.Ho, L.Wo, L.cout), p.lanes, R.B, L.Ho, L.Wo, L.cout, -1, L.Wo,
+                            128 / L.Wo + 2, 1)
+                : act_map_l(&g.ta[0], dY, R.act_ls(L.Ho, L.Wo, L.cout), p.lanes, R.B, L.Ho, L.Wo, L.cout, -1, bx, by, bb);
   if (rc) return rc;
   {
     const int taps = L.k * L.k;
@@ -859,7 +875,7 @@ int conv_dgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
   g.nt = L.cin / BN;
   g.nz = L.stride == 1 ? 1 : (L.k == 1 ? 1 : 4);
   g.ntiles = g.mt * g.nt * g.nz * p.lanes;
-  g.kblocks = L.k * L.k * g.cout_blk;
+  g.kblocks = (HALO ? 3 : L.k * L.k) * g.cout_blk;
   g.out = out;
   g.out_ls = int64_t(R.B) * L.H * L.W * L.cin;
   g.rows = int(Mr);
@@ -872,10 +888,10 @@ int conv_dgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
 }
 
 // wgrad: grads[co][tap][ci] = sum_pix dY[pix][co] X[pix + tap][ci]; split-K
-template <int BN>
+template <int BN, int TG = 1>
 int conv_wgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, const uint16_t* X,
                const char* name) {
-  using G = ConvGemm<BN, CONV_WGRAD>;
+  using G = ConvGemm<BN, CONV_WGRAD, false, TG>;
   G g{};
   g.lanes = p.lane_dev;
   g.ksz = L.k, g.pad = (L.k - 1) / 2, g.stride = L.stride;
@@ -894,19 +910,19 @@ int conv_wgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
   if (rc) return rc;
   const int taps = L.k * L.k;
   g.mt = (L.cout + GEMM_BM - 1) / GEMM_BM;
-  g.nt = L.cin / BN;
+  g.nt = TG > 1 ? 1 : L.cin / BN;
   g.kb_total = int(int64_t(R.B) * L.Ho * L.Wo / 64);
   // split-K count from the per-lane geometry only (never from the lane
   // count), so a job's summation order -- and its bits -- do not depend on
   // how many jobs share the pack
-  const int lane_tiles = g.mt * g.nt * taps;
+  const int lane_tiles = g.mt * g.nt * (taps / TG);
   int splits = std::max(1, std::min((64 + lane_tiles - 1) / lane_tiles, g.kb_total / 8));
   const int64_t wsize = int64_t(L.cout) * taps * L.cin;
   if (splits > 1 && int64_t(splits) * wsize > R.wpart_ls) splits = int(std::max<int64_t>(1, R.wpart_ls / wsize));
   g.kb_split = (g.kb_total + splits - 1) / splits;
   splits = (g.kb_total + g.kb_split - 1) / g.kb_split;
   g.splits = splits;
-  g.nz = taps * splits;
+  g.nz = taps / TG * splits;
   g.ntiles = g.mt * g.nt * g.nz * p.lanes;
   g.kblocks = 0;
   g.taps = taps;
@@ -933,15 +949,22 @@ int conv_wgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
 }
 
 int conv_fwd_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, const char* name) {
+  if (halo_ok(L))
+    return L.cout == 64 ? conv_fwd<64, true>(p, st, R, L, x, name) : conv_fwd<128, true>(p, st, R, L, x, name);
   return L.cout == 64 ? conv_fwd<64>(p, st, R, L, x, name) : conv_fwd<128>(p, st, R, L, x, name);
 }
 int conv_dgrad_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, float* out, int acc,
                    const char* name) {
+  if (halo_ok(L))
+    return L.cin == 64 ? conv_dgrad<64, true>(p, st, R, L, dY, out, acc, name)
+                       : conv_dgrad<128, true>(p, st, R, L, dY, out, acc, name);
   return L.cin == 64 ? conv_dgrad<64>(p, st, R, L, dY, out, acc, name)
                      : conv_dgrad<128>(p, st, R, L, dY, out, acc, name);
 }
 int conv_wgrad_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, const uint16_t* X,
                    const char* name) {
+  if (L.cin == 64 && L.stride == 1 && L.k == 3 && !getenv_flag("TLK_NO_TAPGROUP"))
+    return conv_wgrad<192, 3>(p, st, R, L, dY, X, name);
   return L.cin == 64 ? conv_wgrad<64>(p, st, R, L, dY, X, name) : conv_wgrad<128>(p, st, R, L, dY, X, name);
 }
 

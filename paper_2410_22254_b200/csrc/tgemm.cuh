@@ -25,6 +25,15 @@
 
 namespace tlk {
 
+// One 64-deep k-block of a stage: four K=16 tcgen05.mma into accumulator d.
+template <int BN, bool AMN, bool BMN, uint32_t IDESC>
+TLK_DEV void gemm_stage_mma(uint32_t d, uint32_t a_s, uint32_t b_s, bool acc) {
+#pragma unroll
+  for (int kk = 0; kk < GEMM_BK / 16; ++kk)
+    mma_bf16(d, stage_desc_tma<GEMM_BM, AMN>(a_s, kk), stage_desc_tma<BN, BMN>(b_s, kk), IDESC,
+             (acc || kk > 0) ? 1u : 0u);
+}
+
 template <int BN_, bool AMN, bool BMN, bool ROW>
 struct TGemm {
   static constexpr int BN = BN_;
@@ -66,6 +75,11 @@ struct TGemm {
   TLK_DEV void prefetch() const {
     tma_prefetch_desc(&ta);
     tma_prefetch_desc(&tb);
+  }
+  TLK_DEV uint32_t tx_bytes() const { return STAGE_BYTES; }
+  template <uint32_t IDESC>
+  TLK_DEV void issue_mma(uint32_t d, uint32_t a_s, bool acc) const {
+    gemm_stage_mma<BN_, AMN, BMN, IDESC>(d, a_s, a_s + A_BYTES, acc);
   }
   TLK_DEV void epilogue(const ZWork& w, uint32_t tq, int row0, float* buf, int lane) const {
     g.template tile<BN_>(w, tq, row0, buf, lane, ROW);
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
         for (int kb = w.kb_begin; kb < w.kb_end; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);
-          mbar_expect_tx(&full_bar[s], P::STAGE_BYTES);
+          mbar_expect_tx(&full_bar[s], p.tx_bytes());
           p.load(w, kb, sbase + s * P::STAGE_BYTES, &full_bar[s]);
         }
       }
@@ -149,11 +163,8 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
           const int s = it % STAGES;
           mbar_wait(&full_bar[s], (it / STAGES) & 1);
           tc_fence_after();
-          const uint32_t a_s = sbase + s * P::STAGE_BYTES, b_s = a_s + P::A_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < GEMM_BK / 16; ++kk)
-            mma_bf16(d, stage_desc_tma<GEMM_BM, P::A_MN>(a_s, kk), stage_desc_tma<BN, P::B_MN>(b_s, kk),
-                     IDESC, (kb > w.kb_begin || kk > 0) ? 1u : 0u);
+          const uint32_t a_s = sbase + s * P::STAGE_BYTES;
+          p.template issue_mma<IDESC>(d, a_s, kb > w.kb_begin);
           mma_commit(&empty_bar[s]);
         }
         mma_commit(&tfull[buf]);

@@ -216,11 +216,16 @@ def test_loss_curve_and_packing_invariance():
         for lane, (seed, kw) in enumerate(jobs):
             got = packed.losses(lane, steps)
             ref, _, _ = ojob.train_resnet(seed, steps, B, ooptim.OptState(kind=ooptim.SGD, **kw), bf16=True)
+            ref32, _, _ = ojob.train_resnet(seed, steps, B, ooptim.OptState(kind=ooptim.SGD, **kw), bf16=False)
             # first step: forward only (bf16 rounding flips through 20 BN layers
             # move the loss by ~1e-3); later steps drift with the chaotic
-            # bf16 gradients (see test_layerwise_backward)
+            # bf16 gradients (see test_layerwise_backward): the bound per step
+            # is 0.05 or 3x the oracle's own bf16-vs-fp32 spread, whichever is
+            # larger (any change of fp32 summation order -- e.g. the halo conv
+            # tap order -- moves step 4 by a few 1e-2 at batch 16)
             assert abs(got[0] - ref[0]) < 5e-3 * abs(ref[0])
-            np.testing.assert_allclose(got, ref, atol=0.05, rtol=0)
+            tol = np.maximum(0.05, 3.0 * np.abs(ref - ref32))
+            assert np.all(np.abs(got - ref) <= tol), (got, ref, ref32)
             alone = ctx.pack(rt.MODEL_RESNET18, B, 1, steps)
             alone.load(0, seed=seed, steps=steps, optimizer=rt.OPT_SGD, **kw)
             alone.run(steps)
