@@ -719,9 +719,22 @@ __global__ void __launch_bounds__(256) rn_stem_wgrad_kernel(const LaneState* __r
   const int t0 = grp * 7, tn = grp == 3 ? 6 : 7;
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const uint16_t* dyi = dy + (int64_t(j) * B + img) * 1024 * 64;
+  // one 16-byte dy vector per thread per row (32 px x 64 ch = 256 x 8 bf16),
+  // the next row's vector in flight while this row is consumed
+  uint4 nxt = reinterpret_cast<const uint4*>(dyi)[tid];
   for (int row = 0; row < 32; ++row) {
+    const uint4 cur = nxt;
+    if (row + 1 < 32) nxt = reinterpret_cast<const uint4*>(dyi + (row + 1) * 32 * 64)[tid];
     __syncthreads();
-    for (int i = tid; i < 32 * 64; i += 256) ds[i / 64][i % 64] = bf2f(dyi[row * 32 * 64 + i]);
+    {
+      const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
+      float* dst = &ds[tid >> 3][(tid & 7) * 8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        dst[2 * e] = __uint_as_float(w4[e] << 16);
+        dst[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
+      }
+    }
     __syncthreads();
     for (int px = 0; px < 32; ++px) {
       const float d = ds[px][co];
@@ -948,13 +961,19 @@ int conv_wgrad(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY
   return TLK_OK;
 }
 
+// 256-wide N tiles halve the A-operand (activation) L2 traffic per MMA for
+// the 256/512-channel layers (TLK_CONV_BN256=0 restores 128)
+inline bool wide_n(int channels) { return channels >= 256 && !(getenv("TLK_CONV_BN256") && getenv("TLK_CONV_BN256")[0] == '0'); }
+
 int conv_fwd_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* x, const char* name) {
+  if (wide_n(L.cout) && !halo_ok(L)) return conv_fwd<256>(p, st, R, L, x, name);
   if (halo_ok(L))
     return L.cout == 64 ? conv_fwd<64, true>(p, st, R, L, x, name) : conv_fwd<128, true>(p, st, R, L, x, name);
   return L.cout == 64 ? conv_fwd<64>(p, st, R, L, x, name) : conv_fwd<128>(p, st, R, L, x, name);
 }
 int conv_dgrad_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, float* out, int acc,
                    const char* name) {
+  if (wide_n(L.cin) && !halo_ok(L)) return conv_dgrad<256>(p, st, R, L, dY, out, acc, name);
   if (halo_ok(L))
     return L.cin == 64 ? conv_dgrad<64, true>(p, st, R, L, dY, out, acc, name)
                        : conv_dgrad<128, true>(p, st, R, L, dY, out, acc, name);
@@ -963,6 +982,7 @@ int conv_dgrad_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t
 }
 int conv_wgrad_any(Pack& p, cudaStream_t st, RnBufs& R, ConvL& L, const uint16_t* dY, const uint16_t* X,
                    const char* name) {
+  if (wide_n(L.cin)) return conv_wgrad<256>(p, st, R, L, dY, X, name);
   if (L.cin == 64 && L.stride == 1 && L.k == 3 && !getenv_flag("TLK_NO_TAPGROUP"))
     return conv_wgrad<192, 3>(p, st, R, L, dY, X, name);
   return L.cin == 64 ? conv_wgrad<64>(p, st, R, L, dY, X, name) : conv_wgrad<128>(p, st, R, L, dY, X, name);
