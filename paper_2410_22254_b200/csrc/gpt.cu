@@ -13,6 +13,7 @@
 // bias / gain / embedding gradient are deterministic two-stage reductions.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "pack.cuh"
@@ -412,6 +413,18 @@ int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, con
   return TLK_OK;
 }
 
+// Dense (non-row-epilogue) GEMMs: the widest N tile that divides N (256,
+// 192, else 128).  Wider tiles reuse each A (activation) tile across more
+// columns: fewer L2 -> SM bytes per MMA (TLK_GEMM_BN128=1 forces 128).
+template <bool AMN, bool BMN>
+int gemm_auto(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M, int N, int K,
+              int nb, int nh, const char* name) {
+  static const bool narrow = getenv("TLK_GEMM_BN128") && getenv("TLK_GEMM_BN128")[0] == '1';
+  if (!narrow && N % 256 == 0) return gemm<256, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
+  if (!narrow && N % 192 == 0) return gemm<192, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
+  return gemm<128, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
+}
+
 Epi epi(int kind, int rows, int cols, void* out, int64_t ls, int64_t bs, int64_t hs, int64_t ld) {
   Epi e{};
   e.kind = kind;
@@ -556,7 +569,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       Epi e = epi(EPI_BF16, N, 3 * d, lb.qkv, nd3, 0, 0, 3 * d);
       e.bias = PR + O(T_LAYER(l, K_AB));
       e.bias_ls = PS;
-      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.a, nd, 0, 0, d, 1, N, d),
+      TLK_TRY((gemm_auto<false, false>(p, st, op(lb.a, nd, 0, 0, d, 1, N, d),
                                               op(WB + O(T_LAYER(l, K_AW)), PS, 0, 0, d, 1, 3 * d, d), e,
                                               N, 3 * d, d, 1, 1, "qkv")));
       ++count;
@@ -587,7 +600,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       e.aux = lb.xin;
       e.bias = PR + O(T_LAYER(l, K_PB));
       e.bias_ls = PS;
-      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.y, nd, 0, 0, d, 1, N, d),
+      TLK_TRY((gemm_auto<false, false>(p, st, op(lb.y, nd, 0, 0, d, 1, N, d),
                                               op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, d, 1, d, d), e, N,
                                               d, d, 1, 1, "proj")));
       ++count;
@@ -601,7 +614,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       e.out32b = lb.z;
       e.bias = PR + O(T_LAYER(l, K_FB));
       e.bias_ls = PS;
-      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.m, nd, 0, 0, d, 1, N, d),
+      TLK_TRY((gemm_auto<false, false>(p, st, op(lb.m, nd, 0, 0, d, 1, N, d),
                                               op(WB + O(T_LAYER(l, K_FW)), PS, 0, 0, d, 1, 4 * d, d), e,
                                               N, 4 * d, d, 1, 1, "fc")));
       ++count;
@@ -611,7 +624,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       e.aux = lb.xmid;
       e.bias = PR + O(T_LAYER(l, K_F2B));
       e.bias_ls = PS;
-      TLK_TRY((gemm<128, false, false, false>(p, st, op(lb.f, nd4, 0, 0, 4 * d, 1, N, 4 * d),
+      TLK_TRY((gemm_auto<false, false>(p, st, op(lb.f, nd4, 0, 0, 4 * d, 1, N, 4 * d),
                                               op(WB + O(T_LAYER(l, K_F2W)), PS, 0, 0, 4 * d, 1, d, 4 * d),
                                               e, N, d, 4 * d, 1, 1, "fc2")));
       ++count;
@@ -647,11 +660,11 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   // ---------------------------------------------------------------- backward
   {  // dxf = dl Whead (fp32), dWhead = dl^T xf
     Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
-    TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, Vp, 1, N, V),
+    TLK_TRY((gemm_auto<false, true>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, Vp, 1, N, V),
                                            op(WB + O(tf + 2), PS, 0, 0, 1, d, d, V), e, N, d, V, 1, 1,
                                            "head_dgrad")));
     Epi g = epi(EPI_F32, V, d, G + O(tf + 2), PS, 0, 0, d);
-    TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, 1, Vp, V, N),
+    TLK_TRY((gemm_auto<true, true>(p, st, op(b.dl, int64_t(N) * Vp, 0, 0, 1, Vp, V, N),
                                           op(b.xf, nd, 0, 0, 1, d, d, N), g, V, d, N, 1, 1, "head_wgrad")));
     count += 2;
   }
@@ -705,25 +718,25 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     LayerBufs& lb = b.L[l];
     {  // fc2: dW2 = dxb^T f ; db2 ; dz = (dxb W2) * gelu'(z)
       Epi g = epi(EPI_F32, d, 4 * d, G + O(T_LAYER(l, K_F2W)), PS, 0, 0, 4 * d);
-      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
+      TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
                                             op(lb.f, nd4, 0, 0, 1, 4 * d, 4 * d, N), g, d, 4 * d, N, 1, 1,
                                             "fc2_wgrad")));
       TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_F2B)));
       Epi e = epi(EPI_GELU_BWD, N, 4 * d, b.dz, nd4, 0, 0, 4 * d);
       e.aux = lb.z;
-      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+      TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
                                              op(WB + O(T_LAYER(l, K_F2W)), PS, 0, 0, 1, 4 * d, 4 * d, d), e,
                                              N, 4 * d, d, 1, 1, "fc2_dgrad")));
       count += 2;
     }
     {  // fc: dW1 = dz^T m ; db1 ; dmm = dz W1 (fp32)
       Epi g = epi(EPI_F32, 4 * d, d, G + O(T_LAYER(l, K_FW)), PS, 0, 0, d);
-      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dz, nd4, 0, 0, 1, 4 * d, 4 * d, N),
+      TLK_TRY((gemm_auto<true, true>(p, st, op(b.dz, nd4, 0, 0, 1, 4 * d, 4 * d, N),
                                             op(lb.m, nd, 0, 0, 1, d, d, N), g, 4 * d, d, N, 1, 1,
                                             "fc_wgrad")));
       TLK_TRY(bias_grad(b.dz, 4 * d, T_LAYER(l, K_FB)));
       Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
-      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dz, nd4, 0, 0, 4 * d, 1, N, 4 * d),
+      TLK_TRY((gemm_auto<false, true>(p, st, op(b.dz, nd4, 0, 0, 4 * d, 1, N, 4 * d),
                                              op(WB + O(T_LAYER(l, K_FW)), PS, 0, 0, 1, d, d, 4 * d), e, N,
                                              d, 4 * d, 1, 1, "fc_dgrad")));
       count += 2;
@@ -731,11 +744,11 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     TLK_TRY(ln_bwd(b.dmm, lb.xmid, lb.st2, T_LAYER(l, K_LN2G), T_LAYER(l, K_LN2B), 1, "ln2_bwd"));
     {  // proj: dWo = dxb^T y ; dbo ; dy = dxb Wo (bf16)
       Epi g = epi(EPI_F32, d, d, G + O(T_LAYER(l, K_PW)), PS, 0, 0, d);
-      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
+      TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
                                             op(lb.y, nd, 0, 0, 1, d, d, N), g, d, d, N, 1, 1, "proj_wgrad")));
       TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_PB)));
       Epi e = epi(EPI_BF16, N, d, b.dy, nd, 0, 0, d);
-      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+      TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
                                              op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d), e, N, d, d,
                                              1, 1, "proj_dgrad")));
       count += 2;
@@ -778,12 +791,12 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     }
     {  // qkv: dWqkv = dqkv^T a ; db ; da = dqkv Wqkv (fp32)
       Epi g = epi(EPI_F32, 3 * d, d, G + O(T_LAYER(l, K_AW)), PS, 0, 0, d);
-      TLK_TRY((gemm<128, true, true, false>(p, st, op(b.dqkv, nd3, 0, 0, 1, 3 * d, 3 * d, N),
+      TLK_TRY((gemm_auto<true, true>(p, st, op(b.dqkv, nd3, 0, 0, 1, 3 * d, 3 * d, N),
                                             op(lb.a, nd, 0, 0, 1, d, d, N), g, 3 * d, d, N, 1, 1,
                                             "qkv_wgrad")));
       TLK_TRY(bias_grad(b.dqkv, 3 * d, T_LAYER(l, K_AB)));
       Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
-      TLK_TRY((gemm<128, false, true, false>(p, st, op(b.dqkv, nd3, 0, 0, 3 * d, 1, N, 3 * d),
+      TLK_TRY((gemm_auto<false, true>(p, st, op(b.dqkv, nd3, 0, 0, 3 * d, 1, N, 3 * d),
                                              op(WB + O(T_LAYER(l, K_AW)), PS, 0, 0, 1, d, d, 3 * d), e, N, d,
                                              3 * d, 1, 1, "qkv_dgrad")));
       count += 2;
