@@ -324,18 +324,22 @@ __device__ __forceinline__ void optimizer_loop(const LaneState& s, int lane, int
                                                int64_t a0, int64_t b0, int64_t base, float4* __restrict__ P,
                                                const float4* __restrict__ Gr, float4* __restrict__ M,
                                                float4* __restrict__ V, uint2* __restrict__ Wb, const WtHook& hook) {
+  // SGD never touches v, and without momentum not m either: no traffic for them
+  constexpr bool HASV = KIND != TLK_OPT_SGD;
+  const bool hasm = KIND != TLK_OPT_SGD || s.momentum != 0.0f;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t w = w0 + threadIdx.x; w < w1; w += 2 * blockDim.x) {
     const int64_t wb = w + blockDim.x;
     const bool two = wb < w1;
     const int64_t ia = base + (w < na ? a0 + w : b0 + (w - na));
     const int64_t ib = base + (wb < na ? a0 + wb : b0 + (wb - na));
-    float4 pa = P[ia], ma = M[ia], va = V[ia];
+    float4 pa = P[ia], ma = hasm ? M[ia] : z4, va = HASV ? V[ia] : z4;
     const float4 ga = Gr[ia];
     float4 pb, mb, vb, gb;
     if (two) {
       pb = P[ib];
-      mb = M[ib];
-      vb = V[ib];
+      mb = hasm ? M[ib] : z4;
+      vb = HASV ? V[ib] : z4;
       gb = Gr[ib];
     }
     opt_update_k<KIND>(s, pa.x, ga.x, ma.x, va.x);
@@ -343,8 +347,8 @@ __device__ __forceinline__ void optimizer_loop(const LaneState& s, int lane, int
     opt_update_k<KIND>(s, pa.z, ga.z, ma.z, va.z);
     opt_update_k<KIND>(s, pa.w, ga.w, ma.w, va.w);
     P[ia] = pa;
-    M[ia] = ma;
-    V[ia] = va;
+    if (hasm) M[ia] = ma;
+    if (HASV) V[ia] = va;
     const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
     Wb[ia] = make_uint2(lo, hi);
     if (hook.wt) {
@@ -360,8 +364,8 @@ __device__ __forceinline__ void optimizer_loop(const LaneState& s, int lane, int
       opt_update_k<KIND>(s, pb.z, gb.z, mb.z, vb.z);
       opt_update_k<KIND>(s, pb.w, gb.w, mb.w, vb.w);
       P[ib] = pb;
-      M[ib] = mb;
-      V[ib] = vb;
+      if (hasm) M[ib] = mb;
+      if (HASV) V[ib] = vb;
       const uint32_t lo2 = pack_bf2(pb.x, pb.y), hi2 = pack_bf2(pb.z, pb.w);
       Wb[ib] = make_uint2(lo2, hi2);
       if (hook.wt) {

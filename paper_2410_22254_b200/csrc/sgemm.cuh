@@ -60,7 +60,12 @@ TLK_DEV float tanh_fast(float x) {
 }
 // e^x on the SFU (ex2.approx; ~2 ulp): softmax / CE probabilities are stored
 // as bf16; the CE loss value itself uses logf of the (fp32) sum.
-TLK_DEV float exp_fast(float x) { return exp2f(x * 1.4426950408889634f); }
+TLK_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+TLK_DEV float exp_fast(float x) { return ex2_approx(x * 1.4426950408889634f); }
 
 TLK_DEV float gelu_tanh(float x, float& t) {
   const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
@@ -215,29 +220,48 @@ struct EpiOps {
     const int64_t step = 4 * e.ld;
     float v[32];
     if (e.kind == EPI_SOFTMAX) {
-      // p = 2^(v*k - mx*k), k = scale * log2(e)
+      // p = 2^(v*k - mx*k), k = scale * log2(e), on the SFU (ex2.approx, ~2
+      // ulp; P is stored as bf16).  Only the chunk holding the causal
+      // diagonal (or the ragged last chunk) needs per-element bounds checks.
       const float k2 = e.scale * 1.4426950408889634f;
+      const int cfull = e.causal ? row0 : (ncols & ~31);  // chunks below cfull are whole for every lane
       float mx = -INFINITY;
       for (int c0 = 0; c0 < wlim; c0 += 32) {
         tmem_ld32(taddr + c0, v);
+        if (c0 < cfull) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < lim) mx = fmaxf(mx, v[i]);
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < lim) mx = fmaxf(mx, v[i]);
+        }
       }
       const float mk = mx * k2;
       float s = 0.f;
       for (int c0 = 0; c0 < wlim; c0 += 32) {
         tmem_ld32(taddr + c0, v);
+        if (c0 < cfull) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < lim) s += exp2f(fmaf(v[i], k2, -mk));
+          for (int i = 0; i < 32; ++i) s += ex2_approx(fmaf(v[i], k2, -mk));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < lim) s += ex2_approx(fmaf(v[i], k2, -mk));
+        }
       }
       const float inv = 1.f / s;
       uint16_t* out = static_cast<uint16_t*>(e.out) + off(w, row0 + rsub, c4);
       for (int c0 = 0; c0 < wlim; c0 += 32) {
         tmem_ld32(taddr + c0, v);
+        if (c0 < cfull) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = (c0 + i < lim) ? exp2f(fmaf(v[i], k2, -mk)) * inv : 0.f;
+          for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = ex2_approx(fmaf(v[i], k2, -mk)) * inv;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            buf[lane * 33 + i] = (c0 + i < lim) ? ex2_approx(fmaf(v[i], k2, -mk)) * inv : 0.f;
+        }
         store_chunk(out + c0, step, row0, buf, lane);
       }
     } else if (e.kind == EPI_SOFTMAX_BWD) {
