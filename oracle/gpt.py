@@ -22,7 +22,8 @@ embeddings U(-1/sqrt(fan_in), 1/sqrt(fan_in)) from the shared counter RNG
 
 bf16=True rounds where the CUDA path rounds: GEMM weight operands (bf16
 shadow), LayerNorm outputs, q/k/v, attention probabilities, attention
-outputs, GELU outputs, and every gradient fed to a GEMM; the residual stream
+outputs, GELU outputs and the stored GELU pre-activation (GELU' is evaluated
+at bf16(z)), and every gradient fed to a GEMM; the residual stream
 and its gradient, softmax / LayerNorm statistics, the logits and the GEMM
 outputs consumed by LayerNorm backward stay fp32.  The attention backward
 uses the stored bf16 probabilities (ds = P (dP - D) / sqrt(dh), with
@@ -230,7 +231,11 @@ def gpt_step(cfg: GptCfg, p: dict, toks: np.ndarray, bf16: bool = True):
         g[q_ + "fc2.w"] = dxb.T @ f
         g[q_ + "fc2.b"] = dxb.sum(axis=0)
         df = dxb @ w2
-        dz = _r(df * gelu_bwd(z, tz), bf16)
+        if bf16:  # the CUDA path stores z as bf16 and evaluates GELU' there
+            zb = round_bf16(z)
+            dz = _r(df * gelu_bwd(zb, np.tanh(GELU_C * (zb + GELU_K * zb * zb * zb))), bf16)
+        else:
+            dz = df * gelu_bwd(z, tz)
         g[q_ + "fc.w"] = dz.T @ mm
         g[q_ + "fc.b"] = dz.sum(axis=0)
         dmm = dz @ w1

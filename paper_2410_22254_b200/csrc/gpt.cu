@@ -30,7 +30,8 @@ __constant__ int kMarkovC[8] = {1, 2, 3, 5, 8, 13, 21, 34};
 namespace {
 
 struct LayerBufs {
-  float *xin, *xmid, *st1, *st2, *z;
+  float *xin, *xmid, *st1, *st2;
+  uint16_t* z;  // bf16 GELU pre-activation (the GELU backward evaluates at bf16(z))
   uint16_t *a, *qkv, *P, *y, *m, *f;
 };
 
@@ -484,7 +485,7 @@ int gpt_setup(Pack& p) {
     add(reinterpret_cast<void**>(&lb.xmid), L * N * d * 4);
     add(reinterpret_cast<void**>(&lb.st1), L * N * 2 * 4);
     add(reinterpret_cast<void**>(&lb.st2), L * N * 2 * 4);
-    add(reinterpret_cast<void**>(&lb.z), L * N * 4 * d * 4);
+    add(reinterpret_cast<void**>(&lb.z), L * N * 4 * d * 2);
     add(reinterpret_cast<void**>(&lb.a), L * N * d * 2);
     add(reinterpret_cast<void**>(&lb.qkv), L * N * 3 * d * 2);
     add(reinterpret_cast<void**>(&lb.P), L * p.batch * H * T * T * 2);
@@ -611,7 +612,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     marked("ln2");
     {  // z = m W1^T + b1, f = gelu(z)
       Epi e = epi(EPI_BF16_GELU, N, 4 * d, lb.f, nd4, 0, 0, 4 * d);
-      e.out32b = lb.z;
+      e.out2 = lb.z;
       e.bias = PR + O(T_LAYER(l, K_FB));
       e.bias_ls = PS;
       TLK_TRY((gemm_auto<false, false>(p, st, op(lb.m, nd, 0, 0, d, 1, N, d),

@@ -18,10 +18,10 @@ struct Operand {  // element (mn, k) = base + lane*ls + zb*bs + zh*hs + mn*mn_st
 
 enum EpiKind : int {
   EPI_BF16 = 0,      // out16 = bf16(acc + bias)
-  EPI_BF16_GELU,     // z = acc + bias -> out32 (z); out16 = bf16(gelu_tanh(z))
+  EPI_BF16_GELU,     // z = acc + bias -> out2 = bf16(z); out16 = bf16(gelu_tanh(z))
   EPI_F32,           // out32 = acc
   EPI_RESADD,        // out32 = aux32 + acc + bias
-  EPI_GELU_BWD,      // out16 = bf16(acc * gelu'(aux32))
+  EPI_GELU_BWD,      // out16 = bf16(acc * gelu'(aux16))
   EPI_SOFTMAX,       // row: out16 = bf16(softmax(acc * scale, causal))
   EPI_SOFTMAX_BWD,   // row: out16 = bf16(P (acc - D) * scale), P = aux16, D = rowvec
   EPI_CE,            // row: cross entropy vs targets -> lossrow, out16 = bf16(dlogits)
@@ -32,10 +32,10 @@ struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
   int rows, cols;  // valid output extent (rows = M, cols = N)
   void* out;
   int64_t ls, bs, hs, ld;
-  float* out32b;   // second output (EPI_BF16_GELU: pre-activation z, same indexing)
+  uint16_t* out2;  // second output (EPI_BF16_GELU: bf16 pre-activation z, same indexing)
   const float* bias;  // fp32, + lane * bias_ls
   int64_t bias_ls;
-  const void* aux;    // EPI_RESADD / EPI_GELU_BWD: fp32, EPI_SOFTMAX_BWD: bf16 (same indexing)
+  const void* aux;    // EPI_RESADD: fp32, EPI_GELU_BWD / EPI_SOFTMAX_BWD: bf16 (same indexing)
   float scale;
   int causal;
   const int32_t* targets;  // EPI_CE: [lane][rows] (+ lane*tg_ls)
@@ -108,11 +108,22 @@ struct EpiOps {
     float4 ax[8], nx[8];
     auto fetch = [&](int cc, float4 (&dst)[8]) {
       const int n = w.n0 + cc * 32 + c4;
-      const float* a = static_cast<const float*>(e.aux) + o0 + cc * 32;
+      if constexpr (KIND == EPI_GELU_BWD) {  // bf16 pre-activation
+        const uint16_t* a = static_cast<const uint16_t*>(e.aux) + o0 + cc * 32;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        dst[k] = (n < e.cols && row0 + 4 * k + rsub < e.rows) ? *reinterpret_cast<const float4*>(a + k * step)
-                                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < 8; ++k) {
+          const uint2 u = (n < e.cols && row0 + 4 * k + rsub < e.rows) ? *reinterpret_cast<const uint2*>(a + k * step)
+                                                                       : make_uint2(0u, 0u);
+          dst[k] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                               __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+        }
+      } else {
+        const float* a = static_cast<const float*>(e.aux) + o0 + cc * 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          dst[k] = (n < e.cols && row0 + 4 * k + rsub < e.rows) ? *reinterpret_cast<const float4*>(a + k * step)
+                                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     };
     if constexpr (AUX) fetch(0, nx);
 #pragma unroll 1
@@ -150,7 +161,7 @@ struct EpiOps {
               make_uint2(pack_bf2(y0, y1), pack_bf2(y2, y3));
         } else if constexpr (KIND == EPI_BF16_GELU) {
           float t;
-          *reinterpret_cast<float4*>(e.out32b + oo) = make_float4(y0, y1, y2, y3);
+          *reinterpret_cast<uint2*>(e.out2 + oo) = make_uint2(pack_bf2(y0, y1), pack_bf2(y2, y3));
           const float g0 = gelu_tanh(y0, t), g1 = gelu_tanh(y1, t), g2 = gelu_tanh(y2, t),
                       g3 = gelu_tanh(y3, t);
           *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) =
