@@ -7,8 +7,11 @@ Mirrors the reference CLI's ``plan`` and ``exec`` modes (cli.py:99-142,
 264-337): same flags, same settings precedence (flag > --config JSON >
 default), same artefacts (node_###.sh + plan_summary.json; run_report.json
 in a runs/<ts>-<mode> directory), same exit codes (ConfigError/TripleError
--> 2; exec -> min(failures, 125)).  New: ``--backend {subprocess,packed}``
-and ``--chunk``.  The reference's sim/sweep/report modes model or tabulate
+-> 2; exec -> min(failures, 125)), and the exec-mode telemetry sampler
+(``--provider {none,host,command,const,nvml} --interval --query-cmd`` ->
+telemetry.csv in the reference's schema, cli.py:227-249,298-329; ``nvml`` is
+new: the packed workers' GPUs through NVML).  New: ``--backend
+{subprocess,packed}`` and ``--chunk``.  The reference's sim/sweep/report modes model or tabulate
 runs without touching a GPU; they are outside the packed hot path
  and are rejected here with exit status 2.
 """
@@ -19,12 +22,17 @@ import argparse
 import json
 import os
 import sys
+import threading
 import time
 from pathlib import Path
 
 from .core import NodeSpec, TripleError, TripleSpec, validate_triple
 from .executor import BACKENDS, run_plan
 from .plan import TaskDef, build_plan, emit_script, load_workload, plan_summary
+from .telemetry import (DEFAULT_QUERY_COMMAND, CommandProvider, ConstantProvider, GpuReading, HostProvider,
+                        NvmlProvider, run_sampler, write_series_csv)
+
+QUERY_CMD_ENV = "TRILAUNCH_QUERY_CMD"  # reference cli.py:53
 
 DEFAULTS = {
     "cores": os.cpu_count() or 1,
@@ -35,6 +43,9 @@ DEFAULTS = {
     "node_index": 0,
     "backend": "subprocess",
     "chunk": 64,
+    "provider": "none",
+    "interval": 1.0,
+    "query_cmd": os.environ.get(QUERY_CMD_ENV, DEFAULT_QUERY_COMMAND),
 }
 OUT_OF_SCOPE = ("sim", "sweep", "report")
 
@@ -74,6 +85,10 @@ def _parser():
     p.add_argument("--timeout", type=float)
     p.add_argument("--backend", choices=BACKENDS)
     p.add_argument("--chunk", type=int, help="packed backend: steps per graph-replay chunk")
+    p.add_argument("--provider", choices=("none", "host", "command", "const", "nvml"),
+                   help="telemetry source while executing (telemetry.csv)")
+    p.add_argument("--query-cmd", help=f"device query command for --provider command (or {QUERY_CMD_ENV})")
+    p.add_argument("--interval", type=float, help="sampling interval in seconds")
     return p
 
 
@@ -156,17 +171,56 @@ def _mode_plan(s):
     return 0
 
 
+def _provider(s, node):
+    """Telemetry provider of an exec run (reference cli.py:227-249, + nvml)."""
+    kind = s.get("provider")
+    if kind == "none":
+        return None
+    if not float(s.get("interval")) > 0:
+        raise ConfigError("--interval must be positive")
+    if kind == "host":
+        if node.gpus > 0:
+            raise ConfigError("host provider reports no devices; use --provider command when --gpus > 0")
+        return HostProvider()
+    if kind in ("command", "nvml") and node.gpus < 1:
+        raise ConfigError(f"{kind} provider needs --gpus >= 1")
+    if kind == "command":
+        return CommandProvider(ngpus=node.gpus, command=str(s.get("query_cmd")))
+    if kind == "nvml":
+        try:
+            return NvmlProvider(node.gpus)
+        except ValueError as exc:
+            raise ConfigError(str(exc)) from exc
+    if kind == "const":
+        return ConstantProvider(gpu_readings=tuple(GpuReading(0.0, 0) for _ in range(node.gpus)))
+    raise ConfigError(f"unknown provider {kind!r}")
+
+
 def _mode_exec(s):
-    triple, _, plan = _plan_inputs(s)
+    triple, node, plan = _plan_inputs(s)
     ni = int(s.get("node_index"))
     if not 0 <= ni < triple.nnode:
         raise ConfigError(f"--node-index {ni} outside 0..{triple.nnode - 1}")
+    provider = _provider(s, node)
     d = _run_dir(s, "exec")
+    stop, box, sampler = threading.Event(), {}, None
+    if provider is not None:
+        interval = float(s.get("interval"))
+        sampler = threading.Thread(target=lambda: box.setdefault("series", run_sampler(provider, interval, stop)),
+                                   name="sampler", daemon=True)
+        sampler.start()
     t = s.get("timeout")
     backend = s.get("backend")
     opts = {"chunk": int(s.get("chunk"))} if backend == "packed" else None
-    report = run_plan(plan, ni, timeout_s=float(t) if t is not None else None, log_dir=d / "logs",
-                      backend=backend, packed_options=opts)
+    try:
+        report = run_plan(plan, ni, timeout_s=float(t) if t is not None else None, log_dir=d / "logs",
+                          backend=backend, packed_options=opts)
+    finally:
+        if sampler is not None:
+            stop.set()
+            sampler.join()
+            if "series" in box:
+                write_series_csv(box["series"], d / "telemetry.csv")
     report.write_json(d / "run_report.json")
     print(f"elapsed_ms={report.elapsed_ms} failures={report.failures} "
           f"peak_concurrency={report.max_observed_concurrency}")

@@ -102,3 +102,18 @@ def test_heterogeneous_mix_config4(tmp_path):
         ref = _alone(spec)
         assert out["steps"] == spec.steps
         assert np.float32(out["first_loss"]) == ref[0] and np.float32(out["last_loss"]) == ref[-1], i
+
+
+def test_cli_exec_packed_with_nvml_telemetry(tmp_path):
+    """--backend packed --provider nvml: the packed worker's GPU shows up in
+    telemetry.csv (reference schema) while a few hundred CNN steps run."""
+    from paper_2410_22254_b200 import cli, telemetry as tm
+    specs = [JobSpec(model="cnn", seed=300 + i, steps=400, lr=1e-3) for i in range(4)]
+    (tmp_path / "jobs.jsonl").write_text("".join(json.dumps({"argv": s.argv(sys.executable)}) + "\n" for s in specs))
+    rc = cli.run_cli(["--mode", "exec", "--triple", "1,4,1", "--tasks", str(tmp_path / "jobs.jsonl"), "--gpus", "1",
+                      "--backend", "packed", "--provider", "nvml", "--interval", "0.05", "--outdir", str(tmp_path),
+                      "--run-name", "r"])
+    assert rc == 0
+    series = tm.read_series_csv(tmp_path / "r" / "telemetry.csv")
+    assert series.samples and all(len(s.gpu) == 1 for s in series.samples)
+    assert max(s.gpu[0].mem_mib for s in series.samples) > 0

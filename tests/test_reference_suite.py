@@ -1,8 +1,8 @@
 """Run the REFERENCE's own test files against this package (CPU, here only).
 
 A throwaway shim package named ``trilaunch`` maps ``trilaunch.core``,
-``trilaunch.plan`` and ``trilaunch.executor`` onto paper_2410_22254_b200's
-modules; the reference's out-of-scope modules (sim, report, telemetry, cli)
+``trilaunch.plan``, ``trilaunch.executor`` and ``trilaunch.telemetry`` onto
+paper_2410_22254_b200's modules; the reference's out-of-scope modules (sim, report, cli)
 load from /root/reference unchanged and therefore run ON TOP of our plan
 layer.  The reference's tests in /root/reference/pkg/tests (test_core,
 test_plan, test_executor, test_acceptance criteria 1-10, test_cli) must all
@@ -25,10 +25,12 @@ SHIM = textwrap.dedent(
     import paper_2410_22254_b200.core as _core
     import paper_2410_22254_b200.plan as _plan
     import paper_2410_22254_b200.executor as _executor
+    import paper_2410_22254_b200.telemetry as _telemetry
     sys.modules["trilaunch.core"] = _core
     sys.modules["trilaunch.plan"] = _plan
     sys.modules["trilaunch.executor"] = _executor
-    core, plan, executor = _core, _plan, _executor
+    sys.modules["trilaunch.telemetry"] = _telemetry
+    core, plan, executor, telemetry = _core, _plan, _executor, _telemetry
     __path__ = [%r]
     """
 )
@@ -36,7 +38,8 @@ SHIM = textwrap.dedent(
 
 @pytest.mark.skipif(not os.path.isdir(REF), reason="reference not mounted")
 @pytest.mark.parametrize(
-    "testfile", ["test_core.py", "test_plan.py", "test_executor.py", "test_acceptance.py", "test_cli.py"]
+    "testfile", ["test_core.py", "test_plan.py", "test_executor.py", "test_acceptance.py", "test_cli.py",
+                 "test_telemetry.py"]
 )
 def test_reference_tests_pass_on_our_package(tmp_path, testfile):
     shim = tmp_path / "shim" / "trilaunch"
