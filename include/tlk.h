@@ -156,6 +156,10 @@ int tlk_selftest_gemm(int32_t a_mn, int32_t b_mn, int32_t bn, const void* A, con
 /* Counter RNG + synthetic data generator, for bit-exact checks vs the oracle. */
 int tlk_selftest_datagen(uint64_t seed, int32_t step, int32_t batch, uint8_t* pixels_dev,
                          int32_t* labels_dev, void* stream);
+/* The packed optimizer update (straight-line fast-path sqrt/div) against the
+ * library-intrinsic formulation on n random states of the given TLK_OPT_*
+ * kind; *mismatches = elements whose p, m or v differ in any bit. */
+int tlk_selftest_optimizer(int32_t kind, uint64_t seed, int64_t n, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,7 @@ EXPORTS = (
     "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
     "tlk_selftest_datagen",
+    "tlk_selftest_optimizer",
 )
 
 
@@ -261,6 +262,13 @@ def selftest_gemm(a_mn: bool, b_mn: bool, bn: int, A, B, Cout, batch, M, N, K, s
     check(lib().tlk_selftest_gemm(int(a_mn), int(b_mn), int(bn), C.c_void_p(A.data_ptr()),
                                   C.c_void_p(B.data_ptr()), C.c_void_p(Cout.data_ptr()),
                                   int(batch), int(M), int(N), int(K), C.c_void_p(stream)))
+
+
+def selftest_optimizer(kind: int, seed: int, n: int) -> int:
+    """Bit mismatches of the packed optimizer update vs its library-intrinsic form."""
+    out = C.c_uint64(0)
+    check(lib().tlk_selftest_optimizer(int(kind), C.c_uint64(seed), C.c_int64(n), C.byref(out)))
+    return out.value
 
 
 def selftest_datagen(seed: int, step: int, batch: int, px, labels, stream=0):

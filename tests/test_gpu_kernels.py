@@ -56,3 +56,11 @@ def test_datagen_bit_exact(seed, step):
     ref_px, ref_lb = rng.batch(seed, step, batch)
     assert np.array_equal(px.cpu().numpy(), ref_px)
     assert np.array_equal(lb.cpu().numpy(), ref_lb)
+
+
+@pytest.mark.parametrize("kind", [rt.OPT_ADAM, rt.OPT_ADAMW, rt.OPT_SGD])
+def test_optimizer_fastpath_is_bit_identical_to_library_sqrt_div(kind):
+    """The straight-line sqrt / div of the packed optimizer reproduce the
+    library __fsqrt_rn / __fdiv_rn update bit for bit on 2^28 random states
+    (exponents over the whole float range, zeros, denormals, both signs)."""
+    assert rt.selftest_optimizer(kind, 20251017 + kind, 1 << 28) == 0
