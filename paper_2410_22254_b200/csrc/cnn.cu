@@ -205,49 +205,49 @@ struct Fc1Dgrad {
   TLK_DEV void epilogue(const Work&, int, int, const float (&)[32], Carry&) const {}
   TLK_DEV void finish(const Work&, int, Carry&) const {}
   // tile = dp2^T[128 f][64 b] for f = two pooled positions x 64 channels.
-  // Phase 1, item = (b, position, 8-channel chunk): the 2x2 window of the
-  // chunk is written as four 16-B stores into the dz2 P28 plane (argmax gets
-  // bf16(value) if the pooled output was live, the rest zeros); the rounded
-  // value replaces the tile entry.  Phase 2: colsum[f] = sum_b (fixed order).
+  // Phase 1: a group of 8 lanes owns one (image b, 8-channel chunk ch) and
+  // lane l writes window position r = l & 3 of pooled position pl = l >> 2:
+  // the 16-B store of its dz2 P28 position is bf16(value) on the argmax
+  // channels of a live pooled output, zero elsewhere.  A warp's stores are
+  // then 64-B runs (two pooled positions' window row) instead of 32
+  // scattered 16-B pieces.  The rounded value replaces the tile entry (lane
+  // r == 0).  Phase 2: colsum[f] = sum_b (fixed order).
   TLK_DEV void tile_epilogue(const Work& w, float* tile, int ld) const {
     const int tid = threadIdx.x, B = buf.B;
     const int pos0 = w.m0 >> 6;
-    uint2 codes[4];  // all four items' argmax codes in flight before any math
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = tid + 256 * u, b = i & 63, pl = (i >> 6) >> 3, ch = (i >> 6) & 7;
-      codes[u] = b < B ? *reinterpret_cast<const uint2*>(buf.idx + w.j * buf.p2_st +
-                                                          int64_t(b) * 9216 + (pos0 + pl) * 64 + ch * 8)
-                       : make_uint2(0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = tid + 256 * u;
-      const int b = i & 63, pl = (i >> 6) >> 3, ch = (i >> 6) & 7;
-      if (b >= B) continue;
-      const int pos = pos0 + pl, ph = pos / 12, pw = pos % 12, f = pl * 64 + ch * 8;
-      const uint2 code2 = codes[u];
+    const int l8 = tid & 7, pl = l8 >> 2, r = l8 & 3;
+    const int pos = pos0 + pl, ph = pos / 12, pw = pos % 12;
+    const int dr = r >> 1, dc = r & 1;
+#pragma unroll 2
+    for (int it = tid >> 3; it < 64 * 8; it += 32) {  // (b, ch) pairs; b is warp-uniform-valid (B % 8 == 0)
+      const int b = it & 63, ch = it >> 6;
+      const bool ok = b < B;
+      const uint2 code2 = ok ? *reinterpret_cast<const uint2*>(buf.idx + w.j * buf.p2_st + int64_t(b) * 9216 +
+                                                               pos * 64 + ch * 8)
+                             : make_uint2(0u, 0u);
       const uint32_t cw[2] = {code2.x, code2.y};
+      float* t0 = tile + (pl * 64 + ch * 8) * ld + b;
       uint16_t z[8];
-      int q[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const uint32_t code = (cw[e >> 2] >> (8 * (e & 3))) & 0xFF;
-        float* t = tile + (f + e) * ld + b;
-        z[e] = (code & 4) ? f2bf(*t) : uint16_t(0);
-        q[e] = code & 3;
-        *t = bf2f(z[e]);
+        z[e] = (ok && (code & 4)) ? f2bf(t0[e * ld]) : uint16_t(0);
       }
-      uint16_t* plane = buf.dz2 + (int64_t(w.j) * 8 + ch) * buf.npos * 8;
-      const int64_t p = p28_pos(b, 2 * ph + 2, 2 * pw + 2);
+      __syncwarp();  // every lane has read its tile entries before lane r == 0 rounds them in place
+      uint32_t o[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        uint32_t o[4];
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const int e = 2 * e2;
+        const int q0 = int((cw[e >> 2] >> (8 * (e & 3))) & 3), q1 = int((cw[(e + 1) >> 2] >> (8 * ((e + 1) & 3))) & 3);
+        o[e2] = uint32_t(q0 == r ? z[e] : 0) | (uint32_t(q1 == r ? z[e + 1] : 0) << 16);
+      }
+      if (ok) {
+        if (r == 0) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          o[e] = uint32_t(q[2 * e] == r ? z[2 * e] : 0) |
-                 (uint32_t(q[2 * e + 1] == r ? z[2 * e + 1] : 0) << 16);
-        *reinterpret_cast<uint4*>(plane + (p + (r >> 1) * P28 + (r & 1)) * 8) =
+          for (int e = 0; e < 8; ++e) t0[e * ld] = bf2f(z[e]);
+        }
+        uint16_t* plane = buf.dz2 + (int64_t(w.j) * 8 + ch) * buf.npos * 8;
+        *reinterpret_cast<uint4*>(plane + (p28_pos(b, 2 * ph + 2 + dr, 2 * pw + 2 + dc)) * 8) =
             make_uint4(o[0], o[1], o[2], o[3]);
       }
     }
