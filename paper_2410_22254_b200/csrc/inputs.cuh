@@ -40,13 +40,21 @@ __device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, si
     }
   }
   if (host_input) return;
+  // label = argmax_c sum_i t[c][i] (2 p_i - 255) = 2 sum t p - 255 sum t, four
+  // pixels per dp4a (signed teacher bytes x unsigned pixel bytes): exact
   int acc[CLASSES];
 #pragma unroll
   for (int c = 0; c < CLASSES; ++c) acc[c] = 0;
-  for (int i = tid; i < PIXELS; i += NT) {
-    const int v = 2 * int(pix[i]) - 255;
+  for (int q = tid; q < PIXELS / 4; q += NT) {
+    const uint32_t pw = reinterpret_cast<const uint32_t*>(pix)[q];
 #pragma unroll
-    for (int c = 0; c < CLASSES; ++c) acc[c] += int(teacher[c * PIXELS + i]) * v;
+    for (int c = 0; c < CLASSES; ++c) {
+      const int tw = reinterpret_cast<const int*>(teacher + c * PIXELS)[q];
+      int tp, ts;
+      asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(tp) : "r"(tw), "r"(pw), "r"(0));
+      asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts) : "r"(tw), "r"(0x01010101u), "r"(0));
+      acc[c] += 2 * tp - 255 * ts;
+    }
   }
 #pragma unroll
   for (int c = 0; c < CLASSES; ++c) {
