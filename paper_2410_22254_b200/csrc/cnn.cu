@@ -20,6 +20,8 @@
 //   h1 P28 [4][npos][8] | p2 bf16 [B,12,12,64] | idx u8 [B,12,12,64]
 //   (argmax | live<<2) | h3 bf16 [B,128] | dz3 bf16 [B,128] |
 //   dz2 P28 [8][npos][8] | dz1 P28 [4][npos][8]      (npos = 32 + 784 B + 64)
+#include <cstdlib>
+
 #include "conv_tc.cuh"
 #include "tma.cuh"
 #include "linear.cuh"
@@ -788,15 +790,27 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   Fc1Dgrad f1d{b, p.lane_dev};  // reads this step's fc1 weights
   TLK_CUDA(launch_gemm_tma(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
-  TLK_CUDA(launch(conv2_wgrad_tc_kernel, dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, st, ca));
-  p.mark(st, "conv2_wgrad");
+  // conv2 wgrad (reads dz2, h1; writes its partials) is independent of the
+  // conv2 dgrad -> conv1 wgrad chain: a forked graph branch lets the two
+  // latency-bound kernels share the SMs (TLK_CNN_NOFORK=1: serial)
+  static const bool fork = !(getenv("TLK_CNN_NOFORK") && getenv("TLK_CNN_NOFORK")[0] == '1');
+  cudaStream_t wst = st;
+  if (fork && !p.prof) {
+    TLK_CUDA(cudaEventRecord(p.ev_fork, st));
+    TLK_CUDA(cudaStreamWaitEvent(p.side, p.ev_fork, 0));
+    wst = p.side;
+  }
+  TLK_CUDA(launch(conv2_wgrad_tc_kernel, dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, wst, ca));
+  p.mark(wst, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
+  if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), 128, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
+  if (wst != st) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   {
     Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, p.lane_dev, p.params, p.mom1, p.mom2, p.grads, p.wbf,
                    p.stride, o_f1w,
