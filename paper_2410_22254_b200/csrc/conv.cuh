@@ -235,7 +235,7 @@ struct ConvGemm {
     return ((int64_t(b) * Hf + 2 * u + py) * Wf + 2 * v + px) * cols;
   }
 
-  TLK_DEV void epilogue(const ConvWork& w, uint32_t tq, int row0, float* buf, int lane) const {
+  TLK_DEV void epilogue(const ConvWork& w, uint32_t tq, int row0, float* buf, int lane, int, float*, int) const {
     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
 #pragma unroll 1
     for (int cc = 0; cc < BN_ / 32; ++cc) {

@@ -219,16 +219,36 @@ struct EpiOps {
   // Causal rows skip the 32-column chunks that lie entirely above the
   // diagonal for the whole warp: those entries of P / dS are never written
   // and stay zero from the pack's initial memset (nothing else writes them).
-  // Row-epilogue tiles span all columns (n0 == 0, BN >= cols).
-  template <int BN>
-  TLK_DEV void row_tile(const ZWork& w, uint32_t taddr, int row0, float* buf, int lane) const {
-    const int m = row0 + lane;
+  // Row-epilogue tiles span all columns (n0 == 0, BN >= cols).  With NP = 2
+  // column parts, two warps share each TMEM lane quarter: part p takes
+  // columns [p BN/2, (p+1) BN/2); the row max / sum / target logit of the
+  // two parts are exchanged through `xchg` ([3][2][128] floats of this
+  // accumulator's group, named barrier `bar` over the group's 8 warps) and
+  // combined in part order.
+  template <int BN, int NP>
+  TLK_DEV void row_tile(const ZWork& w, uint32_t taddr, int row0, float* buf, int lane, int part, float* xchg,
+                        int bar) const {
+    const int m = row0 + lane, rl = row0 - w.m0 + lane;
     const bool live = m < e.rows;
     const int ncols = e.cols;
     const int lim = e.causal ? min(ncols, m + 1) : ncols;       // valid columns of this row
     const int wlim = e.causal ? min(ncols, row0 + 32) : ncols;  // warp-uniform chunk bound
+    const int cbeg = part * (BN / NP), cend = min(cbeg + BN / NP, wlim);
     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
     const int64_t step = 4 * e.ld;
+    // combine a per-part row value with the other part's: op(part0, part1)
+    auto combine = [&](int slot, float v, auto op) -> float {
+      if constexpr (NP == 1) {
+        return v;
+      } else {
+        xchg[(slot * 2 + part) * 128 + rl] = v;
+        named_bar_sync(bar, 256);
+        const float o = xchg[(slot * 2 + (1 - part)) * 128 + rl];
+        return part == 0 ? op(v, o) : op(o, v);
+      }
+    };
+    auto fmax_ = [](float x, float y) { return fmaxf(x, y); };
+    auto fadd_ = [](float x, float y) { return x + y; };
     float v[32];
     if (e.kind == EPI_SOFTMAX) {
       // p = 2^(v*k - mx*k), k = scale * log2(e), on the SFU (ex2.approx, ~2
@@ -237,7 +257,7 @@ struct EpiOps {
       const float k2 = e.scale * 1.4426950408889634f;
       const int cfull = e.causal ? row0 : (ncols & ~31);  // chunks below cfull are whole for every lane
       float mx = -INFINITY;
-      for (int c0 = 0; c0 < wlim; c0 += 32) {
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
         tmem_ld32(taddr + c0, v);
         if (c0 < cfull) {
 #pragma unroll
@@ -248,9 +268,10 @@ struct EpiOps {
             if (c0 + i < lim) mx = fmaxf(mx, v[i]);
         }
       }
+      mx = combine(0, mx, fmax_);
       const float mk = mx * k2;
       float s = 0.f;
-      for (int c0 = 0; c0 < wlim; c0 += 32) {
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
         tmem_ld32(taddr + c0, v);
         if (c0 < cfull) {
 #pragma unroll
@@ -261,9 +282,10 @@ struct EpiOps {
             if (c0 + i < lim) s += ex2_approx(fmaf(v[i], k2, -mk));
         }
       }
+      s = combine(1, s, fadd_);
       const float inv = 1.f / s;
       uint16_t* out = static_cast<uint16_t*>(e.out) + off(w, row0 + rsub, c4);
-      for (int c0 = 0; c0 < wlim; c0 += 32) {
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
         tmem_ld32(taddr + c0, v);
         if (c0 < cfull) {
 #pragma unroll
@@ -282,12 +304,12 @@ struct EpiOps {
       const uint16_t* P = static_cast<const uint16_t*>(e.aux) + off(w, row0 + rsub, c4);
       uint16_t* out = static_cast<uint16_t*>(e.out) + off(w, row0 + rsub, c4);
       uint2 nxt[8];
-      fetch_chunk(P, step, row0, nxt, lane);
-      for (int c0 = 0; c0 < wlim; c0 += 32) {
+      if (cbeg < cend) fetch_chunk(P + cbeg, step, row0, nxt, lane);
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
         uint2 cur[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
-        if (c0 + 32 < wlim) fetch_chunk(P + c0 + 32, step, row0, nxt, lane);
+        if (c0 + 32 < cend) fetch_chunk(P + c0 + 32, step, row0, nxt, lane);
         deposit_chunk(cur, buf, lane);
         tmem_ld32(taddr + c0, v);
 #pragma unroll
@@ -296,8 +318,9 @@ struct EpiOps {
       }
     } else if (e.kind == EPI_CE) {
       const int y = live ? e.targets[w.j * e.tg_ls + m] : 0;
+      const int ce = min(cbeg + BN / NP, BN);
       float mx = -INFINITY, ly = 0.f;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = cbeg; c0 < ce; c0 += 32) {
         tmem_ld32(taddr + c0, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -306,18 +329,21 @@ struct EpiOps {
             if (c0 + i == y) ly = v[i];
           }
       }
+      mx = combine(0, mx, fmax_);
+      ly = combine(2, ly, fadd_);  // exactly one part holds the target logit
       float s = 0.f;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = cbeg; c0 < ce; c0 += 32) {
         tmem_ld32(taddr + c0, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (c0 + i < ncols) s += exp_fast(v[i] - mx);
       }
-      if (live) e.lossrow[w.j * int64_t(e.rows) + m] = (mx + logf(s)) - ly;
+      s = combine(1, s, fadd_);
+      if (live && part == 0) e.lossrow[w.j * int64_t(e.rows) + m] = (mx + logf(s)) - ly;
       // dlogits over the padded width e.ld (zeros in the padding columns)
       const float inv = 1.f / s, invt = 1.f / e.tokens;
       uint16_t* out = static_cast<uint16_t*>(e.out) + off(w, row0 + rsub, c4);
-      for (int c0 = 0; c0 < BN && c0 < e.ld; c0 += 32) {
+      for (int c0 = cbeg; c0 < ce && c0 < e.ld; c0 += 32) {
         tmem_ld32(taddr + c0, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -326,12 +352,13 @@ struct EpiOps {
         store_chunk(out + c0, step, row0, buf, lane);
       }
     }
+    if constexpr (NP > 1) named_bar_sync(bar, 256);  // exchange slots reusable by the group's next tile
   }
 
   template <int BN>
   TLK_DEV void tile(const ZWork& w, uint32_t tq, int row0, float* buf, int lane, bool row) const {
     if (row) {
-      row_tile<BN>(w, tq, row0, buf, lane);
+      row_tile<BN, 1>(w, tq, row0, buf, lane, 0, nullptr, 0);
       return;
     }
     switch (e.kind) {

@@ -38,7 +38,16 @@ template <int BN_, bool AMN, bool BMN, bool ROW>
 struct TGemm {
   static constexpr int BN = BN_;
   static constexpr int STAGES = BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : 3;
-  static constexpr int EW = 8;  // epilogue warps (two groups of 4 lane quarters)
+  // epilogue warps: two groups (one per TMEM accumulator) of 4 lane-quarter
+  // warps; whole-row (softmax / CE) epilogues with 64-aligned tiles use two
+  // warps per lane quarter, each taking half of the row's columns
+  // (exchanging the row max / sum through smem): twice the warps to hide the
+  // TMEM / SFU latency of the row passes
+#ifndef TLK_ROW_PARTS
+#define TLK_ROW_PARTS 2
+#endif
+  static constexpr int PARTS = (ROW && BN_ % 64 == 0) ? TLK_ROW_PARTS : 1;
+  static constexpr int EW = 8 * PARTS;
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = AMN, B_MN = BMN, ROW_EPI = ROW;
   using Work = ZWork;
@@ -81,8 +90,12 @@ struct TGemm {
   TLK_DEV void issue_mma(uint32_t d, uint32_t a_s, bool acc) const {
     gemm_stage_mma<BN_, AMN, BMN, IDESC>(d, a_s, a_s + A_BYTES, acc);
   }
-  TLK_DEV void epilogue(const ZWork& w, uint32_t tq, int row0, float* buf, int lane) const {
-    g.template tile<BN_>(w, tq, row0, buf, lane, ROW);
+  TLK_DEV void epilogue(const ZWork& w, uint32_t tq, int row0, float* buf, int lane, int part, float* xchg,
+                        int bar) const {
+    if constexpr (ROW)
+      g.template row_tile<BN_, PARTS>(w, tq, row0, buf, lane, part, xchg, bar);
+    else
+      g.template tile<BN_>(w, tq, row0, buf, lane, false);
   }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
@@ -124,7 +137,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], EW / 2);
     }
     fence_mbar_init();
   }
@@ -171,11 +184,13 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
         ++lt;
       }
     }
-  } else {  // epilogue warps: group (warp >> 2) drains TMEM buffer `group`,
-           // i.e. the CTA's even / odd local tiles, so two tiles' epilogues
-           // run concurrently (4 warps = the 4 TMEM lane quarters each)
-    const int q = warp & 3, group = warp >> 2;
+  } else {  // epilogue warps: group ((warp >> 2) & 1) drains TMEM buffer
+           // `group`, i.e. the CTA's even / odd local tiles, so two tiles'
+           // epilogues run concurrently (4 warps = the 4 TMEM lane quarters
+           // each, x PARTS column parts)
+    const int q = warp & 3, group = (warp >> 2) & 1, part = warp >> 3;
     float* buf = staging + warp * (32 * 33);
+    __shared__ float xchg_s[2][3][2][128];  // [group][max, sum, aux][part][row] (row epilogues)
     int lt = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       typename P::Work w;
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       mbar_wait(&tfull[b], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t tq = tmem + b * BN + (uint32_t(q * 32) << 16);
-      p.epilogue(w, tq, w.m0 + q * 32, buf, lane);
+      p.epilogue(w, tq, w.m0 + q * 32, buf, lane, part, &xchg_s[group][0][0][0], 1 + group);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
