@@ -96,8 +96,12 @@ struct EpiOps {
   }
 
   // ---- dense (per-element) epilogues -------------------------------------
-  template <int KIND, int BN>
-  TLK_DEV void tile4(const ZWork& w, uint32_t tq, int row0, float* buf, int lane) const {
+  // NP column parts: part p of the two warps sharing a TMEM lane quarter
+  // takes the 32-column chunks [p NC/NP, (p+1) NC/NP) of the tile
+  template <int KIND, int BN, int NP = 1>
+  TLK_DEV void tile4(const ZWork& w, uint32_t tq, int row0, float* buf, int lane, int part = 0) const {
+    constexpr int NC = BN / 32;
+    const int cc0 = part * (NC / NP), cc1 = cc0 + NC / NP;
     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
     const int64_t step = 4 * e.ld;
     const int64_t o0 = off(w, row0 + rsub, w.n0 + c4);
@@ -125,23 +129,33 @@ struct EpiOps {
                                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
-    if constexpr (AUX) fetch(0, nx);
+    // one warp per lane quarter (NP == 1): the next chunk's aux rows are in
+    // flight during this chunk; with two (NP == 2, 96-register budget) the
+    // chunk's own aux rows are issued before its TMEM load and staging
+    if constexpr (AUX && NP == 1) fetch(cc0, nx);
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
+    for (int cc = cc0; cc < cc1; ++cc) {
       const int n = w.n0 + cc * 32 + c4;
       const bool col_ok = n < e.cols;
       const int64_t o = o0 + cc * 32;
       if constexpr (AUX) {
+        if constexpr (NP == 1) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) ax[k] = nx[k];
-        if (cc + 1 < BN / 32) fetch(cc + 1, nx);
+          for (int k = 0; k < 8; ++k) ax[k] = nx[k];
+          if (cc + 1 < cc1) fetch(cc + 1, nx);
+        } else {
+          fetch(cc, ax);
+        }
       }
       float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
       if (bias && col_ok) bb = make_float4(bias[n], bias[n + 1], bias[n + 2], bias[n + 3]);
-      float v[32];
-      tmem_ld32(tq + cc * 32, v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+      for (int hf = 0; hf < 2; ++hf) {  // two 16-column TMEM loads: fewer live registers
+        float v[16];
+        tmem_ld16(tq + cc * 32 + hf * 16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) buf[lane * 33 + hf * 16 + i] = v[i];
+      }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -355,18 +369,18 @@ struct EpiOps {
     if constexpr (NP > 1) named_bar_sync(bar, 256);  // exchange slots reusable by the group's next tile
   }
 
-  template <int BN>
-  TLK_DEV void tile(const ZWork& w, uint32_t tq, int row0, float* buf, int lane, bool row) const {
+  template <int BN, int NP = 1>
+  TLK_DEV void tile(const ZWork& w, uint32_t tq, int row0, float* buf, int lane, bool row, int part = 0) const {
     if (row) {
       row_tile<BN, 1>(w, tq, row0, buf, lane, 0, nullptr, 0);
       return;
     }
     switch (e.kind) {
-      case EPI_BF16: tile4<EPI_BF16, BN>(w, tq, row0, buf, lane); break;
-      case EPI_BF16_GELU: tile4<EPI_BF16_GELU, BN>(w, tq, row0, buf, lane); break;
-      case EPI_F32: tile4<EPI_F32, BN>(w, tq, row0, buf, lane); break;
-      case EPI_RESADD: tile4<EPI_RESADD, BN>(w, tq, row0, buf, lane); break;
-      case EPI_GELU_BWD: tile4<EPI_GELU_BWD, BN>(w, tq, row0, buf, lane); break;
+      case EPI_BF16: tile4<EPI_BF16, BN, NP>(w, tq, row0, buf, lane, part); break;
+      case EPI_BF16_GELU: tile4<EPI_BF16_GELU, BN, NP>(w, tq, row0, buf, lane, part); break;
+      case EPI_F32: tile4<EPI_F32, BN, NP>(w, tq, row0, buf, lane, part); break;
+      case EPI_RESADD: tile4<EPI_RESADD, BN, NP>(w, tq, row0, buf, lane, part); break;
+      case EPI_GELU_BWD: tile4<EPI_GELU_BWD, BN, NP>(w, tq, row0, buf, lane, part); break;
       default: break;
     }
   }

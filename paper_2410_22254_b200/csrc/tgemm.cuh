@@ -39,14 +39,17 @@ struct TGemm {
   static constexpr int BN = BN_;
   static constexpr int STAGES = BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : 3;
   // epilogue warps: two groups (one per TMEM accumulator) of 4 lane-quarter
-  // warps; whole-row (softmax / CE) epilogues with 64-aligned tiles use two
-  // warps per lane quarter, each taking half of the row's columns
-  // (exchanging the row max / sum through smem): twice the warps to hide the
-  // TMEM / SFU latency of the row passes
+  // warps, x2 for 64-aligned tiles: two warps per lane quarter, each taking
+  // half of the tile's columns (row epilogues exchange the row max / sum
+  // through smem).  The epilogues (GELU / GELU', softmax, bf16 packing) are
+  // issue-bound: twice the warps hide the TMEM / SFU / store latency.
 #ifndef TLK_ROW_PARTS
 #define TLK_ROW_PARTS 2
 #endif
-  static constexpr int PARTS = (ROW && BN_ % 64 == 0) ? TLK_ROW_PARTS : 1;
+#ifndef TLK_DENSE_PARTS
+#define TLK_DENSE_PARTS 2
+#endif
+  static constexpr int PARTS = BN_ % 64 != 0 ? 1 : ROW ? TLK_ROW_PARTS : TLK_DENSE_PARTS;
   static constexpr int EW = 8 * PARTS;
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = AMN, B_MN = BMN, ROW_EPI = ROW;
@@ -95,7 +98,7 @@ struct TGemm {
     if constexpr (ROW)
       g.template row_tile<BN_, PARTS>(w, tq, row0, buf, lane, part, xchg, bar);
     else
-      g.template tile<BN_>(w, tq, row0, buf, lane, false);
+      g.template tile<BN_, PARTS>(w, tq, row0, buf, lane, false, part);
   }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
@@ -115,6 +118,7 @@ struct TGemm {
   }
 };
 
+// (18 warps: 5 on some SM sub-partitions, so at most 96 registers per thread)
 template <class P>
 __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_constant__ P p) {
   pdl_begin();
