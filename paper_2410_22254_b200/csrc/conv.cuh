@@ -49,8 +49,16 @@ struct ConvGemm {
   static constexpr int A_BYTES = HALO ? 6 * 32 * 128 : GEMM_BM * GEMM_BK * 2;  // halo: <= (128/W + 2) W rows
   static constexpr int B_BYTES = (HALO ? 3 : 1) * BN_ * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = HALO ? (BN_ <= 64 ? 3 : 2) : (BN_ <= 64 ? 6 : BN_ <= 128 ? 4 : BN_ <= 192 ? 4 : 3);
-  static constexpr int EW = 8;
+#ifndef TLK_CONV_PARTS
+#define TLK_CONV_PARTS 2
+#endif
+  // epilogue: two groups (TMEM accumulators) x 4 lane quarters x PARTS
+  // column halves (the bf16 / BN-partial / fp32-accumulate epilogues are
+  // issue- and latency-bound; 64-aligned tiles split their chunks in two)
+  static constexpr int PARTS = BN_ % 64 == 0 ? TLK_CONV_PARTS : 1;
+  static constexpr int EW = 8 * PARTS;
+  static constexpr int STAGES = HALO ? (BN_ <= 64 ? 3 : 2)
+                                     : (BN_ <= 64 ? 6 : BN_ <= 128 ? 4 : BN_ <= 192 ? 4 - (PARTS - 1) : 3);
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = MODE == CONV_WGRAD, B_MN = MODE == CONV_WGRAD, ROW_EPI = false;
   static_assert(!HALO || MODE != CONV_WGRAD, "halo mode is FWD / DGRAD only");
@@ -235,10 +243,12 @@ struct ConvGemm {
     return ((int64_t(b) * Hf + 2 * u + py) * Wf + 2 * v + px) * cols;
   }
 
-  TLK_DEV void epilogue(const ConvWork& w, uint32_t tq, int row0, float* buf, int lane, int, float*, int) const {
+  TLK_DEV void epilogue(const ConvWork& w, uint32_t tq, int row0, float* buf, int lane, int cpart, float*,
+                        int) const {
     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
+    constexpr int NC = BN_ / 32;
 #pragma unroll 1
-    for (int cc = 0; cc < BN_ / 32; ++cc) {
+    for (int cc = cpart * (NC / PARTS); cc < (cpart + 1) * (NC / PARTS); ++cc) {
       const int n = w.n0 + cc * 32 + c4;
       float v[32];
       tmem_ld32(tq + cc * 32, v);
