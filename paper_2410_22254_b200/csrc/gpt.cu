@@ -309,6 +309,31 @@ __global__ void reduce_parts_kernel(const LaneState* __restrict__ lanes, const f
   grads[j * pstride + (c < split ? off0 + c : off1 + (c - split))] = s;
 }
 
+// Same sum over many partial rows: 8 row groups per 32 columns (group g
+// takes rows g, g + 8, ... in order; groups combined in order).
+__global__ void __launch_bounds__(256) reduce_parts8_kernel(const LaneState* __restrict__ lanes,
+                                                            const float* __restrict__ part, int64_t part_st, int nblk,
+                                                            int C, float* __restrict__ grads, int64_t pstride,
+                                                            int64_t off) {
+  pdl_begin();
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5, c = blockIdx.x * 32 + cl, j = blockIdx.y;
+  if (!lanes[j].active) return;
+  __shared__ float sh[8][32];
+  float s = 0.f;
+  if (c < C) {
+    const float* p = part + j * part_st + c;
+#pragma unroll 4
+    for (int b = g; b < nblk; b += 8) s += p[int64_t(b) * C];
+  }
+  sh[g][cl] = s;
+  __syncthreads();
+  if (g == 0 && c < C) {
+    float t = sh[0][cl];
+    for (int k = 1; k < 8; ++k) t += sh[k][cl];
+    grads[j * pstride + off + c] = t;
+  }
+}
+
 // mean token loss (fixed order) -> loss curve; per-step optimizer scalars
 __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ lanes, int N,
                                                        const float* __restrict__ lossrow,
@@ -507,7 +532,8 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
   add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
   // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
-  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d, N / EMB_ROWS * c.V * d});
+  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d, N / EMB_ROWS * c.V * d,
+                               int64_t((N + 31) / 32) * 4 * d});  // + GELU' epilogue bias partials
   b->part_st = ps;
   add(reinterpret_cast<void**>(&b->part), L * ps * 4);
   size_t total = 0;
@@ -725,17 +751,21 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_F2B)));
       Epi e = epi(EPI_GELU_BWD, N, 4 * d, b.dz, nd4, 0, 0, 4 * d);
       e.aux = lb.z;
+      e.colpart = b.part;  // fc.b gradient partials (per 32 rows), summed right below
+      e.cp_ls = b.part_st;
       TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
                                              op(WB + O(T_LAYER(l, K_F2W)), PS, 0, 0, 1, 4 * d, 4 * d, d), e,
                                              N, 4 * d, d, 1, 1, "fc2_dgrad")));
       count += 2;
+      TLK_CUDA(launch(reduce_parts8_kernel, dim3((4 * d + 31) / 32, Lc), 256, 0, st, LS, b.part, b.part_st,
+                      (N + 31) / 32, 4 * d, G, PS, O(T_LAYER(l, K_FB))));
+      marked("bias_reduce");
     }
     {  // fc: dW1 = dz^T m ; db1 ; dmm = dz W1 (fp32)
       Epi g = epi(EPI_F32, 4 * d, d, G + O(T_LAYER(l, K_FW)), PS, 0, 0, d);
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dz, nd4, 0, 0, 1, 4 * d, 4 * d, N),
                                             op(lb.m, nd, 0, 0, 1, d, d, N), g, 4 * d, d, N, 1, 1,
                                             "fc_wgrad")));
-      TLK_TRY(bias_grad(b.dz, 4 * d, T_LAYER(l, K_FB)));
       Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
       TLK_TRY((gemm_auto<false, true>(p, st, op(b.dz, nd4, 0, 0, 4 * d, 1, N, 4 * d),
                                              op(WB + O(T_LAYER(l, K_FW)), PS, 0, 0, 1, d, d, 4 * d), e, N,

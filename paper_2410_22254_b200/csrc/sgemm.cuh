@@ -44,6 +44,8 @@ struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
   float tokens;            // EPI_CE: dlogits are divided by the token count
   const float* rowvec;     // EPI_SOFTMAX_BWD: D[row] at lane*rv_ls + zb*rv_bs + zh*rv_hs + row
   int64_t rv_ls, rv_bs, rv_hs;
+  float* colpart;          // EPI_GELU_BWD (optional): column sums of the stored bf16 output per
+  int64_t cp_ls;           //   32-row block, [lane][row / 32][cols] (bias gradient partials)
 };
 
 struct ZWork {
@@ -149,6 +151,7 @@ struct EpiOps {
       }
       float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
       if (bias && col_ok) bb = make_float4(bias[n], bias[n + 1], bias[n + 2], bias[n + 3]);
+      float cs[4] = {0.f, 0.f, 0.f, 0.f};  // EPI_GELU_BWD column partials
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // two 16-column TMEM loads: fewer live registers
         float v[16];
@@ -188,9 +191,27 @@ struct EpiOps {
               make_float4(r4.x + y0, r4.y + y1, r4.z + y2, r4.w + y3);
         } else if constexpr (KIND == EPI_GELU_BWD) {
           const float4 z = ax[k];
-          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) =
-              make_uint2(pack_bf2(y0 * gelu_tanh_grad(z.x), y1 * gelu_tanh_grad(z.y)),
-                         pack_bf2(y2 * gelu_tanh_grad(z.z), y3 * gelu_tanh_grad(z.w)));
+          const uint32_t lo = pack_bf2(y0 * gelu_tanh_grad(z.x), y1 * gelu_tanh_grad(z.y));
+          const uint32_t hi = pack_bf2(y2 * gelu_tanh_grad(z.z), y3 * gelu_tanh_grad(z.w));
+          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) = make_uint2(lo, hi);
+          cs[0] += __uint_as_float(lo << 16);
+          cs[1] += __uint_as_float(lo & 0xffff0000u);
+          cs[2] += __uint_as_float(hi << 16);
+          cs[3] += __uint_as_float(hi & 0xffff0000u);
+        }
+      }
+      if constexpr (KIND == EPI_GELU_BWD) {
+        // column sums of this warp's 32 rows of the stored (bf16) values:
+        // lanes l, l+8, l+16, l+24 hold the same 4 columns (fixed xor order)
+        if (e.colpart) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
+            cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
+          }
+          if (rsub == 0 && col_ok)
+            *reinterpret_cast<float4*>(e.colpart + w.j * e.cp_ls + int64_t(row0 >> 5) * e.cols + n) =
+                make_float4(cs[0], cs[1], cs[2], cs[3]);
         }
       }
       __syncwarp();

@@ -40,7 +40,10 @@ struct TGemm {
   // row-epilogue GEMMs (attention scores / dP, LM head) have K = head dim or
   // d (1-6 k-blocks per tile): two stages suffice, and the freed smem is L1
   // for the epilogue's global P loads
-  static constexpr int STAGES = ROW ? 2 : BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : 3;
+#ifndef TLK_DENSE_STAGES_WIDE
+#define TLK_DENSE_STAGES_WIDE 3
+#endif
+  static constexpr int STAGES = ROW ? 2 : BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : TLK_DENSE_STAGES_WIDE;
   // epilogue warps: two groups (one per TMEM accumulator) of 4 lane-quarter
   // warps, x2 for 64-aligned tiles: two warps per lane quarter, each taking
   // half of the tile's columns (row epilogues exchange the row max / sum
