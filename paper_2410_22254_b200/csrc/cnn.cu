@@ -34,6 +34,7 @@ namespace {
 constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
 constexpr int C2W_SPLITS = 18;     // conv2 wgrad position splits per lane
 constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
+constexpr int C1W_THREADS = 256;            // 8 warps per image: the per-SM warp count hides latency
 constexpr int CNN_OPT_CTAS = 16;  // per lane: ~5.4k float4 of non-fc1.w parameters
 
 struct CnnBufs {
@@ -83,32 +84,31 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
   for (int i = tid; i < 784; i += 256) xs[i] = float(pix[i]) * (1.0f / 256.0f);  // = bf16 x exactly
   __syncthreads();
   uint16_t* h1 = buf.h1 + int64_t(j) * 4 * buf.npos * 8;
-  const int c = tid & 3;  // this thread's 8-channel chunk: its 72 weights live in registers
-  float w[8][9], bsum[8];
+  // thread = (4-channel half h of 8-channel chunk c, position group): its 36
+  // weights live in registers (low register count -> more resident warps)
+  const int c8 = tid & 7, c = c8 >> 1, h = c8 & 1;
+  float w[4][9], bsum[4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    bsum[e] = bs[c * 8 + e];
+  for (int e = 0; e < 4; ++e) {
+    bsum[e] = bs[c * 8 + h * 4 + e];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) w[e][t] = ws[(c * 8 + e) * 9 + t];
+    for (int t = 0; t < 9; ++t) w[e][t] = ws[(c * 8 + h * 4 + e) * 9 + t];
   }
-  for (int pos = tid >> 2; pos < 676; pos += 64) {
+  for (int pos = tid >> 3; pos < 676; pos += 32) {
     const int oh = pos / 26, ow = pos % 26;
     float xv[9];
 #pragma unroll
     for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
-    float acc[8];
+    float acc[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
       acc[e] = 0.f;
 #pragma unroll
       for (int t = 0; t < 9; ++t) acc[e] += xv[t] * w[e][t];
     }
-    uint32_t o[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      o[e] = pack_bf2(fmaxf(acc[2 * e] + bsum[2 * e], 0.f), fmaxf(acc[2 * e + 1] + bsum[2 * e + 1], 0.f));
-    *reinterpret_cast<uint4*>(h1 + (c * buf.npos + p28_pos(s, oh + 1, ow + 1)) * 8) =
-        make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint2*>(h1 + (c * buf.npos + p28_pos(s, oh + 1, ow + 1)) * 8 + h * 4) =
+        make_uint2(pack_bf2(fmaxf(acc[0] + bsum[0], 0.f), fmaxf(acc[1] + bsum[1], 0.f)),
+                   pack_bf2(fmaxf(acc[2] + bsum[2], 0.f), fmaxf(acc[3] + bsum[3], 0.f)));
   }
 }
 
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
 // One CTA per (image, lane).  Thread = (8-channel chunk c, position group g):
 // acc[e][t] over its positions (t<9: tap products with x, t=9: bias), then a
 // fixed-order reduction over the 32 groups -> part1[lane][image][32][10].
-__global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __restrict__ lanes,
+__global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneState* __restrict__ lanes,
                                                           CnnBufs buf,
                                                           const uint16_t* __restrict__ x) {
   pdl_begin();
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __res
   extern __shared__ __align__(16) uint16_t dzs_raw[];  // this image's dz1 planes (50 KB)
   uint16_t(*dzs)[P28_IMG * 8] = reinterpret_cast<uint16_t(*)[P28_IMG * 8]>(dzs_raw);
   __shared__ float xs[784];
-  __shared__ float red[4][4][80];
+  __shared__ float red[C1W_THREADS / 32][4][80];
   __shared__ __align__(8) uint64_t bar;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -485,54 +485,52 @@ __global__ void __launch_bounds__(128) conv1_wgrad_kernel(const LaneState* __res
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  const int c = tid & 3, g = tid >> 2;  // chunk, position group (32 groups)
-  float acc[8][10];
+  // thread = (4-channel half h of chunk c, position group g): 40 accumulators
+  // (acc[e][t<9] tap products with x, t = 9: bias), few registers -> 4 CTAs
+  // of 8 warps per SM
+  const int c8 = tid & 7, c = c8 >> 1, h = c8 & 1, g = tid >> 3;
+  float acc[4][10];
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
+  for (int e = 0; e < 4; ++e)
 #pragma unroll
     for (int t = 0; t < 10; ++t) acc[e][t] = 0.f;
-  for (int q = g; q < 676; q += 32) {
+  for (int q = g; q < 676; q += C1W_THREADS / 8) {
     const int oh = q / 26, ow = q % 26;
-    const uint4 dv = *reinterpret_cast<const uint4*>(&dzs[c][((oh + 1) * P28 + ow + 1) * 8]);
-    const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w};
-    float d[8];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      d[2 * e] = bf2f(uint16_t(dw[e] & 0xFFFF));
-      d[2 * e + 1] = bf2f(uint16_t(dw[e] >> 16));
-    }
+    const uint2 dv = *reinterpret_cast<const uint2*>(&dzs[c][((oh + 1) * P28 + ow + 1) * 8 + h * 4]);
+    const float d[4] = {__uint_as_float(dv.x << 16), __uint_as_float(dv.x & 0xffff0000u),
+                        __uint_as_float(dv.y << 16), __uint_as_float(dv.y & 0xffff0000u)};
     float xv[9];
 #pragma unroll
     for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
 #pragma unroll
       for (int t = 0; t < 9; ++t) acc[e][t] += d[e] * xv[t];
       acc[e][9] += d[e];
     }
   }
-  // reduce the 8 groups of this warp that share chunk c (lanes c, c+4, ...), fixed order
+  // reduce the 4 groups of this warp that share c8 (lanes c8, c8+8, ...), fixed order
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
+  for (int e = 0; e < 4; ++e)
 #pragma unroll
     for (int t = 0; t < 10; ++t) {
       float v = acc[e][t];
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 8);
       v += __shfl_xor_sync(0xffffffffu, v, 16);
       acc[e][t] = v;
     }
-  if (lane < 4) {
+  if (lane < 8) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
+    for (int e = 0; e < 4; ++e)
 #pragma unroll
-      for (int t = 0; t < 10; ++t) red[warp][c][e * 10 + t] = acc[e][t];
+      for (int t = 0; t < 10; ++t) red[warp][c][(h * 4 + e) * 10 + t] = acc[e][t];
   }
   __syncthreads();
-  for (int o = tid; o < 320; o += 128) {  // o = oc*10 + t
+  for (int o = tid; o < 320; o += C1W_THREADS) {  // o = oc*10 + t; warps summed in order
     const int oc = o / 10, t = o % 10;
-    const float s = red[0][oc >> 3][(oc & 7) * 10 + t] + red[1][oc >> 3][(oc & 7) * 10 + t] +
-                    red[2][oc >> 3][(oc & 7) * 10 + t] + red[3][oc >> 3][(oc & 7) * 10 + t];
+    float s = red[0][oc >> 3][(oc & 7) * 10 + t];
+#pragma unroll
+    for (int w = 1; w < C1W_THREADS / 32; ++w) s += red[w][oc >> 3][(oc & 7) * 10 + t];
     buf.part1[(int64_t(j) * buf.B + b) * 320 + o] = s;
   }
 }
@@ -807,7 +805,7 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
-  TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), 128, C1W_SMEM, st, p.lane_dev, b, p.x));
+  TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (wst != st) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
