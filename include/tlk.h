@@ -128,6 +128,15 @@ int tlk_run(tlk_ctx* ctx, int32_t pack, int32_t steps);
  * i32 labels [lanes,batch], one step, D2H of the per-lane losses [lanes]. */
 int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
                   float* losses_out);
+/* Pipelined form of tlk_step_host: enqueues the step and returns at once.
+ * Step k uses device input slot k & 1: its H2D copy (on a copy stream) waits
+ * only for step k-2, so it overlaps step k-1's kernels.  pixels / labels must
+ * stay valid (and should be pinned) until the copy is done, losses_out until
+ * tlk_step_host_wait(ticket) returns; only the two newest tickets can be
+ * waited on.  Do not interleave with tlk_step_host without waiting first. */
+int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
+                        float* losses_out, int64_t* ticket);
+int tlk_step_host_wait(tlk_ctx* ctx, int32_t pack, int64_t ticket);
 int tlk_lane_status_get(tlk_ctx* ctx, int32_t pack, int32_t lane, tlk_lane_status* out);
 int tlk_lane_losses(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int32_t n);
 int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64_t n);

@@ -52,6 +52,15 @@ struct Pack {
   // side stream + events for concurrent graph branches
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // pipelined host-input steps (tlk_step_host_async): a second input slot and
+  // the step graph captured against it, a copy stream, per-slot events
+  uint8_t* px_alt = nullptr;
+  int32_t* lb_alt = nullptr;
+  cudaGraph_t hgraph_alt = nullptr;
+  cudaGraphExec_t hexec_alt = nullptr;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t h2d_ev[2] = {nullptr, nullptr}, done_ev[2] = {nullptr, nullptr};
+  int64_t host_steps = 0;
   int flags = 0;  // TLK_PACK_* (e.g. write every gradient for tests)
   // named internal buffers (tlk_pack_named): activations, statistics, snapshots
   struct Named {

@@ -5,6 +5,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 
 #include "pack.cuh"
 
@@ -65,6 +66,13 @@ struct tlk_ctx {
 namespace {
 
 void destroy_pack(Pack& p) {
+  if (p.copy_st) cudaStreamDestroy(p.copy_st);
+  for (int k = 0; k < 2; ++k) {
+    if (p.h2d_ev[k]) cudaEventDestroy(p.h2d_ev[k]);
+    if (p.done_ev[k]) cudaEventDestroy(p.done_ev[k]);
+  }
+  if (p.hexec_alt) cudaGraphExecDestroy(p.hexec_alt);
+  if (p.hgraph_alt) cudaGraphDestroy(p.hgraph_alt);
   if (p.side) cudaStreamDestroy(p.side);
   if (p.ev_fork) cudaEventDestroy(p.ev_fork);
   if (p.ev_join) cudaEventDestroy(p.ev_join);
@@ -96,8 +104,7 @@ int enqueue_step(Pack& p, cudaStream_t st) {
   return fail(TLK_EINVAL, "unknown model %d", p.model);
 }
 
-int ensure_graph(Pack& p, cudaStream_t st) {
-  if (p.graph_exec) return TLK_OK;
+int capture_step(Pack& p, cudaStream_t st, cudaGraph_t* graph, cudaGraphExec_t* exec) {
   TLK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_step(p, st);
   cudaGraph_t g = nullptr;
@@ -107,8 +114,38 @@ int ensure_graph(Pack& p, cudaStream_t st) {
     return rc;
   }
   TLK_CUDA(e);
-  p.graph = g;
-  TLK_CUDA(cudaGraphInstantiate(&p.graph_exec, g, 0));
+  *graph = g;
+  TLK_CUDA(cudaGraphInstantiate(exec, g, 0));
+  return TLK_OK;
+}
+
+int ensure_graph(Pack& p, cudaStream_t st) {
+  if (p.graph_exec) return TLK_OK;
+  return capture_step(p, st, &p.graph, &p.graph_exec);
+}
+
+// Second input slot + the step graph captured against it (inputs are kernel
+// arguments of the captured graph), copy stream and per-slot events.
+int ensure_host_pipeline(Pack& p, cudaStream_t st) {
+  int rc = ensure_graph(p, st);
+  if (rc || p.hexec_alt) return rc;
+  const size_t L = size_t(p.lanes), B = size_t(p.batch);
+  void* v = nullptr;
+  if ((rc = pack_alloc(p, &v, L * B * 784))) return rc;
+  p.px_alt = static_cast<uint8_t*>(v);
+  if ((rc = pack_alloc(p, &v, L * B * 4))) return rc;
+  p.lb_alt = static_cast<int32_t*>(v);
+  std::swap(p.pixels, p.px_alt);
+  std::swap(p.labels, p.lb_alt);
+  rc = capture_step(p, st, &p.hgraph_alt, &p.hexec_alt);
+  std::swap(p.pixels, p.px_alt);
+  std::swap(p.labels, p.lb_alt);
+  if (rc) return rc;
+  TLK_CUDA(cudaStreamCreateWithFlags(&p.copy_st, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    TLK_CUDA(cudaEventCreateWithFlags(&p.h2d_ev[k], cudaEventDisableTiming));
+    TLK_CUDA(cudaEventCreateWithFlags(&p.done_ev[k], cudaEventDisableTiming));
+  }
   return TLK_OK;
 }
 
@@ -380,6 +417,44 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
                              ctx->stream));
     TLK_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  return TLK_OK;
+}
+
+// Pipelined host-input step: step k uses input slot k & 1.  The copy stream
+// waits until step k-2 (the slot's previous user) has finished, copies the
+// inputs, and the compute stream waits for that copy, replays the slot's
+// graph and copies the losses back; nothing blocks the caller, so step k+1's
+// H2D overlaps step k's kernels.  tlk_step_host_wait(ticket) returns once the
+// step's losses are in losses_out (valid for the two newest tickets).
+int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
+                        float* losses_out, int64_t* ticket) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(p->host_input, TLK_ESTATE, "pack was created without host_input");
+  TLK_CHECK(pixels && labels && losses_out && ticket, TLK_EINVAL, "null buffers");
+  if ((rc = ensure_host_pipeline(*p, ctx->stream))) return rc;
+  const int s = int(p->host_steps & 1);
+  const size_t L = size_t(p->lanes), B = size_t(p->batch);
+  if (p->host_steps >= 2) TLK_CUDA(cudaStreamWaitEvent(p->copy_st, p->done_ev[s], 0));
+  TLK_CUDA(cudaMemcpyAsync(s ? p->px_alt : p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, p->copy_st));
+  TLK_CUDA(cudaMemcpyAsync(s ? p->lb_alt : p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->copy_st));
+  TLK_CUDA(cudaEventRecord(p->h2d_ev[s], p->copy_st));
+  TLK_CUDA(cudaStreamWaitEvent(ctx->stream, p->h2d_ev[s], 0));
+  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->graph_exec, ctx->stream));
+  TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, L * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  TLK_CUDA(cudaEventRecord(p->done_ev[s], ctx->stream));
+  *ticket = p->host_steps++;
+  return TLK_OK;
+}
+
+int tlk_step_host_wait(tlk_ctx* ctx, int32_t pack, int64_t ticket) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(ticket >= 0 && ticket < p->host_steps && ticket + 2 >= p->host_steps, TLK_EINVAL,
+            "ticket %lld is not one of the two newest host steps", (long long)ticket);
+  TLK_CUDA(cudaEventSynchronize(p->done_ev[ticket & 1]));
   return TLK_OK;
 }
 

@@ -11,6 +11,8 @@ import ctypes as C
 import os
 import threading
 
+import numpy as np
+
 LIB_PATH = os.environ.get("TLK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtlk.so")
 
 TLK_OK, TLK_EINVAL, TLK_ECUDA, TLK_EOOM, TLK_ESTATE = 0, -1, -2, -3, -4
@@ -26,7 +28,7 @@ BUF_PARAMS, BUF_GRADS, BUF_MOM1, BUF_MOM2, BUF_WBF16, BUF_LOSS, BUF_PIXELS, BUF_
 EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
     "tlk_close", "tlk_sync", "tlk_stream", "tlk_pack_create", "tlk_lane_load", "tlk_lane_release",
-    "tlk_run", "tlk_step_host", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
+    "tlk_run", "tlk_step_host", "tlk_step_host_async", "tlk_step_host_wait", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
     "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
     "tlk_selftest_datagen",
@@ -196,6 +198,21 @@ class Pack:
         check(lib().tlk_step_host(self.ctx._ctx, self.id, px.ctypes.data_as(C.c_void_p),
                                   lb.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
         return out
+
+    def step_host_async(self, pixels, labels, losses_out) -> int:
+        """Pipelined end-to-end step (tlk_step_host_async): returns a ticket at once;
+        the buffers (pinned numpy views) must stay alive until step_host_wait(ticket)."""
+        assert pixels.dtype == np.uint8 and labels.dtype == np.int32 and losses_out.dtype == np.float32
+        assert pixels.shape == (self.lanes, self.batch, 784) and labels.shape == (self.lanes, self.batch)
+        assert pixels.flags.c_contiguous and labels.flags.c_contiguous and losses_out.size >= self.lanes
+        t = C.c_int64(0)
+        check(lib().tlk_step_host_async(self.ctx._ctx, self.id, pixels.ctypes.data_as(C.c_void_p),
+                                        labels.ctypes.data_as(C.c_void_p), losses_out.ctypes.data_as(C.c_void_p),
+                                        C.byref(t)))
+        return t.value
+
+    def step_host_wait(self, ticket: int) -> None:
+        check(lib().tlk_step_host_wait(self.ctx._ctx, self.id, C.c_int64(ticket)))
 
     def status(self, lane: int) -> LaneStatus:
         s = LaneStatus()

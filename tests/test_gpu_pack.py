@@ -123,6 +123,39 @@ def test_host_input_step_matches_device_generated():
             assert np.array_equal(dev.params(lane), host.params(lane))
 
 
+@pytest.mark.parametrize("model", [omodels.MODEL_MLP, omodels.MODEL_CNN])
+def test_pipelined_host_steps_match_device_generated(model):
+    """tlk_step_host_async (double-buffered inputs, H2D overlapping the previous
+    step): every step's losses equal the device-generated run, bit for bit."""
+    from oracle import rng
+
+    lanes, batch, steps = 3, 64, 6
+    with rt.Context(0) as ctx:
+        dev = ctx.pack(model, batch, lanes, steps)
+        host = ctx.pack(model, batch, lanes, steps, host_input=True)
+        for p in (dev, host):
+            for lane in range(lanes):
+                p.load(lane, seed=lane + 40, steps=steps)
+        dev.run(steps)
+        bufs = []
+        for t in range(steps):
+            px = np.ascontiguousarray(np.stack([rng.batch(lane + 40, t, batch)[0] for lane in range(lanes)]))
+            lb = np.ascontiguousarray(np.stack([rng.batch(lane + 40, t, batch)[1] for lane in range(lanes)])
+                                      .astype(np.int32))
+            bufs.append((px, lb, np.zeros(lanes, np.float32)))
+        tickets = []
+        for t in range(steps):
+            tickets.append(host.step_host_async(*bufs[t]))
+            if t >= 1:
+                host.step_host_wait(tickets[t - 1])
+        host.step_host_wait(tickets[-1])
+        ctx.sync()
+        for t in range(steps):
+            assert np.array_equal(bufs[t][2], np.array([dev.losses(j, steps)[t] for j in range(lanes)], np.float32))
+        for lane in range(lanes):
+            assert np.array_equal(dev.params(lane), host.params(lane))
+
+
 def test_zero_copy_tensor_view():
     with rt.Context(0) as ctx:
         pack = ctx.pack(omodels.MODEL_MLP, 64, 2, 2)
