@@ -218,8 +218,7 @@ def kernel_work(name, info, lanes, batch):
         # CUDA-core / bookkeeping kernels: compulsory HBM bytes
         "inputs_conv1_fwd": ("hbm", L * B * (784 + 784 * 2 + 4 + 676 * 32 * 2)),
         "conv1_wgrad": ("hbm", L * B * (784 * 2 + 676 * 32 * 2)),
-        "fc1_reduce": ("hbm", L * (18 * 128 * 64 * 4 + B * 128 * 2)),
-        "head": ("hbm", L * B * 128 * 4),
+        "fc1_reduce_head": ("hbm", L * (18 * 128 * 64 * 4 + B * 128 * 2 * 2)),
         "end_step": ("hbm", L * 128),
     }
     return act.get(name, ("hbm", 0.0))

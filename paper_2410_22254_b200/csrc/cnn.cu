@@ -3,11 +3,11 @@
 //   x[28,28] -conv1 3x3 (1->32)+ReLU-> h1[26,26,32] -conv2 3x3 (32->64)+ReLU+maxpool2->
 //   p2[12,12,64] -flatten (h,w,c)-> fc1 (9216->128)+ReLU -> h3 -> fc2 (128->10) + CE
 //
-// Launch sequence of one step (11 kernels, graph-captured):
+// Launch sequence of one step (10 kernels, graph-captured):
 //   inputs + conv1 fwd (CUDA cores, writes h1 in P28 planes) | conv2 fwd
 //   (tcgen05, TMA-bulk patch + tap-shifted descriptors; epilogue bias+ReLU+
 //   2x2 maxpool+argmax) | fc1 fwd (tcgen05 split-K) | fc1 reduce (+bias+ReLU)
-//   | head (fc2+CE+bwd) | fc1 wgrad (tcgen05) | fc1 dgrad (tcgen05; epilogue
+//   + head (fc2+CE+bwd), one 8-CTA cluster per lane | fc1 wgrad (tcgen05) | fc1 dgrad (tcgen05; epilogue
 //   = maxpool/ReLU backward scatter into dz2 P28 planes + conv2 bias partials)
 //   | conv2 wgrad (tcgen05, 9 tap accumulators in TMEM) | conv2 dgrad
 //   (tcgen05; epilogue ReLU mask -> dz1) | conv1 wgrad (CUDA cores) | fc1
@@ -21,6 +21,8 @@
 //   (argmax | live<<2) | h3 bf16 [B,128] | dz3 bf16 [B,128] |
 //   dz2 P28 [8][npos][8] | dz1 P28 [4][npos][8]      (npos = 32 + 784 B + 64)
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "conv_tc.cuh"
 #include "tma.cuh"
@@ -152,22 +154,121 @@ struct Fc1Fwd {
   TLK_DEV void finish(const Work&, int, Carry&) const {}
 };
 
-// h3[b][o] = bf16(relu(sum_s part[s][o][b] + bias[o])), fixed split order.
-__global__ void fc1_reduce_kernel(const LaneState* __restrict__ lanes, CnnBufs buf,
-                                  const float* __restrict__ params, int64_t pstride,
-                                  int64_t b_off) {
+
+// -------------------------------------------- fc1 reduce + head (fused) -----
+// One cluster of 8 CTAs per lane (16 hidden units each).  CTA r reduces its
+// slice of h3 = bf16(relu(sum_s part[s] + b1)) from the split-K partials
+// (split order fixed), forms the partial logits of its 16 units, and the
+// cluster exchanges them through distributed shared memory: every CTA sums
+// the 8 partials in rank order (+ b2), so all hold identical logits.  Then,
+// as head_kernel (kernels.cu): softmax-CE, the loss / step scalars / fc2.b
+// grad (rank 0), and the backward of its 16 units (dz3, fc2.w, fc1.b grads).
+constexpr int HEAD_CL = 8, HEAD_HS = 16;
+__global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
+    cnn_head_kernel(LaneState* __restrict__ lanes, CnnBufs buf, const float* __restrict__ params,
+                    float* __restrict__ grads, int64_t stride, int64_t b1_off, int64_t w_off, int64_t b_off,
+                    const int32_t* __restrict__ labels, float* __restrict__ loss, int max_steps,
+                    float* __restrict__ last_loss) {
   pdl_begin();
-  const int j = blockIdx.y;
-  if (!lanes[j].active) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // e = o*64 + b
-  if (e >= 128 * 64) return;
-  const int o = e >> 6, b = e & 63;
-  if (b >= buf.B) return;
-  const float* pp = buf.part_fc1 + int64_t(j) * FC1_SPLITS * 128 * 64 + e;
-  float s = 0.0f;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int C = CLASSES, H = 128, HS = HEAD_HS;
+  const int j = blockIdx.y, r = int(cluster.block_rank()), tid = threadIdx.x, B = buf.B;
+  const int k0 = r * HS;
+  const bool active = lanes[j].active;  // uniform over the cluster
+  __shared__ float hs[64 * HS], zs[64 * HS], plog[64 * C], logit[64 * C], d[64 * C], lossb[64];
+  __shared__ float wsl[C * HS];
+  const float* P = params + j * stride;
+  if (active) {
+    for (int i = tid; i < C * HS; i += 256) wsl[i] = P[w_off + (i / HS) * H + k0 + i % HS];
+    // h3 slice: (kk, b) = (i / 64, i % 64), 18 partials in split order
+    for (int i = tid; i < HS * 64; i += 256) {
+      const int kk = i >> 6, b = i & 63;
+      if (b >= B) continue;
+      const float* pp = buf.part_fc1 + int64_t(j) * FC1_SPLITS * 128 * 64 + (k0 + kk) * 64 + b;
+      float sacc = 0.0f;
 #pragma unroll
-  for (int k = 0; k < FC1_SPLITS; ++k) s += pp[int64_t(k) * 128 * 64];
-  buf.h3[j * buf.h3_st + b * 128 + o] = f2bf(fmaxf(s + params[j * pstride + b_off + o], 0.0f));
+      for (int k = 0; k < FC1_SPLITS; ++k) sacc += pp[int64_t(k) * 128 * 64];
+      const uint16_t hb = f2bf(fmaxf(sacc + P[b1_off + k0 + kk], 0.0f));
+      buf.h3[j * buf.h3_st + b * 128 + k0 + kk] = hb;
+      hs[b * HS + kk] = bf2f(hb);
+    }
+  }
+  __syncthreads();
+  if (active) {
+    for (int i = tid; i < B * C; i += 256) {  // partial logits of this slice
+      const int b = i / C, c = i % C;
+      float sacc = 0.0f;
+#pragma unroll
+      for (int kk = 0; kk < HS; ++kk) sacc += hs[b * HS + kk] * wsl[c * HS + kk];
+      plog[i] = sacc;
+    }
+  }
+  cluster.sync();
+  if (active) {
+    for (int i = tid; i < B * C; i += 256) {
+      float sacc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < HEAD_CL; ++q) sacc += cluster.map_shared_rank(plog, q)[i];
+      logit[i] = sacc + P[b_off + i % C];
+    }
+  }
+  cluster.sync();  // every CTA has read the partials before any may exit
+  if (!active) return;
+  __syncthreads();
+  if (tid < B) {
+    const int y = labels[size_t(j) * B + tid];
+    const float* l = logit + tid * C;
+    float m = l[0];
+    for (int c = 1; c < C; ++c) m = fmaxf(m, l[c]);
+    float e[C], sacc = 0.0f;
+    for (int c = 0; c < C; ++c) {
+      e[c] = expf(l[c] - m);
+      sacc += e[c];
+    }
+    lossb[tid] = (m + logf(sacc)) - l[y];
+    for (int c = 0; c < C; ++c) d[tid * C + c] = (e[c] / sacc - (c == y ? 1.0f : 0.0f)) / float(B);
+  }
+  __syncthreads();
+  float* G = grads + j * stride;
+  if (r == 0) {
+    if (tid == 0) {
+      float sacc = 0.0f;
+      for (int b = 0; b < B; ++b) sacc += lossb[b];
+      const float L = sacc / float(B);
+      LaneState& ls = lanes[j];
+      loss[size_t(j) * max_steps + ls.steps_done] = L;
+      last_loss[j] = L;
+      lane_step_scalars(ls);
+    }
+    if (tid < C) {
+      float sacc = 0.0f;
+      for (int b = 0; b < B; ++b) sacc += d[b * C + tid];
+      G[b_off + tid] = sacc;
+    }
+  }
+  uint16_t* dzj = buf.dz3 + j * buf.h3_st + k0;
+  for (int i = tid; i < B * HS; i += 256) {
+    const int b = i / HS, kk = i % HS;
+    float dh = 0.0f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) dh += d[b * C + c] * wsl[c * HS + kk];
+    const uint16_t zb = f2bf(hs[i] > 0.0f ? dh : 0.0f);
+    dzj[b * H + kk] = zb;
+    zs[i] = bf2f(zb);
+  }
+  __syncthreads();
+  for (int i = tid; i < HS * (C + 1); i += 256) {
+    const int kk = i % HS, c = i / HS;  // c == C -> fc1.b grad
+    float sacc = 0.0f;
+    if (c < C) {
+      for (int b = 0; b < B; ++b) sacc += d[b * C + c] * hs[b * HS + kk];
+      G[w_off + c * H + k0 + kk] = sacc;
+    } else {
+      for (int b = 0; b < B; ++b) sacc += zs[b * HS + kk];
+      G[b1_off + k0 + kk] = sacc;
+    }
+  }
 }
 
 // ---------------------------------------------- fc1 dgrad + unpool (TC) -----
@@ -754,7 +855,7 @@ int cnn_setup(Pack& p) {
   TLK_CUDA(cudaFuncSetAttribute(fc1_wgrad_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWA_SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
-  p.launches_per_step = 11;
+  p.launches_per_step = 10;
   p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
   p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
@@ -780,11 +881,9 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   Fc1Fwd f1{b, p.lane_dev};
   TLK_CUDA(launch_gemm_tma(f1, dim3(1, 1, L * FC1_SPLITS), st));
   p.mark(st, "fc1_fwd_splitk");
-  TLK_CUDA(launch(fc1_reduce_kernel, dim3(128 * 64 / 256, L), 256, 0, st, p.lane_dev, b, p.params, p.stride,
-                                                              o_f1b));
-  p.mark(st, "fc1_reduce");
-  TLK_CUDA(cudaGetLastError());
-  if ((rc = enqueue_head(p, st, b.h3, 128, o_f2w, o_f2b, b.dz3, o_f1b))) return rc;
+TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.params, p.grads, p.stride, o_f1b,
+                  o_f2w, o_f2b, p.labels, p.loss, p.max_steps, p.last_loss));
+  p.mark(st, "fc1_reduce_head");
   Fc1Dgrad f1d{b, p.lane_dev};  // reads this step's fc1 weights
   TLK_CUDA(launch_gemm_tma(f1d, dim3(9216 / GEMM_BM, 1, L), st));
   p.mark(st, "fc1_dgrad_unpool");
