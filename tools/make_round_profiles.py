@@ -20,7 +20,7 @@ PROF = os.path.join(ROOT, "profiles")
 # capture name -> (model, bench.py kernel label)
 CAPS = {"c_fc1_wgrad_adam": ("cnn", "fc1_wgrad_adam"), "c_conv2_fwd": ("cnn", "conv2_fwd_pool"),
         "c_conv2_wgrad": ("cnn", "conv2_wgrad"), "c_fc1_dgrad": ("cnn", "fc1_dgrad_unpool"),
-        "c_cnn_opt": ("cnn", "grad_finalize_opt"), "r_fwd_l1_halo": ("resnet18", "conv_fwd"),
+        "c_cnn_opt": ("cnn", "grad_finalize_opt"), "c_cnn_head": ("cnn", "fc1_reduce_head"), "r_fwd_l1_halo": ("resnet18", "conv_fwd"),
         "r_dgrad_l1_halo": ("resnet18", "conv_dgrad"), "r_wgrad_l1_tg": ("resnet18", "conv_wgrad"),
         "r_dgrad_bn256": ("resnet18", "conv_dgrad_bn256"), "r_bn_bwd_apply": ("resnet18", "bn_bwd_apply"),
         "g_scores": ("gpt", "attn_scores"), "g_fc": ("gpt", "fc")}
