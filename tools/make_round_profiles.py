@@ -35,7 +35,7 @@ def main(tag):
             except ValueError:
                 continue
             json.dump(d, open(os.path.join(PROF, f"{tag}_bench_{w}.json"), "w"), indent=1)
-    for w, how in (("cnn", "bench.py --steps 3 --warmup 3 (13 kernels per step incl. setup)"),
+    for w, how in (("cnn", "bench.py --steps 3 --warmup 3 (10 kernels per step; lane_init_kernel is setup)"),
                    ("resnet18", "tools/pack_step.py resnet18 8 128 1"), ("gpt", "tools/pack_step.py gpt 16 64 1")):
         f = os.path.join(OUT, f"launches_{w}.csv")
         if os.path.exists(f):
