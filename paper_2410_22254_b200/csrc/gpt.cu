@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ l
 
 // token-embedding gradient, stage 1: per block of 256 positions, smem
 // acc[v][c] (thread = column, positions in order) -> part[lane][blk][v][c]
-constexpr int EMB_ROWS = 1024;  // tokens per partial: the V x d partials are written once per 1024 tokens
+constexpr int EMB_ROWS = 256;
 __global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int d, int V, int cols,
                                  const int32_t* __restrict__ tokens, int T, const float* __restrict__ dx,
                                  float* __restrict__ part, int64_t part_st) {
