@@ -502,21 +502,7 @@ def packed_arm(a, world, rank, local):
     }
     if rank == 0 and world == 1 and a.sweep and MODEL == "cnn":
         # the metric's "vs jobs/GPU" axis: packed throughput for NPPN/GPU = 1..32
-        sweep = []
-        for k in (1, 2, 4, 8, 16, 32):
-            sp = ctx.pack(rt.MODELS[MODEL], BATCH, k, 10 + 50 + 2)
-            for jj in range(k):
-                sp.load(jj, seed=1000 + jj, steps=10 + 50 + 2)
-            sp.run(10)
-            ctx.sync()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            sp.run(50)
-            e1.record(stream)
-            e1.synchronize()
-            t = e0.elapsed_time(e1) / 50
-            sweep.append({"jobs_per_gpu": k, "ms_per_step": t, "samples_per_s": k * BATCH / (t / 1e3)})
-        line["nppn_sweep"] = sweep
+        line["nppn_sweep"] = nppn_sweep(ctx, stream, (1, 2, 4, 8, 16, 32), 10, 50)
     if rank == 0 and world == 1 and not a.no_baselines:
         cpu, cores, _ = cpu_oracle_rate(2, 1)
         line["cpu_baseline"] = {
@@ -535,6 +521,34 @@ def packed_arm(a, world, rank, local):
         print(json.dumps(line), flush=True)
     ctx.close()
     return 0
+
+
+def nppn_sweep(ctx, stream, jobs_list, warm, timed):
+    """Packed throughput vs co-resident jobs per GPU (the metric's NPPN axis):
+    a fresh pack of k lanes per point, `warm` untimed then `timed` timed steps."""
+    import torch
+
+    from paper_2410_22254_b200 import runtime as rt
+
+    opt = WORKLOAD_OPT.get(MODEL, dict(lr=1e-3))
+    kw = dict(optimizer=rt.OPTIMIZERS[opt.get("optim", "adam")], lr=opt.get("lr", 1e-3),
+              momentum=opt.get("momentum", 0.0))
+    out = []
+    for k in jobs_list:
+        sp = ctx.pack(rt.MODELS[MODEL], BATCH, k, warm + timed + 2)
+        for jj in range(k):
+            sp.load(jj, seed=1000 + jj, steps=warm + timed + 2, **kw)
+        sp.run(warm)
+        ctx.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sp.run(timed)
+        e1.record(stream)
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / timed
+        out.append({"jobs_per_gpu": k, "ms_per_step": t, "samples_per_s": k * BATCH / (t / 1e3)})
+        del sp
+    return out
 
 
 def _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_roof, sflops,
@@ -557,6 +571,12 @@ def _finish_gpt_line(a, world, rank, ctx, pack, value, ms_step, clocks, roof, t_
                           "compulsory_bytes_per_step": sbytes},
         "kernels": kernels_out,
     }
+    if rank == 0 and world == 1 and a.sweep:
+        import torch
+
+        stream = torch.cuda.ExternalStream(ctx.stream_handle)
+        line["nppn_sweep"] = nppn_sweep(ctx, stream, (1, 2, 4, 8, 16) if MODEL != "xformer" else (1, 4, 16, 32),
+                                        3, 5)
     if rank == 0 and world == 1 and not a.no_baselines:
         kp, outs = kproc_rate(min(lanes, 8), duration=a.kproc_seconds, lead=60.0)
         line["kproc_baseline"] = {"value": kp, "unit": "samples/s", "procs": min(lanes, 8),
@@ -582,7 +602,7 @@ def main():
     ap.add_argument("--kproc-seconds", type=float, default=10.0)
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-sweep", dest="sweep", action="store_false",
-                    help="skip the jobs/GPU sweep (1..32 packed CNN jobs)")
+                    help="skip the jobs/GPU sweep (packed throughput at 1..32 jobs per GPU)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     global MODEL, BATCH, JOBS_PER_GPU, WORKLOAD
