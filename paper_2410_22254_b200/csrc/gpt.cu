@@ -617,6 +617,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     }
     {  // y = P V
       Epi e = epi(EPI_BF16, T, dh, lb.y, nd, int64_t(T) * d, dh, d);
+      e.causal_k = 1;  // P rows: keys <= query
       TLK_TRY((gemm<64, false, true, false>(
           p, st, op(lb.P, pl, int64_t(H) * tt, tt, T, 1, T, T),
           op(lb.qkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), e, T, dh, T, B, H, "attn_pv")));
@@ -805,16 +806,19 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
         TLK_TRY((gemm<64, false, false, true>(p, st, A, Bv, e, T, T, dh, B, H, "attn_dp")));
       // dq = dS K
       Epi eq = epi(EPI_BF16, T, dh, b.dqkv, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      eq.causal_k = 1;
       TLK_TRY((gemm<64, false, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, T, 1, T, T),
                                             op(lb.qkv + d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), eq,
                                             T, dh, T, B, H, "attn_dq")));
       // dk = dS^T Q
       Epi ek = epi(EPI_BF16, T, dh, b.dqkv + d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      ek.causal_k = 2;  // dS^T rows = keys: queries >= key
       TLK_TRY((gemm<64, true, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, 1, T, T, T),
                                            op(lb.qkv, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), ek, T,
                                            dh, T, B, H, "attn_dk")));
       // dv = P^T dY
       Epi ev = epi(EPI_BF16, T, dh, b.dqkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
+      ev.causal_k = 2;
       TLK_TRY((gemm<64, true, true, false>(p, st, op(lb.P, pl, int64_t(H) * tt, tt, 1, T, T, T),
                                            op(b.dy, nd, int64_t(T) * d, dh, 1, d, dh, T), ev, T, dh, T, B,
                                            H, "attn_dv")));

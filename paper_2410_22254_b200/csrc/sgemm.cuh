@@ -38,6 +38,8 @@ struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
   const void* aux;    // EPI_RESADD: fp32, EPI_GELU_BWD / EPI_SOFTMAX_BWD: bf16 (same indexing)
   float scale;
   int causal;
+  int causal_k;  // A is causal in (row, k): 1 -> only k <= row, 2 -> only k >= row (transposed P / dS);
+                 // the all-zero k-blocks are skipped (adding exact zeros: same bits)
   const int32_t* targets;  // EPI_CE: [lane][rows] (+ lane*tg_ls)
   int64_t tg_ls;
   float* lossrow;          // EPI_CE: [lane][rows]

@@ -87,6 +87,10 @@ struct TGemm {
     w.n0 = n_t * BN_;
     w.kb_begin = 0;
     w.kb_end = g.kblocks;
+    if (g.e.causal_k == 1)
+      w.kb_end = min(w.kb_end, (w.m0 + GEMM_BM + GEMM_BK - 1) / GEMM_BK);
+    else if (g.e.causal_k == 2)
+      w.kb_begin = w.m0 / GEMM_BK;
     w.split = 0;
     return true;
   }
