@@ -500,7 +500,7 @@ def packed_arm(a, world, rank, local):
                           "samples_per_s_roof": lanes * BATCH / t_roof},
         "kernels": kernels_out,
     }
-    if rank == 0 and world == 1 and a.sweep and MODEL == "cnn":
+    if rank == 0 and world == 1 and a.sweep:
         # the metric's "vs jobs/GPU" axis: packed throughput for NPPN/GPU = 1..32
         line["nppn_sweep"] = nppn_sweep(ctx, stream, (1, 2, 4, 8, 16, 32), 10, 50)
     if rank == 0 and world == 1 and not a.no_baselines:

@@ -715,9 +715,11 @@ __global__ void __launch_bounds__(256) rn_stem_wgrad_kernel(const LaneState* __r
     const int gy = yy - 1, gx = xx - 1;
     xs[yy][xx][c] = (gy >= 0 && gy < 32 && gx >= 0 && gx < 32) ? bf2f(xi[(gy * 32 + gx) * 3 + c]) : 0.f;
   }
-  const int co = tid & 63, grp = tid >> 6;  // taps*ci split 7/7/7/6
-  const int t0 = grp * 7, tn = grp == 3 ? 6 : 7;
-  float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // thread (co, ci) (192 of 256 threads): the 9 taps of its (co, ci) with the
+  // 3x3 input window sliding along the row in registers (3 new x values and
+  // 9 FMAs per pixel)
+  const int co = tid & 63, ci = tid >> 6;
+  float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const uint16_t* dyi = dy + (int64_t(j) * B + img) * 1024 * 64;
   // one 16-byte dy vector per thread per row (32 px x 64 ch = 256 x 8 bf16),
   // the next row's vector in flight while this row is consumed
@@ -736,19 +738,34 @@ __global__ void __launch_bounds__(256) rn_stem_wgrad_kernel(const LaneState* __r
       }
     }
     __syncthreads();
-    for (int px = 0; px < 32; ++px) {
-      const float d = ds[px][co];
+    if (ci < 3) {
+      float wv[3][3];
 #pragma unroll
-      for (int u = 0; u < 7; ++u) {
-        if (u < tn) {
-          const int t = t0 + u, kh = t / 9, kw = (t / 3) % 3, ci = t % 3;
-          acc[u] = fmaf(d, xs[row + kh][px + kw][ci], acc[u]);
+      for (int kh = 0; kh < 3; ++kh) {
+        wv[kh][1] = xs[row + kh][0][ci];
+        wv[kh][2] = xs[row + kh][1][ci];
+      }
+#pragma unroll 4
+      for (int px = 0; px < 32; ++px) {
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh) {
+          wv[kh][0] = wv[kh][1];
+          wv[kh][1] = wv[kh][2];
+          wv[kh][2] = xs[row + kh][px + 2][ci];
         }
+        const float d = ds[px][co];
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) acc[kh * 3 + kw] = fmaf(d, wv[kh][kw], acc[kh * 3 + kw]);
       }
     }
   }
-  float* pp = part + j * part_ls + int64_t(img) * 1728 + co * 27 + t0;
-  for (int u = 0; u < tn; ++u) pp[u] = acc[u];
+  if (ci < 3) {  // partial[co][tap * 3 + ci] (tap = kh * 3 + kw)
+    float* pp = part + j * part_ls + int64_t(img) * 1728 + co * 27;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) pp[t * 3 + ci] = acc[t];
+  }
 }
 
 // ------------------------------------------------------------- GEMM glue ----
