@@ -361,42 +361,79 @@ __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ l
 
 // token-embedding gradient, stage 1: per block of 256 positions, smem
 // acc[v][c] (thread = column, positions in order) -> part[lane][blk][v][c]
-constexpr int EMB_ROWS = 256;
-__global__ void embed_bwd_kernel(const LaneState* __restrict__ lanes, int N, int d, int V, int cols,
-                                 const int32_t* __restrict__ tokens, int T, const float* __restrict__ dx,
-                                 float* __restrict__ part, int64_t part_st) {
-  pdl_begin();
-  const int blk = blockIdx.x, cg = blockIdx.y, j = blockIdx.z, c = cg * cols + threadIdx.x;
-  if (!lanes[j].active) return;
-  extern __shared__ float acc[];  // [V][cols]
-  __shared__ int tk[EMB_ROWS];
-  for (int v = 0; v < V; ++v) acc[v * cols + threadIdx.x] = 0.f;
-  for (int i = threadIdx.x; i < EMB_ROWS; i += blockDim.x) {
-    const int row = blk * EMB_ROWS + i;
-    const int b = row / T, t = row % T;
-    tk[i] = row < N ? tokens[(int64_t(j) * (N / T) + b) * (T + 1) + t] : 0;
-  }
-  __syncthreads();
-  if (c < d) {
-    // 16 independent row loads in flight, then the 16 smem accumulations in
-    // position order (same order as one-at-a-time)
-    const float* g = dx + int64_t(j) * N * d + c;
-    const int rows = min(EMB_ROWS, N - blk * EMB_ROWS);
-    for (int i0 = 0; i0 < rows; i0 += 16) {
-      float vals[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        vals[u] = (i0 + u < rows) ? g[int64_t(blk * EMB_ROWS + i0 + u) * d] : 0.f;
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (i0 + u < rows) acc[tk[i0 + u] * cols + threadIdx.x] += vals[u];
-    }
-    float* out = part + j * part_st + int64_t(blk) * V * d + c;
-    for (int v = 0; v < V; ++v) out[int64_t(v) * d] = acc[v * cols + threadIdx.x];
-  }
-}
 
 // dwpe[t][c] = sum_b dx[b*T + t][c] (b in order)
+// Token-embedding gradient by vocabulary row: CTA (vocab block of EMV rows,
+// column slice) scans the lane's input tokens in order, compacts the rows
+// whose token falls in its block (block-wide scan -> token order), and
+// thread c accumulates dx[row][c] into its rows' sums in that order.  Every
+// dx row is read once, nothing is staged through partials, and the sums are
+// per vocabulary row in token order (deterministic).
+constexpr int EMV = 16, EMV_COLS = 128, EMV_CHUNK = 1024;
+__global__ void __launch_bounds__(EMV_COLS) embed_bwd_vocab_kernel(const LaneState* __restrict__ lanes, int N, int d,
+                                                                   int V, const int32_t* __restrict__ tokens, int T,
+                                                                   const float* __restrict__ dx,
+                                                                   float* __restrict__ grads, int64_t pstride,
+                                                                   int64_t o_wte) {
+  pdl_begin();
+  const int v0 = blockIdx.x * EMV, c = blockIdx.y * EMV_COLS + threadIdx.x, j = blockIdx.z, tid = threadIdx.x;
+  if (!lanes[j].active) return;
+  __shared__ float acc[EMV][EMV_COLS];
+  __shared__ int list[EMV_CHUNK];
+  __shared__ int cnt[EMV_COLS + 1];
+  for (int v = 0; v < EMV; ++v) acc[v][tid] = 0.f;
+  constexpr int PER = EMV_CHUNK / EMV_COLS;  // tokens checked per thread per chunk
+  for (int r0 = 0; r0 < N; r0 += EMV_CHUNK) {
+    int mine[PER], m = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int row = r0 + tid * PER + u;
+      int v = -1;
+      if (row < N) {
+        const int b = row / T, t = row % T;
+        v = tokens[(int64_t(j) * (N / T) + b) * (T + 1) + t] - v0;
+      }
+      mine[u] = (v >= 0 && v < EMV) ? (row << 4) | v : -1;
+      m += mine[u] >= 0;
+    }
+    __syncthreads();  // previous chunk's list fully consumed
+    cnt[tid + 1] = m;
+    if (tid == 0) cnt[0] = 0;
+    __syncthreads();
+    if (tid == 0)
+      for (int k = 1; k <= EMV_COLS; ++k) cnt[k] += cnt[k - 1];  // exclusive offsets, thread order = token order
+    __syncthreads();
+    int pos = cnt[tid];
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+      if (mine[u] >= 0) list[pos++] = mine[u];
+    __syncthreads();
+    const int total = cnt[EMV_COLS];
+    if (c < d) {
+      const float* g = dx + int64_t(j) * N * d + c;
+      int k = 0;
+      for (; k + 4 <= total; k += 4) {  // four rows in flight, added in list order
+        float val[4];
+        int vv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = list[k + q];
+          vv[q] = e & 15;
+          val[q] = g[int64_t(e >> 4) * d];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[vv[q]][tid] += val[q];
+      }
+      for (; k < total; ++k) {
+        const int e = list[k];
+        acc[e & 15][tid] += g[int64_t(e >> 4) * d];
+      }
+    }
+  }
+  if (c < d)
+    for (int v = 0; v < EMV && v0 + v < V; ++v) grads[j * pstride + o_wte + int64_t(v0 + v) * d + c] = acc[v][tid];
+}
+
 __global__ void wpe_bwd_kernel(const LaneState* __restrict__ lanes, int B, int T, int d,
                                const float* __restrict__ dx, float* __restrict__ grads,
                                int64_t pstride, int64_t o_wpe) {
@@ -532,7 +569,7 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
   add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
   // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
-  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d, N / EMB_ROWS * c.V * d,
+  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d,
                                int64_t((N + 31) / 32) * 4 * d});  // + GELU' epilogue bias partials
   b->part_st = ps;
   add(reinterpret_cast<void**>(&b->part), L * ps * 4);
@@ -549,9 +586,6 @@ int gpt_setup(Pack& p) {
   }
   p.acts = base;
   p.acts_bytes = total;
-  // dynamic smem opt-in for the token-embedding gradient (acc[V][cols] fp32)
-  TLK_CUDA(cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                200 * 1024));
   p.launches_per_step = 0;  // counted at capture (mark)
   return TLK_OK;
 }
@@ -839,15 +873,10 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     TLK_TRY(ln_bwd(b.dmm, lb.xin, lb.st1, T_LAYER(l, K_LN1G), T_LAYER(l, K_LN1B), 1, "ln1_bwd"));
   }
   {  // embeddings
-    const int cols = std::min(d, (50000 / V) / 32 * 32);  // acc[V][cols] fp32 <= 200 KB
-    const int nblk = (N + EMB_ROWS - 1) / EMB_ROWS;
-    TLK_CUDA(launch(embed_bwd_kernel, dim3(nblk, (d + cols - 1) / cols, Lc), cols, V * cols * 4, st, LS, N, d, V, cols, b.tokens, T, b.dx, b.part, b.part_st));
-    TLK_CUDA(cudaGetLastError());
-    marked("wte_partial");
-    TLK_CUDA(launch(reduce_parts_kernel, dim3((V * d + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, V * d,
-                                                                       G, PS, O(T_WTE), V * d, O(T_WTE)));
-    TLK_CUDA(cudaGetLastError());
-    marked("wte_reduce");
+    TLK_CHECK(int64_t(N) < (int64_t(1) << 27), TLK_EINVAL, "embedding gradient: %d tokens per lane", N);
+    TLK_CUDA(launch(embed_bwd_vocab_kernel, dim3((V + EMV - 1) / EMV, (d + EMV_COLS - 1) / EMV_COLS, Lc), EMV_COLS, 0,
+                    st, LS, N, d, V, b.tokens, T, b.dx, G, PS, O(T_WTE)));
+    marked("wte_grad");
     TLK_CUDA(launch(wpe_bwd_kernel, dim3(T, Lc), 128, 0, st, LS, B, T, d, b.dx, G, PS, O(T_WPE)));
     TLK_CUDA(cudaGetLastError());
     marked("wpe");
