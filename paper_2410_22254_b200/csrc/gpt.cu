@@ -165,14 +165,16 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   constexpr int d = 128 * KV;
   const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
-  extern __shared__ float red[];  // [8][2][d]
-  float4 g[KV], ag[KV], ab[KV];
+  extern __shared__ float red[];  // [8][3][d]
+  // ag / ab: dgamma / dbeta partials; ax: column sums of the stored bf16 dx
+  // (the bias gradient of the GEMM that consumes dxb next)
+  float4 g[KV], ag[KV], ab[KV], ax[KV];
   const float* gp = params + j * pstride + og;
 #pragma unroll
   for (int k = 0; k < KV; ++k) {
     const int i = 4 * (lane + 32 * k);
     g[k] = make_float4(gp[i], gp[i + 1], gp[i + 2], gp[i + 3]);
-    ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ag[k] = ab[k] = ax[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int row0 = blockIdx.x * LNB_ROWS + warp * (LNB_ROWS / 8);
   const int nrows = max(0, min(LNB_ROWS / 8, N - row0));
@@ -218,22 +220,28 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
       const float t2 = a.z + (dv.z * g[k].z - m1 - xh[k].z * m2) * cur.rstd;
       const float t3 = a.w + (dv.w * g[k].w - m1 - xh[k].w * m2) * cur.rstd;
       *reinterpret_cast<float4*>(dxt + ro + i) = make_float4(t0, t1, t2, t3);
-      *reinterpret_cast<uint2*>(dxb + ro + i) = make_uint2(pack_bf2(t0, t1), pack_bf2(t2, t3));
+      const uint32_t lo = pack_bf2(t0, t1), hi = pack_bf2(t2, t3);
+      *reinterpret_cast<uint2*>(dxb + ro + i) = make_uint2(lo, hi);
+      ax[k].x += __uint_as_float(lo << 16);
+      ax[k].y += __uint_as_float(lo & 0xffff0000u);
+      ax[k].z += __uint_as_float(hi << 16);
+      ax[k].w += __uint_as_float(hi & 0xffff0000u);
     }
     cur = nxt;
   }
 #pragma unroll
   for (int k = 0; k < KV; ++k) {
     const int i = 4 * (lane + 32 * k);
-    *reinterpret_cast<float4*>(red + (warp * 2) * d + i) = ag[k];
-    *reinterpret_cast<float4*>(red + (warp * 2 + 1) * d + i) = ab[k];
+    *reinterpret_cast<float4*>(red + (warp * 3) * d + i) = ag[k];
+    *reinterpret_cast<float4*>(red + (warp * 3 + 1) * d + i) = ab[k];
+    *reinterpret_cast<float4*>(red + (warp * 3 + 2) * d + i) = ax[k];
   }
   __syncthreads();
-  float* out = part + j * part_st + int64_t(blockIdx.x) * 2 * d;
-  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) {
+  float* out = part + j * part_st + int64_t(blockIdx.x) * 3 * d;
+  for (int i = threadIdx.x; i < 3 * d; i += blockDim.x) {
     const int f = i / d, c = i % d;
     float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += red[(w * 2 + f) * d + c];
+    for (int w = 0; w < 8; ++w) s += red[(w * 3 + f) * d + c];
     out[i] = s;
   }
 }
@@ -299,14 +307,16 @@ __global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const ui
 // dst0[c] (c < split) / dst1[c - split] = sum_blk part[lane][blk][c], fixed order
 __global__ void reduce_parts_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
                                     int64_t part_st, int nblk, int C, float* __restrict__ grads,
-                                    int64_t pstride, int64_t off0, int split, int64_t off1) {
+                                    int64_t pstride, int64_t off0, int split, int64_t off1, int split2,
+                                    int64_t off2) {
   pdl_begin();
   const int c = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (!lanes[j].active || c >= C) return;
+  if (c >= split2 && off2 < 0) return;  // third partial set without a target
   const float* p = part + j * part_st + c;
   float s = 0.f;
   for (int b = 0; b < nblk; ++b) s += p[int64_t(b) * C];
-  grads[j * pstride + (c < split ? off0 + c : off1 + (c - split))] = s;
+  grads[j * pstride + (c < split ? off0 + c : c < split2 ? off1 + (c - split) : off2 + (c - split2))] = s;
 }
 
 // Same sum over many partial rows: 8 row groups per 32 columns (group g
@@ -569,7 +579,7 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
   add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
   // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
-  const int64_t ps = std::max({N / LNB_ROWS * 2 * d, N / CS_ROWS * 4 * d,
+  const int64_t ps = std::max({(N + LNB_ROWS - 1) / LNB_ROWS * 3 * d, N / CS_ROWS * 4 * d,
                                int64_t((N + 31) / 32) * 4 * d});  // + GELU' epilogue bias partials
   b->part_st = ps;
   add(reinterpret_cast<void**>(&b->part), L * ps * 4);
@@ -730,11 +740,13 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                           op(b.xf, nd, 0, 0, 1, d, d, N), g, V, d, N, 1, 1, "head_wgrad")));
     count += 2;
   }
+  // bias_t >= 0: the stored dxb's column sums are that tensor's gradient (the
+  // bias of the GEMM that consumes dxb next)
   auto ln_bwd = [&](const float* dy, const float* x, const float* stats, int og, int ob, int accumulate,
-                    const char* name) -> int {
+                    const char* name, int bias_t) -> int {
     const int nblk = (N + LNB_ROWS - 1) / LNB_ROWS;
     const dim3 grid(nblk, Lc);
-    const size_t sm = 16 * size_t(d) * 4;
+    const size_t sm = 24 * size_t(d) * 4;
     switch (d / 128) {
       case 1:
         TLK_CUDA(launch(ln_bwd_kernel<1>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
@@ -755,8 +767,8 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     }
     TLK_CUDA(cudaGetLastError());
     marked(name);
-    TLK_CUDA(launch(reduce_parts_kernel, dim3((2 * d + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, 2 * d,
-                                                                     G, PS, O(og), d, O(ob)));
+    TLK_CUDA(launch(reduce_parts_kernel, dim3((3 * d + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, 3 * d,
+                    G, PS, O(og), d, O(ob), 2 * d, bias_t >= 0 ? O(bias_t) : int64_t(-1)));
     TLK_CUDA(cudaGetLastError());
     marked("ln_param_grads");
     return TLK_OK;
@@ -769,12 +781,12 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     TLK_CUDA(cudaGetLastError());
     marked("bias_colsum");
     TLK_CUDA(launch(reduce_parts_kernel, dim3((C + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, C, G, PS,
-                                                                   O(t), C, O(t)));
+                                                                   O(t), C, O(t), 1 << 30, int64_t(-1)));
     TLK_CUDA(cudaGetLastError());
     marked("bias_reduce");
     return TLK_OK;
   };
-  TLK_TRY(ln_bwd(b.dmm, b.xL, b.stf, tf, tf + 1, 0, "lnf_bwd"));
+  TLK_TRY(ln_bwd(b.dmm, b.xL, b.stf, tf, tf + 1, 0, "lnf_bwd", T_LAYER(c.layers - 1, K_F2B)));
 
   for (int l = c.layers - 1; l >= 0; --l) {
     LayerBufs& lb = b.L[l];
@@ -783,7 +795,6 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
                                             op(lb.f, nd4, 0, 0, 1, 4 * d, 4 * d, N), g, d, 4 * d, N, 1, 1,
                                             "fc2_wgrad")));
-      TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_F2B)));
       Epi e = epi(EPI_GELU_BWD, N, 4 * d, b.dz, nd4, 0, 0, 4 * d);
       e.aux = lb.z;
       e.colpart = b.part;  // fc.b gradient partials (per 32 rows), summed right below
@@ -807,12 +818,11 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                              d, 4 * d, 1, 1, "fc_dgrad")));
       count += 2;
     }
-    TLK_TRY(ln_bwd(b.dmm, lb.xmid, lb.st2, T_LAYER(l, K_LN2G), T_LAYER(l, K_LN2B), 1, "ln2_bwd"));
+    TLK_TRY(ln_bwd(b.dmm, lb.xmid, lb.st2, T_LAYER(l, K_LN2G), T_LAYER(l, K_LN2B), 1, "ln2_bwd", T_LAYER(l, K_PB)));
     {  // proj: dWo = dxb^T y ; dbo ; dy = dxb Wo (bf16)
       Epi g = epi(EPI_F32, d, d, G + O(T_LAYER(l, K_PW)), PS, 0, 0, d);
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
                                             op(lb.y, nd, 0, 0, 1, d, d, N), g, d, d, N, 1, 1, "proj_wgrad")));
-      TLK_TRY(bias_grad(b.dxb, d, T_LAYER(l, K_PB)));
       Epi e = epi(EPI_BF16, N, d, b.dy, nd, 0, 0, d);
       TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
                                              op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d), e, N, d, d,
@@ -870,7 +880,8 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                              3 * d, 1, 1, "qkv_dgrad")));
       count += 2;
     }
-    TLK_TRY(ln_bwd(b.dmm, lb.xin, lb.st1, T_LAYER(l, K_LN1G), T_LAYER(l, K_LN1B), 1, "ln1_bwd"));
+    TLK_TRY(ln_bwd(b.dmm, lb.xin, lb.st1, T_LAYER(l, K_LN1G), T_LAYER(l, K_LN1B), 1, "ln1_bwd",
+                   l > 0 ? T_LAYER(l - 1, K_F2B) : -1));
   }
   {  // embeddings
     TLK_CHECK(int64_t(N) < (int64_t(1) << 27), TLK_EINVAL, "embedding gradient: %d tokens per lane", N);
