@@ -277,33 +277,6 @@ __global__ void attn_rowdot_kernel(const LaneState* __restrict__ lanes, int N, i
 }
 
 // ------------------------------------------------------------- reductions --
-// part[lane][blk][c] = sum over rows [blk*64, blk*64+64) of src[row][c] (bf16);
-// a thread owns 8 consecutive columns (one 16-byte load per row)
-constexpr int CS_ROWS = 64;
-__global__ void colsum_bf16_kernel(const LaneState* __restrict__ lanes, const uint16_t* __restrict__ src,
-                                   int64_t src_ls, int ld, int N, int C, float* __restrict__ part,
-                                   int64_t part_st) {
-  pdl_begin();
-  const int cg = blockIdx.x * blockDim.x + threadIdx.x, blk = blockIdx.y, j = blockIdx.z;
-  if (!lanes[j].active || cg * 8 >= C) return;
-  const uint16_t* s = src + j * src_ls + int64_t(blk) * CS_ROWS * ld + cg * 8;
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const int rows = min(CS_ROWS, N - blk * CS_ROWS);
-#pragma unroll 8
-  for (int r = 0; r < rows; ++r) {
-    const uint4 u = *reinterpret_cast<const uint4*>(s + int64_t(r) * ld);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc[2 * e] += __uint_as_float(w[e] << 16);
-      acc[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
-    }
-  }
-  float* o = part + j * part_st + int64_t(blk) * C + cg * 8;
-  *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-}
-
 // dst0[c] (c < split) / dst1[c - split] = sum_blk part[lane][blk][c], fixed order
 __global__ void reduce_parts_kernel(const LaneState* __restrict__ lanes, const float* __restrict__ part,
                                     int64_t part_st, int nblk, int C, float* __restrict__ grads,
@@ -578,9 +551,9 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dS), L * p.batch * H * T * T * 2);
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
   add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
-  // reduction partials: max of LN (N/64 x 2d), colsum (N/128 x 4d), embed (N/256 x V x d)
-  const int64_t ps = std::max({(N + LNB_ROWS - 1) / LNB_ROWS * 3 * d, N / CS_ROWS * 4 * d,
-                               int64_t((N + 31) / 32) * 4 * d});  // + GELU' epilogue bias partials
+  // reduction partials: max of LN-backward (N/LNB_ROWS x 3d) and the GELU' / dq,dk,dv
+  // epilogue bias partials (N/32 x 4d, N/32 x 3d)
+  const int64_t ps = std::max((N + LNB_ROWS - 1) / LNB_ROWS * 3 * d, int64_t((N + 31) / 32) * 4 * d);
   b->part_st = ps;
   add(reinterpret_cast<void**>(&b->part), L * ps * 4);
   size_t total = 0;
@@ -773,19 +746,6 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     marked("ln_param_grads");
     return TLK_OK;
   };
-  auto bias_grad = [&](const uint16_t* src, int C, int t) -> int {
-    const int nblk = (N + CS_ROWS - 1) / CS_ROWS;
-    const int cgs = C / 8, th = std::min(128, (cgs + 31) / 32 * 32);
-    TLK_CUDA(launch(colsum_bf16_kernel, dim3((cgs + th - 1) / th, nblk, Lc), th, 0, st, LS, src, int64_t(N) * C, C, N, C,
-                                                                          b.part, b.part_st));
-    TLK_CUDA(cudaGetLastError());
-    marked("bias_colsum");
-    TLK_CUDA(launch(reduce_parts_kernel, dim3((C + 255) / 256, Lc), 256, 0, st, LS, b.part, b.part_st, nblk, C, G, PS,
-                                                                   O(t), C, O(t), 1 << 30, int64_t(-1)));
-    TLK_CUDA(cudaGetLastError());
-    marked("bias_reduce");
-    return TLK_OK;
-  };
   TLK_TRY(ln_bwd(b.dmm, b.xL, b.stf, tf, tf + 1, 0, "lnf_bwd", T_LAYER(c.layers - 1, K_F2B)));
 
   for (int l = c.layers - 1; l >= 0; --l) {
@@ -851,29 +811,43 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       // dq = dS K
       Epi eq = epi(EPI_BF16, T, dh, b.dqkv, nd3, int64_t(T) * 3 * d, dh, 3 * d);
       eq.causal_k = 1;
+      eq.colpart = b.part;  // qkv.b gradient partials (columns 0 ..)
+      eq.cp_ls = b.part_st;
+      eq.cp_cols = 3 * d;
+      eq.cp_col0 = 0;
       TLK_TRY((gemm<64, false, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, T, 1, T, T),
                                             op(lb.qkv + d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), eq,
                                             T, dh, T, B, H, "attn_dq")));
       // dk = dS^T Q
       Epi ek = epi(EPI_BF16, T, dh, b.dqkv + d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
       ek.causal_k = 2;  // dS^T rows = keys: queries >= key
+      ek.colpart = b.part;  // qkv.b gradient partials (columns d ..)
+      ek.cp_ls = b.part_st;
+      ek.cp_cols = 3 * d;
+      ek.cp_col0 = d;
       TLK_TRY((gemm<64, true, true, false>(p, st, op(b.dS, pl, int64_t(H) * tt, tt, 1, T, T, T),
                                            op(lb.qkv, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), ek, T,
                                            dh, T, B, H, "attn_dk")));
       // dv = P^T dY
       Epi ev = epi(EPI_BF16, T, dh, b.dqkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 3 * d);
       ev.causal_k = 2;
+      ev.colpart = b.part;  // qkv.b gradient partials (columns 2 * d ..)
+      ev.cp_ls = b.part_st;
+      ev.cp_cols = 3 * d;
+      ev.cp_col0 = 2 * d;
       TLK_TRY((gemm<64, true, true, false>(p, st, op(lb.P, pl, int64_t(H) * tt, tt, 1, T, T, T),
                                            op(b.dy, nd, int64_t(T) * d, dh, 1, d, dh, T), ev, T, dh, T, B,
                                            H, "attn_dv")));
       count += 4;
+      TLK_CUDA(launch(reduce_parts8_kernel, dim3((3 * d + 31) / 32, Lc), 256, 0, st, LS, b.part, b.part_st,
+                      (N + 31) / 32, 3 * d, G, PS, O(T_LAYER(l, K_AB))));
+      marked("bias_reduce");
     }
     {  // qkv: dWqkv = dqkv^T a ; db ; da = dqkv Wqkv (fp32)
       Epi g = epi(EPI_F32, 3 * d, d, G + O(T_LAYER(l, K_AW)), PS, 0, 0, d);
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dqkv, nd3, 0, 0, 1, 3 * d, 3 * d, N),
                                             op(lb.a, nd, 0, 0, 1, d, d, N), g, 3 * d, d, N, 1, 1,
                                             "qkv_wgrad")));
-      TLK_TRY(bias_grad(b.dqkv, 3 * d, T_LAYER(l, K_AB)));
       Epi e = epi(EPI_F32, N, d, b.dmm, nd, 0, 0, d);
       TLK_TRY((gemm_auto<false, true>(p, st, op(b.dqkv, nd3, 0, 0, 3 * d, 1, N, 3 * d),
                                              op(WB + O(T_LAYER(l, K_AW)), PS, 0, 0, 1, d, d, 3 * d), e, N, d,

@@ -46,8 +46,9 @@ struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
   float tokens;            // EPI_CE: dlogits are divided by the token count
   const float* rowvec;     // EPI_SOFTMAX_BWD: D[row] at lane*rv_ls + zb*rv_bs + zh*rv_hs + row
   int64_t rv_ls, rv_bs, rv_hs;
-  float* colpart;          // EPI_GELU_BWD (optional): column sums of the stored bf16 output per
-  int64_t cp_ls;           //   32-row block, [lane][row / 32][cols] (bias gradient partials)
+  float* colpart;          // EPI_GELU_BWD / EPI_BF16 (optional): column sums of the stored bf16
+  int64_t cp_ls;           //   output per 32-row block (bias-gradient partials):
+  int cp_cols, cp_col0;    //   [lane][(zb * rows + row) / 32][cp_cols], column cp_col0 + zh*hs + n
 };
 
 struct ZWork {
@@ -176,8 +177,12 @@ struct EpiOps {
         }
         const int64_t oo = o + k * step;
         if constexpr (KIND == EPI_BF16) {
-          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) =
-              make_uint2(pack_bf2(y0, y1), pack_bf2(y2, y3));
+          const uint32_t lo = pack_bf2(y0, y1), hi = pack_bf2(y2, y3);
+          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) = make_uint2(lo, hi);
+          cs[0] += __uint_as_float(lo << 16);
+          cs[1] += __uint_as_float(lo & 0xffff0000u);
+          cs[2] += __uint_as_float(hi << 16);
+          cs[3] += __uint_as_float(hi & 0xffff0000u);
         } else if constexpr (KIND == EPI_BF16_GELU) {
           float t;
           *reinterpret_cast<uint2*>(e.out2 + oo) = make_uint2(pack_bf2(y0, y1), pack_bf2(y2, y3));
@@ -202,7 +207,7 @@ struct EpiOps {
           cs[3] += __uint_as_float(hi & 0xffff0000u);
         }
       }
-      if constexpr (KIND == EPI_GELU_BWD) {
+      if constexpr (KIND == EPI_GELU_BWD || KIND == EPI_BF16) {
         // column sums of this warp's 32 rows of the stored (bf16) values:
         // lanes l, l+8, l+16, l+24 hold the same 4 columns (fixed xor order)
         if (e.colpart) {
@@ -211,9 +216,12 @@ struct EpiOps {
             cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 8);
             cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], 16);
           }
-          if (rsub == 0 && col_ok)
-            *reinterpret_cast<float4*>(e.colpart + w.j * e.cp_ls + int64_t(row0 >> 5) * e.cols + n) =
+          if (rsub == 0 && col_ok && row0 < e.rows) {  // rows past e.rows belong to the next z
+            const int64_t frow = int64_t(w.zb) * (e.bs / e.ld) + row0;  // row within the lane
+            const int pc = e.cp_cols ? e.cp_cols : e.cols;
+            *reinterpret_cast<float4*>(e.colpart + w.j * e.cp_ls + (frow >> 5) * pc + e.cp_col0 + w.zh * e.hs + n) =
                 make_float4(cs[0], cs[1], cs[2], cs[3]);
+          }
         }
       }
       __syncwarp();
