@@ -875,7 +875,7 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
                   p.host_input, p.params, p.stride, o_c1w, o_c1b, b));
   p.mark(st, "inputs_conv1_fwd");
   TLK_CUDA(cudaGetLastError());
-  TLK_CUDA(launch(conv2_tc_kernel<true>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<true>::SMEM, st, ca));
+  TLK_CUDA(launch(conv2_tc_kernel<true>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<true>::SMEM, st, ca));
   p.mark(st, "conv2_fwd_pool");
   TLK_CUDA(cudaGetLastError());
   Fc1Fwd f1{b, p.lane_dev};
@@ -901,7 +901,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   p.mark(wst, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
-  TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_THREADS, ConvPolicy<false>::SMEM, st, ca));
+  TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));

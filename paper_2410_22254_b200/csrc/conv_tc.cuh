@@ -39,6 +39,18 @@ struct ConvArgs {
 //   dgrad : A = dz2 patch (8 planes), B = wd, N = 32, 9 taps x 4 K-steps,
 //           tiles = 128 positions from row 1 of an image (6 per image),
 //           epilogue = ReLU mask with h1 -> dz1 (valid positions only).
+#ifndef TLK_CONV_EPW
+#define TLK_CONV_EPW 8
+#endif
+#ifndef TLK_CONV_DBG
+#define TLK_CONV_DBG 0  // bits: 1 no MMAs, 2 no epilogue work, 4 no patch loads (timing experiments only)
+#endif
+#ifndef TLK_CONV_TS
+#define TLK_CONV_TS 2
+#endif
+#ifndef TLK_CONV_AS
+#define TLK_CONV_AS 2
+#endif
 template <bool FWD>
 struct ConvPolicy {
   static constexpr int PLANES = FWD ? 4 : 8;
@@ -48,38 +60,50 @@ struct ConvPolicy {
   static constexpr int A_BYTES = PLANES * PATCH_BYTES;
   static constexpr int B_BYTES = 9 * 2 * KSTEPS * BCHUNK;  // 36864 for both
   static constexpr int TILE_BYTES = FWD ? 128 * 68 * 4 : 0;
-  static constexpr int SMEM = B_BYTES + 2 * A_BYTES + TILE_BYTES + 128;
-  static constexpr uint32_t TCOLS = 2 * N;     // two accumulators
+  static constexpr int AS = TLK_CONV_AS;         // patch stages
+  static constexpr int SMEM = B_BYTES + AS * A_BYTES + TILE_BYTES + 128;
+  static constexpr int TS = TLK_CONV_TS;         // TMEM accumulators
+  static constexpr uint32_t TCOLS = TS * N;
   TLK_DEV static int tap_off(int t) { return FWD ? tap_off_fwd(t) : tap_off_dgrad(t); }
   TLK_DEV static int64_t tile_p0(int tile) {   // first position of the tile
     const int b = tile / 6, k = tile % 6;
     return P28_FRONT + int64_t(b) * P28_IMG + (FWD ? (2 + 4 * k) * P28 : P28 + 128 * k);
   }
 };
-constexpr int CONV_CTAS_PER_LANE = 36;
-constexpr int CONV_THREADS = 192;
+#ifndef TLK_CONV_CTAS
+#define TLK_CONV_CTAS 36
+#endif
+constexpr int CONV_CTAS_PER_LANE = TLK_CONV_CTAS;
+constexpr int CONV_THREADS = 192;  // conv2 wgrad: 4 epilogue + producer + MMA warps
+// conv2 fwd / dgrad: EPW epilogue warps (two per TMEM lane quarter when 8,
+// each owning half of the accumulator columns), then producer and MMA warps
+
+constexpr int CONV_EPW = TLK_CONV_EPW;
+constexpr int CONV_FD_THREADS = 32 * (CONV_EPW + 2);
+static_assert(CONV_EPW == 4 || CONV_EPW == 8, "conv2 epilogue warps");
 
 template <bool FWD>
-__global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
-  pdl_begin();
+__global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
   using P = ConvPolicy<FWD>;
   const int j = blockIdx.y;
   if (!a.lanes[j].active) return;
   const int ntiles = a.B * 6;
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t wfull, afull[2], aempty[2], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t wfull, afull[P::AS], aempty[P::AS], tfull[P::TS], tempty[P::TS];
   __shared__ uint32_t tmem_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sB = smem_u32(sm), sA0 = sB + P::B_BYTES;
-  float* tileS = reinterpret_cast<float*>(sm + P::B_BYTES + 2 * P::A_BYTES);
+  float* tileS = reinterpret_cast<float*>(sm + P::B_BYTES + P::AS * P::A_BYTES);
 
   if (tid == 0) {
     mbar_init(&wfull, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < P::AS; ++s) {
       mbar_init(&afull[s], 1);
       mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < P::TS; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], CONV_EPW);  // one arrive per epilogue warp
     }
     fence_mbar_init();
   }
@@ -87,38 +111,45 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_begin();  // barrier init / TMEM allocation overlap the previous kernel's flush
   const uint32_t tmem = tmem_s;
   const uint16_t* src = FWD ? a.h1 + int64_t(j) * 4 * a.npos * 8 : a.dz2 + int64_t(j) * 8 * a.npos * 8;
 
-  if (warp == 4) {  // ---------------- TMA producer
+  constexpr int CH = CONV_EPW / 4;  // column halves per lane quarter
+  if (warp == CONV_EPW) {  // ---------------- TMA producer
     if (lane == 0) {
       const uint16_t* w = a.wt + int64_t(j) * a.wt_stride + (FWD ? 0 : CONV2_W);
       mbar_expect_tx(&wfull, P::B_BYTES);
       for (int t = 0; t < 9; ++t) tma_bulk_g2s(sB + t * 4096, w + t * 2048, 4096, &wfull);
       int i = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-        const int s = i & 1;
-        if (i >= 2) mbar_wait(&aempty[s], ((i >> 1) - 1) & 1);
+        const int s = i % P::AS;
+        if (i >= P::AS) mbar_wait(&aempty[s], ((i / P::AS) - 1) & 1);
         const int64_t p0 = P::tile_p0(tile);
+#if TLK_CONV_DBG & 4
+        mbar_arrive(&afull[s]);
+        (void)p0;
+#else
         mbar_expect_tx(&afull[s], P::A_BYTES);
         for (int c = 0; c < P::PLANES; ++c)
           tma_bulk_g2s(sA0 + s * P::A_BYTES + c * PATCH_BYTES, src + (c * a.npos + p0 - HALO) * 8,
                        PATCH_BYTES, &afull[s]);
+#endif
       }
     }
-  } else if (warp == 5) {  // ---------------- MMA issuer
+  } else if (warp == CONV_EPW + 1) {  // ---------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t IDESC = umma_idesc_bf16(128, P::N, false, false);
       const uint64_t bd0 = umma_desc_interleave(sB, P::BCHUNK, 128);
       mbar_wait(&wfull, 0);
       int i = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-        const int s = i & 1;
-        mbar_wait(&afull[s], (i >> 1) & 1);
-        if (i >= 2) mbar_wait(&tempty[s], ((i >> 1) - 1) & 1);
+        const int s = i % P::AS, ts = i % P::TS;
+        mbar_wait(&afull[s], (i / P::AS) & 1);
+        if (i >= P::TS) mbar_wait(&tempty[ts], ((i / P::TS) - 1) & 1);
         tc_fence_after();
         const uint64_t ad0 = umma_desc_interleave(sA0 + s * P::A_BYTES + HALO * 16, PATCH_BYTES, 128);
-        const uint32_t d = tmem + s * P::N;
+        const uint32_t d = tmem + ts * P::N;
 #pragma unroll 1
         for (int t = 0; t < 9; ++t) {
           const int toff = P::tap_off(t);
@@ -127,25 +158,54 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
             // descriptor start field is address >> 4: offsets add directly
             const uint64_t ad = ad0 + uint64_t((2 * k * PATCH_BYTES + toff * 16) >> 4);
             const uint64_t bd = bd0 + uint64_t(((t * 2 * P::KSTEPS + 2 * k) * P::BCHUNK) >> 4);
+#if !(TLK_CONV_DBG & 1)
             mma_bf16(d, ad, bd, IDESC, (t | k) ? 1u : 0u);
+#endif
           }
         }
         mma_commit(&aempty[s]);
-        mma_commit(&tfull[s]);
+        mma_commit(&tfull[ts]);
       }
     }
-  } else {  // ---------------- epilogue warps 0..3 (TMEM lanes 32w..32w+31)
-    const int row = warp * 32 + lane;
+  } else {  // ---------------- epilogue warps (TMEM lanes 32q..32q+31, column half hh)
+    const int q4 = warp & 3, hh = warp >> 2;
+    const int row = q4 * 32 + lane;
+    // dgrad: the h1 ReLU-mask rows of a tile are fetched one tile ahead
+    constexpr int NPL = 4 / CH;  // h1 / dz1 planes (8 channels each) of a dgrad warp
+    const int c0 = hh * NPL;
+    const int64_t hbase = int64_t(j) * 4 * a.npos * 8;
+    auto h1_valid = [&](int64_t p0) {
+      const int r = int(p0 - P28_FRONT) % P28_IMG + row;  // position within the image
+      const int pr = r / P28, pc = r % P28;
+      return pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26;
+    };
+    auto h1_fetch = [&](int tile, uint4 (&hv)[NPL]) {
+      const int64_t p0 = P::tile_p0(tile);
+      const bool ok = tile < ntiles && h1_valid(p0);
+#pragma unroll
+      for (int c = 0; c < NPL; ++c)
+        hv[c] = ok ? *reinterpret_cast<const uint4*>(a.h1 + hbase + ((c0 + c) * a.npos + p0 + row) * 8)
+                   : make_uint4(0, 0, 0, 0);
+    };
+    uint4 hnext[NPL];
+    if constexpr (!FWD) h1_fetch(blockIdx.x, hnext);
+    // fwd: a thread's pooled items all have channel chunk tid & 7 (stride 32 * EPW)
+    float bb[8];
+    if constexpr (FWD) {
+      const float* bias = a.params + j * a.pstride + a.b2_off + (tid & 7) * 8;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) bb[e] = bias[e];
+    }
     int i = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-      const int s = i & 1;
-      const uint32_t taddr = tmem + s * P::N + (uint32_t(warp * 32) << 16);
+      const int s = i % P::TS;
+      const uint32_t taddr = tmem + s * P::N + (uint32_t(q4 * 32) << 16);
       const int64_t p0 = P::tile_p0(tile);
       if constexpr (FWD) {
-        mbar_wait(&tfull[s], (i >> 1) & 1);
+        mbar_wait(&tfull[s], (i / P::TS) & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
+        for (int cc = hh; cc < 2; cc += CH) {
           float v[32];
           tmem_ld32(taddr + cc * 32, v);
 #pragma unroll
@@ -156,15 +216,12 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 32 * CONV_EPW);
         const int b = tile / 6, ti = tile % 6;
-        const float* bias = a.params + j * a.pstride + a.b2_off;
-        for (int it = tid; it < 192; it += 128) {
+        for (int it = tid; it < ((TLK_CONV_DBG & 2) ? 0 : 192); it += 32 * CONV_EPW) {
           const int ch = it & 7, pw = (it >> 3) % 12, phl = (it >> 3) / 12;
-          float mx[8], bb[8];
+          float mx[8];
           int arg[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) bb[e] = bias[ch * 8 + e];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int m = (2 * phl + (q >> 1)) * P28 + 2 + 2 * pw + (q & 1);
@@ -193,29 +250,26 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
           *reinterpret_cast<uint4*>(a.p2 + o) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
           *reinterpret_cast<uint2*>(a.idx + o) = make_uint2(i0, i1);
         }
-        named_bar_sync(1, 128);  // tile buffer free for the next tile
+        named_bar_sync(1, 32 * CONV_EPW);  // tile buffer free for the next tile
       } else {
-        // h1 (ReLU mask) of this row: loaded before the accumulator is ready
-        const int r = int(p0 - P28_FRONT) % P28_IMG + row;  // position within the image
-        const int pr = r / P28, pc = r % P28;
-        const bool valid = pr >= 1 && pr <= 26 && pc >= 1 && pc <= 26;
+        const bool valid = h1_valid(p0);
         const int64_t pos = p0 + row;
-        const int64_t base = int64_t(j) * 4 * a.npos * 8;
-        uint4 hv[4];
+        const int64_t base = hbase;
+        uint4 hv[NPL];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          hv[c] = valid ? *reinterpret_cast<const uint4*>(a.h1 + base + (c * a.npos + pos) * 8)
-                        : make_uint4(0, 0, 0, 0);
-        mbar_wait(&tfull[s], (i >> 1) & 1);
+        for (int c = 0; c < NPL; ++c) hv[c] = hnext[c];
+        h1_fetch(tile + gridDim.x, hnext);  // in flight during this tile's wait and stores
+        mbar_wait(&tfull[s], (i / P::TS) & 1);
         tc_fence_after();
-        float v[32];
-        tmem_ld32(taddr, v);
+        float v[8 * NPL];
+        if constexpr (NPL == 4) tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(v));
+        else tmem_ld16(taddr + 8 * c0, *reinterpret_cast<float(*)[16]>(v));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
-        if (valid) {
+        if (!(TLK_CONV_DBG & 2) && valid) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < NPL; ++c) {
             const uint32_t hw[4] = {hv[c].x, hv[c].y, hv[c].z, hv[c].w};
             uint32_t ow[4];
 #pragma unroll
@@ -224,7 +278,7 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_tc_kernel(ConvArgs a) {
               const float hi = bf2f(uint16_t(hw[e] >> 16)) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f;
               ow[e] = pack_bf2(lo, hi);
             }
-            *reinterpret_cast<uint4*>(a.dz1 + base + (c * a.npos + pos) * 8) =
+            *reinterpret_cast<uint4*>(a.dz1 + base + ((c0 + c) * a.npos + pos) * 8) =
                 make_uint4(ow[0], ow[1], ow[2], ow[3]);
           }
         }
@@ -262,7 +316,6 @@ constexpr int WG_SMEM = WG_STAGES * WG_STAGE + 128;
 constexpr uint32_t WG_TX = 12 * WG_ACOPY + WG_B_BYTES;
 
 __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
-  pdl_begin();
   const int split = blockIdx.x, j = blockIdx.y;
   if (!a.lanes[j].active) return;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -286,6 +339,7 @@ __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_begin();
   const uint32_t tmem = tmem_s;
 
   if (warp == 4) {  // ---------------- TMA producer

@@ -219,7 +219,6 @@ TLK_DEV uint64_t stage_desc_tma(uint32_t base, int kk) {
 template <class P>
 __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
     tc_gemm_tma_kernel(const __grid_constant__ P p) {
-  pdl_begin();
   constexpr int BN = P::BN;
   constexpr int STAGES = P::STAGES;
   using S = GemmSmem<P>;
@@ -247,6 +246,7 @@ __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_begin();  // barrier init / TMEM allocation above touch no upstream data
   const uint32_t tmem = tmem_base_s;
   const int nk = w.kb_end - w.kb_begin;
   if (warp == 0 && lane == 0) {  // producer
