@@ -897,9 +897,31 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     TLK_CUDA(cudaStreamWaitEvent(p.side, p.ev_fork, 0));
     wst = p.side;
   }
+  // fc1 wgrad + Adam (HBM-bound) needs only dz3 / p2 and must follow the fc1
+  // dgrad (which reads this step's fc1 weights).  It runs on the side branch
+  // after the conv2 wgrad, next to the latency-bound conv2 dgrad -> conv1
+  // wgrad chain, on 96 of the 148 SMs (TLK_FWA_CTAS) so that the chain keeps
+  // SMs of its own.  TLK_CNN_FWA_SIDE: 0 = main stream after the join (one
+  // CTA per SM), 1 = side branch after conv2 wgrad (default), 2 = before it.
+  static const int fwa_side = getenv("TLK_CNN_FWA_SIDE") ? atoi(getenv("TLK_CNN_FWA_SIDE")) : 1;
+  static const int fwa_ctas = getenv("TLK_FWA_CTAS") ? atoi(getenv("TLK_FWA_CTAS")) : 0;
+  auto enqueue_fwa = [&](cudaStream_t s2) -> int {
+    Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, p.lane_dev, p.params, p.mom1, p.mom2, p.grads, p.wbf,
+                   p.stride, o_f1w,
+                   (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0, (B + GEMM_BK - 1) / GEMM_BK, L * FWA_FT};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ctas = fwa_ctas > 0 ? std::min(fwa_ctas, sms) : s2 != st ? sms * 96 / 148 : sms;
+    TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(std::min(ctas, L * FWA_FT)), FWA_THREADS, FWA_SMEM, s2, f));
+    p.mark(s2, "fc1_wgrad_adam");
+    return TLK_OK;
+  };
+  if (fwa_side == 2 && wst != st && (rc = enqueue_fwa(wst))) return rc;
   TLK_CUDA(launch(conv2_wgrad_tc_kernel, dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, wst, ca));
   p.mark(wst, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
+  if (fwa_side == 1 && wst != st && (rc = enqueue_fwa(wst))) return rc;
   if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
@@ -908,16 +930,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (wst != st) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
-  {
-    Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, p.lane_dev, p.params, p.mom1, p.mom2, p.grads, p.wbf,
-                   p.stride, o_f1w,
-                   (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0, (B + GEMM_BK - 1) / GEMM_BK, L * FWA_FT};
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(std::min(sms, L * FWA_FT)), FWA_THREADS, FWA_SMEM, st, f));
-  }
-  p.mark(st, "fc1_wgrad_adam");
+  if (!(fwa_side && wst != st) && (rc = enqueue_fwa(st))) return rc;
   {
     const CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
                    reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),

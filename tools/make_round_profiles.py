@@ -19,6 +19,7 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 # capture name -> (model, bench.py kernel label)
 CAPS = {"c_fc1_wgrad_adam": ("cnn", "fc1_wgrad_adam"), "c_conv2_fwd": ("cnn", "conv2_fwd_pool"),
+        "c_conv2_dgrad": ("cnn", "conv2_dgrad"),
         "c_conv2_wgrad": ("cnn", "conv2_wgrad"), "c_fc1_dgrad": ("cnn", "fc1_dgrad_unpool"),
         "c_cnn_opt": ("cnn", "grad_finalize_opt"), "c_cnn_head": ("cnn", "fc1_reduce_head"), "r_fwd_l1_halo": ("resnet18", "conv_fwd"),
         "r_dgrad_l1_halo": ("resnet18", "conv_dgrad"), "r_wgrad_l1_tg": ("resnet18", "conv_wgrad"),

@@ -23,8 +23,9 @@ cap() {  # name regex skip command...
 B="python bench.py --steps 3 --warmup 3 --no-baselines --no-sweep --profile-iters 1"
 cap c_fc1_wgrad_adam fc1_wgrad_adam 5 $B
 cap c_conv2_fwd conv2_tc_kernel 10 $B
+cap c_conv2_dgrad conv2_tc_kernel 11 $B
 cap c_conv2_wgrad conv2_wgrad_tc 5 $B
-cap c_fc1_dgrad Fc1Dgrad 5 $B
+cap c_fc1_dgrad tc_gemm_tma_kernel 5 $B
 cap c_cnn_opt cnn_opt 5 $B
 cap c_cnn_head cnn_head 5 $B
 R="python tools/pack_step.py resnet18 8 128 1"
