@@ -425,6 +425,11 @@ def packed_arm(a, world, rank, local):
                 "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                 "algorithmic_per_launch": work, "ms_per_launch": top_ms,
                 "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
+    # the profile step serialises the kernels on one stream (no graph
+    # branches): a kernel that runs on a side branch in the step graph (CNN
+    # fc1 wgrad+Adam: 96 CTAs next to the conv2 dgrad chain) is timed alone here
+    roof["timing"] = ("CUDA events around each kernel of a serial (unforked) profile step, "
+                      "mean of %d; kernels at their serial-mode grids" % a.profile_iters)
     try:  # dram bytes of this kernel from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(MODEL, {}).get(top_name)
         if tr:
