@@ -133,7 +133,10 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
  * only for step k-2, so it overlaps step k-1's kernels.  pixels / labels must
  * stay valid (and should be pinned) until the copy is done, losses_out until
  * tlk_step_host_wait(ticket) returns; only the two newest tickets can be
- * waited on.  Do not interleave with tlk_step_host without waiting first. */
+ * waited on.  The step writes its losses into mapped pinned host memory (one
+ * slot per input slot, no D2H copy in the stream); tlk_step_host_wait copies
+ * them into losses_out.  Do not interleave with tlk_step_host without
+ * waiting first. */
 int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
                         float* losses_out, int64_t* ticket);
 int tlk_step_host_wait(tlk_ctx* ctx, int32_t pack, int64_t ticket);

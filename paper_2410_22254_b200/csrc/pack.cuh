@@ -56,8 +56,13 @@ struct Pack {
   // the step graph captured against it, a copy stream, per-slot events
   uint8_t* px_alt = nullptr;
   int32_t* lb_alt = nullptr;
-  cudaGraph_t hgraph_alt = nullptr;
-  cudaGraphExec_t hexec_alt = nullptr;
+  cudaGraph_t hgraph_alt = nullptr, hgraph0 = nullptr;
+  cudaGraphExec_t hexec_alt = nullptr, hexec0 = nullptr;
+  // per-slot losses written by the head kernel straight into mapped pinned
+  // host memory (no D2H copy in the step); copied to the caller's buffer
+  // by tlk_step_host_wait
+  float* ll_host = nullptr;  // [2][lanes]
+  float* hout[2] = {nullptr, nullptr};
   cudaStream_t copy_st = nullptr;
   cudaEvent_t h2d_ev[2] = {nullptr, nullptr}, done_ev[2] = {nullptr, nullptr};
   int64_t host_steps = 0;

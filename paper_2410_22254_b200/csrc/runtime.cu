@@ -73,6 +73,9 @@ void destroy_pack(Pack& p) {
   }
   if (p.hexec_alt) cudaGraphExecDestroy(p.hexec_alt);
   if (p.hgraph_alt) cudaGraphDestroy(p.hgraph_alt);
+  if (p.hexec0) cudaGraphExecDestroy(p.hexec0);
+  if (p.hgraph0) cudaGraphDestroy(p.hgraph0);
+  if (p.ll_host) cudaFreeHost(p.ll_host);
   if (p.side) cudaStreamDestroy(p.side);
   if (p.ev_fork) cudaEventDestroy(p.ev_fork);
   if (p.ev_join) cudaEventDestroy(p.ev_join);
@@ -135,11 +138,21 @@ int ensure_host_pipeline(Pack& p, cudaStream_t st) {
   p.px_alt = static_cast<uint8_t*>(v);
   if ((rc = pack_alloc(p, &v, L * B * 4))) return rc;
   p.lb_alt = static_cast<int32_t*>(v);
-  std::swap(p.pixels, p.px_alt);
-  std::swap(p.labels, p.lb_alt);
-  rc = capture_step(p, st, &p.hgraph_alt, &p.hexec_alt);
-  std::swap(p.pixels, p.px_alt);
-  std::swap(p.labels, p.lb_alt);
+  TLK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p.ll_host), 2 * L * 4, cudaHostAllocMapped));
+  float* ll_dev = nullptr;
+  TLK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ll_dev), p.ll_host, 0));
+  float* const last_loss = p.last_loss;
+  p.last_loss = ll_dev;  // slot 0: device inputs of the regular graph, losses to host slot 0
+  rc = capture_step(p, st, &p.hgraph0, &p.hexec0);
+  if (!rc) {
+    p.last_loss = ll_dev + L;
+    std::swap(p.pixels, p.px_alt);
+    std::swap(p.labels, p.lb_alt);
+    rc = capture_step(p, st, &p.hgraph_alt, &p.hexec_alt);
+    std::swap(p.pixels, p.px_alt);
+    std::swap(p.labels, p.lb_alt);
+  }
+  p.last_loss = last_loss;
   if (rc) return rc;
   TLK_CUDA(cudaStreamCreateWithFlags(&p.copy_st, cudaStreamNonBlocking));
   for (int k = 0; k < 2; ++k) {
@@ -441,9 +454,9 @@ int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const
   TLK_CUDA(cudaMemcpyAsync(s ? p->lb_alt : p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->copy_st));
   TLK_CUDA(cudaEventRecord(p->h2d_ev[s], p->copy_st));
   TLK_CUDA(cudaStreamWaitEvent(ctx->stream, p->h2d_ev[s], 0));
-  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->graph_exec, ctx->stream));
-  TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, L * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->hexec0, ctx->stream));
   TLK_CUDA(cudaEventRecord(p->done_ev[s], ctx->stream));
+  p->hout[s] = losses_out;  // filled from the mapped slot by tlk_step_host_wait
   *ticket = p->host_steps++;
   return TLK_OK;
 }
@@ -454,7 +467,15 @@ int tlk_step_host_wait(tlk_ctx* ctx, int32_t pack, int64_t ticket) {
   if (rc) return rc;
   TLK_CHECK(ticket >= 0 && ticket < p->host_steps && ticket + 2 >= p->host_steps, TLK_EINVAL,
             "ticket %lld is not one of the two newest host steps", (long long)ticket);
-  TLK_CUDA(cudaEventSynchronize(p->done_ev[ticket & 1]));
+  const int s = int(ticket & 1);
+  TLK_CUDA(cudaEventSynchronize(p->done_ev[s]));
+  // the step's head kernel wrote the losses into mapped host slot s (visible
+  // once the step has completed); slot s is next written by step ticket + 2,
+  // which cannot have been enqueued while this ticket is still waitable
+  if (p->hout[s]) {
+    std::memcpy(p->hout[s], p->ll_host + size_t(s) * p->lanes, size_t(p->lanes) * 4);
+    p->hout[s] = nullptr;
+  }
   return TLK_OK;
 }
 
