@@ -9,7 +9,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = "/root/reference/pkg/src"
-CAL = os.path.join(ROOT, "profiles", "r1d_sim_calibration_cnn.json")
+CAL = os.path.join(ROOT, "profiles", "r1h_sim_calibration_cnn.json")
 
 
 def test_calibration_is_monotone_and_sublinear():
