@@ -39,7 +39,10 @@ constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
 #endif
 constexpr int C2W_SPLITS = TLK_C2W_SPLITS;  // conv2 wgrad position splits per lane
 constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
-constexpr int C1W_THREADS = 256;            // 8 warps per image: the per-SM warp count hides latency
+#ifndef TLK_C1W_THREADS
+#define TLK_C1W_THREADS 256
+#endif
+constexpr int C1W_THREADS = TLK_C1W_THREADS;  // 8 warps per image: the per-SM warp count hides latency
 constexpr int CNN_OPT_CTAS = 24;  // per lane: ~5.4k float4 of non-fc1.w parameters (~1 per thread)
 
 struct CnnBufs {
