@@ -33,7 +33,11 @@
 namespace tlk {
 namespace {
 
-constexpr int FC1_SPLITS = 18;     // 144 k-blocks / 8
+#ifndef TLK_FC1_SPLITS
+#define TLK_FC1_SPLITS 18
+#endif
+constexpr int FC1_SPLITS = TLK_FC1_SPLITS;  // split-K of the fc1 forward (144 k-blocks / 8)
+static_assert(144 % FC1_SPLITS == 0, "fc1 split-K must divide the 144 k-blocks");
 #ifndef TLK_C2W_SPLITS
 #define TLK_C2W_SPLITS 18
 #endif
