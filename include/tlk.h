@@ -87,6 +87,9 @@ typedef struct {
                                       into a wgrad epilogue (tests/inspection) */
 #define TLK_PACK_SNAPSHOTS 2       /* keep per-layer copies of intermediate gradients
                                       (layer-local parity tests; ResNet packs) */
+#define TLK_PACK_OWN_STREAM 4      /* the pack gets its own CUDA stream (tlk_pack_stream), so
+                                      packs of different models on one GPU run concurrently;
+                                      default: the context stream */
 
 typedef struct {
   int64_t param_count;   /* real parameters per job */
@@ -112,12 +115,26 @@ int tlk_model_tensor(int32_t model, int32_t t, int64_t* offset, int64_t* count, 
 /* -- context: one per GPU (replaces one CUDA context per child process) ---- */
 int tlk_open(int32_t device, tlk_ctx** out);
 int tlk_close(tlk_ctx* ctx);
+/* waits for the context stream and every pack stream */
 int tlk_sync(tlk_ctx* ctx);
+/* Admission budget for pack memory on this context (0 = device memory only).
+ * A pack allocation that would exceed it fails with TLK_EOOM ("out of
+ * memory"), like a device allocation failure: the host admits tasks against
+ * it (the reference simulator's per-device capacity, sim.py:388-402). */
+int tlk_set_mem_limit(tlk_ctx* ctx, int64_t bytes);
+/* bytes currently held by the context's live packs */
+int tlk_mem_in_use(tlk_ctx* ctx, int64_t* bytes);
 /* the context's CUDA stream (cudaStream_t), for event timing by the host */
 int tlk_stream(tlk_ctx* ctx, void** stream);
 
 /* -- packs: K lanes of one model ------------------------------------------ */
 int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id);
+/* Free every device resource of a pack (waits for its stream first); the id
+ * becomes invalid.  The reference frees a task's GPU memory when its process
+ * exits; the packed host destroys a pack once none of its lanes is in use. */
+int tlk_pack_destroy(tlk_ctx* ctx, int32_t pack);
+/* the stream the pack's work is enqueued on (cudaStream_t) */
+int tlk_pack_stream(tlk_ctx* ctx, int32_t pack, void** stream);
 /* (Re)load a lane with a task: device-side init of weights/state from seed.
  * Replaces spawning the task's process (executor.py:199 -> _spawn). */
 int tlk_lane_load(tlk_ctx* ctx, int32_t pack, int32_t lane, const tlk_job_desc* job);

@@ -43,6 +43,7 @@ DEFAULTS = {
     "node_index": 0,
     "backend": "subprocess",
     "chunk": 64,
+    "admit_mem": False,
     "provider": "none",
     "interval": 1.0,
     "query_cmd": os.environ.get(QUERY_CMD_ENV, DEFAULT_QUERY_COMMAND),
@@ -85,6 +86,8 @@ def _parser():
     p.add_argument("--timeout", type=float)
     p.add_argument("--backend", choices=BACKENDS)
     p.add_argument("--chunk", type=int, help="packed backend: steps per graph-replay chunk")
+    p.add_argument("--admit-mem", action="store_true", default=None,
+                   help="packed backend: admit tasks against --gpu-mem MiB per GPU (per-task OOM)")
     p.add_argument("--provider", choices=("none", "host", "command", "const", "nvml"),
                    help="telemetry source while executing (telemetry.csv)")
     p.add_argument("--query-cmd", help=f"device query command for --provider command (or {QUERY_CMD_ENV})")
@@ -211,7 +214,11 @@ def _mode_exec(s):
         sampler.start()
     t = s.get("timeout")
     backend = s.get("backend")
-    opts = {"chunk": int(s.get("chunk"))} if backend == "packed" else None
+    opts = None
+    if backend == "packed":
+        opts = {"chunk": int(s.get("chunk"))}
+        if s.get("admit_mem"):
+            opts["mem_limit_mib"] = node.gpu_mem_mib
     try:
         report = run_plan(plan, ni, timeout_s=float(t) if t is not None else None, log_dir=d / "logs",
                           backend=backend, packed_options=opts)

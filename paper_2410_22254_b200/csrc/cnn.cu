@@ -42,6 +42,9 @@ static_assert(144 % FC1_SPLITS == 0, "fc1 split-K must divide the 144 k-blocks")
 #define TLK_C2W_SPLITS 18
 #endif
 constexpr int C2W_SPLITS = TLK_C2W_SPLITS;  // conv2 wgrad position splits per lane
+// every split needs >= 1 of the B * 784 / 128 position chunks (49 at the
+// smallest batch, 8): an empty split would commit no MMA and write stale TMEM
+static_assert(C2W_SPLITS >= 1 && C2W_SPLITS <= 49, "conv2 wgrad splits must be in [1, 49]");
 constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
 #ifndef TLK_C1W_THREADS
 #define TLK_C1W_THREADS 256

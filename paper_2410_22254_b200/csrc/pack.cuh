@@ -40,8 +40,16 @@ struct Pack {
   size_t acts_bytes = 0;
   uint16_t* wt = nullptr;       // transposed bf16 weight copies (model specific)
   int64_t wt_stride = 0;
-  // all device allocations of this pack, freed on destroy
+  // all device allocations of this pack, freed on destroy; their bytes are
+  // charged to the owning context's budget (tlk_set_mem_limit)
   std::vector<void*> allocs;
+  size_t alloc_bytes = 0;
+  int64_t* ctx_in_use = nullptr;  // the context's running total
+  int64_t ctx_limit = 0;          // 0 = no budget (device memory only)
+  // the stream this pack's work is enqueued on: the context stream, or its
+  // own (TLK_PACK_OWN_STREAM) so packs of different models run concurrently
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
   // CUDA graph of one step
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;

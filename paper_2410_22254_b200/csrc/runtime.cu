@@ -42,13 +42,21 @@ bool pdl_enabled() {
 }
 
 int pack_alloc(Pack& p, void** ptr, size_t bytes) {
-  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+  if (!bytes) bytes = 16;
+  if (p.ctx_in_use && p.ctx_limit > 0 && *p.ctx_in_use + int64_t(bytes) > p.ctx_limit)
+    return fail(TLK_EOOM,
+                "out of memory: pack allocation of %zu bytes exceeds the context budget "
+                "(%lld of %lld bytes in use)",
+                bytes, (long long)*p.ctx_in_use, (long long)p.ctx_limit);
+  cudaError_t e = cudaMalloc(ptr, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(TLK_EOOM, "out of memory: pack allocation of %zu bytes failed (%s)", bytes,
                 cudaGetErrorString(e));
   }
   p.allocs.push_back(*ptr);
+  p.alloc_bytes += bytes;
+  if (p.ctx_in_use) *p.ctx_in_use += int64_t(bytes);
   return TLK_OK;
 }
 
@@ -60,7 +68,9 @@ struct tlk_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int8_t* teacher = nullptr;
-  std::vector<std::unique_ptr<Pack>> packs;
+  std::vector<std::unique_ptr<Pack>> packs;  // destroyed packs leave a null entry (ids stay stable)
+  int64_t mem_in_use = 0;  // bytes held by live packs
+  int64_t mem_limit = 0;   // admission budget (0 = device memory only)
 };
 
 namespace {
@@ -83,6 +93,10 @@ void destroy_pack(Pack& p) {
   if (p.graph) cudaGraphDestroy(p.graph);
   for (void* a : p.allocs) cudaFree(a);
   p.allocs.clear();
+  if (p.ctx_in_use) *p.ctx_in_use -= int64_t(p.alloc_bytes);
+  p.alloc_bytes = 0;
+  if (p.own_stream && p.stream) cudaStreamDestroy(p.stream);
+  p.stream = nullptr;
   if (p.scratch && p.scratch_free) p.scratch_free(p.scratch);
   p.scratch = nullptr;
 }
@@ -164,7 +178,7 @@ int ensure_host_pipeline(Pack& p, cudaStream_t st) {
 
 int upload_lane(tlk_ctx* ctx, Pack& p, int lane) {
   TLK_CUDA(cudaMemcpyAsync(p.lane_dev + lane, &p.lane_host[lane], sizeof(LaneState),
-                           cudaMemcpyHostToDevice, ctx->stream));
+                           cudaMemcpyHostToDevice, p.stream));
   return TLK_OK;
 }
 
@@ -248,7 +262,10 @@ int tlk_close(tlk_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->packs)
-    if (p) destroy_pack(*p);
+    if (p) {
+      cudaStreamSynchronize(p->stream);
+      destroy_pack(*p);
+    }
   if (ctx->teacher) cudaFree(ctx->teacher);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -259,6 +276,43 @@ int tlk_sync(tlk_ctx* ctx) {
   TLK_CHECK(ctx, TLK_EINVAL, "null context");
   TLK_CUDA(cudaSetDevice(ctx->device));
   TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& p : ctx->packs)
+    if (p && p->own_stream) TLK_CUDA(cudaStreamSynchronize(p->stream));
+  return TLK_OK;
+}
+
+int tlk_set_mem_limit(tlk_ctx* ctx, int64_t bytes) {
+  TLK_CHECK(ctx && bytes >= 0, TLK_EINVAL, "bad arguments");
+  ctx->mem_limit = bytes;
+  for (auto& p : ctx->packs)
+    if (p) p->ctx_limit = bytes;
+  return TLK_OK;
+}
+
+int tlk_mem_in_use(tlk_ctx* ctx, int64_t* bytes) {
+  TLK_CHECK(ctx && bytes, TLK_EINVAL, "null argument");
+  *bytes = ctx->mem_in_use;
+  return TLK_OK;
+}
+
+int tlk_pack_destroy(tlk_ctx* ctx, int32_t pack) {
+  TLK_CHECK(ctx, TLK_EINVAL, "null context");
+  TLK_CHECK(pack >= 0 && pack < int32_t(ctx->packs.size()) && ctx->packs[pack], TLK_EINVAL,
+            "bad pack id %d", pack);
+  TLK_CUDA(cudaSetDevice(ctx->device));
+  Pack& p = *ctx->packs[pack];
+  TLK_CUDA(cudaStreamSynchronize(p.stream));
+  destroy_pack(p);
+  ctx->packs[pack].reset();
+  return TLK_OK;
+}
+
+int tlk_pack_stream(tlk_ctx* ctx, int32_t pack, void** stream) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(stream, TLK_EINVAL, "null argument");
+  *stream = p->stream;
   return TLK_OK;
 }
 
@@ -310,6 +364,14 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
     p->stride = mi.param_stride;
   }
   p->teacher = ctx->teacher;
+  p->ctx_in_use = &ctx->mem_in_use;
+  p->ctx_limit = ctx->mem_limit;
+  if (desc->flags & TLK_PACK_OWN_STREAM) {
+    TLK_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  } else {
+    p->stream = ctx->stream;
+  }
   const size_t L = size_t(p->lanes), S = size_t(p->stride), B = size_t(p->batch);
   int rc = 0;
   void* v = nullptr;
@@ -348,11 +410,11 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   p->lane_host.assign(L, LaneState{});
-  TLK_CUDA(cudaMemsetAsync(p->lane_dev, 0, L * sizeof(LaneState), ctx->stream));
-  TLK_CUDA(cudaMemsetAsync(p->loss, 0, L * size_t(p->max_steps) * 4, ctx->stream));
-  TLK_CUDA(cudaMemsetAsync(p->params, 0, L * S * 4, ctx->stream));
-  TLK_CUDA(cudaMemsetAsync(p->grads, 0, L * S * 4, ctx->stream));
-  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  TLK_CUDA(cudaMemsetAsync(p->lane_dev, 0, L * sizeof(LaneState), p->stream));
+  TLK_CUDA(cudaMemsetAsync(p->loss, 0, L * size_t(p->max_steps) * 4, p->stream));
+  TLK_CUDA(cudaMemsetAsync(p->params, 0, L * S * 4, p->stream));
+  TLK_CUDA(cudaMemsetAsync(p->grads, 0, L * S * 4, p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   ctx->packs.push_back(std::move(p));
   *pack_id = int32_t(ctx->packs.size() - 1);
   return TLK_OK;
@@ -384,9 +446,9 @@ int tlk_lane_load(tlk_ctx* ctx, int32_t pack, int32_t lane, const tlk_job_desc* 
   s.b1t = 1.0;
   s.b2t = 1.0;
   p->lane_host[lane] = s;
-  if ((rc = enqueue_lane_init(*p, lane, ctx->stream))) return rc;
+  if ((rc = enqueue_lane_init(*p, lane, p->stream))) return rc;
   TLK_CUDA(cudaMemsetAsync(p->loss + size_t(lane) * p->max_steps, 0, size_t(p->max_steps) * 4,
-                           ctx->stream));
+                           p->stream));
   return upload_lane(ctx, *p, lane);
 }
 
@@ -396,8 +458,8 @@ int tlk_lane_release(tlk_ctx* ctx, int32_t pack, int32_t lane) {
   if (rc) return rc;
   TLK_CHECK(lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
   TLK_CUDA(cudaMemcpyAsync(&p->lane_host[lane], p->lane_dev + lane, sizeof(LaneState),
-                           cudaMemcpyDeviceToHost, ctx->stream));
-  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+                           cudaMemcpyDeviceToHost, p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   p->lane_host[lane].active = 0;
   return upload_lane(ctx, *p, lane);
 }
@@ -408,8 +470,8 @@ int tlk_run(tlk_ctx* ctx, int32_t pack, int32_t steps) {
   if (rc) return rc;
   TLK_CHECK(steps >= 0, TLK_EINVAL, "steps must be >= 0");
   TLK_CHECK(!p->host_input, TLK_ESTATE, "host-input pack: use tlk_step_host");
-  if ((rc = ensure_graph(*p, ctx->stream))) return rc;
-  for (int i = 0; i < steps; ++i) TLK_CUDA(cudaGraphLaunch(p->graph_exec, ctx->stream));
+  if ((rc = ensure_graph(*p, p->stream))) return rc;
+  for (int i = 0; i < steps; ++i) TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
   return TLK_OK;
 }
 
@@ -421,14 +483,14 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
   TLK_CHECK(p->host_input, TLK_ESTATE, "pack was created without host_input");
   TLK_CHECK(pixels && labels, TLK_EINVAL, "null input buffers");
   const size_t L = size_t(p->lanes), B = size_t(p->batch);
-  TLK_CUDA(cudaMemcpyAsync(p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, ctx->stream));
-  TLK_CUDA(cudaMemcpyAsync(p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, ctx->stream));
-  if ((rc = ensure_graph(*p, ctx->stream))) return rc;
-  TLK_CUDA(cudaGraphLaunch(p->graph_exec, ctx->stream));
+  TLK_CUDA(cudaMemcpyAsync(p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, p->stream));
+  TLK_CUDA(cudaMemcpyAsync(p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->stream));
+  if ((rc = ensure_graph(*p, p->stream))) return rc;
+  TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
   if (losses_out) {
     TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, L * 4, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+                             p->stream));
+    TLK_CUDA(cudaStreamSynchronize(p->stream));
   }
   return TLK_OK;
 }
@@ -446,16 +508,16 @@ int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const
   if (rc) return rc;
   TLK_CHECK(p->host_input, TLK_ESTATE, "pack was created without host_input");
   TLK_CHECK(pixels && labels && losses_out && ticket, TLK_EINVAL, "null buffers");
-  if ((rc = ensure_host_pipeline(*p, ctx->stream))) return rc;
+  if ((rc = ensure_host_pipeline(*p, p->stream))) return rc;
   const int s = int(p->host_steps & 1);
   const size_t L = size_t(p->lanes), B = size_t(p->batch);
   if (p->host_steps >= 2) TLK_CUDA(cudaStreamWaitEvent(p->copy_st, p->done_ev[s], 0));
   TLK_CUDA(cudaMemcpyAsync(s ? p->px_alt : p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, p->copy_st));
   TLK_CUDA(cudaMemcpyAsync(s ? p->lb_alt : p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->copy_st));
   TLK_CUDA(cudaEventRecord(p->h2d_ev[s], p->copy_st));
-  TLK_CUDA(cudaStreamWaitEvent(ctx->stream, p->h2d_ev[s], 0));
-  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->hexec0, ctx->stream));
-  TLK_CUDA(cudaEventRecord(p->done_ev[s], ctx->stream));
+  TLK_CUDA(cudaStreamWaitEvent(p->stream, p->h2d_ev[s], 0));
+  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->hexec0, p->stream));
+  TLK_CUDA(cudaEventRecord(p->done_ev[s], p->stream));
   p->hout[s] = losses_out;  // filled from the mapped slot by tlk_step_host_wait
   *ticket = p->host_steps++;
   return TLK_OK;
@@ -486,8 +548,8 @@ int tlk_lane_status_get(tlk_ctx* ctx, int32_t pack, int32_t lane, tlk_lane_statu
   TLK_CHECK(out && lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
   LaneState s;
   TLK_CUDA(cudaMemcpyAsync(&s, p->lane_dev + lane, sizeof(s), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+                           p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   out->active = s.active;
   out->steps_done = s.steps_done;
   out->steps = s.steps;
@@ -502,8 +564,8 @@ int tlk_lane_losses(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int32
   TLK_CHECK(host && lane >= 0 && lane < p->lanes && n >= 0 && n <= p->max_steps, TLK_EINVAL,
             "bad lane/n");
   TLK_CUDA(cudaMemcpyAsync(host, p->loss + size_t(lane) * p->max_steps, size_t(n) * 4,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+                           cudaMemcpyDeviceToHost, p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   return TLK_OK;
 }
 
@@ -514,8 +576,8 @@ int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64
   TLK_CHECK(host && lane >= 0 && lane < p->lanes && n >= 0 && n <= p->stride, TLK_EINVAL,
             "bad lane/n");
   TLK_CUDA(cudaMemcpyAsync(host, p->params + size_t(lane) * p->stride, size_t(n) * 4,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-  TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+                           cudaMemcpyDeviceToHost, p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   return TLK_OK;
 }
 
@@ -585,23 +647,23 @@ int tlk_profile_step(tlk_ctx* ctx, int32_t pack, int32_t iters, float* ms, char*
   std::vector<const char*> nm;
   cudaEvent_t start;
   TLK_CUDA(cudaEventCreate(&start));
-  TLK_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  cudaEventRecordWithFlags(start, ctx->stream, cudaEventRecordExternal);
+  TLK_CUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  cudaEventRecordWithFlags(start, p->stream, cudaEventRecordExternal);
   p->prof = &ev;
   p->prof_names = &nm;
-  rc = enqueue_step(*p, ctx->stream);
+  rc = enqueue_step(*p, p->stream);
   p->prof = nullptr;
   p->prof_names = nullptr;
   cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  cudaError_t e = cudaStreamEndCapture(p->stream, &g);
   if (rc) return rc;
   TLK_CUDA(e);
   cudaGraphExec_t ge = nullptr;
   TLK_CUDA(cudaGraphInstantiate(&ge, g, 0));
   std::vector<double> acc(ev.size(), 0.0);
   for (int it = 0; it < iters; ++it) {
-    TLK_CUDA(cudaGraphLaunch(ge, ctx->stream));
-    TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+    TLK_CUDA(cudaGraphLaunch(ge, p->stream));
+    TLK_CUDA(cudaStreamSynchronize(p->stream));
     cudaEvent_t prev = start;
     for (size_t k = 0; k < ev.size(); ++k) {
       float t = 0.f;

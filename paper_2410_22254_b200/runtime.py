@@ -23,11 +23,13 @@ OPT_ADAM, OPT_ADAMW, OPT_SGD = 1, 2, 3
 OPTIMIZERS = {"adam": OPT_ADAM, "adamw": OPT_ADAMW, "sgd": OPT_SGD}
 PACK_WRITE_ALL_GRADS = 1
 PACK_SNAPSHOTS = 2
+PACK_OWN_STREAM = 4
 BUF_PARAMS, BUF_GRADS, BUF_MOM1, BUF_MOM2, BUF_WBF16, BUF_LOSS, BUF_PIXELS, BUF_LABELS, BUF_ACTS = range(9)
 
 EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
-    "tlk_close", "tlk_sync", "tlk_stream", "tlk_pack_create", "tlk_lane_load", "tlk_lane_release",
+    "tlk_close", "tlk_sync", "tlk_stream", "tlk_set_mem_limit", "tlk_mem_in_use", "tlk_pack_create",
+    "tlk_pack_destroy", "tlk_pack_stream", "tlk_lane_load", "tlk_lane_release",
     "tlk_run", "tlk_step_host", "tlk_step_host_async", "tlk_step_host_wait", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
     "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
@@ -153,6 +155,15 @@ class Context:
         check(lib().tlk_stream(self._ctx, C.byref(s)))
         return s.value or 0
 
+    def set_mem_limit(self, nbytes: int) -> None:
+        """Admission budget for pack memory (0 = device memory only)."""
+        check(lib().tlk_set_mem_limit(self._ctx, C.c_int64(int(nbytes))))
+
+    def mem_in_use(self) -> int:
+        n = C.c_int64()
+        check(lib().tlk_mem_in_use(self._ctx, C.byref(n)))
+        return n.value
+
     def pack(self, model: int, batch: int, lanes: int, max_steps: int, host_input: bool = False,
              flags: int = 0, **cfg):
         return Pack(self, model, batch, lanes, max_steps, host_input, flags, **cfg)
@@ -183,6 +194,18 @@ class Pack:
 
     def release(self, lane: int):
         check(lib().tlk_lane_release(self.ctx._ctx, self.id, lane))
+
+    def destroy(self):
+        """Free the pack's device memory (tlk_pack_destroy); the pack is unusable after."""
+        if self.id >= 0:
+            check(lib().tlk_pack_destroy(self.ctx._ctx, self.id))
+            self.id = -1
+
+    @property
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(lib().tlk_pack_stream(self.ctx._ctx, self.id, C.byref(s)))
+        return s.value or 0
 
     def run(self, steps: int):
         check(lib().tlk_run(self.ctx._ctx, self.id, int(steps)))

@@ -7,14 +7,28 @@ Reference semantics it keeps (executor.py:162-233, plan.py:100-127):
 * timeout -> status 124, bad task -> non-zero status with the reason on the
   task's stderr (OOM text contains "out of memory" -> oom_flag).
 
-What changes: the slots pinned to one GPU are *lanes* of packs (one pack per
-(model, batch) kind) inside one context; a slot's current task occupies lane
-``slot_local_index`` of the pack of its kind.  Whenever a lane finishes, the
-slot's next task is loaded into it (queue refill / job churn, SURVEY §8f
-rank 1) between graph-replayed step chunks.
+What changes: the slots pinned to one GPU are *lanes* of packs (K co-resident
+jobs of one (model, batch) kind inside one context).  A slot's current task
+occupies a free lane of a pack of its kind; whenever a lane finishes, the
+slot's next task is loaded into a free lane (queue refill / job churn, SURVEY
+§8f rank 1) between graph-replayed step chunks.
 
-The backend is abstract (``create_pack``) so this logic is unit-tested on CPU
-with a fake backend (tests/test_scheduler.py); the real one is libtlk.
+Admission is per TASK, like the reference simulator's
+(sim.py:388-402: a task starts if its memory fits the device's free memory,
+else it fails with OOM at once and its slot moves on):
+* a task without a free lane of its kind asks for a new pack sized to the
+  demand of that admission pass (the slots waiting for that kind);
+* if that does not fit, the largest capacity that does is found by bisection
+  (device memory or the context budget), idle packs are destroyed first when
+  even one lane does not fit, and only a task for which not even a one-lane
+  pack fits fails with "out of memory";
+* a pack whose lanes are all free is destroyed (its memory returns to the
+  device, as a finished process's does in the reference).
+Packs of different kinds have their own streams and run concurrently.
+
+The backend is abstract (``create_pack`` / ``destroy_pack``) so this logic is
+unit-tested on CPU with a fake backend (tests/test_scheduler.py); the real
+one is libtlk.
 """
 
 from __future__ import annotations
@@ -38,15 +52,29 @@ class SlotTask:
 @dataclass
 class SlotState:
     slot_index: int
-    local: int  # lane index inside every pack of this GPU
+    local: int  # position of the slot among this GPU's slots
     queue: collections.deque
     current: object = None
 
 
 @dataclass
+class PackSlot:
+    """One live pack: a (model, batch) kind with `capacity` lanes."""
+
+    key: tuple
+    handle: object
+    capacity: int
+    free: list = field(default_factory=list)  # free lane indices (ascending)
+
+    def __post_init__(self):
+        if not self.free:
+            self.free = list(range(self.capacity))
+
+
+@dataclass
 class Running:
     task: SlotTask
-    pack: object
+    pack: PackSlot
     key: tuple
     lane: int
     t_start: float
@@ -63,6 +91,10 @@ class TaskOutcome:
     summary: dict = field(default_factory=dict)
 
 
+def _is_oom(exc: Exception) -> bool:
+    return bool(getattr(exc, "oom", False)) or "out of memory" in str(exc).lower()
+
+
 class LaneScheduler:
     def __init__(self, backend, slots, timeout_s=None, chunk=64, on_start=None, on_end=None,
                  clock=time.monotonic):
@@ -74,33 +106,83 @@ class LaneScheduler:
         self.on_start = on_start or (lambda task_id, slot_index: None)
         self.on_end = on_end or (lambda outcome: None)
         self.clock = clock
-        self.packs: dict = {}
-        self.failed_keys: dict = {}
+        self.packs: list[PackSlot] = []
+        # loss-curve capacity per kind: the longest task of that kind anywhere
+        # in the plan, so any of them fits any pack of its kind
+        self.max_steps: dict = {}
+        for s in self.slots:
+            for t in s.queue:
+                if t.spec is not None:
+                    k = (t.spec.model, t.spec.batch)
+                    self.max_steps[k] = max(self.max_steps.get(k, 1), int(t.spec.steps))
         self.samples = 0
         self.steps_run = 0
         self.busy_s = 0.0
+        self.step_s = None  # measured seconds per step chunk step (caps chunks under a timeout)
+        self.packs_created = 0
+        self.peak_lanes = 0
         self.outcomes: list[TaskOutcome] = []
 
     # -- pack management ---------------------------------------------------
-    def _max_steps(self, key):
-        return max((t.spec.steps for s in self.slots for t in list(s.queue)
-                    + ([s.current.task] if isinstance(s.current, Running) else [])
-                    if t.spec is not None and (t.spec.model, t.spec.batch) == key), default=1)
+    def _create(self, key, lanes):
+        handle = self.backend.create_pack(key[0], key[1], lanes, self.max_steps.get(key, 1))
+        ps = PackSlot(key, handle, lanes)
+        self.packs.append(ps)
+        self.packs_created += 1
+        return ps
 
-    def _pack_for(self, key):
-        if key in self.failed_keys:
-            raise RuntimeError(self.failed_keys[key])
-        if key not in self.packs:
-            try:
-                self.packs[key] = self.backend.create_pack(key[0], key[1], len(self.slots),
-                                                           self._max_steps(key))
-            except Exception as exc:  # admission failure (e.g. out of memory)
-                self.failed_keys[key] = str(exc)
+    def _destroy(self, ps: PackSlot):
+        self.packs.remove(ps)
+        self.backend.destroy_pack(ps.handle)
+
+    def _destroy_idle(self) -> bool:
+        idle = [p for p in self.packs if len(p.free) == p.capacity]
+        for p in idle:
+            self._destroy(p)
+        return bool(idle)
+
+    def _try_create(self, key, lanes):
+        try:
+            return self._create(key, lanes), None
+        except Exception as exc:  # noqa: BLE001 -- classified below
+            if not _is_oom(exc):
                 raise
-        return self.packs[key]
+            return None, exc
+
+    def _new_pack(self, key, want):
+        """A pack of `key` with the largest capacity <= want that fits."""
+        ps, err = self._try_create(key, want)
+        if ps is not None:
+            return ps
+        if self._destroy_idle():
+            ps, err = self._try_create(key, want)
+            if ps is not None:
+                return ps
+        lo, hi = 0, want  # lo fits (0 trivially), hi does not
+        while hi - lo > 1:
+            mid = (lo + hi) // 2
+            ps, e = self._try_create(key, mid)
+            if ps is None:
+                hi, err = mid, e
+            else:
+                self._destroy(ps)
+                lo = mid
+        if lo == 0:
+            raise err
+        return self._create(key, lo)
+
+    def _place(self, key, demand):
+        for ps in self.packs:
+            if ps.key == key and ps.free:
+                return ps, ps.free.pop(0)
+        ps = self._new_pack(key, max(1, demand))
+        return ps, ps.free.pop(0)
 
     def _finish(self, slot, status, err="", summary=None):
         run = slot.current
+        if isinstance(run, Running):
+            run.pack.free.append(run.lane)
+            run.pack.free.sort()
         out = TaskOutcome(run.task.task_id if isinstance(run, Running) else run.task_id,
                           slot.slot_index, status, err, summary or {})
         slot.current = None
@@ -109,8 +191,11 @@ class LaneScheduler:
 
     # -- main loop ----------------------------------------------------------
     def _admit(self):
-        for slot in self.slots:
-            while slot.current is None and slot.queue:
+        while True:
+            waiting = [s for s in self.slots if s.current is None and s.queue]
+            if not waiting:
+                break
+            for k, slot in enumerate(waiting):
                 task = slot.queue.popleft()
                 self.on_start(task.task_id, slot.slot_index)
                 if task.spec is None:
@@ -118,14 +203,34 @@ class LaneScheduler:
                     self._finish(slot, 2, task.error or "not a packable job")
                     continue
                 key = (task.spec.model, task.spec.batch)
+                # demand: this slot and the later slots of this pass waiting for the same kind
+                demand = 1 + sum(1 for s in waiting[k + 1:]
+                                 if s.queue and s.queue[0].spec is not None
+                                 and (s.queue[0].spec.model, s.queue[0].spec.batch) == key)
                 try:
-                    pack = self._pack_for(key)
-                    pack.load(slot.local, task.spec, task_id=task.task_id, slot_index=slot.slot_index)
+                    ps, lane = self._place(key, demand)
                 except Exception as exc:
                     slot.current = task
                     self._finish(slot, 1, f"{type(exc).__name__}: {exc}")
                     continue
-                slot.current = Running(task, pack, key, slot.local, self.clock(), task.spec.steps)
+                try:
+                    ps.handle.load(lane, task.spec, task_id=task.task_id, slot_index=slot.slot_index)
+                except Exception as exc:
+                    ps.free.append(lane)
+                    ps.free.sort()
+                    slot.current = task
+                    self._finish(slot, 1, f"{type(exc).__name__}: {exc}")
+                    continue
+                slot.current = Running(task, ps, key, lane, self.clock(), task.spec.steps)
+        self._destroy_idle()
+
+    def _chunk_steps(self, running, now):
+        n = min(self.chunk, min(s.current.steps - s.current.done for s in running))
+        if self.timeout_s is not None and self.step_s:
+            # never run a chunk past the first task's deadline (parent watchdog backs this up)
+            left = min(self.timeout_s - (now - s.current.t_start) for s in running)
+            n = min(n, int(max(left, 0.0) / self.step_s) + 1)
+        return max(1, n)
 
     def run(self):
         while True:
@@ -133,15 +238,17 @@ class LaneScheduler:
             running = [s for s in self.slots if isinstance(s.current, Running)]
             if not running:
                 break
-            n = min(self.chunk, min(s.current.steps - s.current.done for s in running))
-            n = max(1, n)
+            self.peak_lanes = max(self.peak_lanes, len(running))
             t0 = self.clock()
+            n = self._chunk_steps(running, t0)
             packs = {id(s.current.pack): s.current.pack for s in running}
-            for p in packs.values():
-                p.run(n)
-            for p in packs.values():
-                p.sync()
-            self.busy_s += self.clock() - t0
+            for ps in packs.values():
+                ps.handle.run(n)
+            for ps in packs.values():
+                ps.handle.sync()
+            dt = self.clock() - t0
+            self.busy_s += dt
+            self.step_s = dt / n if self.step_s is None else 0.5 * self.step_s + 0.5 * dt / n
             self.steps_run += n
             now = self.clock()
             for s in running:
@@ -149,30 +256,39 @@ class LaneScheduler:
                 r.done = min(r.steps, r.done + n)
                 self.samples += n * r.task.spec.batch
                 if r.done >= r.steps:
-                    summary = r.pack.summary(r.lane, r.steps)
+                    summary = r.pack.handle.summary(r.lane, r.steps)
                     self._finish(s, 0, "", summary)
                 elif self.timeout_s is not None and now - r.t_start > self.timeout_s:
-                    r.pack.release(r.lane)
+                    r.pack.handle.release(r.lane)
                     self._finish(s, TIMEOUT_EXIT_STATUS, f"timeout after {self.timeout_s}s")
+        for ps in list(self.packs):
+            self._destroy(ps)
         return self.outcomes
 
     def stats(self) -> dict:
         return {"samples": self.samples, "busy_s": self.busy_s, "step_chunks": self.steps_run,
                 "samples_per_s": self.samples / self.busy_s if self.busy_s > 0 else None,
-                "packs": {f"{k[0]}/bs{k[1]}": len(self.slots) for k in self.packs}}
+                "packs_created": self.packs_created, "peak_lanes": self.peak_lanes}
 
 
 class TlkBackend:
-    """libtlk-backed packs for LaneScheduler."""
+    """libtlk-backed packs for LaneScheduler (one context = one GPU)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, mem_limit_bytes: int | None = None):
         from . import runtime as rt
 
         self.rt = rt
         self.ctx = rt.Context(device)
+        if mem_limit_bytes:
+            self.ctx.set_mem_limit(int(mem_limit_bytes))
 
     def create_pack(self, model, batch, lanes, max_steps):
-        return _TlkPack(self, self.ctx.pack(self.rt.MODELS[model], batch, lanes, max_steps))
+        # own stream: packs of different kinds (configs[3] mixes) run concurrently
+        return _TlkPack(self, self.ctx.pack(self.rt.MODELS[model], batch, lanes, max_steps,
+                                            flags=self.rt.PACK_OWN_STREAM))
+
+    def destroy_pack(self, handle):
+        handle.pack.destroy()
 
     def close(self):
         self.ctx.close()

@@ -5,7 +5,7 @@ pin in its environment (CUDA_VISIBLE_DEVICES=<gpu>, core.py:171-179), so it
 sees exactly one device.  Reads one JSON request on stdin:
 
     {"slots": [{"slot_index": s, "tasks": [{"task_id": i, "argv": [...]}, ...]}, ...],
-     "timeout_s": float|null, "log_dir": str|null, "chunk": int}
+     "timeout_s": float|null, "log_dir": str|null, "chunk": int, "mem_limit_mib": int|null}
 
 and streams JSON lines on stdout: {"ev": "start", "task_id": i} when a task
 is loaded into its lane, {"ev": "end", "task_id": i, "status": st, "err": e}
@@ -63,7 +63,8 @@ def main() -> int:
 
     slots = [(int(s["slot_index"]), _tasks(s["tasks"])) for s in req["slots"]]
     try:
-        backend = TlkBackend(0)
+        mib = req.get("mem_limit_mib")
+        backend = TlkBackend(0, int(mib) << 20 if mib else None)
     except Exception as exc:
         # no usable device/library: every task fails loudly (no CPU fallback)
         for si, tasks in slots:

@@ -117,3 +117,81 @@ def test_cli_exec_packed_with_nvml_telemetry(tmp_path):
     series = tm.read_series_csv(tmp_path / "r" / "telemetry.csv")
     assert series.samples and all(len(s.gpu) == 1 for s in series.samples)
     assert max(s.gpu[0].mem_mib for s in series.samples) > 0
+
+
+def test_per_task_admission_against_a_memory_budget(tmp_path):
+    """SURVEY §8f rank 2 / the paper's 48-job run (21 of 48 OOM):
+    with a device budget that holds only 3 CNN lanes, 16 CNN tasks on 8 slots
+    (T > S): the tasks that fit are admitted and train bit-identically to the
+    same task alone; the others fail AT ADMISSION with "out of memory"
+    (oom_flag), and their slots go on with the next task (admitted as soon as
+    memory frees, like sim.py:388-402)."""
+    with rt.Context(0) as ctx:
+        a = ctx.pack(rt.MODEL_CNN, 64, 1, 6)
+        one = ctx.mem_in_use()
+        b = ctx.pack(rt.MODEL_CNN, 64, 2, 6)
+        per_lane = (ctx.mem_in_use() - one) - one  # 2-lane pack minus 1-lane pack
+        fixed = one - per_lane
+        a.destroy()
+        b.destroy()
+        assert ctx.mem_in_use() == 0
+    budget_mib = (fixed + 3 * per_lane + per_lane // 2) >> 20
+    specs = [JobSpec(model="cnn", seed=700 + i, steps=3 + i % 3, lr=1e-3) for i in range(16)]
+    tasks = [TaskDef(i, tuple(s.argv(sys.executable))) for i, s in enumerate(specs)]
+    plan = build_plan(tasks, TripleSpec(1, 8, 1), NodeSpec(cores=8, gpus=1, gpu_mem_mib=budget_mib))
+    report = run_plan(plan, 0, log_dir=tmp_path, backend="packed",
+                      packed_options={"mem_limit_mib": budget_mib})
+    by = {r.task_id: r for r in report.results}
+    ok = sorted(t for t, r in by.items() if r.exit_status == 0)
+    oom = sorted(t for t, r in by.items() if r.exit_status != 0)
+    assert ok == [0, 1, 2, 8, 9, 10], (ok, [(t, (tmp_path / f"task_{t}.err").read_text()) for t in oom])
+    for t in oom:
+        assert by[t].oom_flag and by[t].exit_status == 1
+        assert "out of memory" in (tmp_path / f"task_{t}.err").read_text()
+    assert report.max_observed_concurrency <= 8
+    for t in ok:
+        out = json.loads((tmp_path / f"task_{t}.out").read_text())
+        ref = _alone(specs[t])
+        assert np.float32(out["last_loss"]) == ref[-1], t
+
+
+def test_heterogeneous_packs_run_concurrently_on_their_own_streams():
+    """configs[3]: packs of different models (own streams) overlap on the
+    device -- two packs replayed together finish sooner than back to back --
+    and each lane's losses stay bit-identical to running its pack alone."""
+    import time
+
+    def make(ctx, flags):
+        m = ctx.pack(rt.MODEL_MLP, 64, 4, 200, flags=flags)
+        c = ctx.pack(rt.MODEL_CNN, 64, 4, 200, flags=flags)
+        for p in (m, c):
+            for j in range(4):
+                p.load(j, seed=800 + j, steps=200)
+        return m, c
+
+    with rt.Context(0) as ctx:
+        m, c = make(ctx, rt.PACK_OWN_STREAM)
+        assert m.stream_handle != c.stream_handle
+        m.run(5), c.run(5)
+        ctx.sync()
+        t0 = time.perf_counter()
+        m.run(100), c.run(100)
+        ctx.sync()
+        both = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        m.run(95)
+        ctx.sync()
+        c.run(95)
+        ctx.sync()
+        serial = time.perf_counter() - t0
+        ctx.sync()
+        lm = [m.losses(j, 200) for j in range(4)]
+        lc = [c.losses(j, 200) for j in range(4)]
+    assert both < serial * 1.02, (both, serial)
+    with rt.Context(0) as ctx:
+        m2, c2 = make(ctx, 0)
+        m2.run(200)
+        c2.run(200)
+        ctx.sync()
+        for j in range(4):
+            assert np.array_equal(m2.losses(j, 200), lm[j]) and np.array_equal(c2.losses(j, 200), lc[j])

@@ -70,14 +70,18 @@ def _conv_index():
     return out
 
 
-@pytest.fixture(scope="module")
-def snap():
-    """One step of a 1-lane B=16 pack with gradient snapshots; every named
-    buffer copied to host."""
-    B, seed = 16, 55
+@pytest.fixture(scope="module", params=[(16, 1, 0), (128, 2, 1)], ids=["bs16x1", "bs128x2-lane1"])
+def snap(request):
+    """One step of a pack with gradient snapshots; every named buffer of ONE
+    lane copied to host.  (16, 1 lane) and the BASELINE configs[2] shape
+    (bs 128, 2 lanes, checking lane 1: the per-lane offsets and the
+    batch-dependent wgrad split-K / partial-buffer sizing of resnet.cu)."""
+    B, lanes, lane = request.param
+    seed = 55
     with rt.Context(0) as ctx:
-        p = ctx.pack(rt.MODEL_RESNET18, B, 1, 1, flags=rt.PACK_SNAPSHOTS)
-        p.load(0, seed=seed, steps=1, optimizer=rt.OPT_SGD, lr=0.01)
+        p = ctx.pack(rt.MODEL_RESNET18, B, lanes, 1, flags=rt.PACK_SNAPSHOTS)
+        for j in range(lanes):
+            p.load(j, seed=seed - lane + j, steps=1, optimizer=rt.OPT_SGD, lr=0.01)
         p.run(1)
         ctx.sync()
         names = ["xin", "a0", "stem.G"] + [f"conv{i}.{k}" for i in range(20) for k in ("y", "stats")]
@@ -86,10 +90,13 @@ def snap():
         for n in names:
             kind = "f4" if n.endswith((".stats", ".G")) else "u2"
             v = p.named(n, kind).cpu().numpy()
+            per = v.size // lanes
+            v = v[lane * per:(lane + 1) * per]
             out[n] = _bf(v) if kind == "u2" else v
-        out["grads"] = p.tensor(rt.BUF_GRADS).cpu().numpy()[:p.info.param_stride]
-        out["labels"] = p.tensor(rt.BUF_LABELS).cpu().numpy()[:B]
-        out["loss"] = p.losses(0, 1)[0]
+        S = p.info.param_stride
+        out["grads"] = p.tensor(rt.BUF_GRADS).cpu().numpy()[lane * S:(lane + 1) * S]
+        out["labels"] = p.tensor(rt.BUF_LABELS).cpu().numpy()[lane * B:(lane + 1) * B]
+        out["loss"] = p.losses(lane, 1)[0]
     out["B"], out["seed"] = B, seed
     return out
 
@@ -231,3 +238,23 @@ def test_loss_curve_and_packing_invariance():
             alone.run(steps)
             ctx.sync()
             assert np.array_equal(alone.losses(0, steps), got)
+
+
+def test_loss_curve_bs128_bench_shape():
+    """configs[2] shape: 2 lanes x bs 128, SGD-momentum, 3 steps vs the oracle
+    (same per-step bound as test_loss_curve_and_packing_invariance)."""
+    steps, B = 3, 128
+    jobs = [(64, dict(lr=0.02, momentum=0.9)), (65, dict(lr=0.05, momentum=0.9, weight_decay=5e-4))]
+    with rt.Context(0) as ctx:
+        p = ctx.pack(rt.MODEL_RESNET18, B, len(jobs), steps)
+        for lane, (seed, kw) in enumerate(jobs):
+            p.load(lane, seed=seed, steps=steps, optimizer=rt.OPT_SGD, **kw)
+        p.run(steps)
+        ctx.sync()
+        for lane, (seed, kw) in enumerate(jobs):
+            got = p.losses(lane, steps)
+            ref, _, _ = ojob.train_resnet(seed, steps, B, ooptim.OptState(kind=ooptim.SGD, **kw), bf16=True)
+            ref32, _, _ = ojob.train_resnet(seed, steps, B, ooptim.OptState(kind=ooptim.SGD, **kw), bf16=False)
+            assert abs(got[0] - ref[0]) < 5e-3 * abs(ref[0]), (lane, got, ref)
+            tol = np.maximum(0.05, 3.0 * np.abs(ref - ref32))
+            assert np.all(np.abs(got - ref) <= tol), (lane, got, ref, ref32)
