@@ -87,6 +87,10 @@ typedef struct {
                                       into a wgrad epilogue (tests/inspection) */
 #define TLK_PACK_SNAPSHOTS 2       /* keep per-layer copies of intermediate gradients
                                       (layer-local parity tests; ResNet packs) */
+#define TLK_PACK_PERSISTENT 8      /* CNN packs: run steps on the persistent per-GPU scheduler
+                                      kernel (one launch per chunk of steps, device work
+                                      queue, per-lane dependency counters) instead of the
+                                      per-phase kernel graph; bit-identical results */
 #define TLK_PACK_OWN_STREAM 4      /* the pack gets its own CUDA stream (tlk_pack_stream), so
                                       packs of different models on one GPU run concurrently;
                                       default: the context stream */

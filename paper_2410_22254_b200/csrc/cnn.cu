@@ -24,52 +24,13 @@
 
 #include <cooperative_groups.h>
 
-#include "conv_tc.cuh"
-#include "tma.cuh"
+#include "cnn_common.cuh"
 #include "linear.cuh"
-#include "pack.cuh"
 #include "inputs.cuh"
 
 namespace tlk {
 namespace {
 
-#ifndef TLK_FC1_SPLITS
-#define TLK_FC1_SPLITS 18
-#endif
-constexpr int FC1_SPLITS = TLK_FC1_SPLITS;  // split-K of the fc1 forward (144 k-blocks / 8)
-static_assert(144 % FC1_SPLITS == 0, "fc1 split-K must divide the 144 k-blocks");
-#ifndef TLK_C2W_SPLITS
-#define TLK_C2W_SPLITS 18
-#endif
-constexpr int C2W_SPLITS = TLK_C2W_SPLITS;  // conv2 wgrad position splits per lane
-// every split needs >= 1 of the B * 784 / 128 position chunks (49 at the
-// smallest batch, 8): an empty split would commit no MMA and write stale TMEM
-static_assert(C2W_SPLITS >= 1 && C2W_SPLITS <= 49, "conv2 wgrad splits must be in [1, 49]");
-constexpr int C1W_SMEM = 4 * P28_IMG * 16;  // conv1 wgrad: one image's dz1 planes
-#ifndef TLK_C1W_THREADS
-#define TLK_C1W_THREADS 256
-#endif
-constexpr int C1W_THREADS = TLK_C1W_THREADS;  // 8 warps per image: the per-SM warp count hides latency
-constexpr int CNN_OPT_CTAS = 24;  // per lane: ~5.4k float4 of non-fc1.w parameters (~1 per thread)
-
-struct CnnBufs {
-  // TMA tensor maps of the plain-layout fc1 operands (lanes = dim 2)
-  CUtensorMap w1_k;   // fc1.w bf16 [9216 in][128 out]: box 64 x 128 (K-major A)
-  CUtensorMap w1_mn;  // fc1.w bf16: box 64 x 64 (MN-major A of dgrad)
-  CUtensorMap p2m;    // p2 [9216][B]: box 64 x 64
-  CUtensorMap dz3m;   // dz3 [128][B]: box 64 x 64
-  CUtensorMap fa_p, fa_m, fa_v;  // fc1.w optimizer state tiles (fc1 wgrad + Adam)
-  int B;
-  int64_t npos;
-  uint16_t *h1, *p2, *h3, *dz3, *dz2, *dz1;
-  uint8_t* idx;
-  float *colsum, *part_fc1, *part2, *part1;
-  int64_t p2_st, h3_st;
-};
-
-__host__ __device__ inline int64_t p28_pos(int b, int r, int c) {
-  return P28_FRONT + int64_t(b) * P28_IMG + r * P28 + c;
-}
 
 // ------------------------------------------------------- inputs + conv1 -----
 // One CTA per (sample, lane): the sample's inputs (inputs.cuh: pixel codes,
@@ -176,7 +137,6 @@ struct Fc1Fwd {
 // the 8 partials in rank order (+ b2), so all hold identical logits.  Then,
 // as head_kernel (kernels.cu): softmax-CE, the loss / step scalars / fc2.b
 // grad (rank 0), and the backward of its 16 units (dz3, fc2.w, fc1.b grads).
-constexpr int HEAD_CL = 8, HEAD_HS = 16;
 __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
     cnn_head_kernel(LaneState* __restrict__ lanes, CnnBufs buf, const float* __restrict__ params,
                     float* __restrict__ grads, int64_t stride, int64_t b1_off, int64_t w_off, int64_t b_off,
@@ -397,23 +357,6 @@ struct Fc1Dgrad {
 //            instructions per element: the kernel is issue-bound), coalesced
 //            128-B stores of p, m, v and the bf16 shadow.
 // Must run after every reader of this step's fc1 weights (fc1 dgrad).
-constexpr int FWA_SLOTS = 4, FWA_UPD_WARPS = 16;
-constexpr int FWA_STAGE_BYTES = 2 * 128 * 64 * 2;  // p2^T and dz3^T tiles (two 64-wide boxes each)
-constexpr int FWA_CHUNK = 32 * 128 * 4;            // one tensor's [32 o][128 f] chunk
-constexpr int FWA_SLOT_BYTES = 3 * FWA_CHUNK;
-constexpr int FWA_SMEM = FWA_STAGE_BYTES + FWA_SLOTS * FWA_SLOT_BYTES + 1024;
-constexpr int FWA_THREADS = (2 + FWA_UPD_WARPS) * 32;
-constexpr int FWA_FT = 9216 / 128;  // f tiles per lane
-struct Fc1WgradAdam {
-  CUtensorMap dz3m, p2m;      // operands (bf16, SWIZZLE_128B boxes 64 x 64)
-  CUtensorMap tp, tm, tv;     // fc1.w params / m / v: fp32 [lane][128 o][9216 f], box 128 f x 32 o
-  const LaneState* lanes;
-  float *params, *m1, *m2, *grads;
-  uint16_t* wbf;
-  int64_t pstride, w_off;
-  int write_grads, kblocks, ntiles;
-};
-
 __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __grid_constant__ Fc1WgradAdam p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t gfull, gempty, tfull[2], tempty[2];
@@ -659,44 +602,6 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
 // opt_update; bf16 shadow + transposed conv2.w copies).  The last CTA of a
 // lane ends the lane's step.  Replaces a finalize launch + the batched
 // optimizer launch.
-struct CnnOffs {
-  int64_t c1w, c1b, c2w, c2b;
-};
-struct CnnOpt {
-  LaneState* lanes;
-  int64_t stride, a1, b0;  // float4 units: [0, a1) u [b0, stride/4) of every lane
-  CnnOffs o;
-  float4 *P, *Gr, *M, *V;
-  uint2* Wb;
-  WtHook hook;
-};
-__device__ __forceinline__ void cnn_opt_apply(const CnnOpt& a, const LaneState& s, int j, int64_t idx,
-                                              const float (&g)[4]) {
-  const int64_t i = j * (a.stride / 4) + idx, e = idx * 4;
-  a.Gr[i] = make_float4(g[0], g[1], g[2], g[3]);
-  float4 pa = a.P[i], ma = a.M[i], va = a.V[i];
-  opt_update(s, pa.x, g[0], ma.x, va.x);
-  opt_update(s, pa.y, g[1], ma.y, va.y);
-  opt_update(s, pa.z, g[2], ma.z, va.z);
-  opt_update(s, pa.w, g[3], ma.w, va.w);
-  a.P[i] = pa;
-  a.M[i] = ma;
-  a.V[i] = va;
-  const uint32_t lo = pack_bf2(pa.x, pa.y), hi = pack_bf2(pa.z, pa.w);
-  a.Wb[i] = make_uint2(lo, hi);
-  if (e >= a.hook.off && e < a.hook.off + a.hook.count) {
-    wt_write(a.hook, j, e + 0, uint16_t(lo & 0xFFFF));
-    wt_write(a.hook, j, e + 1, uint16_t(lo >> 16));
-    wt_write(a.hook, j, e + 2, uint16_t(hi & 0xFFFF));
-    wt_write(a.hook, j, e + 3, uint16_t(hi >> 16));
-  }
-}
-// CTAs 0..11 of a lane: the 96 float4 whose gradients are long reductions
-// (conv1.w / conv1.b over the batch's images, conv2.b over the 144 pooled
-// positions), one warp per float4: lane l sums terms l, l+32, ... in order,
-// then a fixed xor-shuffle tree.  CTAs 12..: everything else, one float4 per
-// thread.
-constexpr int CNN_OPT_HEAVY = 12;
 __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ CnnOpt a, CnnBufs buf) {
   pdl_begin();
   const int j = blockIdx.y;
@@ -774,26 +679,6 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
   }
 }
 
-ConvArgs conv_args(const Pack& p, const CnnBufs& b) {
-  ConvArgs a{};
-  a.lanes = p.lane_dev;
-  a.B = b.B;
-  a.npos = b.npos;
-  a.h1 = b.h1;
-  a.dz2 = b.dz2;
-  a.dz1 = b.dz1;
-  a.p2 = b.p2;
-  a.idx = b.idx;
-  a.wt = p.wt;
-  a.wt_stride = p.wt_stride;
-  a.params = p.params;
-  a.pstride = p.stride;
-  a.b2_off = tensor_offset(*p.def, 3);
-  a.part2 = b.part2;
-  a.wgrad_splits = C2W_SPLITS;
-  return a;
-}
-
 }  // namespace
 
 int cnn_setup(Pack& p) {
@@ -810,7 +695,7 @@ int cnn_setup(Pack& p) {
   const size_t acts = size_t(L) * (4 * plane + 2 * b->p2_st + b->p2_st + 2 * 2 * b->h3_st +
                                    8 * plane + 4 * plane);
   const size_t f32s = size_t(L) * (9216 + FC1_SPLITS * 128 * 64 + C2W_SPLITS * 9 * 64 * 32 +
-                                   B * 320);
+                                   B * 320 + HEAD_CL * 64 * CLASSES + 32) + 32;
   void* base = nullptr;
   int rc = pack_alloc(p, &base, acts + f32s * 4 + 256);
   if (rc) return rc;
@@ -834,6 +719,8 @@ int cnn_setup(Pack& p) {
   b->part_fc1 = reinterpret_cast<float*>(take(L * FC1_SPLITS * 128 * 64 * 4));
   b->part2 = reinterpret_cast<float*>(take(L * C2W_SPLITS * 9 * 64 * 32 * 4));
   b->part1 = reinterpret_cast<float*>(take(L * B * 320 * 4));
+  b->plog = reinterpret_cast<float*>(take(L * HEAD_CL * 64 * CLASSES * 4));
+  b->sched = reinterpret_cast<uint32_t*>(take((L + 1) * 32 * 4));
   {  // TMA maps: lanes stacked as the outermost dimension
     const int64_t o_f1w = tensor_offset(*p.def, 4);
     const uint16_t* w1 = p.wbf + o_f1w;
@@ -854,6 +741,13 @@ int cnn_setup(Pack& p) {
         (rc = make_tmap_3d(&b->fa_v, F32, p.mom2 + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 32,
                            CU_TENSOR_MAP_SWIZZLE_NONE)))
       return rc;
+    if ((rc = make_tmap_3d(&b->fh_p, F32, p.params + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 16,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)) ||
+        (rc = make_tmap_3d(&b->fh_m, F32, p.mom1 + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 16,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)) ||
+        (rc = make_tmap_3d(&b->fh_v, F32, p.mom2 + o_f1w, ws, 128, L, ws * 4, p.stride * 4, 128, 16,
+                           CU_TENSOR_MAP_SWIZZLE_NONE)))
+      return rc;
   }
   void* wt = nullptr;
   p.wt_stride = 2 * CONV2_W;
@@ -868,13 +762,14 @@ int cnn_setup(Pack& p) {
   TLK_CUDA(cudaFuncSetAttribute(fc1_wgrad_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWA_SMEM));
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
-  p.launches_per_step = 10;
+  p.launches_per_step = cnn_persist_enabled(p) ? 1 : 10;
   p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
   p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
 }
 
 int cnn_enqueue_step(Pack& p, cudaStream_t st) {
+  if (cnn_persist_enabled(p)) return cnn_persist_enqueue(p, st, 1);
   const CnnBufs& b = *static_cast<CnnBufs*>(p.scratch);
   const ModelDef& d = *p.def;
   const int L = p.lanes, B = p.batch;

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
     if (lane == 0) {
       const uint16_t* w = a.wt + int64_t(j) * a.wt_stride + (FWD ? 0 : CONV2_W);
       mbar_expect_tx(&wfull, P::B_BYTES);
-      for (int t = 0; t < 9; ++t) tma_bulk_g2s(sB + t * 4096, w + t * 2048, 4096, &wfull);
+      tma_bulk_g2s(sB, w, P::B_BYTES, &wfull);  // the 9 taps are contiguous
       int i = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
         const int s = i % P::AS;
@@ -315,7 +315,7 @@ constexpr int WG_SMEM = WG_STAGES * WG_STAGE + 128;
 // the k' = 3 copies (spare MMA rows, never read back) are not loaded
 constexpr uint32_t WG_TX = 12 * WG_ACOPY + WG_B_BYTES;
 
-__global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
+static __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
   const int split = blockIdx.x, j = blockIdx.y;
   if (!a.lanes[j].active) return;
   extern __shared__ __align__(128) uint8_t sm[];

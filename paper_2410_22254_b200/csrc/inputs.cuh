@@ -11,12 +11,19 @@
 
 namespace tlk {
 
-template <int NT>
-__device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, size_t row, int host_input,
-                                              const int8_t* __restrict__ teacher, uint8_t* __restrict__ px,
-                                              int32_t* __restrict__ labels, uint16_t* __restrict__ x,
-                                              uint8_t* pix, int (*part)[CLASSES]) {
-  const int tid = threadIdx.x;
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {  // a named barrier over one thread group of a CTA
+  int id, n;
+  __device__ __forceinline__ void operator()() const { named_bar_sync(id, n); }
+};
+
+// NT threads (tid 0..NT-1 of the group, synchronised by `sync`) produce the sample.
+template <int NT, class Sync>
+__device__ __forceinline__ void sample_inputs_g(int tid, Sync sync, uint64_t seed, int step, int s, size_t row,
+                                                int host_input, const int8_t* teacher, uint8_t* px,
+                                                int32_t* labels, uint16_t* x, uint8_t* pix, int (*part)[CLASSES]) {
   uint64_t* px_row = reinterpret_cast<uint64_t*>(px + row * PIXELS);
   if (!host_input) {
     const uint64_t key = rng_key(seed, STREAM_DATA, uint64_t(step));
@@ -28,7 +35,7 @@ __device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, si
   } else {
     for (int q = tid; q < WORDS_PER_SAMPLE; q += NT) reinterpret_cast<uint64_t*>(pix)[q] = px_row[q];
   }
-  __syncthreads();
+  sync();
   if (x) {
     uint4* xr = reinterpret_cast<uint4*>(x + row * PIXELS);
     for (int q = tid; q < WORDS_PER_SAMPLE; q += NT) {
@@ -62,7 +69,7 @@ __device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, si
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if ((tid & 31) == 0) part[tid >> 5][c] = a;
   }
-  __syncthreads();
+  sync();
   if (tid == 0) {
     int best = 0, bestv = 0;
     for (int c = 0; c < CLASSES; ++c) {
@@ -75,6 +82,15 @@ __device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, si
     }
     labels[row] = best;
   }
+}
+
+template <int NT>
+__device__ __forceinline__ void sample_inputs(uint64_t seed, int step, int s, size_t row, int host_input,
+                                              const int8_t* __restrict__ teacher, uint8_t* __restrict__ px,
+                                              int32_t* __restrict__ labels, uint16_t* __restrict__ x,
+                                              uint8_t* pix, int (*part)[CLASSES]) {
+  sample_inputs_g<NT>(int(threadIdx.x), CtaSync{}, seed, step, s, row, host_input, teacher, px, labels, x, pix,
+                      part);
 }
 
 }  // namespace tlk

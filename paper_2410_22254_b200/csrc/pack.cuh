@@ -104,6 +104,10 @@ int mlp_setup(Pack& p);
 int mlp_enqueue_step(Pack& p, cudaStream_t st);
 int cnn_setup(Pack& p);
 int cnn_enqueue_step(Pack& p, cudaStream_t st);
+// persistent per-GPU scheduler kernel (cnn_persist.cu): `nsteps` steps of
+// every lane in one launch; TLK_PACK_PERSISTENT (or TLK_CNN_PERSIST=1)
+bool cnn_persist_enabled(const Pack& p);
+int cnn_persist_enqueue(Pack& p, cudaStream_t st, int nsteps);
 int gpt_setup(Pack& p);
 int gpt_enqueue_step(Pack& p, cudaStream_t st);
 int resnet_setup(Pack& p);

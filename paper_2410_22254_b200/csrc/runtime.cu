@@ -1,5 +1,6 @@
 // libtlk C ABI: contexts (one per GPU), packs of K job lanes, graph-captured
 // steps, host-buffer end-to-end steps, result readback.  See include/tlk.h.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -470,6 +471,14 @@ int tlk_run(tlk_ctx* ctx, int32_t pack, int32_t steps) {
   if (rc) return rc;
   TLK_CHECK(steps >= 0, TLK_EINVAL, "steps must be >= 0");
   TLK_CHECK(!p->host_input, TLK_ESTATE, "host-input pack: use tlk_step_host");
+  if (p->model == TLK_MODEL_CNN && cnn_persist_enabled(*p)) {
+    // the persistent scheduler kernel runs up to PERSIST_CHUNK steps of every
+    // lane per launch: lanes overlap across steps, no launch chain at all
+    constexpr int PERSIST_CHUNK = 64;
+    for (int done = 0; done < steps; done += PERSIST_CHUNK)
+      if ((rc = cnn_persist_enqueue(*p, p->stream, std::min(PERSIST_CHUNK, steps - done)))) return rc;
+    return TLK_OK;
+  }
   if ((rc = ensure_graph(*p, p->stream))) return rc;
   for (int i = 0; i < steps; ++i) TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
   return TLK_OK;

@@ -24,6 +24,7 @@ OPTIMIZERS = {"adam": OPT_ADAM, "adamw": OPT_ADAMW, "sgd": OPT_SGD}
 PACK_WRITE_ALL_GRADS = 1
 PACK_SNAPSHOTS = 2
 PACK_OWN_STREAM = 4
+PACK_PERSISTENT = 8
 BUF_PARAMS, BUF_GRADS, BUF_MOM1, BUF_MOM2, BUF_WBF16, BUF_LOSS, BUF_PIXELS, BUF_LABELS, BUF_ACTS = range(9)
 
 EXPORTS = (
