@@ -129,11 +129,17 @@ def main():
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--bf16", type=int, default=None,
                     help="1: torch.autocast(bfloat16); default 1 for the transformer / ResNet models")
+    ap.add_argument("--steps", type=int, default=0,
+                    help="run exactly this many steps and exit (a fixed-size training task, as in a "
+                         "parametric job list); 0 = the timed-window mode above")
+    ap.add_argument("--fast", type=int, default=0,
+                    help="1: the strongest plain-PyTorch job: bf16 autocast, fused Adam, no per-step "
+                         "host sync (loss read every 50 steps)")
     a = ap.parse_args()
     torch.manual_seed(a.seed)
     dev = torch.device("cuda")
     if a.bf16 is None:
-        a.bf16 = int(a.model in GPT_CFGS or a.model == "resnet18")
+        a.bf16 = int(a.model in GPT_CFGS or a.model == "resnet18" or bool(a.fast))
     if a.model in GPT_CFGS:
         cfg = GPT_CFGS[a.model]
         model = GPT(*cfg).to(dev)
@@ -144,8 +150,9 @@ def main():
     if a.model == "resnet18":
         opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
     else:
-        opt = torch.optim.Adam(model.parameters(), lr=a.lr)
+        opt = torch.optim.Adam(model.parameters(), lr=a.lr, fused=bool(a.fast))
     torch.backends.cudnn.benchmark = True
+    nstep = [0]
 
     def step():
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=bool(a.bf16)):
@@ -165,7 +172,22 @@ def main():
         opt.zero_grad(set_to_none=True)
         loss.backward()
         opt.step()
+        nstep[0] += 1
+        if a.fast and nstep[0] % 50:
+            return None
         return loss.item()
+
+    if a.steps:
+        t_start = time.time()
+        last = None
+        for _ in range(a.steps):
+            v = step()
+            last = v if v is not None else last
+        torch.cuda.synchronize()
+        el = time.time() - t_start
+        print(json.dumps({"steps": a.steps, "elapsed_s": el, "batch": a.batch, "last_loss": last,
+                          "samples_per_s": a.steps * a.batch / el}))
+        return 0
 
     warm = 0
     while warm < 3 or (not a.sync_dir and time.time() < a.t0):

@@ -158,6 +158,17 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
  * slot per input slot, no D2H copy in the stream); tlk_step_host_wait copies
  * them into losses_out.  Do not interleave with tlk_step_host without
  * waiting first. */
+/* Bytes of one step's host-input blob of a host_input pack, and the step
+ * from such a blob (H2D copies into the model's input buffers on the pack
+ * stream, one step, D2H of the per-lane losses [lanes], synchronous).
+ * Layouts (lanes outermost):
+ *   MLP / CNN: u8 pixels [lanes][batch][784], int32 labels [lanes][batch]
+ *   transformer / tiny-GPT: int32 tokens [lanes][batch][T + 1] (inputs
+ *     tokens[:, :-1], targets tokens[:, 1:])
+ *   ResNet-18: bf16 images [lanes][batch][32][32][3] (NHWC), int32 labels
+ *     [lanes][batch] */
+int tlk_pack_host_input_bytes(tlk_ctx* ctx, int32_t pack, int64_t* bytes);
+int tlk_step_host_blob(tlk_ctx* ctx, int32_t pack, const void* blob, int64_t bytes, float* losses_out);
 int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
                         float* losses_out, int64_t* ticket);
 int tlk_step_host_wait(tlk_ctx* ctx, int32_t pack, int64_t ticket);

@@ -820,7 +820,10 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int ctas = fwa_ctas > 0 ? std::min(fwa_ctas, sms) : s2 != st ? sms * 96 / 148 : sms;
+    // 96 of 148 SMs on the side branch (also when a profile step serialises
+    // the branches: the kernel is timed at its in-graph grid)
+    const bool side = fork && fwa_side != 0;
+    const int ctas = fwa_ctas > 0 ? std::min(fwa_ctas, sms) : side ? sms * 96 / 148 : sms;
     TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(std::min(ctas, L * FWA_FT)), FWA_THREADS, FWA_SMEM, s2, f));
     p.mark(s2, "fc1_wgrad_adam");
     return TLK_OK;

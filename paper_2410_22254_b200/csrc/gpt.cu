@@ -79,6 +79,18 @@ __global__ void gpt_tokens_kernel(const LaneState* __restrict__ lanes, int B, in
   }
 }
 
+// host-input packs: the tokens came from the host (tlk_step_host_blob);
+// targets are the tokens shifted by one
+__global__ void gpt_targets_kernel(const LaneState* __restrict__ lanes, int B, int T,
+                                   const int32_t* __restrict__ tokens, int32_t* __restrict__ targets) {
+  pdl_begin();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (s >= B || !lanes[j].active) return;
+  const int32_t* tk = tokens + (int64_t(j) * B + s) * (T + 1);
+  int32_t* tg = targets + (int64_t(j) * B + s) * T;
+  for (int i = 0; i < T; ++i) tg[i] = tk[i + 1];
+}
+
 // x0[row][c] = wte[tok][c] + wpe[t][c]
 __global__ void gpt_embed_kernel(const LaneState* __restrict__ lanes, GptCfg c, int B,
                                  const int32_t* __restrict__ tokens, const float* __restrict__ params,
@@ -570,6 +582,7 @@ int gpt_setup(Pack& p) {
   p.acts = base;
   p.acts_bytes = total;
   p.launches_per_step = 0;  // counted at capture (mark)
+  p.host_segs = {{b->tokens, size_t(L) * p.batch * (T + 1) * 4}};  // int32 [lanes][batch][T + 1]
   return TLK_OK;
 }
 
@@ -594,7 +607,10 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     ++count;
   };
 
-  TLK_CUDA(launch(gpt_tokens_kernel, dim3((B + 127) / 128, Lc), 128, 0, st, LS, B, T, V, b.tokens, b.targets));
+  if (p.host_input)
+    TLK_CUDA(launch(gpt_targets_kernel, dim3((B + 127) / 128, Lc), 128, 0, st, LS, B, T, b.tokens, b.targets));
+  else
+    TLK_CUDA(launch(gpt_tokens_kernel, dim3((B + 127) / 128, Lc), 128, 0, st, LS, B, T, V, b.tokens, b.targets));
   TLK_CUDA(cudaGetLastError());
   marked("tokens");
   float* x0 = c.layers ? b.L[0].xin : b.xL;

@@ -75,6 +75,12 @@ struct Pack {
   cudaEvent_t h2d_ev[2] = {nullptr, nullptr}, done_ev[2] = {nullptr, nullptr};
   int64_t host_steps = 0;
   int flags = 0;  // TLK_PACK_* (e.g. write every gradient for tests)
+  // one step's host-input blob (tlk_step_host_blob): device segments filled in order
+  struct HostSeg {
+    void* dst;
+    size_t bytes;
+  };
+  std::vector<HostSeg> host_segs;
   // named internal buffers (tlk_pack_named): activations, statistics, snapshots
   struct Named {
     std::string name;

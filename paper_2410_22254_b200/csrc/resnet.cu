@@ -1172,6 +1172,8 @@ int resnet_setup(Pack& p) {
   }
   if (snaps) p.name_buf("stem.G", R->snap_stem, size_t(L) * R->act_ls(32, 32, 64) * 4);
   p.launches_per_step = 0;
+  // bf16 [lanes][batch][32][32][3] images, then int32 [lanes][batch] labels
+  p.host_segs = {{R->xin, size_t(L) * B * IMG * 2}, {p.labels, size_t(L) * B * 4}};
   return TLK_OK;
 }
 
@@ -1196,9 +1198,11 @@ int resnet_enqueue_step(Pack& p, cudaStream_t st) {
     return dim3(unsigned(std::clamp<int64_t>((n8 + 1023) / 1024, 1, cap)), Lc);
   };
 
-  TLK_CUDA(launch(rn_inputs_kernel, dim3(B, Lc), 256, 0, st, LS, B, R.teacher, R.xin, p.labels));
-  TLK_CUDA(cudaGetLastError());
-  marked("inputs");
+  if (!p.host_input) {  // host-input packs: images and labels came from tlk_step_host_blob
+    TLK_CUDA(launch(rn_inputs_kernel, dim3(B, Lc), 256, 0, st, LS, B, R.teacher, R.xin, p.labels));
+    TLK_CUDA(cudaGetLastError());
+    marked("inputs");
+  }
   {  // dgrad weight layouts from this step's bf16 shadow
     WtTable tab{};
     int tiles = 0;

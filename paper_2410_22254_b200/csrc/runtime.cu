@@ -330,14 +330,13 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   TLK_CHECK(d || gpt || rn, TLK_EINVAL, "unknown model %d", desc->model);
   TLK_CHECK(desc->lanes >= 1 && desc->lanes <= 4096, TLK_EINVAL, "lanes must be 1..4096");
   if (rn)
-    TLK_CHECK(desc->batch >= 8 && desc->batch <= 512 && desc->batch % 8 == 0 && !desc->host_input, TLK_EINVAL,
-              "resnet18 packs: batch a multiple of 8 in [8, 512], device-generated inputs only");
+    TLK_CHECK(desc->batch >= 8 && desc->batch <= 512 && desc->batch % 8 == 0, TLK_EINVAL,
+              "resnet18 packs: batch a multiple of 8 in [8, 512]");
   else if (!gpt)
     TLK_CHECK(desc->batch >= 8 && desc->batch <= 64 && desc->batch % 8 == 0, TLK_EINVAL,
               "batch must be a multiple of 8 in [8, 64] (got %d)", desc->batch);
   else
-    TLK_CHECK(desc->batch >= 1 && desc->batch <= 4096 && !desc->host_input, TLK_EINVAL,
-              "transformer packs: batch in [1, 4096], device-generated tokens only");
+    TLK_CHECK(desc->batch >= 1 && desc->batch <= 4096, TLK_EINVAL, "transformer packs: batch in [1, 4096]");
   GptCfg gc = gpt_default(desc->model);
   if (gpt) {
     if (desc->layers > 0) gc.layers = desc->layers;
@@ -407,6 +406,8 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
     destroy_pack(*p);
     return rc;
   }
+  if (p->host_segs.empty())  // MLP / CNN: u8 pixels [lanes][batch][784], then int32 labels [lanes][batch]
+    p->host_segs = {{p->pixels, L * B * 784}, {p->labels, L * B * 4}};
   TLK_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
@@ -501,6 +502,39 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
                              p->stream));
     TLK_CUDA(cudaStreamSynchronize(p->stream));
   }
+  return TLK_OK;
+}
+
+int tlk_pack_host_input_bytes(tlk_ctx* ctx, int32_t pack, int64_t* bytes) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(bytes, TLK_EINVAL, "null argument");
+  int64_t n = 0;
+  for (const auto& sg : p->host_segs) n += int64_t(sg.bytes);
+  *bytes = n;
+  return TLK_OK;
+}
+
+int tlk_step_host_blob(tlk_ctx* ctx, int32_t pack, const void* blob, int64_t bytes, float* losses_out) {
+  Pack* p = nullptr;
+  int rc = get_pack(ctx, pack, &p);
+  if (rc) return rc;
+  TLK_CHECK(p->host_input, TLK_ESTATE, "pack was created without host_input");
+  int64_t need = 0;
+  for (const auto& sg : p->host_segs) need += int64_t(sg.bytes);
+  TLK_CHECK(blob && bytes == need, TLK_EINVAL, "host input blob of %lld bytes, the pack takes %lld",
+            (long long)bytes, (long long)need);
+  const char* src = static_cast<const char*>(blob);
+  for (const auto& sg : p->host_segs) {
+    TLK_CUDA(cudaMemcpyAsync(sg.dst, src, sg.bytes, cudaMemcpyHostToDevice, p->stream));
+    src += sg.bytes;
+  }
+  if ((rc = ensure_graph(*p, p->stream))) return rc;
+  TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
+  if (losses_out)
+    TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, size_t(p->lanes) * 4, cudaMemcpyDeviceToHost, p->stream));
+  TLK_CUDA(cudaStreamSynchronize(p->stream));
   return TLK_OK;
 }
 

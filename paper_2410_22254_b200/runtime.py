@@ -31,7 +31,7 @@ EXPORTS = (
     "tlk_abi_version", "tlk_last_error", "tlk_model_query", "tlk_model_tensor", "tlk_open",
     "tlk_close", "tlk_sync", "tlk_stream", "tlk_set_mem_limit", "tlk_mem_in_use", "tlk_pack_create",
     "tlk_pack_destroy", "tlk_pack_stream", "tlk_lane_load", "tlk_lane_release",
-    "tlk_run", "tlk_step_host", "tlk_step_host_async", "tlk_step_host_wait", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
+    "tlk_run", "tlk_step_host", "tlk_pack_host_input_bytes", "tlk_step_host_blob", "tlk_step_host_async", "tlk_step_host_wait", "tlk_lane_status_get", "tlk_lane_losses", "tlk_lane_params",
     "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
     "tlk_selftest_datagen",
@@ -221,6 +221,19 @@ class Pack:
         out = losses_out if losses_out is not None else np.empty(self.lanes, np.float32)
         check(lib().tlk_step_host(self.ctx._ctx, self.id, px.ctypes.data_as(C.c_void_p),
                                   lb.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def host_input_bytes(self) -> int:
+        n = C.c_int64()
+        check(lib().tlk_pack_host_input_bytes(self.ctx._ctx, self.id, C.byref(n)))
+        return n.value
+
+    def step_host_blob(self, blob, losses_out=None):
+        """One end-to-end step from a host blob (any model; layout in tlk.h)."""
+        blob = np.ascontiguousarray(blob)
+        out = losses_out if losses_out is not None else np.empty(self.lanes, np.float32)
+        check(lib().tlk_step_host_blob(self.ctx._ctx, self.id, blob.ctypes.data_as(C.c_void_p),
+                                       C.c_int64(blob.nbytes), out.ctypes.data_as(C.c_void_p)))
         return out
 
     def step_host_async(self, pixels, labels, losses_out) -> int:
