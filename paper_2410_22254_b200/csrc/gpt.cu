@@ -20,6 +20,7 @@
 #include "rng.cuh"
 #include "sgemm.cuh"
 #include "tgemm.cuh"
+#include "attn.cuh"
 
 namespace tlk {
 
@@ -33,11 +34,13 @@ struct LayerBufs {
   float *xin, *xmid, *st1, *st2;
   uint16_t* z;  // bf16 GELU pre-activation (the GELU backward evaluates at bf16(z))
   uint16_t *a, *qkv, *P, *y, *m, *f;
+  float* stats;  // fused attention: per-query (max * k2, 1 / sum) softmax statistics
 };
 
 struct GptBufs {
   GptCfg c;
   int N, Vp, sms;
+  bool fused_attn;  // attn.cuh kernels (T = 128 / 256) instead of the P / dS GEMM chain
   int32_t *tokens, *targets;
   std::vector<LayerBufs> L;
   float *xL, *stf, *lossrow;
@@ -497,6 +500,66 @@ Epi epi(int kind, int rows, int cols, void* out, int64_t ls, int64_t bs, int64_t
   return e;
 }
 
+// ------------------------------------------------------- fused attention --
+// Epilogue descriptors shared by the fused and the unfused attention paths.
+Epi attn_y_epi(const GptBufs& b, const LayerBufs& lb) {
+  const int64_t T = b.c.T, d = b.c.d, nd = int64_t(b.N) * d;
+  return epi(EPI_BF16, int(T), 64, lb.y, nd, T * d, 64, d);
+}
+Epi attn_dqkv_epi(const GptBufs& b, int which) {  // 0 dq, 1 dk, 2 dv
+  const int64_t T = b.c.T, d = b.c.d, nd3 = int64_t(b.N) * 3 * d;
+  Epi e = epi(EPI_BF16, int(T), 64, b.dqkv + which * d, nd3, T * 3 * d, 64, 3 * d);
+  e.colpart = b.part;  // qkv.b gradient partials
+  e.cp_ls = b.part_st;
+  e.cp_cols = int(3 * d);
+  e.cp_col0 = int(which * d);
+  return e;
+}
+EpiOps epi_ops(const Pack& p, const Epi& e) { return EpiOps{p.lane_dev, e, p.batch, p.gcfg.heads, 1}; }
+
+int attn_args(const Pack& p, const GptBufs& b, const LayerBufs& lb, AttnArgs& a) {
+  const GptCfg c = b.c;
+  const int64_t T = c.T, d = c.d, nd = int64_t(b.N) * d, nd3 = nd * 3;
+  a = AttnArgs{};
+  int rc = make_operand_map(&a.tq, op(lb.qkv, nd3, T * 3 * d, 64, 3 * d, 1, int(T), 64), false, 128, p.lanes,
+                            p.batch, c.heads);
+  if (!rc) rc = make_operand_map(&a.tk, op(lb.qkv + d, nd3, T * 3 * d, 64, 3 * d, 1, int(T), 64), false, 128,
+                                 p.lanes, p.batch, c.heads);
+  if (!rc) rc = make_operand_map(&a.tv, op(lb.qkv + 2 * d, nd3, T * 3 * d, 64, 3 * d, 1, int(T), 64), false, 128,
+                                 p.lanes, p.batch, c.heads);
+  if (!rc) rc = make_operand_map(&a.tdy, op(b.dy, nd, T * d, 64, d, 1, int(T), 64), false, 128, p.lanes, p.batch,
+                                 c.heads);
+  if (rc) return rc;
+  a.lanes = p.lane_dev;
+  a.nb = p.batch;
+  a.nh = c.heads;
+  a.items = p.lanes * p.batch * c.heads;
+  a.scale = 1.0f / sqrtf(64.f);
+  a.stats = lb.stats;
+  a.D = b.D;
+  return TLK_OK;
+}
+
+int attn_fwd(const Pack& p, const GptBufs& b, const LayerBufs& lb, cudaStream_t st) {
+  AttnArgs a;
+  if (int rc = attn_args(p, b, lb, a)) return rc;
+  a.ey = epi_ops(p, attn_y_epi(b, lb));
+  TLK_CUDA(b.c.T == 256 ? launch_attn_fwd<2>(a, b.sms, st) : launch_attn_fwd<1>(a, b.sms, st));
+  const_cast<Pack&>(p).mark(st, "attn_fwd");
+  return TLK_OK;
+}
+
+int attn_bwd(const Pack& p, const GptBufs& b, const LayerBufs& lb, cudaStream_t st) {
+  AttnArgs a;
+  if (int rc = attn_args(p, b, lb, a)) return rc;
+  a.edq = epi_ops(p, attn_dqkv_epi(b, 0));
+  a.edk = epi_ops(p, attn_dqkv_epi(b, 1));
+  a.edv = epi_ops(p, attn_dqkv_epi(b, 2));
+  TLK_CUDA(b.c.T == 256 ? launch_attn_bwd<2>(a, b.sms, st) : launch_attn_bwd<1>(a, b.sms, st));
+  const_cast<Pack&>(p).mark(st, "attn_bwd");
+  return TLK_OK;
+}
+
 #define TLK_TRY(x)              \
   do {                          \
     int rc_ = (x);              \
@@ -525,6 +588,10 @@ int gpt_setup(Pack& p) {
   }
   const int64_t L = p.lanes, N = int64_t(p.batch) * c.T, d = c.d, H = c.heads, T = c.T;
   b->N = int(N);
+  {
+    static const char* f = getenv("TLK_ATTN_FUSED");  // 0: the unfused P / dS GEMM chain
+    b->fused_attn = (T == 128 || T == 256) && !(f && f[0] == '0');
+  }
   b->Vp = (c.V + 31) / 32 * 32;
   if (b->Vp > 256) return fail(TLK_EINVAL, "gpt: vocab too large");
   // sizes (bytes) of everything, one allocation
@@ -545,7 +612,10 @@ int gpt_setup(Pack& p) {
     add(reinterpret_cast<void**>(&lb.z), L * N * 4 * d * 2);
     add(reinterpret_cast<void**>(&lb.a), L * N * d * 2);
     add(reinterpret_cast<void**>(&lb.qkv), L * N * 3 * d * 2);
-    add(reinterpret_cast<void**>(&lb.P), L * p.batch * H * T * T * 2);
+    if (b->fused_attn)
+      add(reinterpret_cast<void**>(&lb.stats), L * p.batch * H * T * 2 * 4);
+    else
+      add(reinterpret_cast<void**>(&lb.P), L * p.batch * H * T * T * 2);
     add(reinterpret_cast<void**>(&lb.y), L * N * d * 2);
     add(reinterpret_cast<void**>(&lb.m), L * N * d * 2);
     add(reinterpret_cast<void**>(&lb.f), L * N * 4 * d * 2);
@@ -560,7 +630,7 @@ int gpt_setup(Pack& p) {
   add(reinterpret_cast<void**>(&b->dxb), L * N * d * 2);
   add(reinterpret_cast<void**>(&b->dz), L * N * 4 * d * 2);
   add(reinterpret_cast<void**>(&b->dy), L * N * d * 2);
-  add(reinterpret_cast<void**>(&b->dS), L * p.batch * H * T * T * 2);
+  if (!b->fused_attn) add(reinterpret_cast<void**>(&b->dS), L * p.batch * H * T * T * 2);
   add(reinterpret_cast<void**>(&b->dqkv), L * N * 3 * d * 2);
   add(reinterpret_cast<void**>(&b->D), L * N * H * 4);
   // reduction partials: max of LN-backward (N/LNB_ROWS x 3d) and the GELU' / dq,dk,dv
@@ -634,6 +704,10 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                               N, 3 * d, d, 1, 1, "qkv")));
       ++count;
     }
+    if (b.fused_attn) {  // Y = softmax(Q K^T / sqrt(dh), causal) V, fused (attn.cuh)
+      TLK_TRY(attn_fwd(p, b, lb, st));
+      ++count;
+    } else {
     {  // P = softmax(Q K^T / sqrt(dh)), per (sequence, head)
       Epi e = epi(EPI_SOFTMAX, T, T, lb.P, pl, int64_t(H) * tt, tt, T);
       e.scale = scale;
@@ -655,6 +729,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
           p, st, op(lb.P, pl, int64_t(H) * tt, tt, T, 1, T, T),
           op(lb.qkv + 2 * d, nd3, int64_t(T) * 3 * d, dh, 1, 3 * d, dh, T), e, T, dh, T, B, H, "attn_pv")));
       ++count;
+    }
     }
     {  // xmid = xin + y Wo^T + bo
       Epi e = epi(EPI_RESADD, N, d, lb.xmid, nd, 0, 0, d);
@@ -809,6 +884,10 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_CUDA(launch(attn_rowdot_kernel, dim3((N * H + 255) / 256, Lc), 256, 0, st, LS, N, T, H, b.dy, lb.y, b.D));
       TLK_CUDA(cudaGetLastError());
       marked("attn_rowdot");
+      if (b.fused_attn) {  // dS on chip; dQ / dK / dV + qkv.b partials (attn.cuh)
+        TLK_TRY(attn_bwd(p, b, lb, st));
+        ++count;
+      } else {
       Epi e = epi(EPI_SOFTMAX_BWD, T, T, b.dS, pl, int64_t(H) * tt, tt, T);
       e.aux = lb.P;
       e.scale = scale;
@@ -855,6 +934,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                            op(b.dy, nd, int64_t(T) * d, dh, 1, d, dh, T), ev, T, dh, T, B,
                                            H, "attn_dv")));
       count += 4;
+      }
       TLK_CUDA(launch(reduce_parts8_kernel, dim3((3 * d + 31) / 32, Lc), 256, 0, st, LS, b.part, b.part_st,
                       (N + 31) / 32, 3 * d, G, PS, O(T_LAYER(l, K_AB))));
       marked("bias_reduce");
