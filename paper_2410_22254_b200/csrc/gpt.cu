@@ -40,6 +40,7 @@ struct LayerBufs {
 struct GptBufs {
   GptCfg c;
   int N, Vp, sms;
+  unsigned long long* atrace = nullptr;  // TLK_ATTN_TRACE=1: [fwd, bwd][64 tiles][32] event clocks
   bool fused_attn;  // attn.cuh kernels (T = 128 / 256) instead of the P / dS GEMM chain
   int32_t *tokens, *targets;
   std::vector<LayerBufs> L;
@@ -515,7 +516,6 @@ Epi attn_dqkv_epi(const GptBufs& b, int which) {  // 0 dq, 1 dk, 2 dv
   e.cp_col0 = int(which * d);
   return e;
 }
-EpiOps epi_ops(const Pack& p, const Epi& e) { return EpiOps{p.lane_dev, e, p.batch, p.gcfg.heads, 1}; }
 
 int attn_args(const Pack& p, const GptBufs& b, const LayerBufs& lb, AttnArgs& a) {
   const GptCfg c = b.c;
@@ -537,13 +537,21 @@ int attn_args(const Pack& p, const GptBufs& b, const LayerBufs& lb, AttnArgs& a)
   a.scale = 1.0f / sqrtf(64.f);
   a.stats = lb.stats;
   a.D = b.D;
+  a.trace = nullptr;
   return TLK_OK;
 }
 
 int attn_fwd(const Pack& p, const GptBufs& b, const LayerBufs& lb, cudaStream_t st) {
   AttnArgs a;
   if (int rc = attn_args(p, b, lb, a)) return rc;
-  a.ey = epi_ops(p, attn_y_epi(b, lb));
+  a.ey = attn_y_epi(b, lb);
+  a.trace = b.atrace;
+  {
+    const int64_t T = b.c.T, d = b.c.d, nd = int64_t(b.N) * d;
+    if (int rc = make_operand_map(&a.to[0], op(lb.y, nd, T * d, 64, d, 1, int(T), 64), false, 32, p.lanes,
+                                  p.batch, b.c.heads))
+      return rc;
+  }
   TLK_CUDA(b.c.T == 256 ? launch_attn_fwd<2>(a, b.sms, st) : launch_attn_fwd<1>(a, b.sms, st));
   const_cast<Pack&>(p).mark(st, "attn_fwd");
   return TLK_OK;
@@ -552,9 +560,17 @@ int attn_fwd(const Pack& p, const GptBufs& b, const LayerBufs& lb, cudaStream_t 
 int attn_bwd(const Pack& p, const GptBufs& b, const LayerBufs& lb, cudaStream_t st) {
   AttnArgs a;
   if (int rc = attn_args(p, b, lb, a)) return rc;
-  a.edq = epi_ops(p, attn_dqkv_epi(b, 0));
-  a.edk = epi_ops(p, attn_dqkv_epi(b, 1));
-  a.edv = epi_ops(p, attn_dqkv_epi(b, 2));
+  a.edq = attn_dqkv_epi(b, 0);
+  a.edk = attn_dqkv_epi(b, 1);
+  a.edv = attn_dqkv_epi(b, 2);
+  a.trace = b.atrace ? b.atrace + 64 * 32 : nullptr;
+  {
+    const int64_t T = b.c.T, d = b.c.d, nd3 = int64_t(b.N) * 3 * d;
+    for (int i = 0; i < 3; ++i)
+      if (int rc = make_operand_map(&a.to[i], op(b.dqkv + i * d, nd3, T * 3 * d, 64, 3 * d, 1, int(T), 64), false,
+                                    32, p.lanes, p.batch, b.c.heads))
+        return rc;
+  }
   TLK_CUDA(b.c.T == 256 ? launch_attn_bwd<2>(a, b.sms, st) : launch_attn_bwd<1>(a, b.sms, st));
   const_cast<Pack&>(p).mark(st, "attn_bwd");
   return TLK_OK;
@@ -590,7 +606,9 @@ int gpt_setup(Pack& p) {
   b->N = int(N);
   {
     static const char* f = getenv("TLK_ATTN_FUSED");  // 0: the unfused P / dS GEMM chain
-    b->fused_attn = (T == 128 || T == 256) && !(f && f[0] == '0');
+    // attn.cuh lists a CTA's work items in shared memory (ATT_MAX_ITEMS per CTA)
+    b->fused_attn = (T == 128 || T == 256) && !(f && f[0] == '0') &&
+                    L * p.batch * H <= int64_t(b->sms) * ATT_MAX_ITEMS;
   }
   b->Vp = (c.V + 31) / 32 * 32;
   if (b->Vp > 256) return fail(TLK_EINVAL, "gpt: vocab too large");
@@ -652,6 +670,14 @@ int gpt_setup(Pack& p) {
   p.acts = base;
   p.acts_bytes = total;
   p.launches_per_step = 0;  // counted at capture (mark)
+  if (b->fused_attn && getenv("TLK_ATTN_TRACE") && getenv("TLK_ATTN_TRACE")[0] == '1') {
+    void* tb = nullptr;
+    int rc2 = pack_alloc(p, &tb, 2 * 64 * 32 * 8);
+    if (rc2) return rc2;
+    TLK_CUDA(cudaMemset(tb, 0, 2 * 64 * 32 * 8));
+    b->atrace = static_cast<unsigned long long*>(tb);
+    p.name_buf("attn.trace", tb, 2 * 64 * 32 * 8);
+  }
   p.host_segs = {{b->tokens, size_t(L) * p.batch * (T + 1) * 4}};  // int32 [lanes][batch][T + 1]
   return TLK_OK;
 }

@@ -62,6 +62,13 @@ TLK_DEV void tma_store_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, in
                "r"(src), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+TLK_DEV void tma_store_5d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 TLK_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N bulk groups still READ their shared-memory source
 template <int N>
