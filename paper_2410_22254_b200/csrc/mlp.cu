@@ -1,8 +1,9 @@
 // MNIST MLP 784-512-512-10 pack: one training step for every lane.
 //
-// Launch sequence (9 kernels, captured once into a CUDA graph):
+// Batch 64 (the configs): mlp2.cu, two launches per step.  Other batch sizes
+// (and TLK_MLP_V1=1): 8 kernels, captured once into a CUDA graph:
 //   inputs -> fc1 fwd -> fc2 fwd -> head(fc3 + CE + bwd) -> fc2 wgrad ->
-//   fc2 dgrad(+mask, fc1 bias grad) -> fc1 wgrad -> optimizer -> end_step
+//   fc2 dgrad(+mask, fc1 bias grad) -> fc1 wgrad -> optimizer (+ end of step)
 #include "linear.cuh"
 #include "pack.cuh"
 
@@ -14,6 +15,9 @@ struct MlpScratch {
 };
 
 }  // namespace
+
+bool mlp2_enabled(const Pack& p);
+int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint16_t* dz1, uint16_t* dz2);
 
 int mlp_setup(Pack& p) {
   const size_t n = size_t(p.lanes) * p.batch * 512 * sizeof(uint16_t);
@@ -28,7 +32,7 @@ int mlp_setup(Pack& p) {
   p.acts_bytes = 4 * n;
   p.scratch = s;
   p.scratch_free = [](void* q) { delete static_cast<MlpScratch*>(q); };
-  p.launches_per_step = 8;
+  p.launches_per_step = mlp2_enabled(p) ? 2 : 8;
   return TLK_OK;
 }
 
@@ -40,6 +44,7 @@ int mlp_enqueue_step(Pack& p, cudaStream_t st) {
   const int64_t o_w1 = tensor_offset(d, 0), o_b1 = tensor_offset(d, 1);
   const int64_t o_w2 = tensor_offset(d, 2), o_b2 = tensor_offset(d, 3);
   const int64_t o_w3 = tensor_offset(d, 4), o_b3 = tensor_offset(d, 5);
+  if (mlp2_enabled(p)) return mlp2_enqueue_step(p, st, s.h1, s.h2, s.dz1, s.dz2);  // mlp2.cu: 2 launches
   int rc;
   if ((rc = enqueue_inputs(p, st))) return rc;
 

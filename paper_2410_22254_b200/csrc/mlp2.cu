@@ -1,0 +1,667 @@
+// MNIST MLP 784-512-512-10 pack, batch 64: one training step in TWO launches.
+//
+//   mlp_step_kernel   one 4-CTA cluster per lane, CTA c owning the 128-wide
+//                     slice c of every hidden layer:
+//                       inputs (counter RNG / host bytes, teacher labels) ->
+//                       fc1 = W1[c] x^T (tcgen05, K = 784) -> h1 slice ->
+//                       h1 slices exchanged by bulk copies into every CTA's
+//                       shared memory -> fc2 = W2[c] h1^T -> h2 slice ->
+//                       partial logits exchanged (st.async) -> CE, dz3 (every
+//                       CTA, identical) -> dz2 slice, fc3 / fc2.b / fc3.b
+//                       grads, loss, step scalars -> dz2 slices exchanged ->
+//                       fc2 dgrad = W2[:, c]^T dz2^T -> dz1 slice, fc1.b grad.
+//                     W1 / W2 / W2^T tiles stream through one TMA ring; the
+//                     exchanges complete on mbarriers (no cluster barrier
+//                     between the phases).
+//   mlp_wgrad_adam_kernel  dW^T tiles (M = 128 input features, N = 128
+//                     outputs, K = batch, both operands MN-major TMA boxes)
+//                     with the optimizer update fused into the epilogue
+//                     (TMEM lane = input feature: a warp's accesses of one
+//                     output row are one 128-B line); one extra CTA per lane
+//                     updates the small tensors (fc1.b, fc2.b, fc3.w, fc3.b);
+//                     the last CTA of a lane ends its step.
+//
+// Numerics are the oracle's (oracle/models.py::mlp_step, bf16 mode) and the
+// 8-kernel path's (mlp.cu) except for fp32 summation order: bf16 GEMM
+// operands, fp32 accumulation, h / dz stored bf16, the classifier head on the
+// fp32 master fc3 weights, the IEEE-exact optimizer (models.cuh opt_update_k).
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "linear.cuh"
+#include "pack.cuh"
+#include "rng.cuh"
+#include "tma.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tlk {
+namespace {
+
+constexpr int MB = 64;         // batch (UMMA N)
+constexpr int MC = 4;          // CTAs per lane (cluster)
+constexpr int MH = 512;        // hidden width
+constexpr int MIN = 784;       // input width
+constexpr int MKB1 = 13;       // fc1 k-blocks (784 -> 832, zero padded)
+constexpr uint32_t KBLK = MB * 128;   // one 64-deep k-block of a 64-row operand (8 KB)
+constexpr uint32_t ABLK = 128 * 128;  // one 64-deep k-block of a 128-row operand (16 KB)
+constexpr int MSTAGES = 3;
+constexpr int M_THREADS = 256;  // warps 0-3: TMEM quarters, 4: TMA, 5: MMA, 6-7: labels
+// dynamic shared memory: X (fc1 B operand, 13 k-blocks) | H1 (8 k-blocks) | W ring
+constexpr uint32_t SM_X = 0, SM_H1 = MKB1 * KBLK, SM_RING = SM_H1 + 8 * KBLK;
+constexpr uint32_t M_SMEM = SM_RING + MSTAGES * ABLK + 1024;
+// X is dead once fc1 has completed; it then holds DZ2 (8 k-blocks), the
+// partial-logit exchange, dz3, h2^T and the fc3 weight slice
+constexpr uint32_t SM_DZ2 = 0, SM_PLOG = 8 * KBLK, SM_DZ3 = SM_PLOG + MC * 640 * 4,
+                   SM_HS = SM_DZ3 + MB * CLASSES * 4, SM_W3 = SM_HS + MB * 136 * 2;
+static_assert(SM_W3 + CLASSES * 128 * 4 <= MKB1 * KBLK, "head scratch fits in X");
+
+struct MlpArgs {
+  CUtensorMap w1, w2, w2t;  // bf16 shadows: W1 {784, 512, lane} box {64,128}; W2 {512, 512, lane}
+                            // box {64,128}; W2 as MN-major A of the dgrad, box {64, 64}
+  LaneState* lanes;
+  const int8_t* teacher;
+  uint8_t* px;
+  int32_t* labels;
+  uint16_t* x;
+  const float* params;
+  float* grads;
+  int64_t stride, o_b1, o_b2, o_w3, o_b3;
+  uint16_t *h1, *h2, *dz1, *dz2;  // [lane][64][512]
+  float *loss, *last_loss;
+  int max_steps, host_input;
+};
+
+TLK_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// shared::cta -> shared::cluster bulk copy completing on the destination CTA's mbarrier
+TLK_DEV void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst),
+               "r"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+TLK_DEV void st_async_f32(uint32_t dst, float v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(__float_as_uint(v)), "r"(mbar)
+               : "memory");
+}
+TLK_DEV void fence_proxy_async_cluster() { asm volatile("fence.proxy.async.shared::cluster;" ::: "memory"); }
+
+// mbarrier wait; -DTLK_HANG_DEBUG: bounded, reports the waiting site and traps
+#ifdef TLK_HANG_DEBUG
+TLK_DEV void mwait(uint64_t* bar, uint32_t parity, int tag) {
+  const uint32_t addr = smem_u32(bar);
+  for (long long i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (i == (1ll << 24)) {
+      printf("mlp2 hang: tag %d block (%d,%d) thread %d parity %u\n", tag, blockIdx.x, blockIdx.y, threadIdx.x, parity);
+      return;  // debug build: give up (wrong numbers) so the kernel ends and printf flushes
+    }
+  }
+}
+#else
+TLK_DEV void mwait(uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); }
+#endif
+
+// element (row s, k) of a 64-row K-major SW128 operand built from 8 KB k-blocks
+TLK_DEV uint32_t kmaj_off(int s, int k) {
+  return uint32_t(k >> 6) * KBLK + sw128(uint32_t(s), uint32_t((k & 63) >> 3)) + uint32_t(k & 7) * 2;
+}
+
+__global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
+    mlp_step_kernel(const __grid_constant__ MlpArgs a) {
+  constexpr uint32_t IDESC = umma_idesc_bf16(128, MB, false, false);
+  constexpr uint32_t IDESC_T = umma_idesc_bf16(128, MB, true, false);
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[MSTAGES], empty[MSTAGES], acc[3], h1_loc, h1_rem, dz2_loc, dz2_rem, plog_rem;
+  __shared__ uint32_t tmem_s;
+  __shared__ int32_t lbl[MB];
+  __shared__ float lossb[MB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = int(cluster.block_rank()), j = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sb = smem_u32(smem);
+  pdl_begin();  // lane state and weights come from the previous step
+  const bool active = a.lanes[j].active;  // uniform over the cluster
+  if (!active) return;
+  if (tid == 0) {
+    for (int s = 0; s < MSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 3; ++i) mbar_init(&acc[i], 1);
+    mbar_init(&h1_loc, 1);
+    mbar_init(&h1_rem, 1);
+    mbar_init(&dz2_loc, 1);
+    mbar_init(&dz2_rem, 1);
+    mbar_init(&plog_rem, 1);
+    fence_mbar_init();
+    // the bytes the three peers will deliver into this CTA
+    mbar_expect_tx(&h1_rem, (MC - 1) * 2 * KBLK);
+    mbar_expect_tx(&dz2_rem, (MC - 1) * 2 * KBLK);
+    mbar_expect_tx(&plog_rem, (MC - 1) * 640 * 4);
+  }
+  if (warp == 5) tmem_alloc<256>(&tmem_s);
+  const LaneState ls = a.lanes[j];
+  const uint64_t key = rng_key(ls.seed, STREAM_DATA, uint64_t(ls.steps_done));
+  // ---- inputs: x (bf16 k/256) of all 64 samples as fc1's K-major B operand;
+  // CTA c also writes samples [16c, 16c+16) of px / x to global
+  for (int i = tid; i < MB * MKB1 * 8; i += M_THREADS) {
+    const int s = i / (MKB1 * 8), q = i % (MKB1 * 8);  // q: 8-pixel word
+    uint64_t wv = 0;
+    if (q < WORDS_PER_SAMPLE) {
+      const size_t g = (size_t(j) * MB + s) * WORDS_PER_SAMPLE + q;
+      wv = a.host_input ? reinterpret_cast<const uint64_t*>(a.px)[g]
+                        : rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
+    }
+    uint32_t w4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      w4[e] = pack_bf2(float((wv >> (16 * e)) & 0xFF) * (1.0f / 256.0f), float((wv >> (16 * e + 8)) & 0xFF) * (1.0f / 256.0f));
+    const uint4 v4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    *reinterpret_cast<uint4*>(smem + SM_X + (q >> 3) * KBLK + sw128(s, q & 7)) = v4;
+    if (q < WORDS_PER_SAMPLE && (s >> 4) == c) {
+      const size_t g = (size_t(j) * MB + s) * WORDS_PER_SAMPLE + q;
+      if (!a.host_input) reinterpret_cast<uint64_t*>(a.px)[g] = wv;
+      reinterpret_cast<uint4*>(a.x)[g] = v4;
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  cluster.sync();  // every CTA's mbarriers are initialised before any remote arrival
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  const float* P = a.params + j * a.stride;
+  float* G = a.grads + j * a.stride;
+
+  if (warp == 4) {  // ------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&a.w1);
+      tma_prefetch_desc(&a.w2);
+      tma_prefetch_desc(&a.w2t);
+      for (int it = 0; it < MKB1 + 16; ++it) {
+        const int s = it % MSTAGES;
+        if (it >= MSTAGES) mwait(&empty[s], ((it / MSTAGES) - 1) & 1, 2);
+        mbar_expect_tx(&full[s], ABLK);
+        const uint32_t dst = sb + SM_RING + s * ABLK;
+        if (it < MKB1) {
+          tma_load_3d(dst, &a.w1, it * 64, c * 128, j, &full[s]);
+        } else if (it < MKB1 + 8) {
+          tma_load_3d(dst, &a.w2, (it - MKB1) * 64, c * 128, j, &full[s]);
+        } else {
+          const int kb = it - MKB1 - 8;  // W2[kb*64 .. +64 o2][c*128 .. +128 o1], o1 contiguous
+          tma_load_3d(dst, &a.w2t, c * 128, kb * 64, j, &full[s]);
+          tma_load_3d(dst + 8192, &a.w2t, c * 128 + 64, kb * 64, j, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 5) {  // -------------------------------------- MMA issuer
+    if (lane == 0) {
+      int it = 0;
+      auto gemm = [&](uint32_t d, uint32_t bbase, int nkb, bool amn, int ai) {
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % MSTAGES;
+          mwait(&full[s], (it / MSTAGES) & 1, 3);
+          tc_fence_after();
+          const uint32_t as = sb + SM_RING + s * ABLK;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = amn ? umma_desc_sw128(as + kk * 2048, 8192, 1024) : umma_desc_sw128(as + kk * 32, 16, 1024);
+            mma_bf16(d, ad, umma_desc_sw128(bbase + kb * KBLK + kk * 32, 16, 1024), amn ? IDESC_T : IDESC,
+                     (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc[ai]);
+      };
+      gemm(tmem, sb + SM_X, MKB1, false, 0);  // fc1
+      mwait(&h1_loc, 0, 4);
+      mwait(&h1_rem, 0, 5);
+      tc_fence_after();
+      gemm(tmem + 64, sb + SM_H1, 8, false, 1);  // fc2
+      mwait(&dz2_loc, 0, 6);
+      mwait(&dz2_rem, 0, 7);
+      tc_fence_after();
+      gemm(tmem + 128, sb + SM_DZ2, 8, true, 2);  // fc2 dgrad
+    }
+  } else if (warp >= 6) {  // --------------------------------- teacher labels
+    const int s = tid - 192;  // one sample per thread
+    if (a.host_input) {
+      lbl[s] = a.labels[size_t(j) * MB + s];
+    } else {
+      int accv[CLASSES];
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) accv[cl] = 0;
+      for (int q = 0; q < WORDS_PER_SAMPLE; ++q) {
+        const uint64_t wv = rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t pw = uint32_t(wv >> (32 * h));
+#pragma unroll
+          for (int cl = 0; cl < CLASSES; ++cl) {
+            const int tw = reinterpret_cast<const int*>(a.teacher + cl * PIXELS)[2 * q + h];
+            int tp, ts;
+            asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(tp) : "r"(tw), "r"(pw), "r"(0));
+            asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts) : "r"(tw), "r"(0x01010101u), "r"(0));
+            accv[cl] += 2 * tp - 255 * ts;
+          }
+        }
+      }
+      int best = 0, bestv = 0;
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl)
+        if (cl == 0 || accv[cl] > bestv) {
+          best = cl;
+          bestv = accv[cl];
+        }
+      lbl[s] = best;
+      if (c == 0) a.labels[size_t(j) * MB + s] = best;
+    }
+    named_bar_arrive(2, 192);  // lbl[] is ready for the cross-entropy (warps 0-3 sync on it)
+  } else {  // ------------------------------- TMEM-quarter warps 0..3 (row o)
+    const int q = warp, r = q * 32 + lane, o = c * 128 + r;  // r: row of the slice, o: unit
+    const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
+    float v[MB];
+    // fc1 -> h1 = bf16(relu(acc + b1)): own H1 k-blocks (2c, 2c+1) + global
+    mwait(&acc[0], 0, 8);
+    tc_fence_after();
+    tmem_ld64(tq, v);
+    {
+      const float bb = P[a.o_b1 + o];
+      uint16_t* hg = a.h1 + size_t(j) * MB * MH + o;
+#pragma unroll
+      for (int s = 0; s < MB; ++s) {
+        const uint16_t h = f2bf(fmaxf(v[s] + bb, 0.0f));
+        *reinterpret_cast<uint16_t*>(smem + SM_H1 + kmaj_off(s, o)) = h;
+        hg[size_t(s) * MH] = h;
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (tid == 0) {  // this CTA's 16 KB of H1 -> every peer's H1 (same offset)
+      mbar_arrive(&h1_loc);
+      const uint32_t src = sb + SM_H1 + 2 * c * KBLK;
+      for (int pr = 1; pr < MC; ++pr) {
+        const uint32_t peer = uint32_t((c + pr) % MC);
+        bulk_s2cluster(mapa(src, peer), src, 2 * KBLK, mapa(smem_u32(&h1_rem), peer));
+      }
+    }
+    // fc2 -> h2 = bf16(relu(acc + b2)) (registers, global, h2^T in smem)
+    mwait(&acc[1], 0, 9);
+    tc_fence_after();
+    tmem_ld64(tq + 64, v);
+    {
+      const float bb = P[a.o_b2 + o];
+      uint16_t* hg = a.h2 + size_t(j) * MB * MH + o;
+      uint16_t* hs = reinterpret_cast<uint16_t*>(smem + SM_HS);
+#pragma unroll
+      for (int s = 0; s < MB; ++s) {
+        const uint16_t h = f2bf(fmaxf(v[s] + bb, 0.0f));
+        v[s] = bf2f(h);
+        hs[s * 136 + r] = h;
+        hg[size_t(s) * MH] = h;
+      }
+      float* w3s = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice] (fp32 master)
+      for (int i = r; i < CLASSES * 128; i += 128) w3s[i] = P[a.o_w3 + (i >> 7) * MH + c * 128 + (i & 127)];
+    }
+    named_bar_sync(1, 128);
+    // partial logits of this slice: plog[c][s * 10 + cl] in every CTA of the cluster
+    {
+      const uint16_t* hs = reinterpret_cast<const uint16_t*>(smem + SM_HS);
+      const float* w3s = reinterpret_cast<const float*>(smem + SM_W3);
+      float* plog = reinterpret_cast<float*>(smem + SM_PLOG);
+      for (int i = r; i < MB * CLASSES; i += 128) {
+        const int s = i / CLASSES, cl = i % CLASSES;
+        float accv = 0.f;
+#pragma unroll 8
+        for (int u = 0; u < 128; ++u) accv += bf2f(hs[s * 136 + u]) * w3s[cl * 128 + u];
+        plog[c * 640 + i] = accv;
+        const uint32_t la = smem_u32(&plog[c * 640 + i]);
+        for (int pr = 1; pr < MC; ++pr) {
+          const uint32_t peer = uint32_t((c + pr) % MC);
+          st_async_f32(mapa(la, peer), accv, mapa(smem_u32(&plog_rem), peer));
+        }
+      }
+    }
+    mwait(&plog_rem, 0, 10);
+    named_bar_sync(2, 192);  // with the label warps: lbl[] written; also orders the local partials
+    // logits (ranks summed in order, + fc3.b), cross entropy, dz3 = (softmax - onehot) / B
+    float* dz3 = reinterpret_cast<float*>(smem + SM_DZ3);
+    if (r < MB) {
+      const float* plog = reinterpret_cast<const float*>(smem + SM_PLOG);
+      float l[CLASSES];
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) sacc += plog[k * 640 + r * CLASSES + cl];
+        l[cl] = sacc + P[a.o_b3 + cl];
+      }
+      const int y = lbl[r];
+      float m = l[0];
+#pragma unroll
+      for (int cl = 1; cl < CLASSES; ++cl) m = fmaxf(m, l[cl]);
+      float e[CLASSES], ssum = 0.f;
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) {
+        e[cl] = expf(l[cl] - m);
+        ssum += e[cl];
+      }
+      lossb[r] = (m + logf(ssum)) - l[y];
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) dz3[r * CLASSES + cl] = (e[cl] / ssum - (cl == y ? 1.0f : 0.0f)) / float(MB);
+    }
+    named_bar_sync(1, 128);
+    if (c == 0 && r == 0) {  // loss, fc3.b grad, this step's optimizer scalars
+      float sl = 0.f;
+      for (int s = 0; s < MB; ++s) sl += lossb[s];
+      const float L = sl / float(MB);
+      LaneState& st = a.lanes[j];
+      a.loss[size_t(j) * a.max_steps + st.steps_done] = L;
+      a.last_loss[j] = L;
+      lane_step_scalars(st);
+    }
+    if (c == 0 && r >= 32 && r < 32 + CLASSES) {
+      const int cl = r - 32;
+      float sacc = 0.f;
+      for (int s = 0; s < MB; ++s) sacc += dz3[s * CLASSES + cl];
+      G[a.o_b3 + cl] = sacc;
+    }
+    // dz2 = bf16(dz3 W3[:, o] * [h2 > 0]), fc2.b / fc3.w grads of unit o
+    {
+      const float* w3s = reinterpret_cast<const float*>(smem + SM_W3);
+      float w3o[CLASSES];
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) w3o[cl] = w3s[cl * 128 + r];
+      uint16_t* zg = a.dz2 + size_t(j) * MB * MH + o;
+      float db = 0.f;
+#pragma unroll 4
+      for (int s = 0; s < MB; ++s) {
+        float dh = 0.f;
+#pragma unroll
+        for (int cl = 0; cl < CLASSES; ++cl) dh += dz3[s * CLASSES + cl] * w3o[cl];
+        const uint16_t z = f2bf(v[s] > 0.0f ? dh : 0.0f);
+        *reinterpret_cast<uint16_t*>(smem + SM_DZ2 + kmaj_off(s, o)) = z;
+        zg[size_t(s) * MH] = z;
+        db += bf2f(z);
+      }
+      G[a.o_b2 + o] = db;
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) {
+        float gw = 0.f;
+        for (int s = 0; s < MB; ++s) gw += dz3[s * CLASSES + cl] * v[s];
+        G[a.o_w3 + cl * MH + o] = gw;
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (tid == 0) {  // this CTA's 16 KB of DZ2 -> every peer
+      mbar_arrive(&dz2_loc);
+      const uint32_t src = sb + SM_DZ2 + 2 * c * KBLK;
+      for (int pr = 1; pr < MC; ++pr) {
+        const uint32_t peer = uint32_t((c + pr) % MC);
+        bulk_s2cluster(mapa(src, peer), src, 2 * KBLK, mapa(smem_u32(&dz2_rem), peer));
+      }
+    }
+    // fc2 dgrad -> dz1 = bf16(acc * [h1 > 0]) of input unit o, fc1.b grad
+    mwait(&acc[2], 0, 11);
+    tc_fence_after();
+    tmem_ld64(tq + 128, v);
+    {
+      uint16_t* zg = a.dz1 + size_t(j) * MB * MH + o;
+      float db = 0.f;
+#pragma unroll
+      for (int s = 0; s < MB; ++s) {
+        const uint16_t h = *reinterpret_cast<const uint16_t*>(smem + SM_H1 + kmaj_off(s, o));
+        const uint16_t z = f2bf(bf2f(h) > 0.0f ? v[s] : 0.0f);
+        zg[size_t(s) * MH] = z;
+        db += bf2f(z);
+      }
+      G[a.o_b1 + o] = db;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<256>(tmem);
+  cluster.sync();  // peers have received every copy out of this CTA's shared memory
+}
+
+// ---------------------------------------------------- fused wgrad + update --
+struct MlpWArgs {
+  CUtensorMap x, h1, dz1, dz2;  // [lane][64][width] bf16 as MN-major boxes {64 units, 64 samples}
+  LaneState* lanes;
+  float *params, *grads, *m1, *m2;
+  uint16_t* wbf;
+  int64_t stride, o_w1, o_b1, o_w2, o_b2, o_w3, o_b3;
+  int write_grads;
+};
+constexpr int W1_MT = 7, W_NT = 4;               // W1^T: 7 x 4 tiles, W2^T: 4 x 4
+constexpr int W_TILES = W1_MT * W_NT + W_NT * W_NT;  // + 1 small-tensor CTA
+constexpr int W_THREADS = 128;
+
+template <int KIND>
+TLK_DEV void adam_cols(const LaneState& s, float* p, float* m1, float* m2, uint16_t* wbf, float* gout,
+                       int64_t rstride, const float (&g)[32]) {
+#pragma unroll
+  for (int c0 = 0; c0 < 32; c0 += 8) {  // 8 columns: 24 loads in flight, then the updates
+    float pv[8], mv[8], vv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t o = (c0 + i) * rstride;
+      pv[i] = p[o];
+      mv[i] = m1[o];
+      vv[i] = KIND != TLK_OPT_SGD ? m2[o] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t o = (c0 + i) * rstride;
+      opt_update_k<KIND>(s, pv[i], g[c0 + i], mv[i], vv[i]);
+      p[o] = pv[i];
+      m1[o] = mv[i];
+      if constexpr (KIND != TLK_OPT_SGD) m2[o] = vv[i];
+      wbf[o] = f2bf(pv[i]);
+      if (gout) gout[o] = g[c0 + i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_constant__ MlpWArgs a) {
+  constexpr uint32_t IDESC = umma_idesc_bf16(128, 128, true, true);
+  pdl_begin();
+  const int j = blockIdx.y, t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef TLK_HANG_DEBUG
+  if (tid == 0 && t < 2) printf("wgrad enter %d %d\n", t, j);
+#endif
+  LaneState* lsp = a.lanes + j;
+  if (!lsp->active) return;
+  const LaneState s = *lsp;
+  const int64_t L0 = int64_t(j) * a.stride;
+  if (t < W_TILES) {
+    extern __shared__ uint8_t wsm_raw[];
+    uint8_t* sm = wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u);  // 2 x 16 KB (SW128 boxes)
+    __shared__ __align__(8) uint64_t full, done;
+    __shared__ uint32_t tmem_s;
+    const bool w1 = t < W1_MT * W_NT;
+    const int tt = w1 ? t : t - W1_MT * W_NT;
+    const int mt = tt / W_NT, nt = tt % W_NT;  // M = input features, N = outputs
+    const int in = w1 ? MIN : MH;
+    const CUtensorMap* am = w1 ? &a.x : &a.h1;
+    const CUtensorMap* bm = w1 ? &a.dz1 : &a.dz2;
+    if (tid == 0) {
+      mbar_init(&full, 1);
+      mbar_init(&done, 1);
+      fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<128>(&tmem_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_s, sb = smem_u32(sm);
+#ifdef TLK_HANG_DEBUG
+    if (tid == 0 && t < 2) printf("wgrad alloc %d %d tmem %u sb %u\n", t, j, tmem, sb);
+#endif
+    if (tid == 0) {
+      // a box that lies wholly outside the tensor never completes its
+      // transaction: skip it (the rows it would hold are never stored)
+      const bool a_hi = mt * 128 + 64 < in;
+      mbar_expect_tx(&full, (a_hi ? 4 : 3) * 8192);
+      tma_load_3d(sb, am, mt * 128, 0, j, &full);
+      if (a_hi) tma_load_3d(sb + 8192, am, mt * 128 + 64, 0, j, &full);
+      tma_load_3d(sb + 16384, bm, nt * 128, 0, j, &full);
+      tma_load_3d(sb + 24576, bm, nt * 128 + 64, 0, j, &full);
+      mwait(&full, 0, 12);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16(tmem, umma_desc_sw128(sb + kk * 2048, 8192, 1024),
+                 umma_desc_sw128(sb + 16384 + kk * 2048, 8192, 1024), IDESC, kk > 0 ? 1u : 0u);
+      mma_commit(&done);
+    }
+    mwait(&done, 0, 13);
+    tc_fence_after();
+    const int i = mt * 128 + warp * 32 + lane;  // input feature (TMEM lane)
+    // tcgen05.ld is warp-collective: every lane of a warp that owns any valid
+    // row loads; only the rows below `in` update parameters
+    if (mt * 128 + warp * 32 < in) {
+      const int64_t base = L0 + (w1 ? a.o_w1 : a.o_w2) + int64_t(nt * 128) * in + i;  // element (o = nt*128, i)
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float g[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c0, g);
+        if (i >= in) continue;
+        const int64_t e = base + int64_t(c0) * in;
+        float* gout = a.write_grads ? a.grads + e : nullptr;
+        if (s.optimizer == TLK_OPT_SGD)
+          adam_cols<TLK_OPT_SGD>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
+        else if (s.optimizer == TLK_OPT_ADAMW)
+          adam_cols<TLK_OPT_ADAMW>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
+        else
+          adam_cols<TLK_OPT_ADAM>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
+  } else {  // the small tensors: fc1.b, fc2.b, fc3.w, fc3.b (grads written by the step kernel)
+    const int64_t seg[4][2] = {{a.o_b1, MH}, {a.o_b2, MH}, {a.o_w3, CLASSES * MH}, {a.o_b3, CLASSES}};
+    for (int k = 0; k < 4; ++k)
+      for (int u = tid; u < seg[k][1]; u += W_THREADS) {
+        const int64_t e = L0 + seg[k][0] + u;
+        float p = a.params[e], m = a.m1[e], v = a.m2[e];
+        opt_update(s, p, a.grads[e], m, v);
+        a.params[e] = p;
+        a.m1[e] = m;
+        a.m2[e] = v;
+        a.wbf[e] = f2bf(p);
+      }
+  }
+  // the last CTA of this lane to finish ends the lane's step
+#ifdef TLK_HANG_DEBUG
+  if (tid == 0 && t < 1) printf("wgrad tail %d %d\n", t, j);
+#endif
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&lsp->done_ctas, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      lsp->done_ctas = 0;
+      lane_end_step(*lsp);
+    }
+  }
+}
+
+struct Mlp2 {
+  MlpArgs k1;
+  MlpWArgs k2;
+};
+
+}  // namespace
+
+bool mlp2_enabled(const Pack& p) {
+  static const char* e = getenv("TLK_MLP_V1");  // 1: the 8-kernel path for every MLP pack
+  return p.batch == MB && !(e && e[0] == '1');
+}
+
+int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint16_t* dz1, uint16_t* dz2) {
+  const ModelDef& d = *p.def;
+  const int L = p.lanes;
+  MlpArgs k{};
+  const int64_t o_w1 = tensor_offset(d, 0), o_w2 = tensor_offset(d, 2);
+  int rc = make_tmap_bf16_3d(&k.w1, p.wbf + o_w1, MIN, MH, L, MIN * 2, uint64_t(p.stride) * 2, 64, 128);
+  if (!rc) rc = make_tmap_bf16_3d(&k.w2, p.wbf + o_w2, MH, MH, L, MH * 2, uint64_t(p.stride) * 2, 64, 128);
+  if (!rc) rc = make_tmap_bf16_3d(&k.w2t, p.wbf + o_w2, MH, MH, L, MH * 2, uint64_t(p.stride) * 2, 64, 64);
+  if (rc) return rc;
+  k.lanes = p.lane_dev;
+  k.teacher = p.teacher;
+  k.px = p.pixels;
+  k.labels = p.labels;
+  k.x = p.x;
+  k.params = p.params;
+  k.grads = p.grads;
+  k.stride = p.stride;
+  k.o_b1 = tensor_offset(d, 1);
+  k.o_b2 = tensor_offset(d, 3);
+  k.o_w3 = tensor_offset(d, 4);
+  k.o_b3 = tensor_offset(d, 5);
+  k.h1 = h1;
+  k.h2 = h2;
+  k.dz1 = dz1;
+  k.dz2 = dz2;
+  k.loss = p.loss;
+  k.last_loss = p.last_loss;
+  k.max_steps = p.max_steps;
+  k.host_input = p.host_input;
+  static bool configured = false;
+  if (!configured) {
+    TLK_CUDA(cudaFuncSetAttribute(mlp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, M_SMEM));
+    configured = true;
+  }
+  static const char* only = getenv("TLK_MLP2_ONLY");  // debug: 1 / 2 = launch only that kernel
+  if (!only || only[0] != '2') {
+    TLK_CUDA(launch(mlp_step_kernel, dim3(MC, L), M_THREADS, M_SMEM, st, k));
+    p.mark(st, "mlp_step");
+  }
+  if (only && only[0] == '1') return TLK_OK;
+
+  MlpWArgs w{};
+  const uint64_t ls = uint64_t(MB) * MH * 2;
+  rc = make_tmap_bf16_3d(&w.x, p.x, MIN, MB, L, MIN * 2, uint64_t(MB) * MIN * 2, 64, 64);
+  if (!rc) rc = make_tmap_bf16_3d(&w.h1, h1, MH, MB, L, MH * 2, ls, 64, 64);
+  if (!rc) rc = make_tmap_bf16_3d(&w.dz1, dz1, MH, MB, L, MH * 2, ls, 64, 64);
+  if (!rc) rc = make_tmap_bf16_3d(&w.dz2, dz2, MH, MB, L, MH * 2, ls, 64, 64);
+  if (rc) return rc;
+  w.lanes = p.lane_dev;
+  w.params = p.params;
+  w.grads = p.grads;
+  w.m1 = p.mom1;
+  w.m2 = p.mom2;
+  w.wbf = p.wbf;
+  w.stride = p.stride;
+  w.o_w1 = o_w1;
+  w.o_b1 = k.o_b1;
+  w.o_w2 = o_w2;
+  w.o_b2 = k.o_b2;
+  w.o_w3 = k.o_w3;
+  w.o_b3 = k.o_b3;
+  w.write_grads = (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0;
+  TLK_CUDA(launch(mlp_wgrad_adam_kernel, dim3(W_TILES + 1, L), W_THREADS, 2 * 16384 + 1024, st, w));
+  p.mark(st, "mlp_wgrad_adam");
+  TLK_CUDA(cudaGetLastError());
+  return TLK_OK;
+}
+
+}  // namespace tlk

@@ -113,6 +113,7 @@ TLK_DEV void fence_proxy_async_smem() {
 
 // sub-CTA barrier over `n` threads (named barrier `id` != 0)
 TLK_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+TLK_DEV void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // --------------------------------------------------------------- tcgen05 --
 template <uint32_t NCOLS>
