@@ -4,6 +4,8 @@
 // (and TLK_MLP_V1=1): 8 kernels, captured once into a CUDA graph:
 //   inputs -> fc1 fwd -> fc2 fwd -> head(fc3 + CE + bwd) -> fc2 wgrad ->
 //   fc2 dgrad(+mask, fc1 bias grad) -> fc1 wgrad -> optimizer (+ end of step)
+#include <cstdlib>
+
 #include "linear.cuh"
 #include "pack.cuh"
 
@@ -33,6 +35,12 @@ int mlp_setup(Pack& p) {
   p.scratch = s;
   p.scratch_free = [](void* q) { delete static_cast<MlpScratch*>(q); };
   p.launches_per_step = mlp2_enabled(p) ? 2 : 8;
+  if (getenv("TLK_MLP_TRACE") && getenv("TLK_MLP_TRACE")[0] == '1') {  // mlp2.cu phase timeline
+    void* tb = nullptr;
+    if ((rc = pack_alloc(p, &tb, 4 * 32 * 8))) return rc;
+    TLK_CUDA(cudaMemset(tb, 0, 4 * 32 * 8));
+    p.name_buf("mlp.trace", tb, 4 * 32 * 8);
+  }
   return TLK_OK;
 }
 

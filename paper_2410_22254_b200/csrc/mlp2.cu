@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "linear.cuh"
 #include "pack.cuh"
@@ -55,7 +56,7 @@ constexpr uint32_t M_SMEM = SM_RING + MSTAGES * ABLK + 1024;
 // partial-logit exchange, dz3, h2^T and the fc3 weight slice
 constexpr uint32_t SM_DZ2 = 0, SM_PLOG = 8 * KBLK, SM_DZ3 = SM_PLOG + MC * 640 * 4,
                    SM_HS = SM_DZ3 + MB * CLASSES * 4, SM_W3 = SM_HS + MB * 136 * 2;
-static_assert(SM_W3 + CLASSES * 128 * 4 <= MKB1 * KBLK, "head scratch fits in X");
+static_assert(SM_W3 + 128 * 12 * 4 <= MKB1 * KBLK, "head scratch fits in X");
 
 struct MlpArgs {
   CUtensorMap w1, w2, w2t;  // bf16 shadows: W1 {784, 512, lane} box {64,128}; W2 {512, 512, lane}
@@ -71,7 +72,12 @@ struct MlpArgs {
   uint16_t *h1, *h2, *dz1, *dz2;  // [lane][64][512]
   float *loss, *last_loss;
   int max_steps, host_input;
+  unsigned long long* trace;  // debug (TLK_MLP_TRACE=1): cluster (0, lane 0) event clocks [CTA][32]
 };
+#define MLP_TR(slot)                                                                     \
+  do {                                                                                   \
+    if (a.trace && j == 0) a.trace[c * 32 + (slot)] = clock64();                         \
+  } while (0)
 
 TLK_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -124,7 +130,8 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   constexpr uint32_t IDESC = umma_idesc_bf16(128, MB, false, false);
   constexpr uint32_t IDESC_T = umma_idesc_bf16(128, MB, true, false);
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[MSTAGES], empty[MSTAGES], acc[3], h1_loc, h1_rem, dz2_loc, dz2_rem, plog_rem;
+  __shared__ __align__(8) uint64_t full[MSTAGES], empty[MSTAGES], acc[3], x_rem, lbl_rem, h1_loc, h1_rem, dz2_loc,
+      dz2_rem, plog_rem;
   __shared__ uint32_t tmem_s;
   __shared__ int32_t lbl[MB];
   __shared__ float lossb[MB];
@@ -142,6 +149,8 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 3; ++i) mbar_init(&acc[i], 1);
+    mbar_init(&x_rem, 1);
+    mbar_init(&lbl_rem, 1);
     mbar_init(&h1_loc, 1);
     mbar_init(&h1_rem, 1);
     mbar_init(&dz2_loc, 1);
@@ -149,40 +158,102 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     mbar_init(&plog_rem, 1);
     fence_mbar_init();
     // the bytes the three peers will deliver into this CTA
+    mbar_expect_tx(&x_rem, (MC - 1) * MKB1 * 16 * 128);  // 16 sample rows of every X k-block
+    mbar_expect_tx(&lbl_rem, (MC - 1) * 16 * 4);
     mbar_expect_tx(&h1_rem, (MC - 1) * 2 * KBLK);
     mbar_expect_tx(&dz2_rem, (MC - 1) * 2 * KBLK);
     mbar_expect_tx(&plog_rem, (MC - 1) * 640 * 4);
   }
   if (warp == 5) tmem_alloc<256>(&tmem_s);
+  if (tid == 0) MLP_TR(0);
   const LaneState ls = a.lanes[j];
   const uint64_t key = rng_key(ls.seed, STREAM_DATA, uint64_t(ls.steps_done));
-  // ---- inputs: x (bf16 k/256) of all 64 samples as fc1's K-major B operand;
-  // CTA c also writes samples [16c, 16c+16) of px / x to global
-  for (int i = tid; i < MB * MKB1 * 8; i += M_THREADS) {
-    const int s = i / (MKB1 * 8), q = i % (MKB1 * 8);  // q: 8-pixel word
-    uint64_t wv = 0;
-    if (q < WORDS_PER_SAMPLE) {
-      const size_t g = (size_t(j) * MB + s) * WORDS_PER_SAMPLE + q;
-      wv = a.host_input ? reinterpret_cast<const uint64_t*>(a.px)[g]
-                        : rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
-    }
-    uint32_t w4[4];
+  // ---- inputs of samples [16c, 16c + 16): x (bf16 k/256) rows of fc1's
+  // K-major B operand, px / x to global, teacher labels (16 threads per
+  // sample, integer dp4a partials summed by shuffles: exact); then the 16
+  // rows of every k-block and the labels go to the three peers
+  cluster.sync();  // every CTA's mbarriers are initialised before any remote arrival
+  {
+    int8_t* tch = reinterpret_cast<int8_t*>(smem + SM_RING);  // teacher [10][784] (the ring is idle)
+    for (int i = tid; i < CLASSES * PIXELS / 16; i += M_THREADS)
+      reinterpret_cast<uint4*>(tch)[i] = reinterpret_cast<const uint4*>(a.teacher)[i];
+    __syncthreads();
+    const int sl = tid >> 4, s = c * 16 + sl, part = tid & 15;  // sample, word phase
+    int accv[CLASSES];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      w4[e] = pack_bf2(float((wv >> (16 * e)) & 0xFF) * (1.0f / 256.0f), float((wv >> (16 * e + 8)) & 0xFF) * (1.0f / 256.0f));
-    const uint4 v4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-    *reinterpret_cast<uint4*>(smem + SM_X + (q >> 3) * KBLK + sw128(s, q & 7)) = v4;
-    if (q < WORDS_PER_SAMPLE && (s >> 4) == c) {
+    for (int cl = 0; cl < CLASSES; ++cl) accv[cl] = 0;
+    for (int q = part; q < MKB1 * 8; q += 16) {  // 8-pixel words (>= 98: zero padding)
+      uint64_t wv = 0;
       const size_t g = (size_t(j) * MB + s) * WORDS_PER_SAMPLE + q;
-      if (!a.host_input) reinterpret_cast<uint64_t*>(a.px)[g] = wv;
-      reinterpret_cast<uint4*>(a.x)[g] = v4;
+      if (q < WORDS_PER_SAMPLE)
+        wv = a.host_input ? reinterpret_cast<const uint64_t*>(a.px)[g] : rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
+      uint32_t w4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w4[e] = pack_bf2(float((wv >> (16 * e)) & 0xFF) * (1.0f / 256.0f),
+                         float((wv >> (16 * e + 8)) & 0xFF) * (1.0f / 256.0f));
+      const uint4 v4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      *reinterpret_cast<uint4*>(smem + SM_X + (q >> 3) * KBLK + sw128(s, q & 7)) = v4;
+      if (q < WORDS_PER_SAMPLE) {
+        if (!a.host_input) reinterpret_cast<uint64_t*>(a.px)[g] = wv;
+        reinterpret_cast<uint4*>(a.x)[g] = v4;
+        if (!a.host_input) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t pw = uint32_t(wv >> (32 * h));
+#pragma unroll
+            for (int cl = 0; cl < CLASSES; ++cl) {
+              const int tw = reinterpret_cast<const int*>(tch + cl * PIXELS)[2 * q + h];
+              int tp, ts;
+              asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(tp) : "r"(tw), "r"(pw), "r"(0));
+              asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts) : "r"(tw), "r"(0x01010101u), "r"(0));
+              accv[cl] += 2 * tp - 255 * ts;
+            }
+          }
+        }
+      }
+    }
+    if (!a.host_input) {
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl)
+#pragma unroll
+        for (int o = 8; o; o >>= 1) accv[cl] += __shfl_xor_sync(0xffffffffu, accv[cl], o);
+    }
+    if (part == 0) {
+      int best = 0;
+      if (a.host_input) {
+        best = a.labels[size_t(j) * MB + s];
+      } else {
+        int bestv = 0;
+#pragma unroll
+        for (int cl = 0; cl < CLASSES; ++cl)
+          if (cl == 0 || accv[cl] > bestv) {
+            best = cl;
+            bestv = accv[cl];
+          }
+        a.labels[size_t(j) * MB + s] = best;
+      }
+      lbl[s] = best;
+      const uint32_t la = smem_u32(&lbl[s]);
+      for (int pr = 1; pr < MC; ++pr) {
+        const uint32_t peer = uint32_t((c + pr) % MC);
+        st_async_f32(mapa(la, peer), __int_as_float(best), mapa(smem_u32(&lbl_rem), peer));
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid < MKB1) {  // k-block tid: this CTA's 16 rows (2 KB) -> every peer
+      const uint32_t src = sb + SM_X + tid * KBLK + c * 16 * 128;
+      for (int pr = 1; pr < MC; ++pr) {
+        const uint32_t peer = uint32_t((c + pr) % MC);
+        bulk_s2cluster(mapa(src, peer), src, 16 * 128, mapa(smem_u32(&x_rem), peer));
+      }
     }
   }
-  fence_proxy_async_smem();
   tc_fence_before();
-  __syncthreads();
-  cluster.sync();  // every CTA's mbarriers are initialised before any remote arrival
+  __syncthreads();  // (the producer may now overwrite the teacher in the ring)
   tc_fence_after();
+  if (tid == 0) MLP_TR(1);
   const uint32_t tmem = tmem_s;
   const float* P = a.params + j * a.stride;
   float* G = a.grads + j * a.stride;
@@ -211,6 +282,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   } else if (warp == 5) {  // -------------------------------------- MMA issuer
     if (lane == 0) {
       int it = 0;
+      mwait(&x_rem, 0, 14);  // the peers' sample rows of X
       auto gemm = [&](uint32_t d, uint32_t bbase, int nkb, bool amn, int ai) {
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % MSTAGES;
@@ -228,55 +300,28 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         mma_commit(&acc[ai]);
       };
       gemm(tmem, sb + SM_X, MKB1, false, 0);  // fc1
+      MLP_TR(2);
       mwait(&h1_loc, 0, 4);
       mwait(&h1_rem, 0, 5);
+      MLP_TR(3);
       tc_fence_after();
       gemm(tmem + 64, sb + SM_H1, 8, false, 1);  // fc2
+      MLP_TR(4);
       mwait(&dz2_loc, 0, 6);
       mwait(&dz2_rem, 0, 7);
+      MLP_TR(5);
       tc_fence_after();
       gemm(tmem + 128, sb + SM_DZ2, 8, true, 2);  // fc2 dgrad
+      MLP_TR(6);
     }
-  } else if (warp >= 6) {  // --------------------------------- teacher labels
-    const int s = tid - 192;  // one sample per thread
-    if (a.host_input) {
-      lbl[s] = a.labels[size_t(j) * MB + s];
-    } else {
-      int accv[CLASSES];
-#pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl) accv[cl] = 0;
-      for (int q = 0; q < WORDS_PER_SAMPLE; ++q) {
-        const uint64_t wv = rng_bits(key, uint64_t(s) * WORDS_PER_SAMPLE + q);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t pw = uint32_t(wv >> (32 * h));
-#pragma unroll
-          for (int cl = 0; cl < CLASSES; ++cl) {
-            const int tw = reinterpret_cast<const int*>(a.teacher + cl * PIXELS)[2 * q + h];
-            int tp, ts;
-            asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(tp) : "r"(tw), "r"(pw), "r"(0));
-            asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts) : "r"(tw), "r"(0x01010101u), "r"(0));
-            accv[cl] += 2 * tp - 255 * ts;
-          }
-        }
-      }
-      int best = 0, bestv = 0;
-#pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl)
-        if (cl == 0 || accv[cl] > bestv) {
-          best = cl;
-          bestv = accv[cl];
-        }
-      lbl[s] = best;
-      if (c == 0) a.labels[size_t(j) * MB + s] = best;
-    }
-    named_bar_arrive(2, 192);  // lbl[] is ready for the cross-entropy (warps 0-3 sync on it)
+  } else if (warp >= 6) {  // (idle after the inputs phase)
   } else {  // ------------------------------- TMEM-quarter warps 0..3 (row o)
     const int q = warp, r = q * 32 + lane, o = c * 128 + r;  // r: row of the slice, o: unit
     const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
     float v[MB];
     // fc1 -> h1 = bf16(relu(acc + b1)): own H1 k-blocks (2c, 2c+1) + global
     mwait(&acc[0], 0, 8);
+    if (tid == 0) MLP_TR(8);
     tc_fence_after();
     tmem_ld64(tq, v);
     {
@@ -292,6 +337,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (tid == 0) {  // this CTA's 16 KB of H1 -> every peer's H1 (same offset)
+      MLP_TR(9);
       mbar_arrive(&h1_loc);
       const uint32_t src = sb + SM_H1 + 2 * c * KBLK;
       for (int pr = 1; pr < MC; ++pr) {
@@ -301,6 +347,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     }
     // fc2 -> h2 = bf16(relu(acc + b2)) (registers, global, h2^T in smem)
     mwait(&acc[1], 0, 9);
+    if (tid == 0) MLP_TR(10);
     tc_fence_after();
     tmem_ld64(tq + 64, v);
     {
@@ -314,30 +361,58 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         hs[s * 136 + r] = h;
         hg[size_t(s) * MH] = h;
       }
-      float* w3s = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice] (fp32 master)
-      for (int i = r; i < CLASSES * 128; i += 128) w3s[i] = P[a.o_w3 + (i >> 7) * MH + c * 128 + (i & 127)];
+      float* w3t = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice]^T (fp32 master), [unit][12]
+      for (int cl = 0; cl < CLASSES; ++cl) w3t[r * 12 + cl] = P[a.o_w3 + cl * MH + o];
     }
     named_bar_sync(1, 128);
-    // partial logits of this slice: plog[c][s * 10 + cl] in every CTA of the cluster
+    // partial logits of this slice, plog[c][s * 10 + cl], in every CTA of the
+    // cluster: thread (s, half) sums 64 of the 128 units for all 10 classes
+    // (ten independent accumulators), the halves meet by one shuffle
     {
       const uint16_t* hs = reinterpret_cast<const uint16_t*>(smem + SM_HS);
-      const float* w3s = reinterpret_cast<const float*>(smem + SM_W3);
+      const float* w3t = reinterpret_cast<const float*>(smem + SM_W3);  // [unit][12]
       float* plog = reinterpret_cast<float*>(smem + SM_PLOG);
-      for (int i = r; i < MB * CLASSES; i += 128) {
-        const int s = i / CLASSES, cl = i % CLASSES;
-        float accv = 0.f;
-#pragma unroll 8
-        for (int u = 0; u < 128; ++u) accv += bf2f(hs[s * 136 + u]) * w3s[cl * 128 + u];
-        plog[c * 640 + i] = accv;
-        const uint32_t la = smem_u32(&plog[c * 640 + i]);
-        for (int pr = 1; pr < MC; ++pr) {
-          const uint32_t peer = uint32_t((c + pr) % MC);
-          st_async_f32(mapa(la, peer), accv, mapa(smem_u32(&plog_rem), peer));
+      const int s = r >> 1, half = r & 1;
+      float acc10[CLASSES];
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) acc10[cl] = 0.f;
+#pragma unroll 4
+      for (int u = half * 64; u < half * 64 + 64; ++u) {
+        const float h = bf2f(hs[s * 136 + u]);
+        const float4 w0 = *reinterpret_cast<const float4*>(w3t + u * 12);
+        const float4 w1 = *reinterpret_cast<const float4*>(w3t + u * 12 + 4);
+        const float2 w2 = *reinterpret_cast<const float2*>(w3t + u * 12 + 8);
+        acc10[0] += h * w0.x;
+        acc10[1] += h * w0.y;
+        acc10[2] += h * w0.z;
+        acc10[3] += h * w0.w;
+        acc10[4] += h * w1.x;
+        acc10[5] += h * w1.y;
+        acc10[6] += h * w1.z;
+        acc10[7] += h * w1.w;
+        acc10[8] += h * w2.x;
+        acc10[9] += h * w2.y;
+      }
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) acc10[cl] += __shfl_xor_sync(0xffffffffu, acc10[cl], 1);
+      if (half == 0) {
+#pragma unroll
+        for (int cl = 0; cl < CLASSES; ++cl) {
+          const int i = s * CLASSES + cl;
+          plog[c * 640 + i] = acc10[cl];
+          const uint32_t la = smem_u32(&plog[c * 640 + i]);
+          for (int pr = 1; pr < MC; ++pr) {
+            const uint32_t peer = uint32_t((c + pr) % MC);
+            st_async_f32(mapa(la, peer), acc10[cl], mapa(smem_u32(&plog_rem), peer));
+          }
         }
       }
     }
+    if (tid == 0) MLP_TR(11);
     mwait(&plog_rem, 0, 10);
-    named_bar_sync(2, 192);  // with the label warps: lbl[] written; also orders the local partials
+    mwait(&lbl_rem, 0, 15);
+    if (tid == 0) MLP_TR(12);
+    named_bar_sync(1, 128);  // the local partials
     // logits (ranks summed in order, + fc3.b), cross entropy, dz3 = (softmax - onehot) / B
     float* dz3 = reinterpret_cast<float*>(smem + SM_DZ3);
     if (r < MB) {
@@ -380,19 +455,33 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       for (int s = 0; s < MB; ++s) sacc += dz3[s * CLASSES + cl];
       G[a.o_b3 + cl] = sacc;
     }
-    // dz2 = bf16(dz3 W3[:, o] * [h2 > 0]), fc2.b / fc3.w grads of unit o
+    // dz2 = bf16(dz3 W3[:, o] * [h2 > 0]), fc2.b / fc3.w grads of unit o: one
+    // pass over the samples (dz3 rows are broadcast loads)
     {
-      const float* w3s = reinterpret_cast<const float*>(smem + SM_W3);
-      float w3o[CLASSES];
+      const float* w3t = reinterpret_cast<const float*>(smem + SM_W3);
+      float w3o[CLASSES], gw[CLASSES];
 #pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl) w3o[cl] = w3s[cl * 128 + r];
+      for (int cl = 0; cl < CLASSES; ++cl) {
+        w3o[cl] = w3t[r * 12 + cl];
+        gw[cl] = 0.f;
+      }
       uint16_t* zg = a.dz2 + size_t(j) * MB * MH + o;
       float db = 0.f;
-#pragma unroll 4
-      for (int s = 0; s < MB; ++s) {
+#pragma unroll
+      for (int s = 0; s < MB; ++s) {  // fully unrolled: v[] stays in registers
+        float d[CLASSES];
+#pragma unroll
+        for (int cl = 0; cl < CLASSES; cl += 2) {
+          const float2 t2 = *reinterpret_cast<const float2*>(dz3 + s * CLASSES + cl);
+          d[cl] = t2.x;
+          d[cl + 1] = t2.y;
+        }
         float dh = 0.f;
 #pragma unroll
-        for (int cl = 0; cl < CLASSES; ++cl) dh += dz3[s * CLASSES + cl] * w3o[cl];
+        for (int cl = 0; cl < CLASSES; ++cl) {
+          dh += d[cl] * w3o[cl];
+          gw[cl] += d[cl] * v[s];
+        }
         const uint16_t z = f2bf(v[s] > 0.0f ? dh : 0.0f);
         *reinterpret_cast<uint16_t*>(smem + SM_DZ2 + kmaj_off(s, o)) = z;
         zg[size_t(s) * MH] = z;
@@ -400,15 +489,12 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       }
       G[a.o_b2 + o] = db;
 #pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl) {
-        float gw = 0.f;
-        for (int s = 0; s < MB; ++s) gw += dz3[s * CLASSES + cl] * v[s];
-        G[a.o_w3 + cl * MH + o] = gw;
-      }
+      for (int cl = 0; cl < CLASSES; ++cl) G[a.o_w3 + cl * MH + o] = gw[cl];
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (tid == 0) {  // this CTA's 16 KB of DZ2 -> every peer
+      MLP_TR(13);
       mbar_arrive(&dz2_loc);
       const uint32_t src = sb + SM_DZ2 + 2 * c * KBLK;
       for (int pr = 1; pr < MC; ++pr) {
@@ -418,6 +504,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     }
     // fc2 dgrad -> dz1 = bf16(acc * [h1 > 0]) of input unit o, fc1.b grad
     mwait(&acc[2], 0, 11);
+    if (tid == 0) MLP_TR(14);
     tc_fence_after();
     tmem_ld64(tq + 128, v);
     {
@@ -436,7 +523,9 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc<256>(tmem);
+  if (tid == 0) MLP_TR(15);
   cluster.sync();  // peers have received every copy out of this CTA's shared memory
+  if (tid == 0) MLP_TR(16);
 }
 
 // ---------------------------------------------------- fused wgrad + update --
@@ -448,25 +537,25 @@ struct MlpWArgs {
   int64_t stride, o_w1, o_b1, o_w2, o_b2, o_w3, o_b3;
   int write_grads;
 };
-constexpr int W1_MT = 7, W_NT = 4;               // W1^T: 7 x 4 tiles, W2^T: 4 x 4
-constexpr int W_TILES = W1_MT * W_NT + W_NT * W_NT;  // + 1 small-tensor CTA
+constexpr int W1_MT = 7, W2_MT = 4, W_NT = 8, W_BN = 64;  // W1^T: 7 x 8 tiles, W2^T: 4 x 8 (128 x 64)
+constexpr int W_TILES = (W1_MT + W2_MT) * W_NT;  // + 1 small-tensor CTA
 constexpr int W_THREADS = 128;
 
 template <int KIND>
 TLK_DEV void adam_cols(const LaneState& s, float* p, float* m1, float* m2, uint16_t* wbf, float* gout,
                        int64_t rstride, const float (&g)[32]) {
 #pragma unroll
-  for (int c0 = 0; c0 < 32; c0 += 8) {  // 8 columns: 24 loads in flight, then the updates
-    float pv[8], mv[8], vv[8];
+  for (int c0 = 0; c0 < 32; c0 += 16) {  // 16 columns: 48 loads in flight, then the updates
+    float pv[16], mv[16], vv[16];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 16; ++i) {
       const int64_t o = (c0 + i) * rstride;
       pv[i] = p[o];
       mv[i] = m1[o];
       vv[i] = KIND != TLK_OPT_SGD ? m2[o] : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 16; ++i) {
       const int64_t o = (c0 + i) * rstride;
       opt_update_k<KIND>(s, pv[i], g[c0 + i], mv[i], vv[i]);
       p[o] = pv[i];
@@ -479,7 +568,7 @@ TLK_DEV void adam_cols(const LaneState& s, float* p, float* m1, float* m2, uint1
 }
 
 __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_constant__ MlpWArgs a) {
-  constexpr uint32_t IDESC = umma_idesc_bf16(128, 128, true, true);
+  constexpr uint32_t IDESC = umma_idesc_bf16(128, W_BN, true, true);
   pdl_begin();
   const int j = blockIdx.y, t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #ifdef TLK_HANG_DEBUG
@@ -491,7 +580,7 @@ __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_
   const int64_t L0 = int64_t(j) * a.stride;
   if (t < W_TILES) {
     extern __shared__ uint8_t wsm_raw[];
-    uint8_t* sm = wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u);  // 2 x 16 KB (SW128 boxes)
+    uint8_t* sm = wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u);  // A 16 KB + B 8 KB (SW128 boxes)
     __shared__ __align__(8) uint64_t full, done;
     __shared__ uint32_t tmem_s;
     const bool w1 = t < W1_MT * W_NT;
@@ -505,7 +594,7 @@ __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_
       mbar_init(&done, 1);
       fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<128>(&tmem_s);
+    if (warp == 0) tmem_alloc<W_BN>(&tmem_s);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -517,11 +606,10 @@ __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_
       // a box that lies wholly outside the tensor never completes its
       // transaction: skip it (the rows it would hold are never stored)
       const bool a_hi = mt * 128 + 64 < in;
-      mbar_expect_tx(&full, (a_hi ? 4 : 3) * 8192);
+      mbar_expect_tx(&full, (a_hi ? 3 : 2) * 8192);
       tma_load_3d(sb, am, mt * 128, 0, j, &full);
       if (a_hi) tma_load_3d(sb + 8192, am, mt * 128 + 64, 0, j, &full);
-      tma_load_3d(sb + 16384, bm, nt * 128, 0, j, &full);
-      tma_load_3d(sb + 24576, bm, nt * 128 + 64, 0, j, &full);
+      tma_load_3d(sb + 16384, bm, nt * W_BN, 0, j, &full);
       mwait(&full, 0, 12);
       tc_fence_after();
 #pragma unroll
@@ -536,9 +624,9 @@ __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_
     // tcgen05.ld is warp-collective: every lane of a warp that owns any valid
     // row loads; only the rows below `in` update parameters
     if (mt * 128 + warp * 32 < in) {
-      const int64_t base = L0 + (w1 ? a.o_w1 : a.o_w2) + int64_t(nt * 128) * in + i;  // element (o = nt*128, i)
+      const int64_t base = L0 + (w1 ? a.o_w1 : a.o_w2) + int64_t(nt * W_BN) * in + i;  // element (o = nt*64, i)
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 0; c0 < W_BN; c0 += 32) {
         float g[32];
         tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c0, g);
         if (i >= in) continue;
@@ -554,7 +642,7 @@ __global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<128>(tmem);
+    if (warp == 0) tmem_dealloc<W_BN>(tmem);
   } else {  // the small tensors: fc1.b, fc2.b, fc3.w, fc3.b (grads written by the step kernel)
     const int64_t seg[4][2] = {{a.o_b1, MH}, {a.o_b2, MH}, {a.o_w3, CLASSES * MH}, {a.o_b3, CLASSES}};
     for (int k = 0; k < 4; ++k)
@@ -625,6 +713,9 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   k.last_loss = p.last_loss;
   k.max_steps = p.max_steps;
   k.host_input = p.host_input;
+  k.trace = nullptr;
+  for (auto& nb : p.named)  // debug timeline buffer (mlp_setup, TLK_MLP_TRACE=1)
+    if (nb.name == "mlp.trace") k.trace = static_cast<unsigned long long*>(nb.ptr);
   static bool configured = false;
   if (!configured) {
     TLK_CUDA(cudaFuncSetAttribute(mlp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, M_SMEM));
@@ -658,7 +749,7 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   w.o_w3 = k.o_w3;
   w.o_b3 = k.o_b3;
   w.write_grads = (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0;
-  TLK_CUDA(launch(mlp_wgrad_adam_kernel, dim3(W_TILES + 1, L), W_THREADS, 2 * 16384 + 1024, st, w));
+  TLK_CUDA(launch(mlp_wgrad_adam_kernel, dim3(W_TILES + 1, L), W_THREADS, 3 * 8192 + 1024, st, w));
   p.mark(st, "mlp_wgrad_adam");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
