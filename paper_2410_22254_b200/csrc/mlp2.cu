@@ -26,6 +26,7 @@
 // operands, fp32 accumulation, h / dz stored bf16, the classifier head on the
 // fp32 master fc3 weights, the IEEE-exact optimizer (models.cuh opt_update_k).
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -66,8 +67,9 @@ struct MlpArgs {
   uint8_t* px;
   int32_t* labels;
   uint16_t* x;
-  const float* params;
-  float* grads;
+  float* params;
+  float *grads, *m1, *m2;
+  uint16_t* wbf;
   int64_t stride, o_b1, o_b2, o_w3, o_b3;
   uint16_t *h1, *h2, *dz1, *dz2;  // [lane][64][512]
   float *loss, *last_loss;
@@ -135,6 +137,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   __shared__ uint32_t tmem_s;
   __shared__ int32_t lbl[MB];
   __shared__ float lossb[MB];
+  __shared__ float b3s[CLASSES];  // fc3.b as read before CTA 0 updates it
   cg::cluster_group cluster = cg::this_cluster();
   const int c = int(cluster.block_rank()), j = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -257,6 +260,20 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   const uint32_t tmem = tmem_s;
   const float* P = a.params + j * a.stride;
   float* G = a.grads + j * a.stride;
+  // the small tensors (fc1.b, fc2.b, fc3.w, fc3.b) are updated here, right
+  // after their gradients (each CTA its slice) -- the step's optimizer scalars
+  // computed from the lane state exactly as the head does for the lane table
+  LaneState ost = ls;
+  lane_step_scalars(ost);
+  auto upd = [&](int64_t e, float g) {  // e: offset within the lane
+    const int64_t i = j * a.stride + e;
+    float pv = a.params[i], mv = a.m1[i], vv = a.m2[i];
+    opt_update(ost, pv, g, mv, vv);
+    a.params[i] = pv;
+    a.m1[i] = mv;
+    a.m2[i] = vv;
+    a.wbf[i] = f2bf(pv);
+  };
 
   if (warp == 4) {  // ------------------------------------------ TMA producer
     if (lane == 0) {
@@ -363,6 +380,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       }
       float* w3t = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice]^T (fp32 master), [unit][12]
       for (int cl = 0; cl < CLASSES; ++cl) w3t[r * 12 + cl] = P[a.o_w3 + cl * MH + o];
+      if (r < CLASSES) b3s[r] = P[a.o_b3 + r];
     }
     named_bar_sync(1, 128);
     // partial logits of this slice, plog[c][s * 10 + cl], in every CTA of the
@@ -423,7 +441,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         float sacc = 0.f;
 #pragma unroll
         for (int k = 0; k < MC; ++k) sacc += plog[k * 640 + r * CLASSES + cl];
-        l[cl] = sacc + P[a.o_b3 + cl];
+        l[cl] = sacc + b3s[cl];
       }
       const int y = lbl[r];
       float m = l[0];
@@ -454,6 +472,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       float sacc = 0.f;
       for (int s = 0; s < MB; ++s) sacc += dz3[s * CLASSES + cl];
       G[a.o_b3 + cl] = sacc;
+      upd(a.o_b3 + cl, sacc);
     }
     // dz2 = bf16(dz3 W3[:, o] * [h2 > 0]), fc2.b / fc3.w grads of unit o: one
     // pass over the samples (dz3 rows are broadcast loads)
@@ -490,6 +509,10 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       G[a.o_b2 + o] = db;
 #pragma unroll
       for (int cl = 0; cl < CLASSES; ++cl) G[a.o_w3 + cl * MH + o] = gw[cl];
+      // fc2.b / fc3.w have been read for the last time this step (h2, logits, dz2)
+      upd(a.o_b2 + o, db);
+#pragma unroll
+      for (int cl = 0; cl < CLASSES; ++cl) upd(a.o_w3 + cl * MH + o, gw[cl]);
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
@@ -518,6 +541,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         db += bf2f(z);
       }
       G[a.o_b1 + o] = db;
+      upd(a.o_b1 + o, db);
     }
   }
   tc_fence_before();
@@ -529,147 +553,204 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
 }
 
 // ---------------------------------------------------- fused wgrad + update --
-struct MlpWArgs {
-  CUtensorMap x, h1, dz1, dz2;  // [lane][64][width] bf16 as MN-major boxes {64 units, 64 samples}
-  LaneState* lanes;
-  float *params, *grads, *m1, *m2;
-  uint16_t* wbf;
-  int64_t stride, o_w1, o_b1, o_w2, o_b2, o_w3, o_b3;
-  int write_grads;
-};
-constexpr int W1_MT = 7, W2_MT = 4, W_NT = 8, W_BN = 64;  // W1^T: 7 x 8 tiles, W2^T: 4 x 8 (128 x 64)
-constexpr int W_TILES = (W1_MT + W2_MT) * W_NT;  // + 1 small-tensor CTA
-constexpr int W_THREADS = 128;
+// dW^T[f][o] = sum_s act[s][f] dz[s][o] (M = 128 input features f, N = 128
+// outputs o, K = batch; both operands MN-major) with the optimizer update as
+// the epilogue, the CNN's fc1 wgrad + Adam design (cnn.cu) over the MLP's
+// two big tensors: W1 (7 f-tiles x 8 o-tiles of 64 per lane) and W2 (4 x 8).
+// Persistent; warp 0 streams the operand boxes and the tile's p, m, v in four
+// [32 o][128 f] fp32 chunks into a 4-slot ring, warp 1 issues the MMA
+// (accumulator double-buffered in TMEM), 16 update warps apply the update and
+// store full 128-B lines.  The last of a lane's 88 x 16 update-warp tiles
+// ends the lane's step.
+constexpr int MW_SLOTS = 4, MW_UPD = 16;
+constexpr int MW_ON = 64, MW_CH = MW_ON / 32;  // outputs per tile, 32-output chunks per tile
+constexpr int MW_STAGE = 3 * 8192;             // two act boxes + one dz box (64 x 64 bf16)
+constexpr int MW_CHUNK = 32 * 128 * 4;
+constexpr int MW_SLOT = 3 * MW_CHUNK;
+constexpr int MW_SMEM = MW_STAGE + MW_SLOTS * MW_SLOT + 1024;
+constexpr int MW_THREADS = (2 + MW_UPD) * 32;
+constexpr int MW_OT = MH / MW_ON;                         // o-tiles per tensor
+constexpr int MW_T1 = 7 * MW_OT, MW_TPL = MW_T1 + 4 * MW_OT;  // W1 tiles, tiles per lane
 
-template <int KIND>
-TLK_DEV void adam_cols(const LaneState& s, float* p, float* m1, float* m2, uint16_t* wbf, float* gout,
-                       int64_t rstride, const float (&g)[32]) {
-#pragma unroll
-  for (int c0 = 0; c0 < 32; c0 += 16) {  // 16 columns: 48 loads in flight, then the updates
-    float pv[16], mv[16], vv[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int64_t o = (c0 + i) * rstride;
-      pv[i] = p[o];
-      mv[i] = m1[o];
-      vv[i] = KIND != TLK_OPT_SGD ? m2[o] : 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int64_t o = (c0 + i) * rstride;
-      opt_update_k<KIND>(s, pv[i], g[c0 + i], mv[i], vv[i]);
-      p[o] = pv[i];
-      m1[o] = mv[i];
-      if constexpr (KIND != TLK_OPT_SGD) m2[o] = vv[i];
-      wbf[o] = f2bf(pv[i]);
-      if (gout) gout[o] = g[c0 + i];
-    }
-  }
+struct MlpWArgs {
+  CUtensorMap x, h1, dz1, dz2;           // [lane][64][width] bf16, boxes {64 units, 64 samples}
+  CUtensorMap p1, q1, v1, p2, q2, v2;    // fp32 W1 / W2 params, m, v: [lane][512 o][in], box {128 f, 32 o}
+  LaneState* lanes;
+  float *params, *m1, *m2, *grads;
+  uint16_t* wbf;
+  int64_t stride, o_w1, o_w2;
+  int write_grads, ntiles;
+};
+
+struct MwTile {
+  int j, w1, f0, o0, in;
+};
+TLK_DEV MwTile mw_tile(int t) {
+  MwTile r;
+  r.j = t / MW_TPL;
+  const int u = t % MW_TPL;
+  r.w1 = u < MW_T1;
+  const int v = r.w1 ? u : u - MW_T1;
+  r.f0 = (v / MW_OT) * 128;
+  r.o0 = (v % MW_OT) * MW_ON;
+  r.in = r.w1 ? MIN : MH;
+  return r;
 }
 
-__global__ void __launch_bounds__(W_THREADS) mlp_wgrad_adam_kernel(const __grid_constant__ MlpWArgs a) {
-  constexpr uint32_t IDESC = umma_idesc_bf16(128, W_BN, true, true);
-  pdl_begin();
-  const int j = blockIdx.y, t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-#ifdef TLK_HANG_DEBUG
-  if (tid == 0 && t < 2) printf("wgrad enter %d %d\n", t, j);
-#endif
-  LaneState* lsp = a.lanes + j;
-  if (!lsp->active) return;
-  const LaneState s = *lsp;
-  const int64_t L0 = int64_t(j) * a.stride;
-  if (t < W_TILES) {
-    extern __shared__ uint8_t wsm_raw[];
-    uint8_t* sm = wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u);  // A 16 KB + B 8 KB (SW128 boxes)
-    __shared__ __align__(8) uint64_t full, done;
-    __shared__ uint32_t tmem_s;
-    const bool w1 = t < W1_MT * W_NT;
-    const int tt = w1 ? t : t - W1_MT * W_NT;
-    const int mt = tt / W_NT, nt = tt % W_NT;  // M = input features, N = outputs
-    const int in = w1 ? MIN : MH;
-    const CUtensorMap* am = w1 ? &a.x : &a.h1;
-    const CUtensorMap* bm = w1 ? &a.dz1 : &a.dz2;
-    if (tid == 0) {
-      mbar_init(&full, 1);
-      mbar_init(&done, 1);
-      fence_mbar_init();
-    }
-    if (warp == 0) tmem_alloc<W_BN>(&tmem_s);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_s, sb = smem_u32(sm);
-#ifdef TLK_HANG_DEBUG
-    if (tid == 0 && t < 2) printf("wgrad alloc %d %d tmem %u sb %u\n", t, j, tmem, sb);
-#endif
-    if (tid == 0) {
-      // a box that lies wholly outside the tensor never completes its
-      // transaction: skip it (the rows it would hold are never stored)
-      const bool a_hi = mt * 128 + 64 < in;
-      mbar_expect_tx(&full, (a_hi ? 3 : 2) * 8192);
-      tma_load_3d(sb, am, mt * 128, 0, j, &full);
-      if (a_hi) tma_load_3d(sb + 8192, am, mt * 128 + 64, 0, j, &full);
-      tma_load_3d(sb + 16384, bm, nt * W_BN, 0, j, &full);
-      mwait(&full, 0, 12);
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, umma_desc_sw128(sb + kk * 2048, 8192, 1024),
-                 umma_desc_sw128(sb + 16384 + kk * 2048, 8192, 1024), IDESC, kk > 0 ? 1u : 0u);
-      mma_commit(&done);
-    }
-    mwait(&done, 0, 13);
-    tc_fence_after();
-    const int i = mt * 128 + warp * 32 + lane;  // input feature (TMEM lane)
-    // tcgen05.ld is warp-collective: every lane of a warp that owns any valid
-    // row loads; only the rows below `in` update parameters
-    if (mt * 128 + warp * 32 < in) {
-      const int64_t base = L0 + (w1 ? a.o_w1 : a.o_w2) + int64_t(nt * W_BN) * in + i;  // element (o = nt*64, i)
-#pragma unroll 1
-      for (int c0 = 0; c0 < W_BN; c0 += 32) {
-        float g[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c0, g);
-        if (i >= in) continue;
-        const int64_t e = base + int64_t(c0) * in;
-        float* gout = a.write_grads ? a.grads + e : nullptr;
-        if (s.optimizer == TLK_OPT_SGD)
-          adam_cols<TLK_OPT_SGD>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
-        else if (s.optimizer == TLK_OPT_ADAMW)
-          adam_cols<TLK_OPT_ADAMW>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
-        else
-          adam_cols<TLK_OPT_ADAM>(s, a.params + e, a.m1 + e, a.m2 + e, a.wbf + e, gout, in, g);
-      }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc<W_BN>(tmem);
-  } else {  // the small tensors: fc1.b, fc2.b, fc3.w, fc3.b (grads written by the step kernel)
-    const int64_t seg[4][2] = {{a.o_b1, MH}, {a.o_b2, MH}, {a.o_w3, CLASSES * MH}, {a.o_b3, CLASSES}};
-    for (int k = 0; k < 4; ++k)
-      for (int u = tid; u < seg[k][1]; u += W_THREADS) {
-        const int64_t e = L0 + seg[k][0] + u;
-        float p = a.params[e], m = a.m1[e], v = a.m2[e];
-        opt_update(s, p, a.grads[e], m, v);
-        a.params[e] = p;
-        a.m1[e] = m;
-        a.m2[e] = v;
-        a.wbf[e] = f2bf(p);
-      }
-  }
-  // the last CTA of this lane to finish ends the lane's step
-#ifdef TLK_HANG_DEBUG
-  if (tid == 0 && t < 1) printf("wgrad tail %d %d\n", t, j);
-#endif
-  __syncthreads();
+__global__ void __launch_bounds__(MW_THREADS, 1) mlp_wgrad_adam_kernel(const __grid_constant__ MlpWArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t gfull, gempty, tfull[2], tempty[2], sfull[MW_SLOTS], sempty[MW_SLOTS];
+  __shared__ uint32_t tmem_s;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem), slot_base = sbase + MW_STAGE;
+  const uint8_t* slot_ptr = smem + MW_STAGE;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&lsp->done_ctas, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence();
-      lsp->done_ctas = 0;
-      lane_end_step(*lsp);
+    mbar_init(&gfull, 1);
+    mbar_init(&gempty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], MW_UPD);
+    }
+    for (int s = 0; s < MW_SLOTS; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], MW_UPD);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<2 * MW_ON>(&tmem_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_begin();
+  const uint32_t tmem = tmem_s;
+  constexpr uint32_t IDESC = umma_idesc_bf16(128, MW_ON, true, true);
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int it = 0, cs = 0;
+      for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const MwTile w = mw_tile(t);
+        if (!a.lanes[w.j].active) continue;
+        const bool a_hi = w.f0 + 64 < w.in;  // a wholly out-of-range box would never complete
+        if (it >= 1) mwait(&gempty, (it - 1) & 1, 20);
+        mbar_expect_tx(&gfull, (a_hi ? 3 : 2) * 8192);
+        const CUtensorMap* am = w.w1 ? &a.x : &a.h1;
+        const CUtensorMap* bm = w.w1 ? &a.dz1 : &a.dz2;
+        tma_load_3d(sbase, am, w.f0, 0, w.j, &gfull);
+        if (a_hi) tma_load_3d(sbase + 8192, am, w.f0 + 64, 0, w.j, &gfull);
+        tma_load_3d(sbase + 16384, bm, w.o0, 0, w.j, &gfull);
+        ++it;
+        const CUtensorMap* tp = w.w1 ? &a.p1 : &a.p2;
+        const CUtensorMap* tm = w.w1 ? &a.q1 : &a.q2;
+        const CUtensorMap* tv = w.w1 ? &a.v1 : &a.v2;
+        for (int c = 0; c < MW_CH; ++c, ++cs) {
+          const int sl = cs % MW_SLOTS;
+          if (cs >= MW_SLOTS) mwait(&sempty[sl], ((cs / MW_SLOTS) - 1) & 1, 21);
+          const uint32_t d = slot_base + sl * MW_SLOT;
+          mbar_expect_tx(&sfull[sl], MW_SLOT);
+          tma_load_3d(d, tp, w.f0, w.o0 + 32 * c, w.j, &sfull[sl]);
+          tma_load_3d(d + MW_CHUNK, tm, w.f0, w.o0 + 32 * c, w.j, &sfull[sl]);
+          tma_load_3d(d + 2 * MW_CHUNK, tv, w.f0, w.o0 + 32 * c, w.j, &sfull[sl]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const MwTile w = mw_tile(t);
+        if (!a.lanes[w.j].active) continue;
+        const int acc = lt & 1;
+        if (lt >= 2) mwait(&tempty[acc], ((lt >> 1) - 1) & 1, 22);
+        mwait(&gfull, it & 1, 23);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16(tmem + acc * MW_ON, umma_desc_sw128(sbase + kk * 2048, 8192, 1024),
+                   umma_desc_sw128(sbase + 16384 + kk * 2048, 8192, 1024), IDESC, kk > 0 ? 1u : 0u);
+        mma_commit(&gempty);
+        mma_commit(&tfull[acc]);
+        ++it;
+        ++lt;
+      }
+    }
+  } else {  // update warps: TMEM lane quarter q = warp & 3 -> f; og = 8-output group
+    const int q = warp & 3, og = (warp - 2) >> 2, fl = q * 32 + lane;
+    int lt = 0, cs = 0;
+    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+      const MwTile w = mw_tile(t);
+      LaneState* lsp = a.lanes + w.j;
+      if (!lsp->active) continue;
+      const LaneState s = *lsp;
+      const int acc = lt & 1;
+      const bool live = w.f0 + fl < w.in;
+      mwait(&tfull[acc], (lt >> 1) & 1, 24);
+      tc_fence_after();
+      for (int c = 0; c < MW_CH; ++c, ++cs) {
+        const int o0 = 32 * c + 8 * og;  // this thread's outputs w.o0 + o0 .. +7
+        float g[8];
+        tmem_ld8(tmem + acc * MW_ON + o0 + (uint32_t(q * 32) << 16), g);
+        if (c == MW_CH - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int sl = cs % MW_SLOTS;
+        mwait(&sfull[sl], (cs / MW_SLOTS) & 1, 25);
+        const float* Ps = reinterpret_cast<const float*>(slot_ptr + sl * MW_SLOT);
+        float pv[8], mv[8], vv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int off = (8 * og + i) * 128 + fl;  // [32 o][128 f]
+          pv[i] = Ps[off];
+          mv[i] = Ps[MW_CHUNK / 4 + off];
+          vv[i] = Ps[MW_CHUNK / 2 + off];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sl]);  // the slot is refillable once read
+        if (s.optimizer == TLK_OPT_SGD) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_SGD>(s, pv[i], g[i], mv[i], vv[i]);
+        } else if (s.optimizer == TLK_OPT_ADAMW) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_ADAMW>(s, pv[i], g[i], mv[i], vv[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) opt_update_k<TLK_OPT_ADAM>(s, pv[i], g[i], mv[i], vv[i]);
+        }
+        if (live) {
+          const int64_t e = w.j * a.stride + (w.w1 ? a.o_w1 : a.o_w2) + int64_t(w.o0 + o0) * w.in + w.f0 + fl;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            a.params[e + int64_t(i) * w.in] = pv[i];
+            a.m1[e + int64_t(i) * w.in] = mv[i];
+            a.m2[e + int64_t(i) * w.in] = vv[i];
+            a.wbf[e + int64_t(i) * w.in] = f2bf(pv[i]);
+          }
+          if (a.write_grads) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a.grads[e + int64_t(i) * w.in] = g[i];
+          }
+        }
+      }
+      // the last update warp of the lane's last tile ends the lane's step
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&lsp->done_ctas, 1u);
+        if (prev == MW_TPL * MW_UPD - 1) {
+          __threadfence();
+          lsp->done_ctas = 0;
+          lane_end_step(*lsp);
+        }
+      }
+      ++lt;
     }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<2 * MW_ON>(tmem);
 }
 
 struct Mlp2 {
@@ -700,6 +781,9 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   k.x = p.x;
   k.params = p.params;
   k.grads = p.grads;
+  k.m1 = p.mom1;
+  k.m2 = p.mom2;
+  k.wbf = p.wbf;
   k.stride = p.stride;
   k.o_b1 = tensor_offset(d, 1);
   k.o_b2 = tensor_offset(d, 3);
@@ -734,6 +818,15 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   if (!rc) rc = make_tmap_bf16_3d(&w.h1, h1, MH, MB, L, MH * 2, ls, 64, 64);
   if (!rc) rc = make_tmap_bf16_3d(&w.dz1, dz1, MH, MB, L, MH * 2, ls, 64, 64);
   if (!rc) rc = make_tmap_bf16_3d(&w.dz2, dz2, MH, MB, L, MH * 2, ls, 64, 64);
+  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUtensorMapSwizzle NS = CU_TENSOR_MAP_SWIZZLE_NONE;
+  const uint64_t ps = uint64_t(p.stride) * 4;
+  if (!rc) rc = make_tmap_3d(&w.p1, F32, p.params + o_w1, MIN, MH, L, MIN * 4, ps, 128, 32, NS);
+  if (!rc) rc = make_tmap_3d(&w.q1, F32, p.mom1 + o_w1, MIN, MH, L, MIN * 4, ps, 128, 32, NS);
+  if (!rc) rc = make_tmap_3d(&w.v1, F32, p.mom2 + o_w1, MIN, MH, L, MIN * 4, ps, 128, 32, NS);
+  if (!rc) rc = make_tmap_3d(&w.p2, F32, p.params + o_w2, MH, MH, L, MH * 4, ps, 128, 32, NS);
+  if (!rc) rc = make_tmap_3d(&w.q2, F32, p.mom1 + o_w2, MH, MH, L, MH * 4, ps, 128, 32, NS);
+  if (!rc) rc = make_tmap_3d(&w.v2, F32, p.mom2 + o_w2, MH, MH, L, MH * 4, ps, 128, 32, NS);
   if (rc) return rc;
   w.lanes = p.lane_dev;
   w.params = p.params;
@@ -743,13 +836,21 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   w.wbf = p.wbf;
   w.stride = p.stride;
   w.o_w1 = o_w1;
-  w.o_b1 = k.o_b1;
   w.o_w2 = o_w2;
-  w.o_b2 = k.o_b2;
-  w.o_w3 = k.o_w3;
-  w.o_b3 = k.o_b3;
   w.write_grads = (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0;
-  TLK_CUDA(launch(mlp_wgrad_adam_kernel, dim3(W_TILES + 1, L), W_THREADS, 3 * 8192 + 1024, st, w));
+  w.ntiles = L * MW_TPL;
+  static bool wconf = false;
+  if (!wconf) {
+    TLK_CUDA(cudaFuncSetAttribute(mlp_wgrad_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MW_SMEM));
+    wconf = true;
+  }
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  TLK_CUDA(launch(mlp_wgrad_adam_kernel, dim3(std::min(w.ntiles, sms)), MW_THREADS, MW_SMEM, st, w));
   p.mark(st, "mlp_wgrad_adam");
   TLK_CUDA(cudaGetLastError());
   return TLK_OK;
