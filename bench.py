@@ -191,6 +191,13 @@ def kernel_work(name, info, lanes, batch):
     are FLOPs for tensor-bound kernels and bytes for HBM-bound ones."""
     B, L = batch, lanes
     if MODEL == "mlp":
+        if B == 64:  # csrc/mlp2.cu: two launches per step
+            return {
+                # fc1, fc2, fc2 dgrad on tcgen05 (+ inputs, head on CUDA cores): a latency chain
+                "mlp_step": ("tensor", 2.0 * B * (784 * 512 + 2 * 512 * 512) * L),
+                # fused wgrad + optimizer of fc1.w / fc2.w: p, m, v read + write and the bf16 shadow
+                "mlp_wgrad_adam": ("hbm", 26.0 * (784 * 512 + 512 * 512) * L),
+            }.get(name, ("hbm", 0.0))
         return {
             "fc1_fwd": ("tensor", 2.0 * B * 784 * 512 * L),
             "fc2_fwd": ("tensor", 2.0 * B * 512 * 512 * L),
@@ -245,6 +252,9 @@ def gpt_kernel_work(name, model, batch, lanes):
     table = {"qkv": 2.0 * N * 3 * d * d, "proj": 2.0 * N * d * d, "fc": 2.0 * N * 4 * d * d,
              "fc2": 2.0 * N * 4 * d * d, "attn_scores": attn, "attn_pv": attn, "attn_dp": attn,
              "attn_dq": attn, "attn_dk": attn, "attn_dv": attn,
+             # fused attention (attn.cuh): S and PV forward; dP, dQ, dK, dV backward
+             # (the backward's recomputed S is not counted)
+             "attn_fwd": 2 * attn, "attn_bwd": 4 * attn,
              "qkv_wgrad": 2.0 * N * 3 * d * d, "qkv_dgrad": 2.0 * N * 3 * d * d,
              "proj_wgrad": 2.0 * N * d * d, "proj_dgrad": 2.0 * N * d * d,
              "fc_wgrad": 2.0 * N * 4 * d * d, "fc_dgrad": 2.0 * N * 4 * d * d,
