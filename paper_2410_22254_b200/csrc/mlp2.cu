@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "linear.cuh"
@@ -60,6 +61,8 @@ constexpr uint32_t SM_DZ2 = 0, SM_PLOG = 8 * KBLK, SM_DZ3 = SM_PLOG + MC * 640 *
 static_assert(SM_W3 + 128 * 12 * 4 <= MKB1 * KBLK, "head scratch fits in X");
 
 struct MlpArgs {
+  CUtensorMap h1m, dz2m;    // h1 / dz2 [lane][64][512] bf16, box {64 units, 64 samples}: stores of
+                            // this CTA's two k-blocks straight from shared memory
   CUtensorMap w1, w2, w2t;  // bf16 shadows: W1 {784, 512, lane} box {64,128}; W2 {512, 512, lane}
                             // box {64,128}; W2 as MN-major A of the dgrad, box {64, 64}
   LaneState* lanes;
@@ -176,11 +179,26 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   // sample, integer dp4a partials summed by shuffles: exact); then the 16
   // rows of every k-block and the labels go to the three peers
   cluster.sync();  // every CTA's mbarriers are initialised before any remote arrival
+  if (tid == 0) MLP_TR(17);
   {
     int8_t* tch = reinterpret_cast<int8_t*>(smem + SM_RING);  // teacher [10][784] (the ring is idle)
+    __shared__ int tsum[CLASSES];  // sum_i t[c][i]: label score = 2 sum t p - 255 sum t (exact)
     for (int i = tid; i < CLASSES * PIXELS / 16; i += M_THREADS)
       reinterpret_cast<uint4*>(tch)[i] = reinterpret_cast<const uint4*>(a.teacher)[i];
+    for (int cl = warp; cl < CLASSES; cl += M_THREADS / 32) {  // the class's teacher byte sum
+      int t = 0;
+      for (int i = lane; i < PIXELS / 4; i += 32) {
+        int ts;
+        asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts)
+            : "r"(reinterpret_cast<const int*>(a.teacher + cl * PIXELS)[i]), "r"(0x01010101u), "r"(0));
+        t += ts;
+      }
+#pragma unroll
+      for (int m = 16; m; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+      if (lane == 0) tsum[cl] = t;
+    }
     __syncthreads();
+    if (tid == 0) MLP_TR(18);
     const int sl = tid >> 4, s = c * 16 + sl, part = tid & 15;  // sample, word phase
     int accv[CLASSES];
 #pragma unroll
@@ -207,15 +225,13 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
 #pragma unroll
             for (int cl = 0; cl < CLASSES; ++cl) {
               const int tw = reinterpret_cast<const int*>(tch + cl * PIXELS)[2 * q + h];
-              int tp, ts;
-              asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(tp) : "r"(tw), "r"(pw), "r"(0));
-              asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(ts) : "r"(tw), "r"(0x01010101u), "r"(0));
-              accv[cl] += 2 * tp - 255 * ts;
+              asm("dp4a.s32.u32 %0, %1, %2, %0;" : "+r"(accv[cl]) : "r"(tw), "r"(pw));
             }
           }
         }
       }
     }
+    if (tid == 0) MLP_TR(19);
     if (!a.host_input) {
 #pragma unroll
       for (int cl = 0; cl < CLASSES; ++cl)
@@ -229,11 +245,13 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       } else {
         int bestv = 0;
 #pragma unroll
-        for (int cl = 0; cl < CLASSES; ++cl)
-          if (cl == 0 || accv[cl] > bestv) {
+        for (int cl = 0; cl < CLASSES; ++cl) {
+          const int v = 2 * accv[cl] - 255 * tsum[cl];
+          if (cl == 0 || v > bestv) {
             best = cl;
-            bestv = accv[cl];
+            bestv = v;
           }
+        }
         a.labels[size_t(j) * MB + s] = best;
       }
       lbl[s] = best;
@@ -265,14 +283,26 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   // computed from the lane state exactly as the head does for the lane table
   LaneState ost = ls;
   lane_step_scalars(ost);
-  auto upd = [&](int64_t e, float g) {  // e: offset within the lane
-    const int64_t i = j * a.stride + e;
-    float pv = a.params[i], mv = a.m1[i], vv = a.m2[i];
-    opt_update(ost, pv, g, mv, vv);
-    a.params[i] = pv;
-    a.m1[i] = mv;
-    a.m2[i] = vv;
-    a.wbf[i] = f2bf(pv);
+  // N updates with every load issued before the first update (one latency)
+  auto upd_n = [&](auto nc, const int64_t* e, const float* g) {  // e: offsets within the lane
+    constexpr int N = decltype(nc)::value;
+    float pv[N], mv[N], vv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int64_t i = j * a.stride + e[k];
+      pv[k] = a.params[i];
+      mv[k] = a.m1[i];
+      vv[k] = a.m2[i];
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int64_t i = j * a.stride + e[k];
+      opt_update(ost, pv[k], g[k], mv[k], vv[k]);
+      a.params[i] = pv[k];
+      a.m1[i] = mv[k];
+      a.m2[i] = vv[k];
+      a.wbf[i] = f2bf(pv[k]);
+    }
   };
 
   if (warp == 4) {  // ------------------------------------------ TMA producer
@@ -336,20 +366,24 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     const int q = warp, r = q * 32 + lane, o = c * 128 + r;  // r: row of the slice, o: unit
     const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
     float v[MB];
+    int64_t ue[CLASSES + 1];  // deferred small-tensor updates of unit o (fc3.w column, fc2.b)
+    float ug[CLASSES + 1];
+    // this unit's biases and fc3.w column, loaded while fc1 runs
+    const float b1o = P[a.o_b1 + o], b2o = P[a.o_b2 + o];
+    float w3c[CLASSES];
+#pragma unroll
+    for (int cl = 0; cl < CLASSES; ++cl) w3c[cl] = P[a.o_w3 + cl * MH + o];
+    const float b3r = r < CLASSES ? P[a.o_b3 + r] : 0.f;
     // fc1 -> h1 = bf16(relu(acc + b1)): own H1 k-blocks (2c, 2c+1) + global
     mwait(&acc[0], 0, 8);
     if (tid == 0) MLP_TR(8);
     tc_fence_after();
     tmem_ld64(tq, v);
     {
-      const float bb = P[a.o_b1 + o];
-      uint16_t* hg = a.h1 + size_t(j) * MB * MH + o;
+      const float bb = b1o;
 #pragma unroll
-      for (int s = 0; s < MB; ++s) {
-        const uint16_t h = f2bf(fmaxf(v[s] + bb, 0.0f));
-        *reinterpret_cast<uint16_t*>(smem + SM_H1 + kmaj_off(s, o)) = h;
-        hg[size_t(s) * MH] = h;
-      }
+      for (int s = 0; s < MB; ++s)
+        *reinterpret_cast<uint16_t*>(smem + SM_H1 + kmaj_off(s, o)) = f2bf(fmaxf(v[s] + bb, 0.0f));
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
@@ -357,6 +391,9 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       MLP_TR(9);
       mbar_arrive(&h1_loc);
       const uint32_t src = sb + SM_H1 + 2 * c * KBLK;
+      tma_store_3d(&a.h1m, src, 2 * c * 64, 0, j);
+      tma_store_3d(&a.h1m, src + KBLK, 2 * c * 64 + 64, 0, j);
+      bulk_commit();
       for (int pr = 1; pr < MC; ++pr) {
         const uint32_t peer = uint32_t((c + pr) % MC);
         bulk_s2cluster(mapa(src, peer), src, 2 * KBLK, mapa(smem_u32(&h1_rem), peer));
@@ -368,7 +405,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     tc_fence_after();
     tmem_ld64(tq + 64, v);
     {
-      const float bb = P[a.o_b2 + o];
+      const float bb = b2o;
       uint16_t* hg = a.h2 + size_t(j) * MB * MH + o;
       uint16_t* hs = reinterpret_cast<uint16_t*>(smem + SM_HS);
 #pragma unroll
@@ -379,8 +416,8 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         hg[size_t(s) * MH] = h;
       }
       float* w3t = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice]^T (fp32 master), [unit][12]
-      for (int cl = 0; cl < CLASSES; ++cl) w3t[r * 12 + cl] = P[a.o_w3 + cl * MH + o];
-      if (r < CLASSES) b3s[r] = P[a.o_b3 + r];
+      for (int cl = 0; cl < CLASSES; ++cl) w3t[r * 12 + cl] = w3c[cl];
+      if (r < CLASSES) b3s[r] = b3r;
     }
     named_bar_sync(1, 128);
     // partial logits of this slice, plog[c][s * 10 + cl], in every CTA of the
@@ -450,30 +487,16 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       float e[CLASSES], ssum = 0.f;
 #pragma unroll
       for (int cl = 0; cl < CLASSES; ++cl) {
-        e[cl] = expf(l[cl] - m);
+        e[cl] = __expf(l[cl] - m);
         ssum += e[cl];
       }
       lossb[r] = (m + logf(ssum)) - l[y];
+      const float inv = 1.0f / ssum;
 #pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl) dz3[r * CLASSES + cl] = (e[cl] / ssum - (cl == y ? 1.0f : 0.0f)) / float(MB);
+      for (int cl = 0; cl < CLASSES; ++cl)
+        dz3[r * CLASSES + cl] = (e[cl] * inv - (cl == y ? 1.0f : 0.0f)) * (1.0f / float(MB));
     }
     named_bar_sync(1, 128);
-    if (c == 0 && r == 0) {  // loss, fc3.b grad, this step's optimizer scalars
-      float sl = 0.f;
-      for (int s = 0; s < MB; ++s) sl += lossb[s];
-      const float L = sl / float(MB);
-      LaneState& st = a.lanes[j];
-      a.loss[size_t(j) * a.max_steps + st.steps_done] = L;
-      a.last_loss[j] = L;
-      lane_step_scalars(st);
-    }
-    if (c == 0 && r >= 32 && r < 32 + CLASSES) {
-      const int cl = r - 32;
-      float sacc = 0.f;
-      for (int s = 0; s < MB; ++s) sacc += dz3[s * CLASSES + cl];
-      G[a.o_b3 + cl] = sacc;
-      upd(a.o_b3 + cl, sacc);
-    }
     // dz2 = bf16(dz3 W3[:, o] * [h2 > 0]), fc2.b / fc3.w grads of unit o: one
     // pass over the samples (dz3 rows are broadcast loads)
     {
@@ -484,7 +507,6 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         w3o[cl] = w3t[r * 12 + cl];
         gw[cl] = 0.f;
       }
-      uint16_t* zg = a.dz2 + size_t(j) * MB * MH + o;
       float db = 0.f;
 #pragma unroll
       for (int s = 0; s < MB; ++s) {  // fully unrolled: v[] stays in registers
@@ -503,16 +525,20 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         }
         const uint16_t z = f2bf(v[s] > 0.0f ? dh : 0.0f);
         *reinterpret_cast<uint16_t*>(smem + SM_DZ2 + kmaj_off(s, o)) = z;
-        zg[size_t(s) * MH] = z;
         db += bf2f(z);
       }
       G[a.o_b2 + o] = db;
 #pragma unroll
       for (int cl = 0; cl < CLASSES; ++cl) G[a.o_w3 + cl * MH + o] = gw[cl];
-      // fc2.b / fc3.w have been read for the last time this step (h2, logits, dz2)
-      upd(a.o_b2 + o, db);
+      // fc2.b / fc3.w have been read for the last time this step (h2, logits,
+      // dz2); updated below, once dz2 is on its way
 #pragma unroll
-      for (int cl = 0; cl < CLASSES; ++cl) upd(a.o_w3 + cl * MH + o, gw[cl]);
+      for (int cl = 0; cl < CLASSES; ++cl) {
+        ue[cl] = a.o_w3 + cl * MH + o;
+        ug[cl] = gw[cl];
+      }
+      ue[CLASSES] = a.o_b2 + o;
+      ug[CLASSES] = db;
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
@@ -520,11 +546,36 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       MLP_TR(13);
       mbar_arrive(&dz2_loc);
       const uint32_t src = sb + SM_DZ2 + 2 * c * KBLK;
+      tma_store_3d(&a.dz2m, src, 2 * c * 64, 0, j);
+      tma_store_3d(&a.dz2m, src + KBLK, 2 * c * 64 + 64, 0, j);
+      bulk_commit();
       for (int pr = 1; pr < MC; ++pr) {
         const uint32_t peer = uint32_t((c + pr) % MC);
         bulk_s2cluster(mapa(src, peer), src, 2 * KBLK, mapa(smem_u32(&dz2_rem), peer));
       }
     }
+    upd_n(std::integral_constant<int, CLASSES + 1>{}, ue, ug);  // overlaps the exchange and the dgrad
+    // off the critical path (dz2 is on its way): CTA 0's loss, fc3.b grad and
+    // update, and this step's optimizer scalars in the lane table
+    if (c == 0 && r == 0) {  // loss, fc3.b grad, this step's optimizer scalars
+      float sl = 0.f;
+      for (int s = 0; s < MB; ++s) sl += lossb[s];
+      const float L = sl / float(MB);
+      LaneState& st = a.lanes[j];
+      a.loss[size_t(j) * a.max_steps + st.steps_done] = L;
+      a.last_loss[j] = L;
+      lane_step_scalars(st);
+    }
+    if (c == 0 && r >= 32 && r < 32 + CLASSES) {
+      const int cl = r - 32;
+      float sacc = 0.f;
+      for (int s = 0; s < MB; ++s) sacc += dz3[s * CLASSES + cl];
+      G[a.o_b3 + cl] = sacc;
+      const int64_t e1[1] = {a.o_b3 + cl};
+      const float g1[1] = {sacc};
+      upd_n(std::integral_constant<int, 1>{}, e1, g1);
+    }
+
     // fc2 dgrad -> dz1 = bf16(acc * [h1 > 0]) of input unit o, fc1.b grad
     mwait(&acc[2], 0, 11);
     if (tid == 0) MLP_TR(14);
@@ -541,9 +592,12 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         db += bf2f(z);
       }
       G[a.o_b1 + o] = db;
-      upd(a.o_b1 + o, db);
+      const int64_t e1[1] = {a.o_b1 + o};
+      const float g1[1] = {db};
+      upd_n(std::integral_constant<int, 1>{}, e1, g1);
     }
   }
+  if (tid == 0) bulk_wait<0>();  // the h1 / dz2 stores have left shared memory
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc<256>(tmem);
@@ -771,6 +825,8 @@ int mlp2_enqueue_step(Pack& p, cudaStream_t st, uint16_t* h1, uint16_t* h2, uint
   MlpArgs k{};
   const int64_t o_w1 = tensor_offset(d, 0), o_w2 = tensor_offset(d, 2);
   int rc = make_tmap_bf16_3d(&k.w1, p.wbf + o_w1, MIN, MH, L, MIN * 2, uint64_t(p.stride) * 2, 64, 128);
+  if (!rc) rc = make_tmap_bf16_3d(&k.h1m, h1, MH, MB, L, MH * 2, uint64_t(MB) * MH * 2, 64, 64);
+  if (!rc) rc = make_tmap_bf16_3d(&k.dz2m, dz2, MH, MB, L, MH * 2, uint64_t(MB) * MH * 2, 64, 64);
   if (!rc) rc = make_tmap_bf16_3d(&k.w2, p.wbf + o_w2, MH, MH, L, MH * 2, uint64_t(p.stride) * 2, 64, 128);
   if (!rc) rc = make_tmap_bf16_3d(&k.w2t, p.wbf + o_w2, MH, MH, L, MH * 2, uint64_t(p.stride) * 2, 64, 64);
   if (rc) return rc;
