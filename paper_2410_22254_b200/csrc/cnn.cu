@@ -70,11 +70,15 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
 #pragma unroll
     for (int t = 0; t < 9; ++t) w[e][t] = ws[(c * 8 + h * 4 + e) * 9 + t];
   }
-  for (int pos = tid >> 3; pos < 676; pos += 32) {
-    const int oh = pos / 26, ow = pos % 26;
+  // positions pos = g, g + 32, ...: (oh, ow) and both addresses advance
+  // incrementally (32 = 26 + 6: one row and six columns, plus a row on wrap)
+  uint2* hout = reinterpret_cast<uint2*>(h1 + (c * buf.npos + p28_pos(s, 1, 1)) * 8 + h * 4);
+  int pos = tid >> 3, oh = pos / 26, ow = pos % 26;
+  for (; pos < 676; pos += 32) {
+    const float* xp = xs + oh * 28 + ow;
     float xv[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
+    for (int t = 0; t < 9; ++t) xv[t] = xp[(t / 3) * 28 + t % 3];
     float acc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -82,9 +86,14 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restr
 #pragma unroll
       for (int t = 0; t < 9; ++t) acc[e] += xv[t] * w[e][t];
     }
-    *reinterpret_cast<uint2*>(h1 + (c * buf.npos + p28_pos(s, oh + 1, ow + 1)) * 8 + h * 4) =
+    hout[(oh * P28 + ow) * 2] =
         make_uint2(pack_bf2(fmaxf(acc[0] + bsum[0], 0.f), fmaxf(acc[1] + bsum[1], 0.f)),
                    pack_bf2(fmaxf(acc[2] + bsum[2], 0.f), fmaxf(acc[3] + bsum[3], 0.f)));
+    {  // next position: one row and six columns on, a row more on wrap (branch-free)
+      const int wrap = ow >= 20;
+      ow += 6 - 26 * wrap;
+      oh += 1 + wrap;
+    }
   }
 }
 
@@ -205,15 +214,6 @@ __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
   __syncthreads();
   float* G = grads + j * stride;
   if (r == 0) {
-    if (tid == 0) {
-      float sacc = 0.0f;
-      for (int b = 0; b < B; ++b) sacc += lossb[b];
-      const float L = sacc / float(B);
-      LaneState& ls = lanes[j];
-      loss[size_t(j) * max_steps + ls.steps_done] = L;
-      last_loss[j] = L;
-      lane_step_scalars(ls);
-    }
     if (tid < C) {
       float sacc = 0.0f;
       for (int b = 0; b < B; ++b) sacc += d[b * C + tid];
@@ -241,6 +241,17 @@ __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
       for (int b = 0; b < B; ++b) sacc += zs[b * HS + kk];
       G[b1_off + k0 + kk] = sacc;
     }
+  }
+  // last (off the critical path of this kernel): rank 0's loss and the
+  // lane's optimizer scalars for this step (read by the later kernels)
+  if (r == 0 && tid == 255) {
+    float sacc = 0.0f;
+    for (int b = 0; b < B; ++b) sacc += lossb[b];
+    const float L = sacc / float(B);
+    LaneState& ls = lanes[j];
+    loss[size_t(j) * max_steps + ls.steps_done] = L;
+    last_loss[j] = L;
+    lane_step_scalars(ls);
   }
 }
 
@@ -517,6 +528,8 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
   uint16_t(*dzs)[P28_IMG * 8] = reinterpret_cast<uint16_t(*)[P28_IMG * 8]>(dzs_raw);
   __shared__ float xs[784];
   __shared__ float red[C1W_THREADS / 32][4][80];
+  // one barrier for the four chunk planes: every warp holds all four chunks, so
+  // a wait per plane would diverge the warp (and turn its shuffles collective)
   __shared__ __align__(8) uint64_t bar;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -541,7 +554,6 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
     }
   }
   __syncthreads();
-  mbar_wait(&bar, 0);
   // thread = (4-channel half h of chunk c, position group g): 40 accumulators
   // (acc[e][t<9] tap products with x, t = 9: bias), few registers -> 4 CTAs
   // of 8 warps per SM
@@ -551,14 +563,23 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
   for (int e = 0; e < 4; ++e)
 #pragma unroll
     for (int t = 0; t < 10; ++t) acc[e][t] = 0.f;
-  for (int q = g; q < 676; q += C1W_THREADS / 8) {
-    const int oh = q / 26, ow = q % 26;
-    const uint2 dv = *reinterpret_cast<const uint2*>(&dzs[c][((oh + 1) * P28 + ow + 1) * 8 + h * 4]);
+  mbar_wait(&bar, 0);
+  static_assert(C1W_THREADS / 8 == 32, "conv1 wgrad walks positions g, g + 32, ...");
+  const uint2* dzp = reinterpret_cast<const uint2*>(&dzs[c][(P28 + 1) * 8 + h * 4]);  // position (1, 1)
+  int oh = g / 26, ow = g % 26;
+  for (int q = g; q < 676; q += 32) {
+    const uint2 dv = dzp[(oh * P28 + ow) * 2];
     const float d[4] = {__uint_as_float(dv.x << 16), __uint_as_float(dv.x & 0xffff0000u),
                         __uint_as_float(dv.y << 16), __uint_as_float(dv.y & 0xffff0000u)};
+    const float* xp = xs + oh * 28 + ow;
     float xv[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) xv[t] = xs[(oh + t / 3) * 28 + ow + t % 3];
+    for (int t = 0; t < 9; ++t) xv[t] = xp[(t / 3) * 28 + t % 3];
+    {  // next position: one row and six columns on, a row more on wrap (branch-free)
+      const int wrap = ow >= 20;
+      ow += 6 - 26 * wrap;
+      oh += 1 + wrap;
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
 #pragma unroll
