@@ -230,8 +230,8 @@ TLK_DEV void att_qstore(const CUtensorMap* m, uint8_t* stg, int q, const ZWork& 
 // work on S(t).  P is double-buffered in smem (NB = 2:
 // a 128-key buffer for qb 0 tiles and a 256-key one for qb 1 tiles); once
 // O(t) is complete, the first 16 KB of P(t)'s buffer stage Y(t) (a quarter's
-// Y rows overlay only that quarter's P rows).  Ring order per item: Q0 K0 Q1
-// K1 .. V0 V1 .. (the next item's Q / K blocks load as soon as this item's
+// Y rows overlay only that quarter's P rows).  Ring order per item: Q0 Q1 ..
+// K0 K1 .. V0 V1 .. (the next item's Q / K blocks load as soon as this item's
 // S products are done).
 constexpr int ATT_FCW = 16;                       // forward compute warps
 constexpr int ATT_FTHREADS = (ATT_FCW + 2) * 32;  // + TMA producer + MMA issuer
@@ -253,7 +253,9 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
   using C = AttnFwdCfg<NB>;
   constexpr int T = C::T, NSLOT = C::NSLOT, PROD = ATT_FCW, MMA = ATT_FCW + 1;
   constexpr uint32_t IDESC_S = umma_idesc_bf16(128, 128, false, false);
+  constexpr uint32_t IDESC_S256 = umma_idesc_bf16(128, 256, false, false);
   constexpr uint32_t IDESC_O = umma_idesc_bf16(128, 64, false, true);
+  static_assert(NB != 2 || C::NSLOT == 3 * NB, "an item must start at slot 0 (adjacent K blocks)");
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[NSLOT], empty[NSLOT], sfull[2], sfree[2], pfull, ofull[2], oempty[2];
   __shared__ uint32_t tmem_s;
@@ -296,20 +298,23 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
       for (int k = 0; k < nitems; ++k) {
         ZWork w;
         att_decode(a, ilist[k], w);
-        for (int i = 0; i < 3 * NB; ++i, ++bc) {  // Q0 K0 Q1 K1 .. V0 V1 ..
+        for (int i = 0; i < 3 * NB; ++i, ++bc) {  // Q0 Q1 .. K0 K1 .. V0 V1 ..
           const int s = bc % NSLOT;
           if (bc >= NSLOT) mbar_wait(&empty[s], ((bc / NSLOT) - 1) & 1);
           ATT_TR(k * NB, 16 + i);
           mbar_expect_tx(&full[s], ATT_BOX);
-          const CUtensorMap* m = i >= 2 * NB ? &a.tv : (i & 1) ? &a.tk : &a.tq;
-          const int blk = i >= 2 * NB ? i - 2 * NB : i >> 1;
+          const CUtensorMap* m = i < NB ? &a.tq : i < 2 * NB ? &a.tk : &a.tv;
+          const int blk = i % NB;
           tma_load_5d(ring + s * ATT_BOX, m, 0, blk * ATT_ROWS, w.zh, w.zb, w.j, &full[s]);
         }
       }
     }
   } else if (warp == MMA) {  // ---------------------------------- MMA issuer
     if (lane == 0) {
-      auto pos = [](int qb, int k) { return k == 2 ? 2 * NB + qb : 2 * qb + k; };
+      // ring position of block qb of tensor k (0 Q, 1 K, 2 V); with NSLOT = 3 NB
+      // (NB = 2) every item starts at slot 0, so K0 K1 are adjacent slots: the
+      // 256-key S of a qb 1 tile is ONE N = 256 MMA per k step
+      auto pos = [](int qb, int k) { return k * NB + qb; };
       auto slot = [&](int base, int qb, int k) { return (base + pos(qb, k)) % NSLOT; };
       auto par = [&](int base, int qb, int k) { return uint32_t(((base + pos(qb, k)) / NSLOT) & 1); };
       const uint32_t pa[2] = {smem_u32(Pbuf[0]), smem_u32(Pbuf[1])};
@@ -326,11 +331,12 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
           mbar_wait(&full[slot(pbase, kb, 2)], par(pbase, kb, 2));
           tc_fence_after();
           const uint32_t vs = ring + slot(pbase, kb, 2) * ATT_BOX;
+          const uint64_t pd0 = att_kdesc(ps, 0), vd0 = att_mdesc(vs, 0, 8192);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
+          for (int kk = 0; kk < 8; ++kk) {  // descriptors advance by (bytes >> 4) in the address field
             const int key = kb * 128 + kk * 16;
-            mma_bf16(d, att_kdesc(ps + (key >> 6) * ATT_BOX, (key & 63) >> 4), att_mdesc(vs, kk, 8192), IDESC_O,
-                     (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16(d, pd0 + uint64_t(((key >> 6) * ATT_BOX + ((key & 63) >> 4) * 32) >> 4),
+                     vd0 + uint64_t(kk * (2048 >> 4)), IDESC_O, (kb > 0 || kk > 0) ? 1u : 0u);
           }
         }
         mma_commit(&ofull[ob]);
@@ -347,14 +353,24 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
           mbar_wait(&full[slot(base, qb, 0)], par(base, qb, 0));
           tc_fence_after();
           const uint32_t qs = ring + slot(base, qb, 0) * ATT_BOX;
+          const uint64_t qd0 = att_kdesc(qs, 0);
           for (int kb = 0; kb <= qb; ++kb) {
             mbar_wait(&full[slot(base, kb, 1)], par(base, kb, 1));
             tc_fence_after();
-            const uint32_t ks = ring + slot(base, kb, 1) * ATT_BOX;
+          }
+          const uint32_t dS = tmem + (sb ? C::S_OFF1 : 0u);
+          if (NB == 2 && qb == 1) {  // keys 0..255: K0, K1 adjacent -> N = 256
+            const uint64_t kd0 = att_kdesc(ring + slot(base, 0, 1) * ATT_BOX, 0);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(tmem + (sb ? C::S_OFF1 : 0u) + kb * 128, att_kdesc(qs, kk), att_kdesc(ks, kk), IDESC_S,
-                       kk > 0 ? 1u : 0u);
+              mma_bf16(dS, qd0 + uint64_t(kk * 2), kd0 + uint64_t(kk * 2), IDESC_S256, kk > 0 ? 1u : 0u);
+          } else {
+            for (int kb = 0; kb <= qb; ++kb) {
+              const uint64_t kd0 = att_kdesc(ring + slot(base, kb, 1) * ATT_BOX, 0);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16(dS + kb * 128, qd0 + uint64_t(kk * 2), kd0 + uint64_t(kk * 2), IDESC_S, kk > 0 ? 1u : 0u);
+            }
           }
           mma_commit(&sfull[sb]);
           ATT_TR(t, 10);
