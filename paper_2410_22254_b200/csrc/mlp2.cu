@@ -180,8 +180,33 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   // rows of every k-block and the labels go to the three peers
   cluster.sync();  // every CTA's mbarriers are initialised before any remote arrival
   if (tid == 0) MLP_TR(17);
+  // the producer thread starts the W1 stream now (the weights do not depend on
+  // the inputs): the first MSTAGES tiles land while the inputs are generated
+  auto produce = [&](int it) {
+    const int s = it % MSTAGES;
+    if (it >= MSTAGES) mwait(&empty[s], ((it / MSTAGES) - 1) & 1, 2);
+    mbar_expect_tx(&full[s], ABLK);
+    const uint32_t dst = sb + SM_RING + s * ABLK;
+    if (it < MKB1) {
+      tma_load_3d(dst, &a.w1, it * 64, c * 128, j, &full[s]);
+    } else if (it < MKB1 + 8) {
+      tma_load_3d(dst, &a.w2, (it - MKB1) * 64, c * 128, j, &full[s]);
+    } else {
+      const int kb = it - MKB1 - 8;  // W2[kb*64 .. +64 o2][c*128 .. +128 o1], o1 contiguous
+      tma_load_3d(dst, &a.w2t, c * 128, kb * 64, j, &full[s]);
+      tma_load_3d(dst + 8192, &a.w2t, c * 128 + 64, kb * 64, j, &full[s]);
+    }
+  };
+  if (tid == 128) {
+    tma_prefetch_desc(&a.w1);
+    tma_prefetch_desc(&a.w2);
+    tma_prefetch_desc(&a.w2t);
+    for (int it = 0; it < MSTAGES; ++it) produce(it);
+  }
   {
-    int8_t* tch = reinterpret_cast<int8_t*>(smem + SM_RING);  // teacher [10][784] (the ring is idle)
+    // teacher [10][784] in H1, idle until this CTA's fc1 epilogue (no peer
+    // sends h1 before it has this CTA's x rows, i.e. before this phase ends)
+    int8_t* tch = reinterpret_cast<int8_t*>(smem + SM_H1);
     __shared__ int tsum[CLASSES];  // sum_i t[c][i]: label score = 2 sum t p - 255 sum t (exact)
     for (int i = tid; i < CLASSES * PIXELS / 16; i += M_THREADS)
       reinterpret_cast<uint4*>(tch)[i] = reinterpret_cast<const uint4*>(a.teacher)[i];
@@ -272,7 +297,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();  // (the producer may now overwrite the teacher in the ring)
+  __syncthreads();
   tc_fence_after();
   if (tid == 0) MLP_TR(1);
   const uint32_t tmem = tmem_s;
@@ -306,26 +331,8 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
   };
 
   if (warp == 4) {  // ------------------------------------------ TMA producer
-    if (lane == 0) {
-      tma_prefetch_desc(&a.w1);
-      tma_prefetch_desc(&a.w2);
-      tma_prefetch_desc(&a.w2t);
-      for (int it = 0; it < MKB1 + 16; ++it) {
-        const int s = it % MSTAGES;
-        if (it >= MSTAGES) mwait(&empty[s], ((it / MSTAGES) - 1) & 1, 2);
-        mbar_expect_tx(&full[s], ABLK);
-        const uint32_t dst = sb + SM_RING + s * ABLK;
-        if (it < MKB1) {
-          tma_load_3d(dst, &a.w1, it * 64, c * 128, j, &full[s]);
-        } else if (it < MKB1 + 8) {
-          tma_load_3d(dst, &a.w2, (it - MKB1) * 64, c * 128, j, &full[s]);
-        } else {
-          const int kb = it - MKB1 - 8;  // W2[kb*64 .. +64 o2][c*128 .. +128 o1], o1 contiguous
-          tma_load_3d(dst, &a.w2t, c * 128, kb * 64, j, &full[s]);
-          tma_load_3d(dst + 8192, &a.w2t, c * 128 + 64, kb * 64, j, &full[s]);
-        }
-      }
-    }
+    if (lane == 0)
+      for (int it = MSTAGES; it < MKB1 + 16; ++it) produce(it);
   } else if (warp == 5) {  // -------------------------------------- MMA issuer
     if (lane == 0) {
       int it = 0;
@@ -334,6 +341,7 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % MSTAGES;
           mwait(&full[s], (it / MSTAGES) & 1, 3);
+          if (it < 12) MLP_TR(20 + it);
           tc_fence_after();
           const uint32_t as = sb + SM_RING + s * ABLK;
 #pragma unroll
@@ -406,14 +414,14 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
     tmem_ld64(tq + 64, v);
     {
       const float bb = b2o;
-      uint16_t* hg = a.h2 + size_t(j) * MB * MH + o;
+
       uint16_t* hs = reinterpret_cast<uint16_t*>(smem + SM_HS);
 #pragma unroll
       for (int s = 0; s < MB; ++s) {
         const uint16_t h = f2bf(fmaxf(v[s] + bb, 0.0f));
         v[s] = bf2f(h);
         hs[s * 136 + r] = h;
-        hg[size_t(s) * MH] = h;
+
       }
       float* w3t = reinterpret_cast<float*>(smem + SM_W3);  // fc3.w[:, slice]^T (fp32 master), [unit][12]
       for (int cl = 0; cl < CLASSES; ++cl) w3t[r * 12 + cl] = w3c[cl];
@@ -428,6 +436,12 @@ __global__ void __cluster_dims__(MC, 1, 1) __launch_bounds__(M_THREADS, 1)
       const float* w3t = reinterpret_cast<const float*>(smem + SM_W3);  // [unit][12]
       float* plog = reinterpret_cast<float*>(smem + SM_PLOG);
       const int s = r >> 1, half = r & 1;
+      {  // h2[s][slice units half*64 .. +64] -> global: eight 16-B stores per thread
+        const uint4* src = reinterpret_cast<const uint4*>(hs + s * 136 + half * 64);
+        uint4* dst = reinterpret_cast<uint4*>(a.h2 + (size_t(j) * MB + s) * MH + c * 128 + half * 64);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = src[i];
+      }
       float acc10[CLASSES];
 #pragma unroll
       for (int cl = 0; cl < CLASSES; ++cl) acc10[cl] = 0.f;

@@ -12,7 +12,8 @@ lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 NAMES = {0: "start", 1: "inputs+sync", 2: "M:fc1 issued", 3: "M:h1 all", 4: "M:fc2 issued", 5: "M:dz2 all",
          6: "M:dgrad issued", 7: "labels", 8: "E:fc1 done", 9: "E:h1 sent", 10: "E:fc2 done", 11: "E:plog sent",
          12: "E:plog all", 13: "E:dz2 sent", 14: "E:dgrad done", 15: "end", 16: "cluster exit",
-         17: "cluster.sync", 18: "teacher", 19: "words done"}
+         17: "cluster.sync", 18: "teacher", 19: "words done",
+         **{20 + i: f"M:w1 tile {i}" for i in range(12)}}
 with rt.Context(0) as ctx:
     p = ctx.pack(rt.MODEL_MLP, 64, lanes, 8)
     for j in range(lanes):
