@@ -413,11 +413,11 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
         const int cw = (qb + 1) * 32;                              // columns per warp: ncols / 4
         const int c0 = part * cw;
         const bool any = c0 <= row0 + 31;  // some row of the warp sees a key here
-        float xv[32];                      // one chunk of exponentials
         // NV = this warp's columns (32, or 64 for the 256-key tile), handled
         // as NV / 32 chunks: compile-time, so the per-element loops are
         // straight-line code (selects, no branches) on 32 live values
-        auto softmax = [&](auto nvc) {
+        float xv[32];  // softmax3: one chunk of exponentials
+        auto softmax3 = [&](auto nvc) {  // NV = 64: three 32-column passes over TMEM (register budget)
           constexpr int NV = decltype(nvc)::value, NC = NV / 32;
           const int sb = t & 1;
           mbar_wait(&sfull[sb], (t >> 1) & 1);
@@ -489,10 +489,70 @@ __global__ void __launch_bounds__(ATT_FTHREADS, 1) attn_fwd_kernel(const __grid_
           __syncwarp();
           if (lane == 0) mbar_arrive(&sfree[sb]);  // S(t)'s buffer may take S(t + 2)
         };
+        auto softmax1 = [&](auto nvc) {  // NV = 32: S read once into registers
+          constexpr int NV = decltype(nvc)::value, NC = NV / 32;
+          const int sb = t & 1;
+          mbar_wait(&sfull[sb], (t >> 1) & 1);
+          if (warp == 0 && lane == 0) ATT_TR(t, 0);
+          tc_fence_after();
+          const uint32_t ts = tmem + (sb ? C::S_OFF1 : 0u) + (uint32_t(q * 32) << 16) + c0;
+          // ONE pass over TMEM (its read bandwidth, 64 B/clk/SM, is the
+          // scarce resource here): S -> registers, mask, max; exponentials in
+          // place; P from the registers
+          float v[NV];
+          float mx = -INFINITY;
+          if (any) {
+            if constexpr (NV == 64)
+              tmem_ld64(ts, v);
+            else
+              tmem_ld32(ts, v);
+#pragma unroll
+            for (int h = 0; h < NC; ++h)
+              if (c0 + h * 32 + 31 > row0) {  // the causal diagonal crosses this chunk
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[h * 32 + i] = (c0 + h * 32 + i > m) ? -INFINITY : v[h * 32 + i];
+              }
+#pragma unroll
+            for (int i = 0; i < NV; ++i) mx = fmaxf(mx, v[i]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sfree[sb]);  // S(t) consumed: its buffer may take S(t + 2)
+          if (warp == 0 && lane == 0) ATT_TR(t, 1);
+          xchg[0][part][r] = mx;
+          named_bar_sync(1 + q, 128);
+          if (warp == 0 && lane == 0) ATT_TR(t, 2);
+          mx = fmaxf(fmaxf(xchg[0][0][r], xchg[0][1][r]), fmaxf(xchg[0][2][r], xchg[0][3][r]));
+          const float mk = mx * k2;
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (any) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+              v[i] = ex2_approx(fmaf(v[i], k2, -mk));  // masked: ex2(-inf) = 0
+              s4[i & 3] += v[i];
+            }
+          }
+          xchg[1][part][r] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          if (qleader) bulk_wait_read<0>();  // Y(t - 2)'s store has read this quarter's rows of P(t)'s buffer
+          named_bar_sync(1 + q, 128);
+          const float s = (xchg[1][0][r] + xchg[1][1][r]) + (xchg[1][2][r] + xchg[1][3][r]);
+          const float inv = 1.f / s;
+          if (part == 0) reinterpret_cast<float2*>(a.stats)[att_row(a, w, T, m)] = make_float2(mk, inv);
+          // P(t) -> smem buffer t & 1 (free: O(t - 2) completed before Y(t - 2) was drained)
+          uint8_t* P = Pbuf[NB == 2 ? qb : (t & 1)];
+#pragma unroll
+          for (int h = 0; h < NC; ++h) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              pk[i] = any ? pack_bf2(v[h * 32 + 2 * i] * inv, v[h * 32 + 2 * i + 1] * inv) : 0u;
+            att_put32(P, r, c0 + h * 32, pk);
+          }
+        };
         if (NB == 2 && qb == 1)
-          softmax(std::integral_constant<int, 64>{});
+          softmax3(std::integral_constant<int, 64>{});
         else
-          softmax(std::integral_constant<int, 32>{});
+          softmax1(std::integral_constant<int, 32>{});
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull);
