@@ -60,7 +60,7 @@ struct ConvGemm {
   static constexpr int STAGES = HALO ? (BN_ <= 64 ? 3 : 2)
                                      : (BN_ <= 64 ? 6 : BN_ <= 128 ? 4 : BN_ <= 192 ? 4 - (PARTS - 1) : 3);
   static constexpr int THREADS = (EW + 2) * 32;
-  static constexpr bool A_MN = MODE == CONV_WGRAD, B_MN = MODE == CONV_WGRAD, ROW_EPI = false;
+  static constexpr bool A_MN = MODE == CONV_WGRAD, B_MN = MODE == CONV_WGRAD, ROW_EPI = false, TMA_EPI = false;
   static_assert(!HALO || MODE != CONV_WGRAD, "halo mode is FWD / DGRAD only");
   static constexpr int STAGING_BYTES = EW * 32 * 33 * 4;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024;

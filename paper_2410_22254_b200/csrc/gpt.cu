@@ -358,10 +358,59 @@ __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ l
   }
 }
 
-// token-embedding gradient, stage 1: per block of 256 positions, smem
-// acc[v][c] (thread = column, positions in order) -> part[lane][blk][v][c]
+// Token-embedding gradient for a small vocabulary (V x d fp32 fits shared
+// memory): CTA (row chunk, lane) streams its rows of dx once, thread c owns
+// float4 column c of every vocabulary row, acc[token][c] += dx[row][c] in row
+// order (EMT_U rows in flight per thread), and writes part[lane][chunk][v][c];
+// reduce_parts8 sums the chunks in fixed order.  Every dx row is read once at
+// full width (the vocabulary-block kernel below rescans the token list per
+// block and keeps only a few loads in flight).
+constexpr int EMT_U = 16;
+constexpr size_t EMT_SMEM_MAX = 112 * 1024;  // two CTAs per SM
+__global__ void __launch_bounds__(128) embed_bwd_tok_kernel(const LaneState* __restrict__ lanes, int N, int d, int V,
+                                                            const int32_t* __restrict__ tokens, int T,
+                                                            const float* __restrict__ dx, float* __restrict__ part,
+                                                            int64_t part_st, int rows_per) {
+  pdl_begin();
+  extern __shared__ float4 acc4[];  // [V][d / 4]
+  const int j = blockIdx.y, tid = threadIdx.x, d4 = d >> 2;
+  if (!lanes[j].active) return;
+  for (int i = tid; i < V * d4; i += blockDim.x) acc4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  const int r0 = blockIdx.x * rows_per, r1 = min(N, r0 + rows_per);
+  if (tid < d4) {
+    const float4* g = reinterpret_cast<const float4*>(dx + int64_t(j) * N * d) + tid;
+    const int32_t* tk = tokens + int64_t(j) * (N / T) * (T + 1);
+    int r = r0;
+    for (; r + EMT_U <= r1; r += EMT_U) {
+      float4 val[EMT_U];
+      int v[EMT_U];
+#pragma unroll
+      for (int u = 0; u < EMT_U; ++u) {
+        const int row = r + u;
+        v[u] = tk[(row / T) * (T + 1) + row % T];
+        val[u] = g[int64_t(row) * d4];
+      }
+#pragma unroll
+      for (int u = 0; u < EMT_U; ++u)
+        if (unsigned(v[u]) < unsigned(V)) {
+          float4& a = acc4[v[u] * d4 + tid];
+          a.x += val[u].x, a.y += val[u].y, a.z += val[u].z, a.w += val[u].w;
+        }
+    }
+    for (; r < r1; ++r) {
+      const int v = tk[(r / T) * (T + 1) + r % T];
+      const float4 x = g[int64_t(r) * d4];
+      if (unsigned(v) < unsigned(V)) {
+        float4& a = acc4[v * d4 + tid];
+        a.x += x.x, a.y += x.y, a.z += x.z, a.w += x.w;
+      }
+    }
+    float4* out = reinterpret_cast<float4*>(part + j * part_st + int64_t(blockIdx.x) * V * d) + tid;
+    for (int w = 0; w < V; ++w) out[int64_t(w) * d4] = acc4[w * d4 + tid];
+  }
+}
 
-// dwpe[t][c] = sum_b dx[b*T + t][c] (b in order)
 // Token-embedding gradient by vocabulary row: CTA (vocab block of EMV rows,
 // column slice) scans the lane's input tokens in order, compacts the rows
 // whose token falls in its block (block-wide scan -> token order), and
@@ -433,6 +482,7 @@ __global__ void __launch_bounds__(EMV_COLS) embed_bwd_vocab_kernel(const LaneSta
     for (int v = 0; v < EMV && v0 + v < V; ++v) grads[j * pstride + o_wte + int64_t(v0 + v) * d + c] = acc[v][tid];
 }
 
+// dwpe[t][c] = sum_b dx[b*T + t][c] (b in order)
 __global__ void wpe_bwd_kernel(const LaneState* __restrict__ lanes, int B, int T, int d,
                                const float* __restrict__ dx, float* __restrict__ grads,
                                int64_t pstride, int64_t o_wpe) {
@@ -452,10 +502,37 @@ Operand op(const uint16_t* base, int64_t ls, int64_t bs, int64_t hs, int64_t mn_
   return Operand{base, ls, bs, hs, mn_st, k_st, MN, K};
 }
 
-template <int BN, bool AMN, bool BMN, bool ROW>
+// Tensor maps of a dense epilogue's outputs / aux operand ({16 columns, 32
+// rows} boxes, SW32 for bf16 rows, SW64 for fp32 rows; dims {cols, rows, h,
+// b, lane} over the Epi strides).  `on` stays 0 (per-element tile4 path) for
+// layouts the TMA tiles cannot express or when TLK_TMA_EPI=0.
+int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, const Epi& e, int lanes, int nb,
+                 int nh) {
+  static const bool off = getenv("TLK_TMA_EPI") && getenv("TLK_TMA_EPI")[0] == '0';
+  on = 0;
+  const bool dense = e.kind == EPI_BF16 || e.kind == EPI_BF16_GELU || e.kind == EPI_F32 || e.kind == EPI_RESADD ||
+                     e.kind == EPI_GELU_BWD;
+  if (off || !dense || e.cols % 16 != 0) return TLK_OK;
+  const bool f32 = e.kind == EPI_F32 || e.kind == EPI_RESADD;
+  auto mk = [&](CUtensorMap& m, const void* base, bool is_f32) {
+    const uint64_t eb = is_f32 ? 4 : 2;
+    const uint64_t dims[5] = {uint64_t(e.cols), uint64_t(e.rows), uint64_t(nh), uint64_t(nb), uint64_t(lanes)};
+    const uint64_t st[4] = {uint64_t(e.ld) * eb, uint64_t(e.hs) * eb, uint64_t(e.bs) * eb, uint64_t(e.ls) * eb};
+    return make_tmap_5d(&m, is_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, dims,
+                        st, 16, 32, is_f32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  };
+  int rc = mk(mo, e.out, f32);
+  if (!rc && e.kind == EPI_BF16_GELU) rc = mk(mo2, e.out2, false);
+  if (!rc && (e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD)) rc = mk(ma, e.aux, e.kind == EPI_RESADD);
+  if (rc) return rc;
+  on = 1;
+  return TLK_OK;
+}
+
+template <int BN, bool AMN, bool BMN, bool ROW, bool LIGHT = false>
 int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M,
          int N, int K, int nb, int nh, const char* name) {
-  using G = TGemm<BN, AMN, BMN, ROW>;
+  using G = TGemm<BN, AMN, BMN, ROW, LIGHT>;
   G g{};
   g.g = EpiOps{p.lane_dev, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
   // vector-epilogue contract (sgemm.cuh): 4-element aligned rows and z strides
@@ -465,6 +542,7 @@ int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, con
   TLK_CHECK(!ROW || N <= BN, TLK_EINVAL, "%s: row epilogue needs the whole row in one tile", name);
   int rc = make_operand_map(&g.ta, A, AMN, GEMM_BM, p.lanes, nb, nh);
   if (!rc) rc = make_operand_map(&g.tb, B, BMN, BN, p.lanes, nb, nh);
+  if (!rc && !ROW) rc = tma_epi_maps(g.to, g.to2, g.tx, g.tma_epi, e, p.lanes, nb, nh);
   if (rc) return rc;
   g.mt = (M + GEMM_BM - 1) / GEMM_BM;
   g.nt = (N + BN - 1) / BN;
@@ -482,6 +560,13 @@ template <bool AMN, bool BMN>
 int gemm_auto(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M, int N, int K,
               int nb, int nh, const char* name) {
   static const bool narrow = getenv("TLK_GEMM_BN128") && getenv("TLK_GEMM_BN128")[0] == '1';
+  if constexpr (!(AMN && BMN)) {
+    // plain fp32 output (dgrads): one epilogue warp per lane quarter, deeper pipeline
+    if (e.kind == EPI_F32 && !narrow) {
+      if (N % 256 == 0) return gemm<256, AMN, BMN, false, true>(p, st, A, B, e, M, N, K, nb, nh, name);
+      if (N % 192 == 0) return gemm<192, AMN, BMN, false, true>(p, st, A, B, e, M, N, K, nb, nh, name);
+    }
+  }
   if (!narrow && N % 256 == 0) return gemm<256, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
   if (!narrow && N % 192 == 0) return gemm<192, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
   return gemm<128, AMN, BMN, false>(p, st, A, B, e, M, N, K, nb, nh, name);
@@ -981,8 +1066,26 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   }
   {  // embeddings
     TLK_CHECK(int64_t(N) < (int64_t(1) << 27), TLK_EINVAL, "embedding gradient: %d tokens per lane", N);
-    TLK_CUDA(launch(embed_bwd_vocab_kernel, dim3((V + EMV - 1) / EMV, (d + EMV_COLS - 1) / EMV_COLS, Lc), EMV_COLS, 0,
-                    st, LS, N, d, V, b.tokens, T, b.dx, G, PS, O(T_WTE)));
+    const size_t emt_smem = size_t(V) * d * 4;
+    const int emt_chunks = std::min<int64_t>({int64_t(N + 255) / 256, (2 * b.sms + Lc - 1) / Lc,
+                                              b.part_st / (int64_t(V) * d)});
+    if (d % 4 == 0 && d <= 512 && emt_smem <= EMT_SMEM_MAX && emt_chunks >= 1) {
+      static bool emt_configured = false;
+      if (!emt_configured) {
+        TLK_CUDA(cudaFuncSetAttribute(embed_bwd_tok_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(EMT_SMEM_MAX)));
+        emt_configured = true;
+      }
+      const int rows_per = (N + emt_chunks - 1) / emt_chunks;
+      TLK_CUDA(launch(embed_bwd_tok_kernel, dim3((N + rows_per - 1) / rows_per, Lc), 128, emt_smem, st, LS, N, d, V,
+                      b.tokens, T, b.dx, b.part, b.part_st, rows_per));
+      TLK_CUDA(launch(reduce_parts8_kernel, dim3((V * d + 31) / 32, Lc), 256, 0, st, LS, b.part, b.part_st,
+                      (N + rows_per - 1) / rows_per, V * d, G, PS, O(T_WTE)));
+      ++count;
+    } else {
+      TLK_CUDA(launch(embed_bwd_vocab_kernel, dim3((V + EMV - 1) / EMV, (d + EMV_COLS - 1) / EMV_COLS, Lc), EMV_COLS,
+                      0, st, LS, N, d, V, b.tokens, T, b.dx, G, PS, O(T_WTE)));
+    }
     marked("wte_grad");
     TLK_CUDA(launch(wpe_bwd_kernel, dim3(T, Lc), 128, 0, st, LS, B, T, d, b.dx, G, PS, O(T_WPE)));
     TLK_CUDA(cudaGetLastError());

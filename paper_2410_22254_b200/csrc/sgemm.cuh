@@ -7,6 +7,7 @@
 #pragma once
 #include "models.cuh"
 #include "tc_gemm.cuh"
+#include "tma.cuh"
 
 namespace tlk {
 
@@ -72,16 +73,43 @@ TLK_DEV float ex2_approx(float x) {
 }
 TLK_DEV float exp_fast(float x) { return ex2_approx(x * 1.4426950408889634f); }
 
+// gelu(x) = 0.5 x (1 + tanh(u)), u = c0 x + c1 x^3, written as FMA chains
+// (x^2 once; 0.5 folded into the final FMA).
+constexpr float GELU_C0 = 0.7978845608028654f, GELU_C1 = 0.7978845608028654f * 0.044715f;
 TLK_DEV float gelu_tanh(float x, float& t) {
-  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  t = tanh_fast(u);
-  return 0.5f * x * (1.0f + t);
+  const float x2 = x * x;
+  t = tanh_fast(x * fmaf(x2, GELU_C1, GELU_C0));
+  const float h = 0.5f * x;
+  return fmaf(h, t, h);
 }
-TLK_DEV float gelu_tanh_grad(float x) {
-  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  const float t = tanh_fast(u);
-  const float du = 0.7978845608028654f * (1.0f + 3.0f * 0.044715f * x * x);
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+// y * gelu'(x) = 0.5 y (1 + t + x du (1 - t^2)),  du = c0 + 3 c1 x^2
+TLK_DEV float gelu_bwd_mul(float y, float x) {
+  const float x2 = x * x;
+  const float t = tanh_fast(x * fmaf(x2, GELU_C1, GELU_C0));
+  const float xd = x * fmaf(x2, 3.0f * GELU_C1, GELU_C0);
+  const float q = fmaf(xd, fmaf(-t, t, 1.0f), t);
+  const float hy = 0.5f * y;
+  return fmaf(hy, q, hy);
+}
+
+// the same two functions on f32x2 pairs (bit-identical per lane: the FMA
+// chains are the scalar ones, with -(3 c1 x^2 + c0) and t^2 - 1 carrying the
+// signs so that no negation instruction is needed)
+TLK_DEV f2 gelu2(f2 x) {
+  const f2 x2 = f2_mul(x, x);
+  const f2 u = f2_mul(x, f2_fma(x2, f2_make(GELU_C1, GELU_C1), f2_make(GELU_C0, GELU_C0)));
+  const f2 t = f2_make(tanh_fast(f2_lo(u)), tanh_fast(f2_hi(u)));
+  const f2 h = f2_mul(x, f2_make(0.5f, 0.5f));
+  return f2_fma(h, t, h);
+}
+TLK_DEV f2 gelu_bwd_mul2(f2 y, f2 x) {
+  const f2 x2 = f2_mul(x, x);
+  const f2 u = f2_mul(x, f2_fma(x2, f2_make(GELU_C1, GELU_C1), f2_make(GELU_C0, GELU_C0)));
+  const f2 t = f2_make(tanh_fast(f2_lo(u)), tanh_fast(f2_hi(u)));
+  const f2 xdn = f2_mul(x, f2_fma(x2, f2_make(-3.0f * GELU_C1, -3.0f * GELU_C1), f2_make(-GELU_C0, -GELU_C0)));
+  const f2 q = f2_fma(xdn, f2_fma(t, t, f2_make(-1.0f, -1.0f)), t);
+  const f2 hy = f2_mul(y, f2_make(0.5f, 0.5f));
+  return f2_fma(hy, q, hy);
 }
 
 // Epilogue state of one launch + the per-kind tile routines.  A warp owns 32
@@ -198,8 +226,8 @@ struct EpiOps {
               make_float4(r4.x + y0, r4.y + y1, r4.z + y2, r4.w + y3);
         } else if constexpr (KIND == EPI_GELU_BWD) {
           const float4 z = ax[k];
-          const uint32_t lo = pack_bf2(y0 * gelu_tanh_grad(z.x), y1 * gelu_tanh_grad(z.y));
-          const uint32_t hi = pack_bf2(y2 * gelu_tanh_grad(z.z), y3 * gelu_tanh_grad(z.w));
+          const uint32_t lo = pack_bf2(gelu_bwd_mul(y0, z.x), gelu_bwd_mul(y1, z.y));
+          const uint32_t hi = pack_bf2(gelu_bwd_mul(y2, z.z), gelu_bwd_mul(y3, z.w));
           *reinterpret_cast<uint2*>(static_cast<uint16_t*>(e.out) + oo) = make_uint2(lo, hi);
           cs[0] += __uint_as_float(lo << 16);
           cs[1] += __uint_as_float(lo & 0xffff0000u);
@@ -225,6 +253,204 @@ struct EpiOps {
         }
       }
       __syncwarp();
+    }
+  }
+
+  // ---- TMA-staged dense epilogues (thread = accumulator row) ---------------
+  // tile4 transposes every 32 x 32 chunk through `buf` so that global stores
+  // coalesce; here each thread keeps its TMEM row, works on 16-column chunks
+  // in registers and writes them (one or two 16 B vectors per 8 columns) into
+  // a per-warp 2 KB staging tile laid out in the TMA swizzle of a {16, 32}
+  // box, which one lane stores with cp.async.bulk.tensor.  The aux operand
+  // (GELU' input, residual) is TMA-loaded into the same tile one chunk ahead
+  // and overwritten in place.  Two tiles per warp (ping-pong on `cnt`);
+  // rows / columns past the tensor are clipped by TMA, so there are no
+  // per-element bounds checks.  Bias-gradient column partials are summed
+  // from the staged bf16 tile.
+  template <int KIND>
+  static constexpr int tma_ob() {
+    return (KIND == EPI_F32 || KIND == EPI_RESADD) ? 4 : 2;
+  }
+  template <int KIND>
+  static constexpr uint32_t tma_aux_bytes() {
+    return KIND == EPI_GELU_BWD ? 32 * 16 * 2 : KIND == EPI_RESADD ? 32 * 16 * 4 : 0;
+  }
+  // byte offset of 16 B vector c of row r in a swizzled {16, 32} box tile
+  template <int OB>
+  TLK_DEV static uint32_t sw_off(int r, int c) {
+    if constexpr (OB == 2)
+      return uint32_t(r * 32 + ((c ^ ((r >> 2) & 1)) << 4));  // SWIZZLE_32B
+    else
+      return uint32_t(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));  // SWIZZLE_64B
+  }
+  TLK_DEV bool tma_live(const ZWork& w, int row0, int n) const { return row0 < e.rows && n < e.cols; }
+
+  // issue the aux load of the warp's first chunk of a tile (before its TMEM wait)
+  template <int KIND, int BN, int NP>
+  TLK_DEV void tma_pre(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar, uint32_t cnt,
+                       const CUtensorMap* ma) const {
+    if constexpr (tma_aux_bytes<KIND>() > 0) {
+      const int n = w.n0 + part * (BN / 16 / NP) * 16;
+      if (lane == 0 && tma_live(w, row0, n)) {
+        const uint32_t b = cnt & 1;
+        bulk_wait_read<1>();  // the store that last read buffer b (two chunks ago) is done
+        mbar_expect_tx(&abar[b], tma_aux_bytes<KIND>());
+        tma_load_5d(stg + b * 2048, ma, n, row0, w.zh, w.zb, w.j, &abar[b]);
+      }
+    }
+  }
+
+  template <int KIND, int BN, int NP>
+  TLK_DEV void tile_tma(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg_p, uint64_t* abar,
+                        uint32_t& cnt, const CUtensorMap* mo, const CUtensorMap* mo2, const CUtensorMap* ma) const {
+    constexpr int NC = BN / 16;
+    constexpr uint32_t AUXB = tma_aux_bytes<KIND>();
+    constexpr bool BIAS = KIND == EPI_BF16 || KIND == EPI_BF16_GELU || KIND == EPI_RESADD;
+    constexpr bool CP = KIND == EPI_GELU_BWD || KIND == EPI_BF16;
+    const int cc0 = part * (NC / NP), cc1 = cc0 + NC / NP;
+    const float* bias = (BIAS && e.bias) ? e.bias + w.j * e.bias_ls : nullptr;
+    const uint32_t stg = smem_u32(stg_p);
+    // bias-gradient partials of this warp's 32-row block (per tile)
+    float* cpb = nullptr;
+    bool cp_full = true;
+    if constexpr (CP) {
+      if (e.colpart) {
+        const int64_t frow = int64_t(w.zb) * (e.bs / e.ld) + row0;  // row within the lane
+        const int pc = e.cp_cols ? e.cp_cols : e.cols;
+        cpb = e.colpart + w.j * e.cp_ls + (frow >> 5) * pc + e.cp_col0 + w.zh * e.hs;
+        cp_full = row0 + 32 <= e.rows;
+      }
+    }
+#pragma unroll 1
+    for (int cc = cc0; cc < cc1; ++cc) {
+      const int n = w.n0 + cc * 16;
+      if (!tma_live(w, row0, n)) break;  // warp-uniform: the rest of the row block is outside too
+      const uint32_t b = cnt & 1;
+      uint8_t* bp = stg_p + b * 2048;
+      f2 a[8];
+      {
+        float v[16];
+        tmem_ld16(tq + cc * 16, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = f2_make(v[2 * i], v[2 * i + 1]);
+      }
+      if (bias) {
+        const float4* b4 = reinterpret_cast<const float4*>(bias + n);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = b4[i];
+          a[2 * i] = f2_add(a[2 * i], f2_make(x.x, x.y));
+          a[2 * i + 1] = f2_add(a[2 * i + 1], f2_make(x.z, x.w));
+        }
+      }
+      if constexpr (AUXB > 0) mbar_wait(&abar[b], (cnt >> 1) & 1);
+      if constexpr (KIND == EPI_BF16) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          *reinterpret_cast<uint4*>(bp + sw_off<2>(lane, c)) =
+              make_uint4(bf2_from_f2(a[4 * c]), bf2_from_f2(a[4 * c + 1]), bf2_from_f2(a[4 * c + 2]),
+                         bf2_from_f2(a[4 * c + 3]));
+      } else if constexpr (KIND == EPI_BF16_GELU) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          *reinterpret_cast<uint4*>(bp + 1024 + sw_off<2>(lane, c)) =
+              make_uint4(bf2_from_f2(a[4 * c]), bf2_from_f2(a[4 * c + 1]), bf2_from_f2(a[4 * c + 2]),
+                         bf2_from_f2(a[4 * c + 3]));
+          *reinterpret_cast<uint4*>(bp + sw_off<2>(lane, c)) =
+              make_uint4(bf2_from_f2(gelu2(a[4 * c])), bf2_from_f2(gelu2(a[4 * c + 1])),
+                         bf2_from_f2(gelu2(a[4 * c + 2])), bf2_from_f2(gelu2(a[4 * c + 3])));
+        }
+      } else if constexpr (KIND == EPI_F32) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<ulonglong2*>(bp + sw_off<4>(lane, c)) = make_ulonglong2(a[2 * c], a[2 * c + 1]);
+      } else if constexpr (KIND == EPI_RESADD) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          ulonglong2* r = reinterpret_cast<ulonglong2*>(bp + sw_off<4>(lane, c));
+          const ulonglong2 r2 = *r;
+          *r = make_ulonglong2(f2_add(r2.x, a[2 * c]), f2_add(r2.y, a[2 * c + 1]));
+        }
+      } else if constexpr (KIND == EPI_GELU_BWD) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint4* z4 = reinterpret_cast<uint4*>(bp + sw_off<2>(lane, c));
+          const uint4 z = *z4;
+          *z4 = make_uint4(bf2_from_f2(gelu_bwd_mul2(a[4 * c], f2_from_bf2(z.x))),
+                           bf2_from_f2(gelu_bwd_mul2(a[4 * c + 1], f2_from_bf2(z.y))),
+                           bf2_from_f2(gelu_bwd_mul2(a[4 * c + 2], f2_from_bf2(z.z))),
+                           bf2_from_f2(gelu_bwd_mul2(a[4 * c + 3], f2_from_bf2(z.w))));
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if constexpr (CP) {
+        if (cpb) {
+          // lane = (row group g, column pair cp): rows 8g.. in a rotated order
+          // (the four groups hit four different 32 B bank segments)
+          const int cp = lane & 7, g = lane >> 3;
+          const uint8_t* col = bp + (cp & 3) * 4;
+          f2 sum = f2_make(0.f, 0.f);
+          if (cp_full) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 8 * g + ((i + g) & 7);
+              sum = f2_add(sum, f2_from_bf2(*reinterpret_cast<const uint32_t*>(col + sw_off<2>(r, cp >> 2))));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 8 * g + ((i + g) & 7);
+              const uint32_t u = *reinterpret_cast<const uint32_t*>(col + sw_off<2>(r, cp >> 2));
+              sum = f2_add(sum, f2_from_bf2(row0 + r < e.rows ? u : 0u));
+            }
+          }
+          float s0 = f2_lo(sum), s1 = f2_hi(sum);
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 8);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 8);
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          if (lane < 8) *reinterpret_cast<float2*>(cpb + n + 2 * cp) = make_float2(s0, s1);
+        }
+      }
+      if (lane == 0) {
+        tma_store_5d(mo, stg + b * 2048, n, row0, w.zh, w.zb, w.j);
+        if constexpr (KIND == EPI_BF16_GELU) tma_store_5d(mo2, stg + b * 2048 + 1024, n, row0, w.zh, w.zb, w.j);
+        bulk_commit();
+        bulk_wait_read<1>();  // buffer b ^ 1 (two chunks ago) is free again
+        if constexpr (AUXB > 0) {
+          if (cc + 1 < cc1 && tma_live(w, row0, n + 16)) {
+            mbar_expect_tx(&abar[b ^ 1], AUXB);
+            tma_load_5d(stg + (b ^ 1) * 2048, ma, n + 16, row0, w.zh, w.zb, w.j, &abar[b ^ 1]);
+          }
+        }
+      }
+      __syncwarp();
+      ++cnt;
+    }
+  }
+
+  template <int BN, int NP>
+  TLK_DEV void tma_pre_any(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar, uint32_t cnt,
+                           const CUtensorMap* ma) const {
+    if (e.kind == EPI_RESADD) tma_pre<EPI_RESADD, BN, NP>(w, row0, lane, part, stg, abar, cnt, ma);
+    else if (e.kind == EPI_GELU_BWD) tma_pre<EPI_GELU_BWD, BN, NP>(w, row0, lane, part, stg, abar, cnt, ma);
+  }
+  template <int BN, int NP>
+  TLK_DEV void tile_tma_any(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg_p,
+                            uint64_t* abar, uint32_t& cnt, const CUtensorMap* mo, const CUtensorMap* mo2,
+                            const CUtensorMap* ma) const {
+    switch (e.kind) {
+      case EPI_BF16: tile_tma<EPI_BF16, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_BF16_GELU:
+        tile_tma<EPI_BF16_GELU, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
+        break;
+      case EPI_F32: tile_tma<EPI_F32, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_RESADD: tile_tma<EPI_RESADD, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_GELU_BWD:
+        tile_tma<EPI_GELU_BWD, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
+        break;
+      default: break;
     }
   }
 

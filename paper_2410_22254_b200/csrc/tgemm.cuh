@@ -34,28 +34,31 @@ TLK_DEV void gemm_stage_mma(uint32_t d, uint32_t a_s, uint32_t b_s, bool acc) {
              (acc || kk > 0) ? 1u : 0u);
 }
 
-template <int BN_, bool AMN, bool BMN, bool ROW>
+template <int BN_, bool AMN, bool BMN, bool ROW, bool LIGHT = false>
 struct TGemm {
   static constexpr int BN = BN_;
-  // row-epilogue GEMMs (attention scores / dP, LM head) have K = head dim or
-  // d (1-6 k-blocks per tile): two stages suffice, and the freed smem is L1
-  // for the epilogue's global P loads
-#ifndef TLK_DENSE_STAGES_WIDE
-#define TLK_DENSE_STAGES_WIDE 3
-#endif
-  static constexpr int STAGES = ROW ? 2 : BN_ <= 64 ? 6 : BN_ <= 96 ? 5 : BN_ <= 128 ? 4 : TLK_DENSE_STAGES_WIDE;
   // epilogue warps: two groups (one per TMEM accumulator) of 4 lane-quarter
   // warps, x2 for 64-aligned tiles: two warps per lane quarter, each taking
   // half of the tile's columns (row epilogues exchange the row max / sum
   // through smem).  The epilogues (GELU / GELU', softmax, bf16 packing) are
-  // issue-bound: twice the warps hide the TMEM / SFU / store latency.
+  // issue-bound: twice the warps hide the TMEM / SFU / store latency.  Weight
+  // gradients (both operands MN-major, K = tokens) have a small fp32 output
+  // and a long DRAM-streaming mainloop, and LIGHT tiles (plain fp32 output:
+  // the dgrads, K = d or 4d) a cheap epilogue: one warp per lane quarter,
+  // and the freed staging smem becomes pipeline stages.
 #ifndef TLK_ROW_PARTS
 #define TLK_ROW_PARTS 2
 #endif
 #ifndef TLK_DENSE_PARTS
 #define TLK_DENSE_PARTS 2
 #endif
-  static constexpr int PARTS = BN_ % 64 != 0 ? 1 : ROW ? TLK_ROW_PARTS : TLK_DENSE_PARTS;
+#ifndef TLK_WGRAD_PARTS
+#define TLK_WGRAD_PARTS 1
+#endif
+  static constexpr int PARTS = BN_ % 64 != 0 ? 1
+                               : ROW         ? TLK_ROW_PARTS
+                               : (AMN && BMN) || LIGHT ? TLK_WGRAD_PARTS
+                                              : TLK_DENSE_PARTS;
   static constexpr int EW = 8 * PARTS;
   static constexpr int THREADS = (EW + 2) * 32;
   static constexpr bool A_MN = AMN, B_MN = BMN, ROW_EPI = ROW;
@@ -64,14 +67,27 @@ struct TGemm {
   static constexpr int B_BYTES = BN_ * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGING_BYTES = EW * 32 * 33 * 4;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 1024;
+  static constexpr int XCHG_BYTES = ROW ? 2 * 3 * 2 * 128 * 4 : 0;  // [group][max, sum, aux][part][row]
+  // row-epilogue GEMMs (attention scores / dP, LM head) have K = head dim or
+  // d (1-6 k-blocks per tile): two stages suffice, and the freed smem is L1
+  // for the epilogue's global P loads.  Dense tiles take as many stages as
+  // the 227 KB (less 1 KB of static barriers) hold, up to 8.
+  static constexpr int DYN_LIMIT = 232448 - 1024;
+  static constexpr int FIT = (DYN_LIMIT - STAGING_BYTES - XCHG_BYTES - 1024) / STAGE_BYTES;
+  static constexpr int STAGES = ROW ? 2 : (FIT < 8 ? FIT : 8);
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + XCHG_BYTES + 1024;
   static constexpr uint32_t TCOLS = BN_ <= 64 ? 128 : BN_ <= 128 ? 256 : 512;  // 2 accumulators
+  static_assert(STAGES >= 2, "at least two pipeline stages");
+  static_assert(ROW || STAGING_BYTES >= EW * 4096, "TMA epilogue staging: 4 KB per warp");
   static_assert(2 * BN_ <= 512, "two accumulators must fit TMEM");
   static_assert(!BMN || BN_ % 64 == 0, "MN-major B is loaded in 64-wide boxes");
 
   CUtensorMap ta, tb;
-  EpiOps g;  // epilogue state (g.e, g.lanes, z decomposition)
+  CUtensorMap to, to2, tx;  // TMA-staged dense epilogue: out, out2 (GELU z), aux
+  EpiOps g;                 // epilogue state (g.e, g.lanes, z decomposition)
   int mt, nt, ntiles;
+  int tma_epi;  // dense epilogue through EpiOps::tile_tma (host-checked layout)
+  static constexpr bool TMA_EPI = !ROW;
 
   TLK_DEV bool tile(int t, ZWork& w) const {
     const int n_t = t % nt;
@@ -110,6 +126,14 @@ struct TGemm {
     else
       g.template tile<BN_, PARTS>(w, tq, row0, buf, lane, false, part);
   }
+  TLK_DEV void epi_pre(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar,
+                       uint32_t cnt) const {
+    g.template tma_pre_any<BN_, PARTS>(w, row0, lane, part, stg, abar, cnt, &tx);
+  }
+  TLK_DEV void epi_tma(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg, uint64_t* abar,
+                       uint32_t& cnt) const {
+    g.template tile_tma_any<BN_, PARTS>(w, tq, row0, lane, part, stg, abar, cnt, &to, &to2, &tx);
+  }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
     if (!AMN) {
@@ -136,6 +160,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
   constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, P::A_MN, P::B_MN);
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t abar_s[P::TMA_EPI ? EW : 1][2];  // TMA epilogue aux loads, per warp
   __shared__ uint32_t tmem_base_s;
   // align by offsetting smem_raw (not via an integer cast) so that pointers
   // derived from it stay in the shared window (STS/LDS, not generic ST/LD)
@@ -153,6 +178,11 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EW / 2);
     }
+    if constexpr (P::TMA_EPI)
+      for (int w = 0; w < EW; ++w) {
+        mbar_init(&abar_s[w][0], 1);
+        mbar_init(&abar_s[w][1], 1);
+      }
     fence_mbar_init();
   }
   if (warp == EW) tmem_alloc<P::TCOLS>(&tmem_base_s);
@@ -204,7 +234,12 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
            // each, x PARTS column parts)
     const int q = warp & 3, group = (warp >> 2) & 1, part = warp >> 3;
     float* buf = staging + warp * (32 * 33);
-    __shared__ float xchg_s[2][3][2][128];  // [group][max, sum, aux][part][row] (row epilogues)
+    float* xchg = staging + EW * (32 * 33) + group * (3 * 2 * 128);  // row epilogues only
+    // TMA epilogue: 2 x 2 KB staging tiles per warp (1 KB aligned) in the same area
+    uint8_t* stg = reinterpret_cast<uint8_t*>(staging) + warp * 4096;
+    uint32_t ecnt = 0;
+    bool tma_epi = false;
+    if constexpr (P::TMA_EPI) tma_epi = p.tma_epi != 0;
     int lt = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       typename P::Work w;
@@ -214,15 +249,29 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
         ++lt;
         continue;
       }
-      mbar_wait(&tfull[b], (lt >> 1) & 1);
+      if constexpr (P::TMA_EPI)
+        if (tma_epi) p.epi_pre(w, w.m0 + q * 32, lane, part, smem_u32(stg), abar_s[warp], ecnt);
+      // one warp of the group polls the accumulator barrier; the others
+      // block on a named barrier (no issue slots spent spinning)
+      if (q == 0 && part == 0) mbar_wait(&tfull[b], (lt >> 1) & 1);
+      named_bar_sync(3 + group, EW * 16);
       tc_fence_after();
       const uint32_t tq = tmem + b * BN + (uint32_t(q * 32) << 16);
-      p.epilogue(w, tq, w.m0 + q * 32, buf, lane, part, &xchg_s[group][0][0][0], 1 + group);
+      if constexpr (P::TMA_EPI) {
+        if (tma_epi)
+          p.epi_tma(w, tq, w.m0 + q * 32, lane, part, stg, abar_s[warp], ecnt);
+        else
+          p.epilogue(w, tq, w.m0 + q * 32, buf, lane, part, xchg, 1 + group);
+      } else {
+        p.epilogue(w, tq, w.m0 + q * 32, buf, lane, part, xchg, 1 + group);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
       ++lt;
     }
+    if constexpr (P::TMA_EPI)
+      if (tma_epi && lane == 0) bulk_wait<0>();  // stores complete before the grid ends
   }
   tc_fence_before();
   __syncthreads();

@@ -64,6 +64,48 @@ TLK_DEV uint32_t pack_bf2(float lo, float hi) {
   return r;
 }
 
+// ---------------------------------------------------- packed fp32 (f32x2) --
+// sm_100 FFMA2 / FMUL2 / FADD2: two IEEE fp32 lanes per instruction (each
+// lane rounds exactly like the scalar op).  f2 = {lo, hi} in a 64-bit reg.
+using f2 = unsigned long long;
+TLK_DEV f2 f2_make(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+TLK_DEV float f2_lo(f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+TLK_DEV float f2_hi(f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+TLK_DEV f2 f2_fma(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+TLK_DEV f2 f2_mul(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+TLK_DEV f2 f2_add(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// bf16x2 word <-> f2 (lo = low half)
+TLK_DEV f2 f2_from_bf2(uint32_t u) { return f2_make(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u)); }
+TLK_DEV uint32_t bf2_from_f2(f2 v) {
+  uint32_t r;
+  asm("{\n\t.reg .f32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tcvt.rn.bf16x2.f32 %0, hi, lo;\n\t}" : "=r"(r) : "l"(v));
+  return r;
+}
+
 // ------------------------------------------------------------- smem addr --
 TLK_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,8 +124,24 @@ TLK_DEV void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 // Blocking wait for the phase with parity `parity` to complete.
+// The suspend-time hint lets a waiting warp sleep until the phase completes
+// instead of re-polling every few hundred cycles: idle epilogue / producer
+// warps otherwise spend issue slots (try_wait + branch + yield) that the
+// working warps on the same scheduler need.
+#ifndef TLK_MBAR_SUSPEND_NS
+#define TLK_MBAR_SUSPEND_NS 1000000
+#endif
 TLK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#if TLK_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity), "n"(TLK_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -91,6 +149,7 @@ TLK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // -------------------------------------------------------------- cp.async --

@@ -47,6 +47,11 @@ TLK_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int
       : "memory");
 }
 
+// Generic 5-D tensor map (dims[0] contiguous, byte strides of dims 1..4),
+// box {b0, b1, 1, 1, 1}, given element type and swizzle (epilogue tiles).
+int make_tmap_5d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, const uint64_t dims[5],
+                 const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw);
+
 // Generic 3-D tensor map (dims[0] contiguous), box {b0, b1, 1}, given element
 // type and swizzle; used for the fp32 optimizer-state tiles and the bf16
 // shadow tile of the CNN's fused fc1 wgrad + Adam kernel.

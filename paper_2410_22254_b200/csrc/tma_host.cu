@@ -63,6 +63,27 @@ int make_tmap_bf16_5d(CUtensorMap* out, const void* base, const uint64_t dims[5]
   return TLK_OK;
 }
 
+int make_tmap_5d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, const uint64_t dims[5],
+                 const uint64_t strides_bytes[4], uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  TLK_CHECK(fn, TLK_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t d[5], st[4];
+  for (int i = 0; i < 5; ++i) d[i] = dims[i] ? dims[i] : 1;
+  for (int i = 0; i < 4; ++i) {
+    st[i] = strides_bytes[i];
+    if (d[i + 1] == 1 || st[i] == 0) st[i] = 16;  // never stepped: any legal stride
+    TLK_CHECK(st[i] % 16 == 0 && st[i] < (uint64_t(1) << 40), TLK_EINVAL,
+              "tensor map stride %llu of dim %d not a multiple of 16 bytes", (unsigned long long)st[i], i + 1);
+  }
+  TLK_CHECK(reinterpret_cast<uintptr_t>(base) % 16 == 0, TLK_EINVAL, "tensor map base not 16-byte aligned");
+  const cuuint32_t box[5] = {b0, b1, 1, 1, 1};
+  const cuuint32_t estride[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(out, dt, 5, const_cast<void*>(base), d, st, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TLK_CHECK(r == CUDA_SUCCESS, TLK_ECUDA, "cuTensorMapEncodeTiled (5d, dt %d) failed (%d)", int(dt), int(r));
+  return TLK_OK;
+}
+
 int make_tmap_3d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
                  uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
                  CUtensorMapSwizzle sw) {
