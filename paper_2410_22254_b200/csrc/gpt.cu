@@ -506,13 +506,22 @@ Operand op(const uint16_t* base, int64_t ls, int64_t bs, int64_t hs, int64_t mn_
 // rows} boxes, SW32 for bf16 rows, SW64 for fp32 rows; dims {cols, rows, h,
 // b, lane} over the Epi strides).  `on` stays 0 (per-element tile4 path) for
 // layouts the TMA tiles cannot express or when TLK_TMA_EPI=0.
-int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, const Epi& e, int lanes, int nb,
-                 int nh) {
+bool tma_epi_usable(const Epi& e) {
   static const bool off = getenv("TLK_TMA_EPI") && getenv("TLK_TMA_EPI")[0] == '0';
-  on = 0;
   const bool dense = e.kind == EPI_BF16 || e.kind == EPI_BF16_GELU || e.kind == EPI_F32 || e.kind == EPI_RESADD ||
                      e.kind == EPI_GELU_BWD;
-  if (off || !dense || e.cols % 16 != 0) return TLK_OK;
+  const bool f32 = e.kind == EPI_F32 || e.kind == EPI_RESADD;
+  const int64_t eb = f32 ? 4 : 2;
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return !off && dense && e.cols % 16 == 0 && (e.ld * eb) % 16 == 0 && (e.hs * eb) % 16 == 0 &&
+         (e.bs * eb) % 16 == 0 && (e.ls * eb) % 16 == 0 && al(e.out) && (e.kind != EPI_BF16_GELU || al(e.out2)) &&
+         (!(e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD) || al(e.aux));
+}
+
+int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, const Epi& e, int lanes, int nb,
+                 int nh) {
+  on = 0;
+  if (!tma_epi_usable(e)) return TLK_OK;
   const bool f32 = e.kind == EPI_F32 || e.kind == EPI_RESADD;
   auto mk = [&](CUtensorMap& m, const void* base, bool is_f32) {
     const uint64_t eb = is_f32 ? 4 : 2;
@@ -529,10 +538,10 @@ int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, co
   return TLK_OK;
 }
 
-template <int BN, bool AMN, bool BMN, bool ROW, bool LIGHT = false>
+template <int BN, bool AMN, bool BMN, bool ROW, bool LIGHT = false, bool COMPACT = false>
 int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, const Epi& e, int M,
          int N, int K, int nb, int nh, const char* name) {
-  using G = TGemm<BN, AMN, BMN, ROW, LIGHT>;
+  using G = TGemm<BN, AMN, BMN, ROW, LIGHT, COMPACT>;
   G g{};
   g.g = EpiOps{p.lane_dev, e, nb, nh, (K + GEMM_BK - 1) / GEMM_BK};
   // vector-epilogue contract (sgemm.cuh): 4-element aligned rows and z strides
@@ -544,6 +553,7 @@ int gemm(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B, con
   if (!rc) rc = make_operand_map(&g.tb, B, BMN, BN, p.lanes, nb, nh);
   if (!rc && !ROW) rc = tma_epi_maps(g.to, g.to2, g.tx, g.tma_epi, e, p.lanes, nb, nh);
   if (rc) return rc;
+  TLK_CHECK(!COMPACT || g.tma_epi, TLK_EINVAL, "%s: compact epilogue tiles need the TMA epilogue", name);
   g.mt = (M + GEMM_BM - 1) / GEMM_BM;
   g.nt = (N + BN - 1) / BN;
   g.ntiles = g.mt * g.nt * p.lanes * nb * nh;
@@ -561,6 +571,11 @@ int gemm_auto(const Pack& p, cudaStream_t st, const Operand& A, const Operand& B
               int nb, int nh, const char* name) {
   static const bool narrow = getenv("TLK_GEMM_BN128") && getenv("TLK_GEMM_BN128")[0] == '1';
   if constexpr (!(AMN && BMN)) {
+    // bf16-output epilogues on the TMA path: 1 KB staging tiles, one more stage
+    if ((e.kind == EPI_BF16 || e.kind == EPI_GELU_BWD) && !narrow && tma_epi_usable(e)) {
+      if (N % 256 == 0) return gemm<256, AMN, BMN, false, false, true>(p, st, A, B, e, M, N, K, nb, nh, name);
+      if (N % 192 == 0) return gemm<192, AMN, BMN, false, false, true>(p, st, A, B, e, M, N, K, nb, nh, name);
+    }
     // plain fp32 output (dgrads): one epilogue warp per lane quarter, deeper pipeline
     if (e.kind == EPI_F32 && !narrow) {
       if (N % 256 == 0) return gemm<256, AMN, BMN, false, true>(p, st, A, B, e, M, N, K, nb, nh, name);

@@ -263,7 +263,8 @@ struct EpiOps {
   // a per-warp 2 KB staging tile laid out in the TMA swizzle of a {16, 32}
   // box, which one lane stores with cp.async.bulk.tensor.  The aux operand
   // (GELU' input, residual) is TMA-loaded into the same tile one chunk ahead
-  // and overwritten in place.  Two tiles per warp (ping-pong on `cnt`);
+  // and overwritten in place, NB - 1 chunks ahead (NB tiles per warp, ring
+  // position `cnt`);
   // rows / columns past the tensor are clipped by TMA, so there are no
   // per-element bounds checks.  Bias-gradient column partials are summed
   // from the staged bf16 tile.
@@ -286,27 +287,34 @@ struct EpiOps {
   TLK_DEV bool tma_live(const ZWork& w, int row0, int n) const { return row0 < e.rows && n < e.cols; }
 
   // issue the aux load of the warp's first chunk of a tile (before its TMEM wait)
-  template <int KIND, int BN, int NP>
+  template <int KIND, int BN, int NP, int TB, int NB>
   TLK_DEV void tma_pre(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar, uint32_t cnt,
                        const CUtensorMap* ma) const {
     if constexpr (tma_aux_bytes<KIND>() > 0) {
-      const int n = w.n0 + part * (BN / 16 / NP) * 16;
-      if (lane == 0 && tma_live(w, row0, n)) {
-        const uint32_t b = cnt & 1;
-        bulk_wait_read<1>();  // the store that last read buffer b (two chunks ago) is done
-        mbar_expect_tx(&abar[b], tma_aux_bytes<KIND>());
-        tma_load_5d(stg + b * 2048, ma, n, row0, w.zh, w.zb, w.j, &abar[b]);
+      if (lane == 0) {
+        const int c0 = part * (BN / 16 / NP);
+        bulk_wait_read<1>();  // stores that last read these buffers are done
+#pragma unroll
+        for (int k = 0; k < NB - 1; ++k) {
+          const int n = w.n0 + (c0 + k) * 16;
+          if (k < BN / 16 / NP && tma_live(w, row0, n)) {
+            const uint32_t b = (cnt + k) % NB;
+            mbar_expect_tx(&abar[b], tma_aux_bytes<KIND>());
+            tma_load_5d(stg + b * TB, ma, n, row0, w.zh, w.zb, w.j, &abar[b]);
+          }
+        }
       }
     }
   }
 
-  template <int KIND, int BN, int NP>
+  template <int KIND, int BN, int NP, int TB, int NB>
   TLK_DEV void tile_tma(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg_p, uint64_t* abar,
                         uint32_t& cnt, const CUtensorMap* mo, const CUtensorMap* mo2, const CUtensorMap* ma) const {
     constexpr int NC = BN / 16;
     constexpr uint32_t AUXB = tma_aux_bytes<KIND>();
     constexpr bool BIAS = KIND == EPI_BF16 || KIND == EPI_BF16_GELU || KIND == EPI_RESADD;
     constexpr bool CP = KIND == EPI_GELU_BWD || KIND == EPI_BF16;
+    static_assert(TB >= (KIND == EPI_BF16_GELU || tma_ob<KIND>() == 4 ? 2048 : 1024), "staging tile too small");
     const int cc0 = part * (NC / NP), cc1 = cc0 + NC / NP;
     const float* bias = (BIAS && e.bias) ? e.bias + w.j * e.bias_ls : nullptr;
     const uint32_t stg = smem_u32(stg_p);
@@ -325,8 +333,8 @@ struct EpiOps {
     for (int cc = cc0; cc < cc1; ++cc) {
       const int n = w.n0 + cc * 16;
       if (!tma_live(w, row0, n)) break;  // warp-uniform: the rest of the row block is outside too
-      const uint32_t b = cnt & 1;
-      uint8_t* bp = stg_p + b * 2048;
+      const uint32_t b = cnt % NB;
+      uint8_t* bp = stg_p + b * TB;
       f2 a[8];
       {
         float v[16];
@@ -343,7 +351,7 @@ struct EpiOps {
           a[2 * i + 1] = f2_add(a[2 * i + 1], f2_make(x.z, x.w));
         }
       }
-      if constexpr (AUXB > 0) mbar_wait(&abar[b], (cnt >> 1) & 1);
+      if constexpr (AUXB > 0) mbar_wait(&abar[b], (cnt / NB) & 1);
       if constexpr (KIND == EPI_BF16) {
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -414,14 +422,16 @@ struct EpiOps {
         }
       }
       if (lane == 0) {
-        tma_store_5d(mo, stg + b * 2048, n, row0, w.zh, w.zb, w.j);
-        if constexpr (KIND == EPI_BF16_GELU) tma_store_5d(mo2, stg + b * 2048 + 1024, n, row0, w.zh, w.zb, w.j);
+        tma_store_5d(mo, stg + b * TB, n, row0, w.zh, w.zb, w.j);
+        if constexpr (KIND == EPI_BF16_GELU) tma_store_5d(mo2, stg + b * TB + 1024, n, row0, w.zh, w.zb, w.j);
         bulk_commit();
-        bulk_wait_read<1>();  // buffer b ^ 1 (two chunks ago) is free again
-        if constexpr (AUXB > 0) {
-          if (cc + 1 < cc1 && tma_live(w, row0, n + 16)) {
-            mbar_expect_tx(&abar[b ^ 1], AUXB);
-            tma_load_5d(stg + (b ^ 1) * 2048, ma, n + 16, row0, w.zh, w.zb, w.j, &abar[b ^ 1]);
+        bulk_wait_read<1>();  // only this chunk's store may still read its buffer
+        if constexpr (AUXB > 0) {  // aux of chunk cc + NB - 1 into the buffer chunk cc - 1 used
+          const int nn = n + (NB - 1) * 16;
+          if (cc + NB - 1 < cc1 && tma_live(w, row0, nn)) {
+            const uint32_t bn = (cnt + NB - 1) % NB;
+            mbar_expect_tx(&abar[bn], AUXB);
+            tma_load_5d(stg + bn * TB, ma, nn, row0, w.zh, w.zb, w.j, &abar[bn]);
           }
         }
       }
@@ -430,25 +440,28 @@ struct EpiOps {
     }
   }
 
-  template <int BN, int NP>
+  template <int BN, int NP, int TB, int NB>
   TLK_DEV void tma_pre_any(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar, uint32_t cnt,
                            const CUtensorMap* ma) const {
-    if (e.kind == EPI_RESADD) tma_pre<EPI_RESADD, BN, NP>(w, row0, lane, part, stg, abar, cnt, ma);
-    else if (e.kind == EPI_GELU_BWD) tma_pre<EPI_GELU_BWD, BN, NP>(w, row0, lane, part, stg, abar, cnt, ma);
+    if (e.kind == EPI_GELU_BWD) {
+      tma_pre<EPI_GELU_BWD, BN, NP, TB, NB>(w, row0, lane, part, stg, abar, cnt, ma);
+    } else if (e.kind == EPI_RESADD) {
+      if constexpr (TB >= 2048) tma_pre<EPI_RESADD, BN, NP, TB, NB>(w, row0, lane, part, stg, abar, cnt, ma);
+    }
   }
-  template <int BN, int NP>
+  template <int BN, int NP, int TB, int NB>
   TLK_DEV void tile_tma_any(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg_p,
                             uint64_t* abar, uint32_t& cnt, const CUtensorMap* mo, const CUtensorMap* mo2,
                             const CUtensorMap* ma) const {
     switch (e.kind) {
-      case EPI_BF16: tile_tma<EPI_BF16, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_BF16: tile_tma<EPI_BF16, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
       case EPI_BF16_GELU:
-        tile_tma<EPI_BF16_GELU, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
+        if constexpr (TB >= 2048) tile_tma<EPI_BF16_GELU, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); else __trap();
         break;
-      case EPI_F32: tile_tma<EPI_F32, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
-      case EPI_RESADD: tile_tma<EPI_RESADD, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_F32: if constexpr (TB >= 2048) tile_tma<EPI_F32, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); else __trap(); break;
+      case EPI_RESADD: if constexpr (TB >= 2048) tile_tma<EPI_RESADD, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); else __trap(); break;
       case EPI_GELU_BWD:
-        tile_tma<EPI_GELU_BWD, BN, NP>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
+        tile_tma<EPI_GELU_BWD, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
         break;
       default: break;
     }

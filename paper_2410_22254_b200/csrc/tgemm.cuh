@@ -34,7 +34,7 @@ TLK_DEV void gemm_stage_mma(uint32_t d, uint32_t a_s, uint32_t b_s, bool acc) {
              (acc || kk > 0) ? 1u : 0u);
 }
 
-template <int BN_, bool AMN, bool BMN, bool ROW, bool LIGHT = false>
+template <int BN_, bool AMN, bool BMN, bool ROW, bool LIGHT = false, bool COMPACT = false>
 struct TGemm {
   static constexpr int BN = BN_;
   // epilogue warps: two groups (one per TMEM accumulator) of 4 lane-quarter
@@ -66,7 +66,17 @@ struct TGemm {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr int B_BYTES = BN_ * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGING_BYTES = EW * 32 * 33 * 4;
+  // COMPACT (bf16-output kinds on the TMA epilogue only): 2 x 1 KB staging
+  // tiles per warp instead of the 32 x 33 fp32 transpose buffer -> one more
+  // pipeline stage for the wide tiles
+  // TMA_NB tiles per warp: the aux operand is prefetched TMA_NB - 1 chunks
+  // ahead (two chunks hide the load latency behind the chunk math)
+  static constexpr int TMA_TB = COMPACT ? 1024 : 2048;
+  static constexpr int TMA_NB = COMPACT || BN_ <= 192 ? 3 : 2;
+  static constexpr int TILE4_BYTES = EW * 32 * 33 * 4;
+  static constexpr int STAGING_BYTES = COMPACT                                ? EW * TMA_NB * TMA_TB
+                                       : TILE4_BYTES > EW * TMA_NB * TMA_TB ? TILE4_BYTES
+                                                                            : EW * TMA_NB * TMA_TB;
   static constexpr int XCHG_BYTES = ROW ? 2 * 3 * 2 * 128 * 4 : 0;  // [group][max, sum, aux][part][row]
   // row-epilogue GEMMs (attention scores / dP, LM head) have K = head dim or
   // d (1-6 k-blocks per tile): two stages suffice, and the freed smem is L1
@@ -78,7 +88,8 @@ struct TGemm {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + XCHG_BYTES + 1024;
   static constexpr uint32_t TCOLS = BN_ <= 64 ? 128 : BN_ <= 128 ? 256 : 512;  // 2 accumulators
   static_assert(STAGES >= 2, "at least two pipeline stages");
-  static_assert(ROW || STAGING_BYTES >= EW * 4096, "TMA epilogue staging: 4 KB per warp");
+  static_assert(ROW || STAGING_BYTES >= EW * TMA_NB * TMA_TB, "TMA epilogue staging tiles");
+  static_assert(!COMPACT || !ROW, "compact staging is for dense epilogues");
   static_assert(2 * BN_ <= 512, "two accumulators must fit TMEM");
   static_assert(!BMN || BN_ % 64 == 0, "MN-major B is loaded in 64-wide boxes");
 
@@ -123,16 +134,18 @@ struct TGemm {
                         int bar) const {
     if constexpr (ROW)
       g.template row_tile<BN_, PARTS>(w, tq, row0, buf, lane, part, xchg, bar);
-    else
+    else if constexpr (!COMPACT)
       g.template tile<BN_, PARTS>(w, tq, row0, buf, lane, false, part);
+    else
+      __trap();  // compact tiles exist only on the TMA epilogue path (host-checked)
   }
   TLK_DEV void epi_pre(const ZWork& w, int row0, int lane, int part, uint32_t stg, uint64_t* abar,
                        uint32_t cnt) const {
-    g.template tma_pre_any<BN_, PARTS>(w, row0, lane, part, stg, abar, cnt, &tx);
+    g.template tma_pre_any<BN_, PARTS, TMA_TB, TMA_NB>(w, row0, lane, part, stg, abar, cnt, &tx);
   }
   TLK_DEV void epi_tma(const ZWork& w, uint32_t tq, int row0, int lane, int part, uint8_t* stg, uint64_t* abar,
                        uint32_t& cnt) const {
-    g.template tile_tma_any<BN_, PARTS>(w, tq, row0, lane, part, stg, abar, cnt, &to, &to2, &tx);
+    g.template tile_tma_any<BN_, PARTS, TMA_TB, TMA_NB>(w, tq, row0, lane, part, stg, abar, cnt, &to, &to2, &tx);
   }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
@@ -160,7 +173,7 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
   constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN, P::A_MN, P::B_MN);
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull[2], tempty[2];
-  __shared__ __align__(8) uint64_t abar_s[P::TMA_EPI ? EW : 1][2];  // TMA epilogue aux loads, per warp
+  __shared__ __align__(8) uint64_t abar_s[P::TMA_EPI ? EW : 1][3];  // TMA epilogue aux loads, per warp
   __shared__ uint32_t tmem_base_s;
   // align by offsetting smem_raw (not via an integer cast) so that pointers
   // derived from it stay in the shared window (STS/LDS, not generic ST/LD)
@@ -179,10 +192,8 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       mbar_init(&tempty[b], EW / 2);
     }
     if constexpr (P::TMA_EPI)
-      for (int w = 0; w < EW; ++w) {
-        mbar_init(&abar_s[w][0], 1);
-        mbar_init(&abar_s[w][1], 1);
-      }
+      for (int w = 0; w < EW; ++w)
+        for (int k = 0; k < 3; ++k) mbar_init(&abar_s[w][k], 1);
     fence_mbar_init();
   }
   if (warp == EW) tmem_alloc<P::TCOLS>(&tmem_base_s);
@@ -236,7 +247,8 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
     float* buf = staging + warp * (32 * 33);
     float* xchg = staging + EW * (32 * 33) + group * (3 * 2 * 128);  // row epilogues only
     // TMA epilogue: 2 x 2 KB staging tiles per warp (1 KB aligned) in the same area
-    uint8_t* stg = reinterpret_cast<uint8_t*>(staging) + warp * 4096;
+    uint8_t* stg = nullptr;
+    if constexpr (P::TMA_EPI) stg = reinterpret_cast<uint8_t*>(staging) + warp * (P::TMA_NB * P::TMA_TB);
     uint32_t ecnt = 0;
     bool tma_epi = false;
     if constexpr (P::TMA_EPI) tma_epi = p.tma_epi != 0;
