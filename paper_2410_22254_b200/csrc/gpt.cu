@@ -509,13 +509,13 @@ Operand op(const uint16_t* base, int64_t ls, int64_t bs, int64_t hs, int64_t mn_
 bool tma_epi_usable(const Epi& e) {
   static const bool off = getenv("TLK_TMA_EPI") && getenv("TLK_TMA_EPI")[0] == '0';
   const bool dense = e.kind == EPI_BF16 || e.kind == EPI_BF16_GELU || e.kind == EPI_F32 || e.kind == EPI_RESADD ||
-                     e.kind == EPI_GELU_BWD;
+                     e.kind == EPI_GELU_BWD || e.kind == EPI_BF16_ROWDOT;
   const bool f32 = e.kind == EPI_F32 || e.kind == EPI_RESADD;
   const int64_t eb = f32 ? 4 : 2;
   auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   return !off && dense && e.cols % 16 == 0 && (e.ld * eb) % 16 == 0 && (e.hs * eb) % 16 == 0 &&
          (e.bs * eb) % 16 == 0 && (e.ls * eb) % 16 == 0 && al(e.out) && (e.kind != EPI_BF16_GELU || al(e.out2)) &&
-         (!(e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD) || al(e.aux));
+         (!(e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD || e.kind == EPI_BF16_ROWDOT) || al(e.aux));
 }
 
 int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, const Epi& e, int lanes, int nb,
@@ -532,7 +532,8 @@ int tma_epi_maps(CUtensorMap& mo, CUtensorMap& mo2, CUtensorMap& ma, int& on, co
   };
   int rc = mk(mo, e.out, f32);
   if (!rc && e.kind == EPI_BF16_GELU) rc = mk(mo2, e.out2, false);
-  if (!rc && (e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD)) rc = mk(ma, e.aux, e.kind == EPI_RESADD);
+  if (!rc && (e.kind == EPI_GELU_BWD || e.kind == EPI_RESADD || e.kind == EPI_BF16_ROWDOT))
+    rc = mk(ma, e.aux, e.kind == EPI_RESADD);
   if (rc) return rc;
   on = 1;
   return TLK_OK;
@@ -967,6 +968,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
 
   for (int l = c.layers - 1; l >= 0; --l) {
     LayerBufs& lb = b.L[l];
+    bool rowdot_fused = false;
     {  // fc2: dW2 = dxb^T f ; db2 ; dz = (dxb W2) * gelu'(z)
       Epi g = epi(EPI_F32, d, 4 * d, G + O(T_LAYER(l, K_F2W)), PS, 0, 0, 4 * d);
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
@@ -1001,15 +1003,33 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
       TLK_TRY((gemm_auto<true, true>(p, st, op(b.dxb, nd, 0, 0, 1, d, d, N),
                                             op(lb.y, nd, 0, 0, 1, d, d, N), g, d, d, N, 1, 1, "proj_wgrad")));
       Epi e = epi(EPI_BF16, N, d, b.dy, nd, 0, 0, d);
-      TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
-                                             op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d), e, N, d, d,
-                                             1, 1, "proj_dgrad")));
+      // fused attention: the softmax-backward row term D = rowsum(dY o Y)
+      // comes out of this GEMM's epilogue (one 64-column head per epilogue
+      // warp, BN = 128); otherwise attn_rowdot_kernel computes it
+      Epi er = e;
+      er.kind = EPI_BF16_ROWDOT;
+      er.aux = lb.y;
+      er.rowout = b.D;
+      er.rv_T = T;
+      er.rv_H = H;
+      rowdot_fused = b.fused_attn && tma_epi_usable(er) && d % 128 == 0 && d == 64 * H;
+      if (rowdot_fused)
+        TLK_TRY((gemm<128, false, true, false, false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+                                                            op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d),
+                                                            er, N, d, d, 1, 1, "proj_dgrad")));
+      else
+        TLK_TRY((gemm_auto<false, true>(p, st, op(b.dxb, nd, 0, 0, d, 1, N, d),
+                                               op(WB + O(T_LAYER(l, K_PW)), PS, 0, 0, 1, d, d, d), e, N, d, d,
+                                               1, 1, "proj_dgrad")));
       count += 2;
     }
     {  // attention backward per (sequence, head)
-      TLK_CUDA(launch(attn_rowdot_kernel, dim3((N * H + 255) / 256, Lc), 256, 0, st, LS, N, T, H, b.dy, lb.y, b.D));
-      TLK_CUDA(cudaGetLastError());
-      marked("attn_rowdot");
+      if (!rowdot_fused) {
+        TLK_CUDA(launch(attn_rowdot_kernel, dim3((N * H + 255) / 256, Lc), 256, 0, st, LS, N, T, H, b.dy, lb.y,
+                        b.D));
+        TLK_CUDA(cudaGetLastError());
+        marked("attn_rowdot");
+      }
       if (b.fused_attn) {  // dS on chip; dQ / dK / dV + qkv.b partials (attn.cuh)
         TLK_TRY(attn_bwd(p, b, lb, st));
         ++count;

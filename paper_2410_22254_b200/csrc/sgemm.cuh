@@ -26,6 +26,7 @@ enum EpiKind : int {
   EPI_SOFTMAX,       // row: out16 = bf16(softmax(acc * scale, causal))
   EPI_SOFTMAX_BWD,   // row: out16 = bf16(P (acc - D) * scale), P = aux16, D = rowvec
   EPI_CE,            // row: cross entropy vs targets -> lossrow, out16 = bf16(dlogits)
+  EPI_BF16_ROWDOT,   // out16 = bf16(acc); rowout[row, head] = sum_c out16 * aux16 (TMA path, 64-col parts)
 };
 
 struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
@@ -46,6 +47,8 @@ struct Epi {  // out[row][col] = base + lane*ls + zb*bs + zh*hs + row*ld + col
   float* lossrow;          // EPI_CE: [lane][rows]
   float tokens;            // EPI_CE: dlogits are divided by the token count
   const float* rowvec;     // EPI_SOFTMAX_BWD: D[row] at lane*rv_ls + zb*rv_bs + zh*rv_hs + row
+  float* rowout;           // EPI_BF16_ROWDOT: [lane][row / rv_T][head][row % rv_T], head = column / 64
+  int rv_T, rv_H;
   int64_t rv_ls, rv_bs, rv_hs;
   float* colpart;          // EPI_GELU_BWD / EPI_BF16 (optional): column sums of the stored bf16
   int64_t cp_ls;           //   output per 32-row block (bias-gradient partials):
@@ -274,7 +277,7 @@ struct EpiOps {
   }
   template <int KIND>
   static constexpr uint32_t tma_aux_bytes() {
-    return KIND == EPI_GELU_BWD ? 32 * 16 * 2 : KIND == EPI_RESADD ? 32 * 16 * 4 : 0;
+    return (KIND == EPI_GELU_BWD || KIND == EPI_BF16_ROWDOT) ? 32 * 16 * 2 : KIND == EPI_RESADD ? 32 * 16 * 4 : 0;
   }
   // byte offset of 16 B vector c of row r in a swizzled {16, 32} box tile
   template <int OB>
@@ -318,6 +321,7 @@ struct EpiOps {
     const int cc0 = part * (NC / NP), cc1 = cc0 + NC / NP;
     const float* bias = (BIAS && e.bias) ? e.bias + w.j * e.bias_ls : nullptr;
     const uint32_t stg = smem_u32(stg_p);
+    f2 dot = f2_make(0.f, 0.f);  // EPI_BF16_ROWDOT: this part's head (even, odd columns)
     // bias-gradient partials of this warp's 32-row block (per tile)
     float* cpb = nullptr;
     bool cp_full = true;
@@ -358,6 +362,19 @@ struct EpiOps {
           *reinterpret_cast<uint4*>(bp + sw_off<2>(lane, c)) =
               make_uint4(bf2_from_f2(a[4 * c]), bf2_from_f2(a[4 * c + 1]), bf2_from_f2(a[4 * c + 2]),
                          bf2_from_f2(a[4 * c + 3]));
+      } else if constexpr (KIND == EPI_BF16_ROWDOT) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint4* y4 = reinterpret_cast<uint4*>(bp + sw_off<2>(lane, c));
+          const uint4 y = *y4;
+          const uint4 o = make_uint4(bf2_from_f2(a[4 * c]), bf2_from_f2(a[4 * c + 1]), bf2_from_f2(a[4 * c + 2]),
+                                     bf2_from_f2(a[4 * c + 3]));
+          *y4 = o;
+          dot = f2_fma(f2_from_bf2(o.x), f2_from_bf2(y.x), dot);
+          dot = f2_fma(f2_from_bf2(o.y), f2_from_bf2(y.y), dot);
+          dot = f2_fma(f2_from_bf2(o.z), f2_from_bf2(y.z), dot);
+          dot = f2_fma(f2_from_bf2(o.w), f2_from_bf2(y.w), dot);
+        }
       } else if constexpr (KIND == EPI_BF16_GELU) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -438,6 +455,14 @@ struct EpiOps {
       __syncwarp();
       ++cnt;
     }
+    if constexpr (KIND == EPI_BF16_ROWDOT) {
+      const int m = row0 + lane;
+      if (m < e.rows && tma_live(w, row0, w.n0 + cc0 * 16)) {
+        const int h = (w.n0 + cc0 * 16) >> 6;
+        e.rowout[((int64_t(w.j) * (e.rows / e.rv_T) + m / e.rv_T) * e.rv_H + h) * e.rv_T + m % e.rv_T] =
+            f2_lo(dot) + f2_hi(dot);
+      }
+    }
   }
 
   template <int BN, int NP, int TB, int NB>
@@ -445,6 +470,8 @@ struct EpiOps {
                            const CUtensorMap* ma) const {
     if (e.kind == EPI_GELU_BWD) {
       tma_pre<EPI_GELU_BWD, BN, NP, TB, NB>(w, row0, lane, part, stg, abar, cnt, ma);
+    } else if (e.kind == EPI_BF16_ROWDOT) {
+      if constexpr (BN / NP == 64) tma_pre<EPI_BF16_ROWDOT, BN, NP, TB, NB>(w, row0, lane, part, stg, abar, cnt, ma);
     } else if (e.kind == EPI_RESADD) {
       if constexpr (TB >= 2048) tma_pre<EPI_RESADD, BN, NP, TB, NB>(w, row0, lane, part, stg, abar, cnt, ma);
     }
@@ -455,6 +482,12 @@ struct EpiOps {
                             const CUtensorMap* ma) const {
     switch (e.kind) {
       case EPI_BF16: tile_tma<EPI_BF16, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); break;
+      case EPI_BF16_ROWDOT:  // one 64-column head per part warp (host-checked)
+        if constexpr (BN / NP == 64)
+          tile_tma<EPI_BF16_ROWDOT, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma);
+        else
+          __trap();
+        break;
       case EPI_BF16_GELU:
         if constexpr (TB >= 2048) tile_tma<EPI_BF16_GELU, BN, NP, TB, NB>(w, tq, row0, lane, part, stg_p, abar, cnt, mo, mo2, ma); else __trap();
         break;
