@@ -145,6 +145,66 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LaneState* __restrict
   }
 }
 
+// Vector LayerNorm forward (d = 128 KV): lane l owns the float4 columns
+// 4 (l + 32 k); a warp normalises LNF_WROWS consecutive rows with the next
+// row's loads in flight, gain / bias held in registers, packed bf16 stores.
+constexpr int LNF_WROWS = 8;
+template <int KV>
+__global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const LaneState* __restrict__ lanes, int N,
+                                                         const float* __restrict__ x,
+                                                         const float* __restrict__ params, int64_t pstride,
+                                                         int64_t og, int64_t ob, uint16_t* __restrict__ y,
+                                                         float* __restrict__ stats) {
+  pdl_begin();
+  constexpr int d = 128 * KV;
+  const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!lanes[j].active) return;
+  const int row0 = (blockIdx.x * 8 + warp) * LNF_WROWS;
+  const int nrows = max(0, min(LNF_WROWS, N - row0));
+  if (nrows == 0) return;
+  float4 g[KV], bb[KV], cur[KV], nxt[KV];
+  const float* gp = params + j * pstride + og;
+  const float* bp = params + j * pstride + ob;
+  const float* xr = x + (int64_t(j) * N + row0) * d;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int i = 4 * (lane + 32 * k);
+    g[k] = *reinterpret_cast<const float4*>(gp + i);
+    bb[k] = *reinterpret_cast<const float4*>(bp + i);
+    cur[k] = *reinterpret_cast<const float4*>(xr + i);
+  }
+  for (int r = 0; r < nrows; ++r) {
+    if (r + 1 < nrows)
+#pragma unroll
+      for (int k = 0; k < KV; ++k) nxt[k] = *reinterpret_cast<const float4*>(xr + (r + 1) * d + 4 * (lane + 32 * k));
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) s += (cur[k].x + cur[k].y) + (cur[k].z + cur[k].w);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / float(d);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const float c0 = cur[k].x - mu, c1 = cur[k].y - mu, c2 = cur[k].z - mu, c3 = cur[k].w - mu;
+      q += (c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3);
+    }
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = 1.0f / sqrtf(q / float(d) + 1e-5f);
+    uint16_t* yr = y + (int64_t(j) * N + row0 + r) * d;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const float4 v = cur[k];
+      *reinterpret_cast<uint2*>(yr + 4 * (lane + 32 * k)) =
+          make_uint2(pack_bf2((v.x - mu) * rstd * g[k].x + bb[k].x, (v.y - mu) * rstd * g[k].y + bb[k].y),
+                     pack_bf2((v.z - mu) * rstd * g[k].z + bb[k].z, (v.w - mu) * rstd * g[k].w + bb[k].w));
+    }
+    if (lane == 0)
+      *reinterpret_cast<float2*>(stats + (int64_t(j) * N + row0 + r) * 2) = make_float2(mu, rstd);
+#pragma unroll
+    for (int k = 0; k < KV; ++k) cur[k] = nxt[k];
+  }
+}
+
 // LayerNorm backward for 64 rows per CTA (8 warps x 8 rows):
 //   dxh = dy g; dx = (dxh - mean(dxh) - xh mean(dxh xh)) rstd
 //   dxt (fp32 residual grad) = (accumulate ? dxt : 0) + dx; dxb = bf16(dxt)
@@ -815,11 +875,24 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   TLK_CUDA(cudaGetLastError());
   marked("embed");
 
+  auto ln_fwd = [&](const float* x, int64_t og, int64_t ob, uint16_t* y, float* stats) -> int {
+    const dim3 gv((N + 8 * LNF_WROWS - 1) / (8 * LNF_WROWS), Lc);
+    if (d == 128)
+      TLK_CUDA(launch(ln_fwd_vec_kernel<1>, gv, 256, 0, st, LS, N, x, PR, PS, og, ob, y, stats));
+    else if (d == 256)
+      TLK_CUDA(launch(ln_fwd_vec_kernel<2>, gv, 256, 0, st, LS, N, x, PR, PS, og, ob, y, stats));
+    else if (d == 384)
+      TLK_CUDA(launch(ln_fwd_vec_kernel<3>, gv, 256, 0, st, LS, N, x, PR, PS, og, ob, y, stats));
+    else if (d == 512)
+      TLK_CUDA(launch(ln_fwd_vec_kernel<4>, gv, 256, 0, st, LS, N, x, PR, PS, og, ob, y, stats));
+    else
+      TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, x, PR, PS, og, ob, y, stats));
+    return TLK_OK;
+  };
   for (int l = 0; l < c.layers; ++l) {
     LayerBufs& lb = b.L[l];
     float* xnext = (l + 1 < c.layers) ? b.L[l + 1].xin : b.xL;
-    TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, lb.xin, PR, PS, O(T_LAYER(l, K_LN1G)),
-                                                         O(T_LAYER(l, K_LN1B)), lb.a, lb.st1));
+    TLK_TRY(ln_fwd(lb.xin, O(T_LAYER(l, K_LN1G)), O(T_LAYER(l, K_LN1B)), lb.a, lb.st1));
     TLK_CUDA(cudaGetLastError());
     marked("ln1");
     {  // qkv = a Wqkv^T + b
@@ -868,8 +941,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                                               d, d, 1, 1, "proj")));
       ++count;
     }
-    TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, lb.xmid, PR, PS, O(T_LAYER(l, K_LN2G)),
-                                                         O(T_LAYER(l, K_LN2B)), lb.m, lb.st2));
+    TLK_TRY(ln_fwd(lb.xmid, O(T_LAYER(l, K_LN2G)), O(T_LAYER(l, K_LN2B)), lb.m, lb.st2));
     TLK_CUDA(cudaGetLastError());
     marked("ln2");
     {  // z = m W1^T + b1, f = gelu(z)
@@ -894,8 +966,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
     }
   }
   const int tf = T_LNFG(c);
-  TLK_CUDA(launch(ln_fwd_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, N, d, b.xL, PR, PS, O(tf), O(tf + 1), b.xf,
-                                                       b.stf));
+  TLK_TRY(ln_fwd(b.xL, O(tf), O(tf + 1), b.xf, b.stf));
   TLK_CUDA(cudaGetLastError());
   marked("lnf");
   {  // logits -> CE row epilogue: lossrow, dl = (softmax - onehot) / N
