@@ -212,7 +212,13 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const LaneState* __rest
 // Lane l of a warp owns the float4 columns 4*(l + 32k), k < KV (d = 128 KV);
 // the next row's x / dy / dxt are fetched before the current row is reduced,
 // so every warp keeps two rows of loads in flight.
-constexpr int LNB_ROWS = 64;
+// LNB_WARPS warps of LNB_WROWS rows per CTA.  KV = 3 needs ~150 registers
+// unconstrained (one CTA, 8 warps of loads per SM); capped at 128 (two CTAs
+// per SM, a few spilled values in L1) it runs 10% faster.
+#ifndef TLK_LNB_WARPS
+#define TLK_LNB_WARPS 8
+#endif
+constexpr int LNB_WARPS = TLK_LNB_WARPS, LNB_WROWS = 8, LNB_ROWS = LNB_WARPS * LNB_WROWS;
 template <int KV>
 struct LnRow {
   float4 x[KV], dy[KV], acc[KV];
@@ -232,7 +238,7 @@ TLK_DEV void ln_row_load(LnRow<KV>& r, const float* x, const float* dy, const fl
   r.rstd = stats[so + 1];
 }
 template <int KV>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
+__global__ void __launch_bounds__(LNB_WARPS * 32, KV <= 3 ? 2 : 1) ln_bwd_kernel(
     const LaneState* __restrict__ lanes, int N, const float* __restrict__ dy,
     const float* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ params,
     int64_t pstride, int64_t og, float* __restrict__ dxt, uint16_t* __restrict__ dxb, int accumulate,
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   constexpr int d = 128 * KV;
   const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
-  extern __shared__ float red[];  // [8][3][d]
+  extern __shared__ float red[];  // [LNB_WARPS][3][d]
   // ag / ab: dgamma / dbeta partials; ax: column sums of the stored bf16 dx
   // (the bias gradient of the GEMM that consumes dxb next)
   float4 g[KV], ag[KV], ab[KV], ax[KV];
@@ -252,8 +258,8 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     g[k] = make_float4(gp[i], gp[i + 1], gp[i + 2], gp[i + 3]);
     ag[k] = ab[k] = ax[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int row0 = blockIdx.x * LNB_ROWS + warp * (LNB_ROWS / 8);
-  const int nrows = max(0, min(LNB_ROWS / 8, N - row0));
+  const int row0 = blockIdx.x * LNB_ROWS + warp * LNB_WROWS;
+  const int nrows = max(0, min(LNB_WROWS, N - row0));
   LnRow<KV> cur, nxt;
   if (nrows > 0)
     ln_row_load(cur, x, dy, dxt, stats, (int64_t(j) * N + row0) * d, (int64_t(j) * N + row0) * 2, lane,
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   for (int i = threadIdx.x; i < 3 * d; i += blockDim.x) {
     const int f = i / d, c = i % d;
     float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += red[(w * 3 + f) * d + c];
+    for (int w = 0; w < LNB_WARPS; ++w) s += red[(w * 3 + f) * d + c];
     out[i] = s;
   }
 }
@@ -1008,22 +1014,22 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
                     const char* name, int bias_t) -> int {
     const int nblk = (N + LNB_ROWS - 1) / LNB_ROWS;
     const dim3 grid(nblk, Lc);
-    const size_t sm = 24 * size_t(d) * 4;
+    const size_t sm = LNB_WARPS * 3 * size_t(d) * 4;
     switch (d / 128) {
       case 1:
-        TLK_CUDA(launch(ln_bwd_kernel<1>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+        TLK_CUDA(launch(ln_bwd_kernel<1>, grid, LNB_WARPS * 32, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
                                                 b.part, b.part_st));
         break;
       case 2:
-        TLK_CUDA(launch(ln_bwd_kernel<2>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+        TLK_CUDA(launch(ln_bwd_kernel<2>, grid, LNB_WARPS * 32, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
                                                 b.part, b.part_st));
         break;
       case 3:
-        TLK_CUDA(launch(ln_bwd_kernel<3>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+        TLK_CUDA(launch(ln_bwd_kernel<3>, grid, LNB_WARPS * 32, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
                                                 b.part, b.part_st));
         break;
       default:
-        TLK_CUDA(launch(ln_bwd_kernel<4>, grid, 256, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
+        TLK_CUDA(launch(ln_bwd_kernel<4>, grid, LNB_WARPS * 32, sm, st, LS, N, dy, x, stats, PR, PS, O(og), b.dx, b.dxb, accumulate,
                                                 b.part, b.part_st));
         break;
     }

@@ -19,4 +19,12 @@ cap gpt_attn_fwd attn_fwd 1 python tools/pack_step.py gpt 16 64 1
 cap gpt_attn_bwd attn_bwd 1 python tools/pack_step.py gpt 16 64 1
 cap xf_attn_fwd attn_fwd 1 python tools/pack_step.py xformer 32 32 1
 cap xf_attn_bwd attn_bwd 1 python tools/pack_step.py xformer 32 32 1
+# tiny-GPT dense GEMMs (launch order of one step: qkv, proj, fc, fc2 per layer;
+# backward of the last layer after the 24 forward + 3 head GEMMs)
+cap gpt_gemm_qkv tgemm 0 python tools/pack_step.py gpt 16 64 1
+cap gpt_gemm_fc tgemm 2 python tools/pack_step.py gpt 16 64 1
+cap gpt_gemm_fc2 tgemm 3 python tools/pack_step.py gpt 16 64 1
+cap gpt_gemm_fc2_wgrad tgemm 27 python tools/pack_step.py gpt 16 64 1
+cap gpt_gemm_fc2_dgrad tgemm 28 python tools/pack_step.py gpt 16 64 1
+cap gpt_gemm_fc_dgrad tgemm 30 python tools/pack_step.py gpt 16 64 1
 ls gpurun_out/cap_*
