@@ -427,11 +427,12 @@ __global__ void __launch_bounds__(512) gpt_loss_kernel(LaneState* __restrict__ l
 // Token-embedding gradient for a small vocabulary (V x d fp32 fits shared
 // memory): CTA (row chunk, lane) streams its rows of dx once, thread c owns
 // float4 column c of every vocabulary row, acc[token][c] += dx[row][c] in row
-// order (EMT_U rows in flight per thread), and writes part[lane][chunk][v][c];
+// order (the next EMT_U rows in flight while a batch is added), and writes
+// part[lane][chunk][v][c] (one wave of CTAs: two per SM);
 // reduce_parts8 sums the chunks in fixed order.  Every dx row is read once at
 // full width (the vocabulary-block kernel below rescans the token list per
 // block and keeps only a few loads in flight).
-constexpr int EMT_U = 16;
+constexpr int EMT_U = 8;
 constexpr size_t EMT_SMEM_MAX = 112 * 1024;  // two CTAs per SM
 __global__ void __launch_bounds__(128) embed_bwd_tok_kernel(const LaneState* __restrict__ lanes, int N, int d, int V,
                                                             const int32_t* __restrict__ tokens, int T,
@@ -447,31 +448,34 @@ __global__ void __launch_bounds__(128) embed_bwd_tok_kernel(const LaneState* __r
   if (tid < d4) {
     const float4* g = reinterpret_cast<const float4*>(dx + int64_t(j) * N * d) + tid;
     const int32_t* tk = tokens + int64_t(j) * (N / T) * (T + 1);
-    int r = r0;
-    for (; r + EMT_U <= r1; r += EMT_U) {
-      float4 val[EMT_U];
-      int v[EMT_U];
-#pragma unroll
-      for (int u = 0; u < EMT_U; ++u) {
-        const int row = r + u;
-        v[u] = tk[(row / T) * (T + 1) + row % T];
-        val[u] = g[int64_t(row) * d4];
-      }
-#pragma unroll
-      for (int u = 0; u < EMT_U; ++u)
-        if (unsigned(v[u]) < unsigned(V)) {
-          float4& a = acc4[v[u] * d4 + tid];
-          a.x += val[u].x, a.y += val[u].y, a.z += val[u].z, a.w += val[u].w;
-        }
-    }
-    for (; r < r1; ++r) {
-      const int v = tk[(r / T) * (T + 1) + r % T];
-      const float4 x = g[int64_t(r) * d4];
+    auto tok = [&](int row) { return tk[(row / T) * (T + 1) + row % T]; };
+    auto add = [&](int v, const float4& x) {
       if (unsigned(v) < unsigned(V)) {
         float4& a = acc4[v * d4 + tid];
         a.x += x.x, a.y += x.y, a.z += x.z, a.w += x.w;
       }
+    };
+    // software pipeline: the next EMT_U rows are loaded while this batch is added
+    float4 val[EMT_U], nval[EMT_U];
+    int v[EMT_U], nv[EMT_U];
+    int r = r0;
+    const bool full0 = r + EMT_U <= r1;
+    if (full0)
+#pragma unroll
+      for (int u = 0; u < EMT_U; ++u) v[u] = tok(r + u), val[u] = g[int64_t(r + u) * d4];
+    while (full0 && r + EMT_U <= r1) {
+      const bool more = r + 2 * EMT_U <= r1;
+      if (more)
+#pragma unroll
+        for (int u = 0; u < EMT_U; ++u) nv[u] = tok(r + EMT_U + u), nval[u] = g[int64_t(r + EMT_U + u) * d4];
+#pragma unroll
+      for (int u = 0; u < EMT_U; ++u) add(v[u], val[u]);
+      r += EMT_U;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < EMT_U; ++u) v[u] = nv[u], val[u] = nval[u];
     }
+    for (; r < r1; ++r) add(tok(r), g[int64_t(r) * d4]);
     float4* out = reinterpret_cast<float4*>(part + j * part_st + int64_t(blockIdx.x) * V * d) + tid;
     for (int w = 0; w < V; ++w) out[int64_t(w) * d4] = acc4[w * d4 + tid];
   }
@@ -1179,7 +1183,7 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   {  // embeddings
     TLK_CHECK(int64_t(N) < (int64_t(1) << 27), TLK_EINVAL, "embedding gradient: %d tokens per lane", N);
     const size_t emt_smem = size_t(V) * d * 4;
-    const int emt_chunks = std::min<int64_t>({int64_t(N + 255) / 256, (2 * b.sms + Lc - 1) / Lc,
+    const int emt_chunks = std::min<int64_t>({int64_t(N + 255) / 256, std::max(1, 2 * b.sms / Lc),  // one wave
                                               b.part_st / (int64_t(V) * d)});
     if (d % 4 == 0 && d <= 512 && emt_smem <= EMT_SMEM_MAX && emt_chunks >= 1) {
       static bool emt_configured = false;
