@@ -95,19 +95,32 @@ __global__ void gpt_targets_kernel(const LaneState* __restrict__ lanes, int B, i
   for (int i = 0; i < T; ++i) tg[i] = tk[i + 1];
 }
 
-// x0[row][c] = wte[tok][c] + wpe[t][c]
-__global__ void gpt_embed_kernel(const LaneState* __restrict__ lanes, GptCfg c, int B,
-                                 const int32_t* __restrict__ tokens, const float* __restrict__ params,
-                                 int64_t pstride, int64_t o_wte, int64_t o_wpe, float* __restrict__ x) {
+// x0[row][c] = wte[tok][c] + wpe[t][c]: one warp per row, 8 rows per CTA,
+// float4 columns when the arena offsets allow it (`vec`)
+__global__ void __launch_bounds__(256) gpt_embed_kernel(const LaneState* __restrict__ lanes, GptCfg c, int B,
+                                                        const int32_t* __restrict__ tokens,
+                                                        const float* __restrict__ params, int64_t pstride,
+                                                        int64_t o_wte, int64_t o_wpe, float* __restrict__ x,
+                                                        int vec) {
   pdl_begin();
-  const int row = blockIdx.x, j = blockIdx.y;
+  const int j = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!lanes[j].active) return;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= B * c.T) return;
   const int b = row / c.T, t = row % c.T;
   const int tok = tokens[(int64_t(j) * B + b) * (c.T + 1) + t];
   const float* P = params + j * pstride;
+  const float* we = P + o_wte + int64_t(tok) * c.d;
+  const float* pe = P + o_wpe + int64_t(t) * c.d;
   float* xr = x + (int64_t(j) * B * c.T + row) * c.d;
-  for (int i = threadIdx.x; i < c.d; i += blockDim.x)
-    xr[i] = P[o_wte + int64_t(tok) * c.d + i] + P[o_wpe + int64_t(t) * c.d + i];
+  if (vec) {
+    for (int i = lane; i < c.d / 4; i += 32) {
+      const float4 u = reinterpret_cast<const float4*>(we)[i], v = reinterpret_cast<const float4*>(pe)[i];
+      reinterpret_cast<float4*>(xr)[i] = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+    }
+  } else {
+    for (int i = lane; i < c.d; i += 32) xr[i] = we[i] + pe[i];
+  }
 }
 
 // ------------------------------------------------------------- LayerNorm ----
@@ -881,7 +894,12 @@ int gpt_enqueue_step(Pack& p, cudaStream_t st) {
   TLK_CUDA(cudaGetLastError());
   marked("tokens");
   float* x0 = c.layers ? b.L[0].xin : b.xL;
-  TLK_CUDA(launch(gpt_embed_kernel, dim3(N, Lc), 128, 0, st, LS, c, B, b.tokens, PR, PS, O(T_WTE), O(T_WPE), x0));
+  {
+    const int vec = d % 4 == 0 && O(T_WTE) % 4 == 0 && O(T_WPE) % 4 == 0 && PS % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(PR) & 15) == 0 && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
+    TLK_CUDA(launch(gpt_embed_kernel, dim3((N + 7) / 8, Lc), 256, 0, st, LS, c, B, b.tokens, PR, PS, O(T_WTE),
+                    O(T_WPE), x0, vec));
+  }
   TLK_CUDA(cudaGetLastError());
   marked("embed");
 
