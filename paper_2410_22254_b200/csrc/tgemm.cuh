@@ -147,6 +147,19 @@ struct TGemm {
                        uint32_t& cnt) const {
     g.template tile_tma_any<BN_, PARTS, TMA_TB, TMA_NB>(w, tq, row0, lane, part, stg, abar, cnt, &to, &to2, &tx);
   }
+  // L2 prefetch of a tile's A boxes (the activation operand streams from
+  // DRAM; B, the weights, stays L2-resident)
+  TLK_DEV void prefetch_tile(const ZWork& w) const {
+    for (int kb = w.kb_begin; kb < w.kb_end; ++kb) {
+      const int k0 = kb * GEMM_BK;
+      if (!AMN) {
+        tma_prefetch_l2_5d(&ta, k0, w.m0, w.zh, w.zb, w.j);
+      } else {
+        tma_prefetch_l2_5d(&ta, w.m0, k0, w.zh, w.zb, w.j);
+        tma_prefetch_l2_5d(&ta, w.m0 + 64, k0, w.zh, w.zb, w.j);
+      }
+    }
+  }
   TLK_DEV void load(const ZWork& w, int kb, uint32_t a_s, uint64_t* bar) const {
     const int k0 = kb * GEMM_BK;
     if (!AMN) {
@@ -165,6 +178,9 @@ struct TGemm {
   }
 };
 
+#ifndef TLK_GEMM_L2PF
+#define TLK_GEMM_L2PF 0
+#endif
 // (18 warps: 5 on some SM sub-partitions, so at most 96 registers per thread)
 template <class P>
 __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_constant__ P p) {
@@ -209,6 +225,13 @@ __global__ void __launch_bounds__(P::THREADS, 1) tgemm_kernel(const __grid_const
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         typename P::Work w;
         if (!p.tile(t, w)) continue;
+#if TLK_GEMM_L2PF
+        if constexpr (P::TMA_EPI) {  // this CTA's tile after next: its A into L2 now
+          typename P::Work wn;
+          const int tn = t + TLK_GEMM_L2PF * gridDim.x;
+          if (tn < p.ntiles && p.tile(tn, wn) && wn.kb_end - wn.kb_begin <= 8) p.prefetch_tile(wn);
+        }
+#endif
         for (int kb = w.kb_begin; kb < w.kb_end; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) - 1) & 1);

@@ -47,6 +47,14 @@ TLK_DEV void tma_load_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int
       : "memory");
 }
 
+// L2 prefetch of the same box (no shared-memory destination, no completion)
+TLK_DEV void tma_prefetch_l2_5d(const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+
 // Generic 5-D tensor map (dims[0] contiguous, byte strides of dims 1..4),
 // box {b0, b1, 1, 1, 1}, given element type and swizzle (epilogue tiles).
 int make_tmap_5d(CUtensorMap* out, CUtensorMapDataType dt, const void* base, const uint64_t dims[5],
