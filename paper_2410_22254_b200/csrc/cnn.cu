@@ -33,11 +33,14 @@ namespace {
 
 
 // ------------------------------------------------------- inputs + conv1 -----
+#ifndef TLK_C1F_MINB
+#define TLK_C1F_MINB 1  // CTAs per SM the register budget must allow
+#endif
 // One CTA per (sample, lane): the sample's inputs (inputs.cuh: pixel codes,
 // bf16 x for conv1 wgrad, teacher label) straight into shared memory, then
 // conv1 in fp32 on the fp32 master weights, writing the 26x26 interior of
 // h1's P28 planes (16 B = 8 channels per store).
-__global__ void __launch_bounds__(256) conv1_fwd_kernel(const LaneState* __restrict__ lanes,
+__global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const LaneState* __restrict__ lanes,
                                                         const int8_t* __restrict__ teacher,
                                                         uint8_t* __restrict__ px, int32_t* __restrict__ labels,
                                                         uint16_t* __restrict__ x, int host_input,
@@ -121,12 +124,14 @@ struct Fc1Fwd {
   TLK_DEV void prefetch() const {
     tma_prefetch_desc(&buf.w1_k);
     tma_prefetch_desc(&buf.p2m);
+    tma_prefetch_desc(&buf.p2m_alt);
   }
   TLK_DEV void load_a(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
     tma_load_3d(dst, &buf.w1_k, kb * GEMM_BK, 0, w.j, bar);
   }
   TLK_DEV void load_b(const Work& w, int kb, uint32_t dst, uint64_t* bar) const {
-    tma_load_3d(dst, &buf.p2m, kb * GEMM_BK, 0, w.j, bar);
+    // this step's p2 buffer (conv2_tc_kernel<true>: odd steps -> p2_alt)
+    tma_load_3d(dst, (lanes[w.j].steps_done & 1) ? &buf.p2m_alt : &buf.p2m, kb * GEMM_BK, 0, w.j, bar);
   }
   TLK_DEV void epilogue(const Work& w, int m, int n0, const float (&v)[32], Carry&) const {
     float* o = buf.part_fc1 + ((int64_t(w.j) * FC1_SPLITS + w.split) * 128 + m) * 64 + n0;
@@ -197,6 +202,9 @@ __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
   }
   cluster.sync();  // every CTA has read the partials before any may exit
   if (!active) return;
+  // this step's fc1.w update (fc1 wgrad + Adam, possibly after the lane's end
+  // of step) is due, reading p2 of this step's parity
+  if (r == 0 && tid == 0) lanes[j].fc1_due = 1 + (lanes[j].steps_done & 1);
   __syncthreads();
   if (tid < B) {
     const int y = labels[size_t(j) * B + tid];
@@ -403,18 +411,21 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
     if (lane == 0) {  // producer
       tma_prefetch_desc(&p.dz3m);
       tma_prefetch_desc(&p.p2m);
+      tma_prefetch_desc(&p.p2m_alt);
       tma_prefetch_desc(&p.tp);
       tma_prefetch_desc(&p.tm);
       tma_prefetch_desc(&p.tv);
       int it = 0, cs = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const int j = t / FWA_FT, f0 = (t % FWA_FT) * 128;
-        if (!p.lanes[j].active) continue;
+        const int due = p.lanes[j].fc1_due;
+        if (!due) continue;
+        const CUtensorMap* p2m = due == 2 ? &p.p2m_alt : &p.p2m;
         for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
           if (it >= 1) mbar_wait(&gempty, (it - 1) & 1);
           mbar_expect_tx(&gfull, FWA_STAGE_BYTES);
-          tma_load_3d(sbase, &p.p2m, f0, kb * GEMM_BK, j, &gfull);
-          tma_load_3d(sbase + 8192, &p.p2m, f0 + 64, kb * GEMM_BK, j, &gfull);
+          tma_load_3d(sbase, p2m, f0, kb * GEMM_BK, j, &gfull);
+          tma_load_3d(sbase + 8192, p2m, f0 + 64, kb * GEMM_BK, j, &gfull);
           tma_load_3d(sbase + 16384, &p.dz3m, 0, kb * GEMM_BK, j, &gfull);
           tma_load_3d(sbase + 24576, &p.dz3m, 64, kb * GEMM_BK, j, &gfull);
         }
@@ -433,7 +444,7 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
     if (lane == 0) {  // MMA issuer
       int it = 0, lt = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        if (!p.lanes[t / FWA_FT].active) continue;
+        if (!p.lanes[t / FWA_FT].fc1_due) continue;
         const int acc = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
         tc_fence_after();
@@ -456,8 +467,8 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
     int lt = 0, cs = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       const int j = t / FWA_FT, f0 = (t % FWA_FT) * 128;
-      if (!p.lanes[j].active) continue;
-      const LaneState s = p.lanes[j];
+      if (!p.lanes[j].fc1_due) continue;
+      const LaneState s = p.lanes[j];  // step scalars of the due step (the head writes the next ones)
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -512,6 +523,14 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<256>(tmem);
+  if (tid == 0) {  // every CTA has read fc1_due: the last one clears it
+    __threadfence();
+    if (atomicAdd(p.cnt, 1u) == gridDim.x - 1) {
+      __threadfence();
+      for (int j = 0; j < p.ntiles / FWA_FT; ++j) p.lanes[j].fc1_due = 0;
+      *p.cnt = 0;
+    }
+  }
 }
 
 // ------------------------------------------------ conv1 wgrad (SIMT) --------
@@ -527,7 +546,10 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
   extern __shared__ __align__(16) uint16_t dzs_raw[];  // this image's dz1 planes (50 KB)
   uint16_t(*dzs)[P28_IMG * 8] = reinterpret_cast<uint16_t(*)[P28_IMG * 8]>(dzs_raw);
   __shared__ float xs[784];
-  __shared__ float red[C1W_THREADS / 32][4][80];
+  // the per-warp partials reuse the dz1 planes' space once every warp is done
+  // with them: 53 KB per CTA -> 4 CTAs per SM, all 512 CTAs of 8 lanes in one wave
+  static_assert(C1W_THREADS / 32 * 4 * 80 * 4 <= C1W_SMEM, "conv1 wgrad partials fit the dz1 space");
+  float(*red)[4][80] = reinterpret_cast<float(*)[4][80]>(dzs_raw);
   // one barrier for the four chunk planes: every warp holds all four chunks, so
   // a wait per plane would diverge the warp (and turn its shuffles collective)
   __shared__ __align__(8) uint64_t bar;
@@ -597,6 +619,7 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
       v += __shfl_xor_sync(0xffffffffu, v, 16);
       acc[e][t] = v;
     }
+  __syncthreads();  // every warp is done reading dzs (red aliases it)
   if (lane < 8) {
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -700,6 +723,41 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
   }
 }
 
+bool cnn_fork() {
+  static const bool fork = !(getenv("TLK_CNN_NOFORK") && getenv("TLK_CNN_NOFORK")[0] == '1');
+  return fork;
+}
+int cnn_fwa_side() {
+  static const int side = getenv("TLK_CNN_FWA_SIDE") ? atoi(getenv("TLK_CNN_FWA_SIDE")) : 3;
+  return side;
+}
+// CTAs of the fc1 wgrad + Adam stream for placement `mode` (TLK_CNN_FWA_SIDE
+// values): all SMs when it runs alone (0); next to other kernels a share of
+// them, so that the latency-bound chain keeps SMs of its own -- 96 of 148 on
+// the graph's side branch (1, 2), 72 of 148 deferred (3), measured best at
+// 8 lanes.  TLK_FWA_CTAS overrides.
+int fwa_ctas(const Pack& p, int mode) {
+  static const int env = getenv("TLK_FWA_CTAS") ? atoi(getenv("TLK_FWA_CTAS")) : 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = env > 0 ? std::min(env, sms) : mode == 3 ? sms * 72 / 148 : mode ? sms * 96 / 148 : sms;
+  return std::min(ctas, p.lanes * FWA_FT);
+}
+int enqueue_fwa(Pack& p, cudaStream_t s2, int ctas) {
+  const CnnBufs& b = *static_cast<CnnBufs*>(p.scratch);
+  const int64_t o_f1w = tensor_offset(*p.def, 4);
+  Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, b.p2m_alt, p.lane_dev, p.params, p.mom1, p.mom2,
+                 p.grads, p.wbf, p.stride, o_f1w, (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0,
+                 (p.batch + GEMM_BK - 1) / GEMM_BK, p.lanes * FWA_FT, b.fwa_cnt};
+  TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(ctas), FWA_THREADS, FWA_SMEM, s2, f));
+  p.mark(s2, "fc1_wgrad_adam");
+  return TLK_OK;
+}
+// the deferred fc1 wgrad + Adam of the step graph just launched (runtime.cu
+// launches it on p.defer_st after waiting for the graph's ev_defer_in)
+int cnn_defer_fwa(Pack& p, cudaStream_t st) { return enqueue_fwa(p, st, fwa_ctas(p, 3)); }
+
 }  // namespace
 
 int cnn_setup(Pack& p) {
@@ -714,9 +772,9 @@ int cnn_setup(Pack& p) {
   b->h3_st = B * 128;
   const size_t plane = size_t(b->npos) * 16;  // bytes per chunk plane
   const size_t acts = size_t(L) * (4 * plane + 2 * b->p2_st + b->p2_st + 2 * 2 * b->h3_st +
-                                   8 * plane + 4 * plane);
+                                   8 * plane + 4 * plane + 2 * b->p2_st) + 16 * 8;
   const size_t f32s = size_t(L) * (9216 + FC1_SPLITS * 128 * 64 + C2W_SPLITS * 9 * 64 * 32 +
-                                   B * 320 + HEAD_CL * 64 * CLASSES + 32) + 32;
+                                   B * 320 + HEAD_CL * 64 * CLASSES + 32) + 32 + 16;
   void* base = nullptr;
   int rc = pack_alloc(p, &base, acts + f32s * 4 + 256);
   if (rc) return rc;
@@ -734,6 +792,7 @@ int cnn_setup(Pack& p) {
   b->dz3 = reinterpret_cast<uint16_t*>(take(L * b->h3_st * 2));
   b->dz2 = reinterpret_cast<uint16_t*>(take(L * 8 * plane));
   b->dz1 = reinterpret_cast<uint16_t*>(take(L * 4 * plane));
+  b->p2_alt = reinterpret_cast<uint16_t*>(take(L * b->p2_st * 2));  // after the round-1 layout
   p.acts = base;
   p.acts_bytes = size_t(c - static_cast<char*>(base));
   b->colsum = reinterpret_cast<float*>(take(L * 9216 * 4));
@@ -742,6 +801,7 @@ int cnn_setup(Pack& p) {
   b->part1 = reinterpret_cast<float*>(take(L * B * 320 * 4));
   b->plog = reinterpret_cast<float*>(take(L * HEAD_CL * 64 * CLASSES * 4));
   b->sched = reinterpret_cast<uint32_t*>(take((L + 1) * 32 * 4));
+  b->fwa_cnt = reinterpret_cast<uint32_t*>(take(64));
   {  // TMA maps: lanes stacked as the outermost dimension
     const int64_t o_f1w = tensor_offset(*p.def, 4);
     const uint16_t* w1 = p.wbf + o_f1w;
@@ -749,7 +809,8 @@ int cnn_setup(Pack& p) {
       return rc;
     if ((rc = make_tmap_bf16_3d(&b->w1_mn, w1, 9216, 128, L, 9216 * 2, p.stride * 2, 64, 64)))
       return rc;
-    if ((rc = make_tmap_bf16_3d(&b->p2m, b->p2, 9216, B, L, 9216 * 2, b->p2_st * 2, 64, 64)))
+    if ((rc = make_tmap_bf16_3d(&b->p2m, b->p2, 9216, B, L, 9216 * 2, b->p2_st * 2, 64, 64)) ||
+        (rc = make_tmap_bf16_3d(&b->p2m_alt, b->p2_alt, 9216, B, L, 9216 * 2, b->p2_st * 2, 64, 64)))
       return rc;
     if ((rc = make_tmap_bf16_3d(&b->dz3m, b->dz3, 128, B, L, 128 * 2, b->h3_st * 2, 64, 64)))
       return rc;
@@ -784,6 +845,12 @@ int cnn_setup(Pack& p) {
   TLK_CUDA(cudaFuncSetAttribute(conv2_wgrad_tc_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, WG_SMEM));
   p.launches_per_step = cnn_persist_enabled(p) ? 1 : 10;
+  if (!cnn_persist_enabled(p) && cnn_fork() && cnn_fwa_side() == 3) {
+    p.defer = cnn_defer_fwa;
+    TLK_CUDA(cudaStreamCreateWithFlags(&p.defer_st, cudaStreamNonBlocking));
+    TLK_CUDA(cudaEventCreateWithFlags(&p.ev_defer_in, cudaEventDisableTiming));
+    TLK_CUDA(cudaEventCreateWithFlags(&p.ev_defer_out, cudaEventDisableTiming));
+  }
   p.fused_lo = tensor_offset(*p.def, 4);  // fc1.w: updated inside its wgrad epilogue
   p.fused_hi = p.fused_lo + p.def->t[4].count;
   return TLK_OK;
@@ -807,6 +874,9 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   TLK_CUDA(launch(conv2_tc_kernel<true>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<true>::SMEM, st, ca));
   p.mark(st, "conv2_fwd_pool");
   TLK_CUDA(cudaGetLastError());
+  // deferred mode: the previous step's fc1 wgrad + Adam (cnn_defer_fwa) has
+  // written the fc1 weights this forward reads
+  if (p.defer && !p.prof) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_defer_out, cudaEventWaitExternal));
   Fc1Fwd f1{b, p.lane_dev};
   TLK_CUDA(launch_gemm_tma(f1, dim3(1, 1, L * FC1_SPLITS), st));
   p.mark(st, "fc1_fwd_splitk");
@@ -819,41 +889,30 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   // conv2 wgrad (reads dz2, h1; writes its partials) is independent of the
   // conv2 dgrad -> conv1 wgrad chain: a forked graph branch lets the two
   // latency-bound kernels share the SMs (TLK_CNN_NOFORK=1: serial)
-  static const bool fork = !(getenv("TLK_CNN_NOFORK") && getenv("TLK_CNN_NOFORK")[0] == '1');
   cudaStream_t wst = st;
-  if (fork && !p.prof) {
+  if (cnn_fork() && !p.prof) {
     TLK_CUDA(cudaEventRecord(p.ev_fork, st));
     TLK_CUDA(cudaStreamWaitEvent(p.side, p.ev_fork, 0));
     wst = p.side;
   }
-  // fc1 wgrad + Adam (HBM-bound) needs only dz3 / p2 and must follow the fc1
-  // dgrad (which reads this step's fc1 weights).  It runs on the side branch
-  // after the conv2 wgrad, next to the latency-bound conv2 dgrad -> conv1
-  // wgrad chain, on 96 of the 148 SMs (TLK_FWA_CTAS) so that the chain keeps
-  // SMs of its own.  TLK_CNN_FWA_SIDE: 0 = main stream after the join (one
-  // CTA per SM), 1 = side branch after conv2 wgrad (default), 2 = before it.
-  static const int fwa_side = getenv("TLK_CNN_FWA_SIDE") ? atoi(getenv("TLK_CNN_FWA_SIDE")) : 1;
-  static const int fwa_ctas = getenv("TLK_FWA_CTAS") ? atoi(getenv("TLK_FWA_CTAS")) : 0;
-  auto enqueue_fwa = [&](cudaStream_t s2) -> int {
-    Fc1WgradAdam f{b.dz3m, b.p2m, b.fa_p, b.fa_m, b.fa_v, p.lane_dev, p.params, p.mom1, p.mom2, p.grads, p.wbf,
-                   p.stride, o_f1w,
-                   (p.flags & TLK_PACK_WRITE_ALL_GRADS) ? 1 : 0, (B + GEMM_BK - 1) / GEMM_BK, L * FWA_FT};
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // 96 of 148 SMs on the side branch (also when a profile step serialises
-    // the branches: the kernel is timed at its in-graph grid)
-    const bool side = fork && fwa_side != 0;
-    const int ctas = fwa_ctas > 0 ? std::min(fwa_ctas, sms) : side ? sms * 96 / 148 : sms;
-    TLK_CUDA(launch(fc1_wgrad_adam_kernel, dim3(std::min(ctas, L * FWA_FT)), FWA_THREADS, FWA_SMEM, s2, f));
-    p.mark(s2, "fc1_wgrad_adam");
-    return TLK_OK;
-  };
-  if (fwa_side == 2 && wst != st && (rc = enqueue_fwa(wst))) return rc;
+  // fc1 wgrad + Adam (HBM-bound) needs dz3 / p2 of this step and must follow
+  // the fc1 dgrad (which reads this step's fc1 weights).  TLK_CNN_FWA_SIDE:
+  //   3 (default) = deferred: launched by the runtime after the step graph on
+  //     a stream of its own (cnn_defer_fwa), after this graph's conv2 wgrad
+  //     (event recorded below), overlapping this step's conv2 dgrad -> conv1
+  //     wgrad -> optimizer tail and the next step's conv1 / conv2 forward; the
+  //     next step's fc1 forward waits for it (p2 is double-buffered by step
+  //     parity, so the next forward does not overwrite its input);
+  //   1 = side branch after conv2 wgrad, 2 = before it, 0 = main stream after
+  //     the join.  A profile step (p.prof) serialises every kernel: 0.
+  int side_mode = p.prof ? 0 : wst == st ? 0 : cnn_fwa_side();
+  if (side_mode == 3 && !p.defer) side_mode = 0;
+  if (side_mode == 2 && (rc = enqueue_fwa(p, wst, fwa_ctas(p, 2)))) return rc;
   TLK_CUDA(launch(conv2_wgrad_tc_kernel, dim3(C2W_SPLITS, L), CONV_THREADS, WG_SMEM, wst, ca));
   p.mark(wst, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
-  if (fwa_side == 1 && wst != st && (rc = enqueue_fwa(wst))) return rc;
+  if (side_mode == 1 && (rc = enqueue_fwa(p, wst, fwa_ctas(p, 1)))) return rc;
+  if (side_mode == 3 && p.defer) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, wst, cudaEventRecordExternal));
   if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
@@ -862,7 +921,9 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (wst != st) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
-  if (!(fwa_side && wst != st) && (rc = enqueue_fwa(st))) return rc;
+  // (a profile step times the kernel at the grid it has in the step)
+  if (side_mode == 0 && (rc = enqueue_fwa(p, st, fwa_ctas(p, p.prof && cnn_fork() ? cnn_fwa_side() : 0))))
+    return rc;
   {
     const CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
                    reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),

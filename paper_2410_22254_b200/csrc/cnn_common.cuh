@@ -33,12 +33,17 @@ struct CnnBufs {
   CUtensorMap w1_k;   // fc1.w bf16 [9216 in][128 out]: box 64 x 128 (K-major A)
   CUtensorMap w1_mn;  // fc1.w bf16: box 64 x 64 (MN-major A of dgrad)
   CUtensorMap p2m;    // p2 [9216][B]: box 64 x 64
+  CUtensorMap p2m_alt;  // the second p2 buffer (odd steps of a lane; graph path)
   CUtensorMap dz3m;   // dz3 [128][B]: box 64 x 64
   CUtensorMap fa_p, fa_m, fa_v;  // fc1.w optimizer state tiles (fc1 wgrad + Adam), box 128 f x 32 o
   CUtensorMap fh_p, fh_m, fh_v;  // the same, box 128 f x 16 o (persistent path)
   int B;
   int64_t npos;
   uint16_t *h1, *p2, *h3, *dz3, *dz2, *dz1;
+  // graph path: conv2 fwd of a lane's odd steps writes p2_alt, so the fc1
+  // wgrad + Adam of step k can still read p2(k) while step k+1's forward runs
+  uint16_t* p2_alt;
+  uint32_t* fwa_cnt;  // fc1 wgrad + Adam: finished CTAs (the last one clears fc1_due)
   uint8_t* idx;
   float *colsum, *part_fc1, *part2, *part1;
   float* plog;      // [L][HEAD_CL][64][10] partial logits of the 16-unit slices (persistent path)
@@ -62,11 +67,13 @@ constexpr int FWA_FT = 9216 / 128;  // f tiles per lane
 struct Fc1WgradAdam {
   CUtensorMap dz3m, p2m;      // operands (bf16, SWIZZLE_128B boxes 64 x 64)
   CUtensorMap tp, tm, tv;     // fc1.w params / m / v: fp32 [lane][128 o][9216 f], box 128 f x 32 o
-  const LaneState* lanes;
+  CUtensorMap p2m_alt;        // p2 of the lane's odd steps
+  LaneState* lanes;           // fc1_due selects the lanes (and their p2 buffer)
   float *params, *m1, *m2, *grads;
   uint16_t* wbf;
   int64_t pstride, w_off;
   int write_grads, kblocks, ntiles;
+  uint32_t* cnt;              // finished-CTA counter (last CTA clears fc1_due)
 };
 
 
@@ -118,6 +125,7 @@ inline ConvArgs conv_args(const Pack& p, const CnnBufs& b) {
   a.dz2 = b.dz2;
   a.dz1 = b.dz1;
   a.p2 = b.p2;
+  a.p2_alt = b.p2_alt;
   a.idx = b.idx;
   a.wt = p.wt;
   a.wt_stride = p.wt_stride;

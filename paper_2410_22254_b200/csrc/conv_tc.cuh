@@ -15,6 +15,7 @@ struct ConvArgs {
   uint16_t* dz2;         // [L][8][npos][8]
   uint16_t* dz1;         // [L][4][npos][8]
   uint16_t* p2;          // [L][B][144][64]
+  uint16_t* p2_alt;      // p2 of a lane's odd steps (graph path; null: one buffer)
   uint8_t* idx;          // [L][B][144][64]: argmax (bits 0-1) | live (bit 2)
   const uint16_t* wt;    // [L][wt_stride] (wf | wd)
   int64_t wt_stride;
@@ -191,6 +192,8 @@ __global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
     if constexpr (!FWD) h1_fetch(blockIdx.x, hnext);
     // fwd: a thread's pooled items all have channel chunk tid & 7 (stride 32 * EPW)
     float bb[8];
+    // p2 buffer of this step: a lane's odd steps write the second one (graph path)
+    uint16_t* const p2 = (a.p2_alt && (a.lanes[j].steps_done & 1)) ? a.p2_alt : a.p2;
     if constexpr (FWD) {
       const float* bias = a.params + j * a.pstride + a.b2_off + (tid & 7) * 8;
 #pragma unroll
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
             i0 |= uint32_t(arg[e] | (mx[e] > 0.0f ? 4 : 0)) << (8 * e);
             i1 |= uint32_t(arg[e + 4] | (mx[e + 4] > 0.0f ? 4 : 0)) << (8 * e);
           }
-          *reinterpret_cast<uint4*>(a.p2 + o) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          *reinterpret_cast<uint4*>(p2 + o) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
           *reinterpret_cast<uint2*>(a.idx + o) = make_uint2(i0, i1);
         }
         named_bar_sync(1, 32 * CONV_EPW);  // tile buffer free for the next tile

@@ -57,6 +57,15 @@ struct Pack {
   // parameter range (floats, within a lane) whose update is fused into its
   // wgrad epilogue (see cnn.cu); the end-of-step optimizer skips it
   int64_t fused_lo = 0, fused_hi = 0;
+  // work of a step that runs after its graph, on a stream of its own (CNN:
+  // fc1 wgrad + Adam, overlapping the next step's forward; cnn.cu): the
+  // runtime launches defer() after every step-graph launch, once the graph's
+  // ev_defer_in has fired, and records ev_defer_out after it; the next step
+  // graph waits for ev_defer_out where it needs the result, and every API call
+  // that exposes pack state first makes the pack stream wait for it (settle)
+  int (*defer)(Pack&, cudaStream_t) = nullptr;
+  cudaStream_t defer_st = nullptr;
+  cudaEvent_t ev_defer_in = nullptr, ev_defer_out = nullptr;
   // side stream + events for concurrent graph branches
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

@@ -82,6 +82,14 @@ void destroy_pack(Pack& p) {
     if (p.h2d_ev[k]) cudaEventDestroy(p.h2d_ev[k]);
     if (p.done_ev[k]) cudaEventDestroy(p.done_ev[k]);
   }
+  if (p.defer_st) {
+    cudaStreamSynchronize(p.defer_st);
+    cudaStreamDestroy(p.defer_st);
+    cudaEventDestroy(p.ev_defer_in);
+    cudaEventDestroy(p.ev_defer_out);
+    p.defer_st = nullptr;
+    p.defer = nullptr;
+  }
   if (p.hexec_alt) cudaGraphExecDestroy(p.hexec_alt);
   if (p.hgraph_alt) cudaGraphDestroy(p.hgraph_alt);
   if (p.hexec0) cudaGraphExecDestroy(p.hexec0);
@@ -174,6 +182,25 @@ int ensure_host_pipeline(Pack& p, cudaStream_t st) {
     TLK_CUDA(cudaEventCreateWithFlags(&p.h2d_ev[k], cudaEventDisableTiming));
     TLK_CUDA(cudaEventCreateWithFlags(&p.done_ev[k], cudaEventDisableTiming));
   }
+  return TLK_OK;
+}
+
+// Launch one step graph, then the step's deferred work (Pack::defer) on the
+// pack's defer stream once the graph's ev_defer_in has fired.
+int launch_step(Pack& p, cudaGraphExec_t g) {
+  TLK_CUDA(cudaGraphLaunch(g, p.stream));
+  if (!p.defer) return TLK_OK;
+  TLK_CUDA(cudaStreamWaitEvent(p.defer_st, p.ev_defer_in, 0));
+  int rc = p.defer(p, p.defer_st);
+  if (rc) return rc;
+  TLK_CUDA(cudaEventRecord(p.ev_defer_out, p.defer_st));
+  return TLK_OK;
+}
+
+// Make the pack stream wait for the last step's deferred work: from here on
+// the pack's parameters / optimizer state are those after every launched step.
+int settle(Pack& p) {
+  if (p.defer) TLK_CUDA(cudaStreamWaitEvent(p.stream, p.ev_defer_out, 0));
   return TLK_OK;
 }
 
@@ -277,6 +304,11 @@ int tlk_sync(tlk_ctx* ctx) {
   TLK_CHECK(ctx, TLK_EINVAL, "null context");
   TLK_CUDA(cudaSetDevice(ctx->device));
   TLK_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& p : ctx->packs)
+    if (p && p->defer) {
+      TLK_CUDA(cudaStreamSynchronize(p->defer_st));
+      if (int rc = settle(*p)) return rc;
+    }
   for (auto& p : ctx->packs)
     if (p && p->own_stream) TLK_CUDA(cudaStreamSynchronize(p->stream));
   return TLK_OK;
@@ -426,6 +458,7 @@ int tlk_lane_load(tlk_ctx* ctx, int32_t pack, int32_t lane, const tlk_job_desc* 
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(job && lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
   TLK_CHECK(job->steps >= 1 && job->steps <= p->max_steps, TLK_EINVAL,
             "steps %d outside 1..max_steps=%d", job->steps, p->max_steps);
@@ -458,6 +491,7 @@ int tlk_lane_release(tlk_ctx* ctx, int32_t pack, int32_t lane) {
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(lane >= 0 && lane < p->lanes, TLK_EINVAL, "bad lane %d", lane);
   TLK_CUDA(cudaMemcpyAsync(&p->lane_host[lane], p->lane_dev + lane, sizeof(LaneState),
                            cudaMemcpyDeviceToHost, p->stream));
@@ -481,8 +515,9 @@ int tlk_run(tlk_ctx* ctx, int32_t pack, int32_t steps) {
     return TLK_OK;
   }
   if ((rc = ensure_graph(*p, p->stream))) return rc;
-  for (int i = 0; i < steps; ++i) TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
-  return TLK_OK;
+  for (int i = 0; i < steps; ++i)
+    if ((rc = launch_step(*p, p->graph_exec))) return rc;
+  return settle(*p);  // a run ends with every step complete
 }
 
 int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32_t* labels,
@@ -496,7 +531,7 @@ int tlk_step_host(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const int32
   TLK_CUDA(cudaMemcpyAsync(p->pixels, pixels, L * B * 784, cudaMemcpyHostToDevice, p->stream));
   TLK_CUDA(cudaMemcpyAsync(p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->stream));
   if ((rc = ensure_graph(*p, p->stream))) return rc;
-  TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
+  if ((rc = launch_step(*p, p->graph_exec)) || (rc = settle(*p))) return rc;
   if (losses_out) {
     TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, L * 4, cudaMemcpyDeviceToHost,
                              p->stream));
@@ -531,7 +566,7 @@ int tlk_step_host_blob(tlk_ctx* ctx, int32_t pack, const void* blob, int64_t byt
     src += sg.bytes;
   }
   if ((rc = ensure_graph(*p, p->stream))) return rc;
-  TLK_CUDA(cudaGraphLaunch(p->graph_exec, p->stream));
+  if ((rc = launch_step(*p, p->graph_exec)) || (rc = settle(*p))) return rc;
   if (losses_out)
     TLK_CUDA(cudaMemcpyAsync(losses_out, p->last_loss, size_t(p->lanes) * 4, cudaMemcpyDeviceToHost, p->stream));
   TLK_CUDA(cudaStreamSynchronize(p->stream));
@@ -559,7 +594,9 @@ int tlk_step_host_async(tlk_ctx* ctx, int32_t pack, const uint8_t* pixels, const
   TLK_CUDA(cudaMemcpyAsync(s ? p->lb_alt : p->labels, labels, L * B * 4, cudaMemcpyHostToDevice, p->copy_st));
   TLK_CUDA(cudaEventRecord(p->h2d_ev[s], p->copy_st));
   TLK_CUDA(cudaStreamWaitEvent(p->stream, p->h2d_ev[s], 0));
-  TLK_CUDA(cudaGraphLaunch(s ? p->hexec_alt : p->hexec0, p->stream));
+  // (the deferred work of the step stays in flight: the next step's graph
+  // waits for it where it must, tlk_sync and the lane calls settle it)
+  if ((rc = launch_step(*p, s ? p->hexec_alt : p->hexec0))) return rc;
   TLK_CUDA(cudaEventRecord(p->done_ev[s], p->stream));
   p->hout[s] = losses_out;  // filled from the mapped slot by tlk_step_host_wait
   *ticket = p->host_steps++;
@@ -616,6 +653,7 @@ int tlk_lane_params(tlk_ctx* ctx, int32_t pack, int32_t lane, float* host, int64
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(host && lane >= 0 && lane < p->lanes && n >= 0 && n <= p->stride, TLK_EINVAL,
             "bad lane/n");
   TLK_CUDA(cudaMemcpyAsync(host, p->params + size_t(lane) * p->stride, size_t(n) * 4,
@@ -628,6 +666,7 @@ int tlk_pack_tensor(tlk_ctx* ctx, int32_t pack, int32_t which, void** dev_ptr, i
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(dev_ptr && bytes, TLK_EINVAL, "null argument");
   const int64_t L = p->lanes, S = p->stride, B = p->batch;
   switch (which) {
@@ -649,6 +688,7 @@ int tlk_pack_named(tlk_ctx* ctx, int32_t pack, const char* name, void** dev_ptr,
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(name && dev_ptr && bytes, TLK_EINVAL, "null argument");
   for (const auto& nb : p->named)
     if (nb.name == name) {
@@ -682,6 +722,7 @@ int tlk_profile_step(tlk_ctx* ctx, int32_t pack, int32_t iters, float* ms, char*
   Pack* p = nullptr;
   int rc = get_pack(ctx, pack, &p);
   if (rc) return rc;
+  if ((rc = settle(*p))) return rc;
   TLK_CHECK(iters >= 1 && ms && n_out && max_n > 0, TLK_EINVAL, "bad arguments");
   TLK_CHECK(!p->host_input, TLK_ESTATE, "profile needs a device-input pack");
   // One step captured with an event node after every kernel, replayed

@@ -222,18 +222,21 @@ def _p28_to_nhwc(planes, B, size, off):
     return np.ascontiguousarray(x.transpose(1, 2, 3, 0, 4).reshape(B, size, size, 8 * C))
 
 
-def _cnn_acts(pack, lane, B):
-    """Split TLK_BUF_ACTS (csrc/cnn.cu layout) into this lane's NHWC fp32 tensors."""
+def _cnn_acts(pack, lane, B, t=0):
+    """Split TLK_BUF_ACTS (csrc/cnn.cu layout) into this lane's NHWC fp32 tensors
+    of the lane's step t (p2 of odd steps is the second p2 buffer, after dz1)."""
     L = pack.lanes
     npos = 32 + B * 784 + 64
     raw = pack.tensor(rt.BUF_ACTS).cpu().numpy().view(np.uint8)
     sizes = [("h1", 4 * npos * 16), ("p2", B * 9216 * 2), ("idx", B * 9216), ("h3", B * 128 * 2),
-             ("dz3", B * 128 * 2), ("dz2", 8 * npos * 16), ("dz1", 4 * npos * 16)]
+             ("dz3", B * 128 * 2), ("dz2", 8 * npos * 16), ("dz1", 4 * npos * 16), ("p2_alt", B * 9216 * 2)]
     out, off = {}, 0
     for name, per in sizes:
         blob = raw[off + lane * per: off + (lane + 1) * per]
         out[name] = blob.copy() if name == "idx" else _bf(blob.view(np.uint16))
         off += (L * per + 15) // 16 * 16
+    if t & 1:
+        out["p2"] = out["p2_alt"]
     out["h1"] = _p28_to_nhwc(out["h1"].reshape(4, npos, 8), B, 26, 1)
     out["p2"] = out["p2"].reshape(B, 12, 12, 64)
     out["live"] = (out["idx"].reshape(B, 12, 12, 64) & 4) != 0
@@ -251,7 +254,7 @@ def _cnn_layerwise(pack, lane, seed, t, p0, g, batch):
     from oracle.bf16 import round_bf16 as r
 
     B = batch
-    a = _cnn_acts(pack, lane, B)
+    a = _cnn_acts(pack, lane, B, t)
     prm = omodels.unflatten(omodels.MODEL_CNN, p0)
     px, y = rng.batch(seed, t, B)
     x = (px.astype(np.float32) / np.float32(256)).reshape(B, 28, 28, 1)

@@ -2,8 +2,9 @@
 
 Each run is a fresh process (the switches are read once per process):
 programmatic dependent launch off, the serial CNN graph (no forked conv2 wgrad
-branch), fc1 wgrad+Adam on the main stream / before the conv2 wgrad on an odd
-CTA count -> bit-identical loss curves; the ResNet conv variants (no halo
+branch), fc1 wgrad+Adam on the main stream / on the graph's side branch / before
+the conv2 wgrad on an odd CTA count instead of deferred past the step graph
+(the default) -> bit-identical loss curves; the ResNet conv variants (no halo
 tiles, no three-tap wgrad, 128-wide N tiles) only reorder fp32 sums -> loss
 curves within the oracle's own bf16 spread of the default."""
 import json
@@ -41,7 +42,8 @@ def _curves(env, *args):
 
 
 @pytest.mark.parametrize("env", [{"TLK_PDL": "0"}, {"TLK_CNN_NOFORK": "1"}, {"TLK_CNN_FWA_SIDE": "0"},
-                                 {"TLK_CNN_FWA_SIDE": "2", "TLK_FWA_CTAS": "37"}])
+                                 {"TLK_CNN_FWA_SIDE": "1"}, {"TLK_CNN_FWA_SIDE": "2", "TLK_FWA_CTAS": "37"},
+                                 {"TLK_FWA_CTAS": "23"}])
 def test_launch_switches_are_bit_identical(env):
     base = _curves({}, "cnn", 3, 64, 6)
     assert np.array_equal(_curves(env, "cnn", 3, 64, 6), base)
