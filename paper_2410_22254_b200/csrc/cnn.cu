@@ -652,9 +652,9 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
   if (!a.lanes[j].active) return;
   const LaneState s = a.lanes[j];
   const CnnOffs& o = a.o;
-  if (blockIdx.x < CNN_OPT_HEAVY) {
+  if (int(blockIdx.x) < a.nheavy) {
     const int l = threadIdx.x & 31;
-    const int h = blockIdx.x * 8 + (threadIdx.x >> 5);  // 0..71 conv1.w, 72..79 conv1.b, 80..95 conv2.b
+    const int h = (a.hb0 + blockIdx.x) * 8 + (threadIdx.x >> 5);  // 0..71 conv1.w, 72..79 conv1.b, 80..95 conv2.b
     {
       float g[4] = {0.f, 0.f, 0.f, 0.f};
       int64_t e;
@@ -685,9 +685,9 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
     }
   } else {
     const int64_t s4 = a.stride / 4, work = a.a1 + (s4 - a.b0);
-    const int nl = gridDim.x - CNN_OPT_HEAVY;
+    const int nl = gridDim.x - a.nheavy;
     const int64_t per = (work + nl - 1) / nl;
-    const int64_t w0 = (blockIdx.x - CNN_OPT_HEAVY) * per, w1 = min(work, w0 + per);
+    const int64_t w0 = (blockIdx.x - a.nheavy) * per, w1 = min(work, w0 + per);
     for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
       const int64_t idx = w < a.a1 ? w : a.b0 + (w - a.a1);
       const int64_t e = idx * 4;
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&a.lanes[j].done_ctas, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == (a.total ? unsigned(a.total) : gridDim.x) - 1) {
       __threadfence();
       a.lanes[j].done_ctas = 0;
       lane_end_step(a.lanes[j]);
@@ -917,6 +917,28 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
+  // TLK_CNN_SPLIT_OPT=1: the optimizer of every parameter but conv1's runs
+  // on the side branch once the conv2 dgrad (which reads this step's conv2
+  // weights) is done, beside the conv1 wgrad; the chain then ends with the
+  // conv1 update alone (10 CTAs per lane).  The last of the 36 CTAs per lane
+  // over both launches ends the lane's step.  Bit-identical, but measured
+  // slower at 8 lanes (0.182 vs 0.176 ms/step), so off by default.
+  static const bool split_env = getenv("TLK_CNN_SPLIT_OPT") && getenv("TLK_CNN_SPLIT_OPT")[0] == '1';
+  const bool split_opt = split_env && wst != st;
+  if (split_opt) {
+    TLK_CUDA(cudaEventRecord(p.ev_fork, st));
+    TLK_CUDA(cudaStreamWaitEvent(wst, p.ev_fork, 0));
+    CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
+             reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),
+             reinterpret_cast<float4*>(p.mom1), reinterpret_cast<float4*>(p.mom2),
+             reinterpret_cast<uint2*>(p.wbf), WtHook{p.wt, p.wt_stride, o_c2w, CONV2_W}};
+    a.hb0 = 10;
+    a.nheavy = 2;
+    a.total = CNN_OPT_HEAVY + CNN_OPT_CTAS;
+    TLK_CUDA(launch(cnn_opt_kernel, dim3(2 + CNN_OPT_CTAS, L), 256, 0, wst, a, b));
+    p.mark(wst, "grad_finalize_opt");
+    TLK_CUDA(cudaEventRecord(p.ev_join, wst));
+  }
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
@@ -924,11 +946,17 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   // (a profile step times the kernel at the grid it has in the step)
   if (side_mode == 0 && (rc = enqueue_fwa(p, st, fwa_ctas(p, p.prof && cnn_fork() ? cnn_fwa_side() : 0))))
     return rc;
-  {
-    const CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
-                   reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),
-                   reinterpret_cast<float4*>(p.mom1), reinterpret_cast<float4*>(p.mom2),
-                   reinterpret_cast<uint2*>(p.wbf), WtHook{p.wt, p.wt_stride, o_c2w, CONV2_W}};
+  CnnOpt a{p.lane_dev, p.stride, p.fused_lo / 4, p.fused_hi / 4, CnnOffs{o_c1w, o_c1b, o_c2w, o_c2b},
+           reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),
+           reinterpret_cast<float4*>(p.mom1), reinterpret_cast<float4*>(p.mom2),
+           reinterpret_cast<uint2*>(p.wbf), WtHook{p.wt, p.wt_stride, o_c2w, CONV2_W}};
+  if (split_opt) {  // conv1 parameters only (their gradient is the chain's last one)
+    a.hb0 = 0;
+    a.nheavy = 10;
+    a.total = CNN_OPT_HEAVY + CNN_OPT_CTAS;
+    TLK_CUDA(launch(cnn_opt_kernel, dim3(10, L), 256, 0, st, a, b));
+    p.mark(st, "conv1_opt");
+  } else {
     TLK_CUDA(launch(cnn_opt_kernel, dim3(CNN_OPT_HEAVY + CNN_OPT_CTAS, L), 256, 0, st, a, b));
     p.mark(st, "grad_finalize_opt");
   }

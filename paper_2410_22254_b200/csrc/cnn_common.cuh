@@ -77,6 +77,7 @@ struct Fc1WgradAdam {
 };
 
 
+constexpr int CNN_OPT_HEAVY_N = 12;
 struct CnnOffs {
   int64_t c1w, c1b, c2w, c2b;
 };
@@ -87,6 +88,10 @@ struct CnnOpt {
   float4 *P, *Gr, *M, *V;
   uint2* Wb;
   WtHook hook;
+  // graph-path launch split (cnn.cu): heavy CTAs cover warps h = (hb0 + blockIdx.x) * 8 + w
+  // for blockIdx.x < nheavy (h < 80: conv1, 80..95: conv2.b), the rest are light
+  // CTAs; `total` CTAs per lane over every launch of the step end it (0: gridDim.x)
+  int hb0 = 0, nheavy = CNN_OPT_HEAVY_N, total = 0;
 };
 __device__ __forceinline__ void cnn_opt_apply(const CnnOpt& a, const LaneState& s, int j, int64_t idx,
                                               const float (&g)[4]) {
@@ -114,7 +119,7 @@ __device__ __forceinline__ void cnn_opt_apply(const CnnOpt& a, const LaneState& 
 // positions), one warp per float4: lane l sums terms l, l+32, ... in order,
 // then a fixed xor-shuffle tree.  CTAs 12..: everything else, one float4 per
 // thread.
-constexpr int CNN_OPT_HEAVY = 12;
+constexpr int CNN_OPT_HEAVY = CNN_OPT_HEAVY_N;
 
 inline ConvArgs conv_args(const Pack& p, const CnnBufs& b) {
   ConvArgs a{};
