@@ -204,6 +204,11 @@ int tlk_selftest_datagen(uint64_t seed, int32_t step, int32_t batch, uint8_t* pi
  * library-intrinsic formulation on n random states of the given TLK_OPT_*
  * kind; *mismatches = elements whose p, m or v differ in any bit. */
 int tlk_selftest_optimizer(int32_t kind, uint64_t seed, int64_t n, uint64_t* mismatches);
+/* In-graph timeline of the CNN step kernels (libtlk built with -DTLK_KTRACE;
+ * otherwise TLK_EINVAL).  reset != 0 clears it; else copies n >= 288 values:
+ * [step mod 8][kernel id 0..11][earliest CTA entry, earliest end of the PDL
+ * wait, latest warp exit], %globaltimer ns (tools/cnn_timeline.py). */
+int tlk_cnn_ktrace(int32_t reset, uint64_t* out, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -47,7 +47,9 @@ __global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const Lane
                                                         const float* __restrict__ params,
                                                         int64_t pstride, int64_t w_off,
                                                         int64_t b_off, CnnBufs buf) {
+  TLK_KT(0, lanes[0].steps_done);
   pdl_begin();
+  TLK_KT_WAITED();
   const int s = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
   if (!lanes[j].active) return;
   __shared__ __align__(16) uint8_t pix[PIXELS];
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const Lane
 // ------------------------------------------------------ fc1 fwd (TC) --------
 // Z^T[o, b] partial sums over a K-split: part[lane][split][o][b].
 struct Fc1Fwd {
+  static constexpr int KT_ID = 2;  // TLK_KTRACE kernel id
   static constexpr int BN = 64, STAGES = 4;
   static constexpr bool A_MN = false, B_MN = false;
   static constexpr bool TILE_EPILOGUE = false;
@@ -156,7 +159,9 @@ __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
                     float* __restrict__ grads, int64_t stride, int64_t b1_off, int64_t w_off, int64_t b_off,
                     const int32_t* __restrict__ labels, float* __restrict__ loss, int max_steps,
                     float* __restrict__ last_loss) {
+  TLK_KT(3, lanes[0].steps_done);
   pdl_begin();
+  TLK_KT_WAITED();
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   constexpr int C = CLASSES, H = 128, HS = HEAD_HS;
@@ -268,6 +273,7 @@ __global__ void __cluster_dims__(HEAD_CL, 1, 1) __launch_bounds__(256)
 // argmax (live bit = pooled value > 0) into the dz2 P28 planes and
 // accumulates the conv2 bias-gradient partial colsum[f] = sum_b dz2 value.
 struct Fc1Dgrad {
+  static constexpr int KT_ID = 4;  // TLK_KTRACE kernel id
   static constexpr int BN = 64, STAGES = 2, THREADS = 256;
   static constexpr bool A_MN = true, B_MN = false;
   static constexpr bool TILE_EPILOGUE = true;
@@ -386,6 +392,10 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
   const uint32_t slot_base = sbase + FWA_STAGE_BYTES;
   const uint8_t* slot_ptr = smem + FWA_STAGE_BYTES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef TLK_KTRACE  // the step being updated: lane 0's due parity vs its (possibly advanced) counter
+  const int kt_s = p.lanes[0].steps_done, kt_d = p.lanes[0].fc1_due;
+  TLK_KT(8, ((kt_s & 1) == ((kt_d - 1) & 1)) ? kt_s : kt_s - 1);
+#endif
   if (tid == 0) {
     mbar_init(&gfull, 1);
     mbar_init(&gempty, 1);
@@ -404,6 +414,7 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
   __syncthreads();
   tc_fence_after();
   pdl_begin();
+  TLK_KT_WAITED();
   const uint32_t tmem = tmem_base_s;
   constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, 128, true, true);
 
@@ -540,7 +551,9 @@ __global__ void __launch_bounds__(FWA_THREADS, 1) fc1_wgrad_adam_kernel(const __
 __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneState* __restrict__ lanes,
                                                           CnnBufs buf,
                                                           const uint16_t* __restrict__ x) {
+  TLK_KT(7, lanes[0].steps_done);
   pdl_begin();
+  TLK_KT_WAITED();
   const int b = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (!lanes[j].active) return;
   extern __shared__ __align__(16) uint16_t dzs_raw[];  // this image's dz1 planes (50 KB)
@@ -647,7 +660,9 @@ __global__ void __launch_bounds__(C1W_THREADS) conv1_wgrad_kernel(const LaneStat
 // lane ends the lane's step.  Replaces a finalize launch + the batched
 // optimizer launch.
 __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ CnnOpt a, CnnBufs buf) {
+  TLK_KT(a.nheavy == 10 ? 10 : 9, a.lanes[0].steps_done);
   pdl_begin();
+  TLK_KT_WAITED();
   const int j = blockIdx.y;
   if (!a.lanes[j].active) return;
   const LaneState s = a.lanes[j];
@@ -964,3 +979,24 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
 }
 
 }  // namespace tlk
+
+// In-graph kernel timeline (-DTLK_KTRACE builds; tools/cnn_timeline.py).
+extern "C" int tlk_cnn_ktrace(int32_t reset, uint64_t* out, int32_t n) {
+#ifdef TLK_KTRACE
+  constexpr int N = 8 * tlk::KT_KERNELS * 3;
+  if (reset) {
+    static uint64_t init[N];
+    for (int i = 0; i < N; ++i) init[i] = (i % 3 == 2) ? 0 : ~0ull;
+    TLK_CUDA(cudaMemcpyToSymbol(tlk::g_ktrace, init, sizeof(init)));
+    return TLK_OK;
+  }
+  TLK_CHECK(out && n >= N, TLK_EINVAL, "need %d slots", N);
+  TLK_CUDA(cudaMemcpyFromSymbol(out, tlk::g_ktrace, N * sizeof(uint64_t)));
+  return TLK_OK;
+#else
+  (void)reset;
+  (void)out;
+  (void)n;
+  return tlk::fail(TLK_EINVAL, "libtlk was built without TLK_KTRACE");
+#endif
+}

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
   using P = ConvPolicy<FWD>;
   const int j = blockIdx.y;
   if (!a.lanes[j].active) return;
+  TLK_KT(FWD ? 1 : 6, a.lanes[0].steps_done);
   const int ntiles = a.B * 6;
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t wfull, afull[P::AS], aempty[P::AS], tfull[P::TS], tempty[P::TS];
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(CONV_FD_THREADS) conv2_tc_kernel(ConvArgs a) {
   __syncthreads();
   tc_fence_after();
   pdl_begin();  // barrier init / TMEM allocation overlap the previous kernel's flush
+  TLK_KT_WAITED();
   const uint32_t tmem = tmem_s;
   const uint16_t* src = FWD ? a.h1 + int64_t(j) * 4 * a.npos * 8 : a.dz2 + int64_t(j) * 8 * a.npos * 8;
 
@@ -321,6 +323,7 @@ constexpr uint32_t WG_TX = 12 * WG_ACOPY + WG_B_BYTES;
 static __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(ConvArgs a) {
   const int split = blockIdx.x, j = blockIdx.y;
   if (!a.lanes[j].active) return;
+  TLK_KT(5, a.lanes[0].steps_done);
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ __align__(8) uint64_t full_bar[WG_STAGES], empty_bar[WG_STAGES], done_bar;
   __shared__ uint32_t tmem_s;
@@ -343,6 +346,7 @@ static __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(Con
   __syncthreads();
   tc_fence_after();
   pdl_begin();
+  TLK_KT_WAITED();
   const uint32_t tmem = tmem_s;
 
   if (warp == 4) {  // ---------------- TMA producer

@@ -216,6 +216,22 @@ TLK_DEV uint64_t stage_desc_tma(uint32_t base, int kk) {
   return umma_desc_sw128(base + kk * 2 * 1024, 8192, 1024);
 }
 
+#ifdef TLK_KTRACE
+template <class P, class = void>
+struct KtId {
+  static constexpr int value = -1;
+};
+template <class P>
+struct KtId<P, std::void_t<decltype(P::KT_ID)>> {
+  static constexpr int value = P::KT_ID;
+};
+template <class P>
+TLK_DEV int kt_step(const P& p) {
+  if constexpr (KtId<P>::value >= 0) return p.lanes[0].steps_done;
+  return 0;
+}
+#endif
+
 template <class P>
 __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
     tc_gemm_tma_kernel(const __grid_constant__ P p) {
@@ -234,6 +250,7 @@ __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   typename P::Work w;
   if (!p.work(w)) return;
+  TLK_KT(KtId<P>::value, kt_step(p));
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -247,6 +264,7 @@ __global__ void __launch_bounds__(GemmThreads<P>::value, 1)
   __syncthreads();
   tc_fence_after();
   pdl_begin();  // barrier init / TMEM allocation above touch no upstream data
+  TLK_KT_WAITED();
   const uint32_t tmem = tmem_base_s;
   const int nk = w.kb_end - w.kb_begin;
   if (warp == 0 && lane == 0) {  // producer

@@ -35,7 +35,7 @@ EXPORTS = (
     "tlk_pack_tensor", "tlk_pack_named", "tlk_pack_info", "tlk_pack_launches_per_step", "tlk_profile_step",
     "tlk_selftest_gemm",
     "tlk_selftest_datagen",
-    "tlk_selftest_optimizer",
+    "tlk_selftest_optimizer", "tlk_cnn_ktrace",
 )
 
 
