@@ -392,7 +392,7 @@ def packed_arm(a, world, rank, local):
 
     lanes = a.jobs
     ctx = rt.Context(local)
-    total_steps = a.warmup + a.steps + a.profile_iters + 2
+    total_steps = a.warmup + a.steps + 2 * a.profile_iters + 2  # (+ the CNN full-grid re-profile)
     # the workload as a parametric task list through the triples mapping:
     # triples [1, jobs*world, 1] on a world-GPU node; this rank trains the
     # slots pinned to GPU `rank` (task i -> slot i -> GPU i % world).
@@ -473,9 +473,26 @@ def packed_arm(a, world, rank, local):
                 "share_of_step": top_ms / step_ms, "peak_source": peak_kind}
     # the profile step serialises the kernels on one stream (no graph
     # branches); each kernel runs at its in-graph grid (CNN fc1 wgrad+Adam:
-    # the 96 CTAs it gets on the side branch next to the conv2 dgrad chain)
+    # the 72 of 148 CTAs it gets on the defer stream, beside the step's tail
+    # and the next step's forward)
     roof["timing"] = ("CUDA events around each kernel of a serial (unforked) profile step, "
                       "mean of %d; kernels at their in-graph grids" % a.profile_iters)
+    if MODEL == "cnn" and top_name == "fc1_wgrad_adam":
+        # the same kernel re-profiled on one CTA per SM (its grid when it runs alone)
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        old = os.environ.get("TLK_FWA_CTAS")
+        os.environ["TLK_FWA_CTAS"] = str(sms)
+        try:
+            full = dict(pack.profile_step(a.profile_iters)).get("fc1_wgrad_adam")
+        finally:
+            if old is None:
+                os.environ.pop("TLK_FWA_CTAS")
+            else:
+                os.environ["TLK_FWA_CTAS"] = old
+        if full:
+            ach = work / (full / 1e3) / 1e9
+            roof["full_grid"] = {"ctas": sms, "ms_per_launch": full, "achieved": ach, "frac": ach / hbm,
+                                 "in_graph_ctas": sms * 72 // 148}
     try:  # dram bytes of this kernel from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(MODEL, {}).get(top_name)
         if tr:
@@ -518,6 +535,7 @@ def packed_arm(a, world, rank, local):
             prev = t
         hpack.step_host_wait(prev)
         seen.append(float(lons[(n - 1) & 1][0]))
+        ctx.sync()  # the last step's deferred fc1 update (CNN) is inside the timed region
 
     run_host_steps(max(1, a.warmup))
     barrier(world)

@@ -752,11 +752,13 @@ int cnn_fwa_side() {
 // the graph's side branch (1, 2), 72 of 148 deferred (3), measured best at
 // 8 lanes.  TLK_FWA_CTAS overrides.
 int fwa_ctas(const Pack& p, int mode) {
-  static const int env = getenv("TLK_FWA_CTAS") ? atoi(getenv("TLK_FWA_CTAS")) : 0;
+  // read at every capture (bench.py re-profiles the kernel on the full grid)
+  const int env = getenv("TLK_FWA_CTAS") ? atoi(getenv("TLK_FWA_CTAS")) : 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ctas = env > 0 ? std::min(env, sms) : mode == 3 ? sms * 72 / 148 : mode ? sms * 96 / 148 : sms;
+  // (mode 4: the side branch until the end of the step, 96 of 148)
   return std::min(ctas, p.lanes * FWA_FT);
 }
 int enqueue_fwa(Pack& p, cudaStream_t s2, int ctas) {
@@ -929,6 +931,11 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   if (side_mode == 1 && (rc = enqueue_fwa(p, wst, fwa_ctas(p, 1)))) return rc;
   if (side_mode == 3 && p.defer) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, wst, cudaEventRecordExternal));
   if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
+  // 4 = on the side branch after conv2 wgrad, joined only at the end of the step
+  if (side_mode == 4) {
+    if ((rc = enqueue_fwa(p, wst, fwa_ctas(p, 4)))) return rc;
+    TLK_CUDA(cudaEventRecord(p.ev_tail, wst));
+  }
   TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
   p.mark(st, "conv2_dgrad");
   TLK_CUDA(cudaGetLastError());
@@ -954,10 +961,14 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     p.mark(wst, "grad_finalize_opt");
     TLK_CUDA(cudaEventRecord(p.ev_join, wst));
   }
+  // TLK_CNN_JOIN_EARLY=1: join the side branch before the conv1 wgrad (the
+  // conv1 wgrad -> optimizer edge stays a programmatic one) instead of after it
+  static const bool join_early = getenv("TLK_CNN_JOIN_EARLY") && getenv("TLK_CNN_JOIN_EARLY")[0] == '1';
+  if (wst != st && join_early) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
-  if (wst != st) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
+  if (wst != st && !join_early) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   // (a profile step times the kernel at the grid it has in the step)
   if (side_mode == 0 && (rc = enqueue_fwa(p, st, fwa_ctas(p, p.prof && cnn_fork() ? cnn_fwa_side() : 0))))
     return rc;
@@ -975,6 +986,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     TLK_CUDA(launch(cnn_opt_kernel, dim3(CNN_OPT_HEAVY + CNN_OPT_CTAS, L), 256, 0, st, a, b));
     p.mark(st, "grad_finalize_opt");
   }
+  if (side_mode == 4) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_tail, 0));
   return enqueue_end_step(p, st);
 }
 

@@ -68,7 +68,7 @@ struct Pack {
   cudaEvent_t ev_defer_in = nullptr, ev_defer_out = nullptr;
   // side stream + events for concurrent graph branches
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tail = nullptr;
   // pipelined host-input steps (tlk_step_host_async): a second input slot and
   // the step graph captured against it, a copy stream, per-slot events
   uint8_t* px_alt = nullptr;

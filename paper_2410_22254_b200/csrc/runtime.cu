@@ -98,6 +98,7 @@ void destroy_pack(Pack& p) {
   if (p.side) cudaStreamDestroy(p.side);
   if (p.ev_fork) cudaEventDestroy(p.ev_fork);
   if (p.ev_join) cudaEventDestroy(p.ev_join);
+  if (p.ev_tail) cudaEventDestroy(p.ev_tail);
   if (p.graph_exec) cudaGraphExecDestroy(p.graph_exec);
   if (p.graph) cudaGraphDestroy(p.graph);
   for (void* a : p.allocs) cudaFree(a);
@@ -443,6 +444,7 @@ int tlk_pack_create(tlk_ctx* ctx, const tlk_pack_desc* desc, int32_t* pack_id) {
   TLK_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   TLK_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  TLK_CUDA(cudaEventCreateWithFlags(&p->ev_tail, cudaEventDisableTiming));
   p->lane_host.assign(L, LaneState{});
   TLK_CUDA(cudaMemsetAsync(p->lane_dev, 0, L * sizeof(LaneState), p->stream));
   TLK_CUDA(cudaMemsetAsync(p->loss, 0, L * size_t(p->max_steps) * 4, p->stream));

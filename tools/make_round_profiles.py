@@ -21,14 +21,15 @@ PROF = os.path.join(ROOT, "profiles")
 CAPS = {"c_fc1_wgrad_adam": ("cnn", "fc1_wgrad_adam"), "c_conv2_fwd": ("cnn", "conv2_fwd_pool"),
         "c_conv2_dgrad": ("cnn", "conv2_dgrad"),
         "c_conv2_wgrad": ("cnn", "conv2_wgrad"), "c_fc1_dgrad": ("cnn", "fc1_dgrad_unpool"),
-        "c_cnn_opt": ("cnn", "grad_finalize_opt"), "c_cnn_head": ("cnn", "fc1_reduce_head"), "r_fwd_l1_halo": ("resnet18", "conv_fwd"),
+        "c_cnn_opt": ("cnn", "grad_finalize_opt"), "c_conv1_wgrad": ("cnn", "conv1_wgrad"),
+        "c_conv1_fwd": ("cnn", "inputs_conv1_fwd"), "c_cnn_head": ("cnn", "fc1_reduce_head"), "r_fwd_l1_halo": ("resnet18", "conv_fwd"),
         "r_dgrad_l1_halo": ("resnet18", "conv_dgrad"), "r_wgrad_l1_tg": ("resnet18", "conv_wgrad"),
         "r_dgrad_bn256": ("resnet18", "conv_dgrad_bn256"), "r_bn_bwd_apply": ("resnet18", "bn_bwd_apply"),
         "g_scores": ("gpt", "attn_scores"), "g_fc": ("gpt", "fc")}
 
 
 def main(tag):
-    for w in ("cnn", "mlp", "resnet18", "xformer", "gpt", "reference"):
+    for w in ("cnn", "mlp", "resnet18", "xformer", "gpt", "mix", "reference"):
         f = os.path.join(OUT, f"bench_{w}.json")
         if os.path.exists(f) and os.path.getsize(f):
             try:
@@ -37,7 +38,8 @@ def main(tag):
                 continue
             json.dump(d, open(os.path.join(PROF, f"{tag}_bench_{w}.json"), "w"), indent=1)
     for w, how in (("cnn", "bench.py --steps 3 --warmup 3 (10 kernels per step; lane_init_kernel is setup)"),
-                   ("resnet18", "tools/pack_step.py resnet18 8 128 1"), ("gpt", "tools/pack_step.py gpt 16 64 1")):
+                   ("resnet18", "tools/pack_step.py resnet18 8 128 1"), ("gpt", "tools/pack_step.py gpt 16 64 1"),
+                   ("mlp", "tools/pack_step.py mlp 4 64 1"), ("xformer", "tools/pack_step.py xformer 32 32 1")):
         f = os.path.join(OUT, f"launches_{w}.csv")
         if os.path.exists(f):
             hdr = (f"# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
