@@ -906,6 +906,12 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   // conv2 wgrad (reads dz2, h1; writes its partials) is independent of the
   // conv2 dgrad -> conv1 wgrad chain: a forked graph branch lets the two
   // latency-bound kernels share the SMs (TLK_CNN_NOFORK=1: serial)
+  // where the deferred fc1 wgrad + Adam may start (TLK_FWA_DEFER_AT): 0 right
+  // after the fc1 dgrad (beside the conv2 wgrad), 1 after the conv2 wgrad
+  // (default), 2 after the conv1 wgrad (beside the optimizer only)
+  static const int defer_at = getenv("TLK_FWA_DEFER_AT") ? atoi(getenv("TLK_FWA_DEFER_AT")) : 1;
+  const bool deferring = p.defer && !p.prof && cnn_fork() && cnn_fwa_side() == 3;
+  if (deferring && defer_at == 0) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, st, cudaEventRecordExternal));
   cudaStream_t wst = st;
   if (cnn_fork() && !p.prof) {
     TLK_CUDA(cudaEventRecord(p.ev_fork, st));
@@ -929,7 +935,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   p.mark(wst, "conv2_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (side_mode == 1 && (rc = enqueue_fwa(p, wst, fwa_ctas(p, 1)))) return rc;
-  if (side_mode == 3 && p.defer) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, wst, cudaEventRecordExternal));
+  if (deferring && defer_at == 1) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, wst, cudaEventRecordExternal));
   if (wst != st) TLK_CUDA(cudaEventRecord(p.ev_join, wst));
   // 4 = on the side branch after conv2 wgrad, joined only at the end of the step
   if (side_mode == 4) {
@@ -968,6 +974,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
+  if (deferring && defer_at == 2) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, st, cudaEventRecordExternal));
   if (wst != st && !join_early) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   // (a profile step times the kernel at the grid it has in the step)
   if (side_mode == 0 && (rc = enqueue_fwa(p, st, fwa_ctas(p, p.prof && cnn_fork() ? cnn_fwa_side() : 0))))
