@@ -33,6 +33,9 @@ namespace {
 
 
 // ------------------------------------------------------- inputs + conv1 -----
+#ifndef TLK_C1F_PAIR
+#define TLK_C1F_PAIR 1  // conv1 fwd: two positions per iteration
+#endif
 #ifndef TLK_C1F_MINB
 #define TLK_C1F_MINB 1  // CTAs per SM the register budget must allow
 #endif
@@ -54,7 +57,7 @@ __global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const Lane
   if (!lanes[j].active) return;
   __shared__ __align__(16) uint8_t pix[PIXELS];
   __shared__ int part[8][CLASSES];
-  __shared__ float xs[784];
+  __shared__ __align__(16) float xs[784];
   __shared__ float ws[32 * 9];
   __shared__ float bs[32];
   for (int i = tid; i < 288; i += 256) ws[i] = params[j * pstride + w_off + i];
@@ -78,6 +81,42 @@ __global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const Lane
   // positions pos = g, g + 32, ...: (oh, ow) and both addresses advance
   // incrementally (32 = 26 + 6: one row and six columns, plus a row on wrap)
   uint2* hout = reinterpret_cast<uint2*>(h1 + (c * buf.npos + p28_pos(s, 1, 1)) * 8 + h * 4);
+#if TLK_C1F_PAIR
+  // two horizontally adjacent positions per iteration (pairs q = g, g + 32,
+  // ... of the 13 x 26 pairs; 32 = 2 rows + 6 pairs): a 3 x 4 input window in
+  // six 8-byte loads serves both; every output keeps its tap-ordered FMA chain
+  int q = tid >> 3, oh = q / 13, pw = q % 13;
+  for (; q < 338; q += 32) {
+    const int ow = 2 * pw;
+    const float* xp = xs + oh * 28 + ow;
+    float xv[3][4];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const float2 a = *reinterpret_cast<const float2*>(xp + r * 28);
+      const float2 b = *reinterpret_cast<const float2*>(xp + r * 28 + 2);
+      xv[r][0] = a.x, xv[r][1] = a.y, xv[r][2] = b.x, xv[r][3] = b.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float acc[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[e] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[e] += xv[t / 3][t % 3 + u] * w[e][t];
+      }
+      hout[(oh * P28 + ow + u) * 2] =
+          make_uint2(pack_bf2(fmaxf(acc[0] + bsum[0], 0.f), fmaxf(acc[1] + bsum[1], 0.f)),
+                     pack_bf2(fmaxf(acc[2] + bsum[2], 0.f), fmaxf(acc[3] + bsum[3], 0.f)));
+    }
+    pw += 6;
+    oh += 2;
+    if (pw >= 13) {
+      pw -= 13;
+      oh += 1;
+    }
+  }
+#else
   int pos = tid >> 3, oh = pos / 26, ow = pos % 26;
   for (; pos < 676; pos += 32) {
     const float* xp = xs + oh * 28 + ow;
@@ -100,6 +139,7 @@ __global__ void __launch_bounds__(256, TLK_C1F_MINB) conv1_fwd_kernel(const Lane
       oh += 1 + wrap;
     }
   }
+#endif
 }
 
 // ------------------------------------------------------ fc1 fwd (TC) --------
