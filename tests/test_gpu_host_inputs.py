@@ -65,3 +65,34 @@ def test_cnn_host_blob():
         return np.concatenate([px.reshape(-1), lb.reshape(-1).view(np.uint8)])
 
     _run_pair(rt.MODEL_CNN, B, lanes, 3, blob)
+
+
+def test_cnn_host_async_then_params_without_sync():
+    """Pipelined host steps (tlk_step_host_async) leave the CNN's deferred fc1
+    wgrad + Adam of the last step in flight; tlk_lane_params must settle it
+    without an explicit tlk_sync: the parameters then equal those of the
+    device-input pack after the same steps, bit for bit."""
+    lanes, B, steps = 3, 64, 4
+    with rt.Context(0) as ctx:
+        dev = ctx.pack(rt.MODEL_CNN, B, lanes, steps)
+        host = ctx.pack(rt.MODEL_CNN, B, lanes, steps, host_input=True)
+        for p in (dev, host):
+            for lane in range(lanes):
+                p.load(lane, seed=700 + lane, steps=steps)
+        dev.run(steps)
+        outs = [np.zeros(lanes, np.float32) for _ in range(2)]
+        keep = []  # the host buffers of a step stay alive until its wait
+        prev = None
+        for t in range(steps):
+            px = np.ascontiguousarray(np.stack([orng.batch(700 + j, t, B)[0] for j in range(lanes)])
+                                      .astype(np.uint8).reshape(lanes, B, 784))
+            lb = np.ascontiguousarray(np.stack([orng.batch(700 + j, t, B)[1] for j in range(lanes)]).astype(np.int32))
+            keep.append((px, lb))
+            tk = host.step_host_async(px, lb, outs[t & 1])
+            if prev is not None:
+                host.step_host_wait(prev)
+            prev = tk
+        host.step_host_wait(prev)
+        for lane in range(lanes):  # no ctx.sync(): the lane call settles the deferred update
+            assert np.array_equal(dev.params(lane), host.params(lane)), lane
+            assert np.array_equal(dev.losses(lane, steps), host.losses(lane, steps)), lane
