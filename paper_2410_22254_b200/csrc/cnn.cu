@@ -707,6 +707,14 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
   if (!a.lanes[j].active) return;
   const LaneState s = a.lanes[j];
   const CnnOffs& o = a.o;
+  if (a.c2w_done) {  // flag join: the lane's conv2 wgrad partials (side branch) are complete
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = gtimer_ns();
+      while (ld_acquire_u32(a.c2w_done + j) < unsigned(C2W_SPLITS))
+        if (gtimer_ns() - t0 > 2000000000ull) __trap();  // 2 s: a lost producer is an error, not a hang
+    }
+    __syncthreads();
+  }
   if (int(blockIdx.x) < a.nheavy) {
     const int l = threadIdx.x & 31;
     const int h = (a.hb0 + blockIdx.x) * 8 + (threadIdx.x >> 5);  // 0..71 conv1.w, 72..79 conv1.b, 80..95 conv2.b
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
         const float* pp = buf.part2 + ((int64_t(j) * C2W_SPLITS * 9 + tap) * 64 + oc) * 32 + ic;
         float4 v[C2W_SPLITS];
 #pragma unroll
-        for (int k = 0; k < C2W_SPLITS; ++k) v[k] = *reinterpret_cast<const float4*>(pp + int64_t(k) * 9 * 64 * 32);
+        for (int k = 0; k < C2W_SPLITS; ++k) v[k] = __ldcg(reinterpret_cast<const float4*>(pp + int64_t(k) * 9 * 64 * 32));
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < C2W_SPLITS; ++k) acc.x += v[k].x, acc.y += v[k].y, acc.z += v[k].z, acc.w += v[k].w;
@@ -773,6 +781,7 @@ __global__ void __launch_bounds__(256) cnn_opt_kernel(const __grid_constant__ Cn
     if (prev == (a.total ? unsigned(a.total) : gridDim.x) - 1) {
       __threadfence();
       a.lanes[j].done_ctas = 0;
+      if (a.c2w_done) a.c2w_done[j] = 0;  // every CTA of the lane has passed its wait
       lane_end_step(a.lanes[j]);
     }
   }
@@ -831,7 +840,7 @@ int cnn_setup(Pack& p) {
   const size_t acts = size_t(L) * (4 * plane + 2 * b->p2_st + b->p2_st + 2 * 2 * b->h3_st +
                                    8 * plane + 4 * plane + 2 * b->p2_st) + 16 * 8;
   const size_t f32s = size_t(L) * (9216 + FC1_SPLITS * 128 * 64 + C2W_SPLITS * 9 * 64 * 32 +
-                                   B * 320 + HEAD_CL * 64 * CLASSES + 32) + 32 + 16;
+                                   B * 320 + HEAD_CL * 64 * CLASSES + 32) + 32 + 16 + L + 16;
   void* base = nullptr;
   int rc = pack_alloc(p, &base, acts + f32s * 4 + 256);
   if (rc) return rc;
@@ -859,6 +868,7 @@ int cnn_setup(Pack& p) {
   b->plog = reinterpret_cast<float*>(take(L * HEAD_CL * 64 * CLASSES * 4));
   b->sched = reinterpret_cast<uint32_t*>(take((L + 1) * 32 * 4));
   b->fwa_cnt = reinterpret_cast<uint32_t*>(take(64));
+  b->c2w_done = reinterpret_cast<uint32_t*>(take(L * 4));
   {  // TMA maps: lanes stacked as the outermost dimension
     const int64_t o_f1w = tensor_offset(*p.def, 4);
     const uint16_t* w1 = p.wbf + o_f1w;
@@ -922,7 +932,18 @@ int cnn_enqueue_step(Pack& p, cudaStream_t st) {
   const int64_t o_c2w = tensor_offset(d, 2), o_c2b = tensor_offset(d, 3);
   const int64_t o_f1w = tensor_offset(d, 4), o_f1b = tensor_offset(d, 5);
   const int64_t o_f2w = tensor_offset(d, 6), o_f2b = tensor_offset(d, 7);
-  const ConvArgs ca = conv_args(p, b);
+  // TLK_CNN_FLAG_JOIN=1: the optimizer waits for the side branch's
+  // conv2 wgrad through a per-lane completion count (conv2 wgrad CTAs
+  // release, the optimizer acquires; bounded spin) instead of an event join,
+  // so the conv1 wgrad -> optimizer edge keeps its programmatic launch; the
+  // side branch rejoins the stream after the optimizer.  The conv2 wgrad is
+  // launched ~70 us before the optimizer, so it is resident long before.
+  // Bit-identical, measured no faster (0.1732 vs 0.1728 ms/step): off.
+  static const bool flag_env = getenv("TLK_CNN_FLAG_JOIN") && getenv("TLK_CNN_FLAG_JOIN")[0] == '1';
+  const bool split_req = getenv("TLK_CNN_SPLIT_OPT") && getenv("TLK_CNN_SPLIT_OPT")[0] == '1';
+  const bool flag_join = flag_env && cnn_fork() && !p.prof && !split_req;
+  ConvArgs ca = conv_args(p, b);
+  if (flag_join) ca.c2w_done = b.c2w_done;
   int rc;
   TLK_CUDA(launch(conv1_fwd_kernel, dim3(B, L), 256, 0, st, p.lane_dev, p.teacher, p.pixels, p.labels, p.x,
                   p.host_input, p.params, p.stride, o_c1w, o_c1b, b));
@@ -1010,12 +1031,12 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   // TLK_CNN_JOIN_EARLY=1: join the side branch before the conv1 wgrad (the
   // conv1 wgrad -> optimizer edge stays a programmatic one) instead of after it
   static const bool join_early = getenv("TLK_CNN_JOIN_EARLY") && getenv("TLK_CNN_JOIN_EARLY")[0] == '1';
-  if (wst != st && join_early) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
+  if (wst != st && join_early && !flag_join) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   TLK_CUDA(launch(conv1_wgrad_kernel, dim3(B, L), C1W_THREADS, C1W_SMEM, st, p.lane_dev, b, p.x));
   p.mark(st, "conv1_wgrad");
   TLK_CUDA(cudaGetLastError());
   if (deferring && defer_at == 2) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, st, cudaEventRecordExternal));
-  if (wst != st && !join_early) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
+  if (wst != st && !join_early && !flag_join) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));
   // (a profile step times the kernel at the grid it has in the step)
   if (side_mode == 0 && (rc = enqueue_fwa(p, st, fwa_ctas(p, p.prof && cnn_fork() ? cnn_fwa_side() : 0))))
     return rc;
@@ -1023,6 +1044,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
            reinterpret_cast<float4*>(p.params), reinterpret_cast<float4*>(p.grads),
            reinterpret_cast<float4*>(p.mom1), reinterpret_cast<float4*>(p.mom2),
            reinterpret_cast<uint2*>(p.wbf), WtHook{p.wt, p.wt_stride, o_c2w, CONV2_W}};
+  if (flag_join && !split_opt) a.c2w_done = b.c2w_done;
   if (split_opt) {  // conv1 parameters only (their gradient is the chain's last one)
     a.hb0 = 0;
     a.nheavy = 10;
@@ -1034,6 +1056,7 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     p.mark(st, "grad_finalize_opt");
   }
   if (side_mode == 4) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_tail, 0));
+  if (flag_join) TLK_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0));  // the side branch rejoins at the end
   return enqueue_end_step(p, st);
 }
 

@@ -44,6 +44,7 @@ struct CnnBufs {
   // wgrad + Adam of step k can still read p2(k) while step k+1's forward runs
   uint16_t* p2_alt;
   uint32_t* fwa_cnt;  // fc1 wgrad + Adam: finished CTAs (the last one clears fc1_due)
+  uint32_t* c2w_done;  // [L] finished conv2 wgrad CTAs of the step (flag join; reset by the optimizer)
   uint8_t* idx;
   float *colsum, *part_fc1, *part2, *part1;
   float* plog;      // [L][HEAD_CL][64][10] partial logits of the 16-unit slices (persistent path)
@@ -88,6 +89,7 @@ struct CnnOpt {
   float4 *P, *Gr, *M, *V;
   uint2* Wb;
   WtHook hook;
+  uint32_t* c2w_done = nullptr;  // flag join: wait for C2W_SPLITS finished conv2 wgrad CTAs per lane
   // graph-path launch split (cnn.cu): heavy CTAs cover warps h = (hb0 + blockIdx.x) * 8 + w
   // for blockIdx.x < nheavy (h < 80: conv1, 80..95: conv2.b), the rest are light
   // CTAs; `total` CTAs per lane over every launch of the step end it (0: gridDim.x)

@@ -23,6 +23,9 @@ struct ConvArgs {
   int64_t pstride, b2_off;
   float* part2;          // conv2 wgrad partials [L][splits][9][64][32]
   int wgrad_splits;
+  // graph path, TLK_CNN_FLAG_JOIN: per-lane count of finished conv2 wgrad
+  // CTAs (release); the optimizer waits for it instead of an event join
+  uint32_t* c2w_done;
 };
 
 
@@ -417,6 +420,10 @@ static __global__ void __launch_bounds__(CONV_THREADS) conv2_wgrad_tc_kernel(Con
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<256>(tmem);
+  if (a.c2w_done && tid == 0) {  // this CTA's partials are written (release to the optimizer)
+    __threadfence();
+    atomicAdd(a.c2w_done + j, 1u);
+  }
 }
 
 }  // namespace tlk

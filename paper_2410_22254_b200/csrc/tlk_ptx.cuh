@@ -35,6 +35,18 @@ TLK_DEV void pdl_begin() {
 
 bool pdl_enabled();  // runtime.cu: TLK_PDL=0 disables the attribute
 
+// Acquire load of a flag another kernel releases (threadfence + atomic).
+TLK_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+TLK_DEV unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                           Args&&... args) {
