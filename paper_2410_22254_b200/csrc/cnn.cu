@@ -973,6 +973,15 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
   static const int defer_at = getenv("TLK_FWA_DEFER_AT") ? atoi(getenv("TLK_FWA_DEFER_AT")) : 1;
   const bool deferring = p.defer && !p.prof && cnn_fork() && cnn_fwa_side() == 3;
   if (deferring && defer_at == 0) TLK_CUDA(cudaEventRecordWithFlags(p.ev_defer_in, st, cudaEventRecordExternal));
+  // TLK_CNN_FORK_LATE=1: fork the conv2 wgrad branch after the conv2 dgrad
+  // (beside the conv1 wgrad) instead of after the fc1 dgrad
+  static const bool fork_late = getenv("TLK_CNN_FORK_LATE") && getenv("TLK_CNN_FORK_LATE")[0] == '1';
+  const bool dgrad_first = fork_late && cnn_fork() && !p.prof;
+  if (dgrad_first) {
+    TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
+    p.mark(st, "conv2_dgrad");
+    TLK_CUDA(cudaGetLastError());
+  }
   cudaStream_t wst = st;
   if (cnn_fork() && !p.prof) {
     TLK_CUDA(cudaEventRecord(p.ev_fork, st));
@@ -1003,9 +1012,11 @@ TLK_CUDA(launch(cnn_head_kernel, dim3(HEAD_CL, L), 256, 0, st, p.lane_dev, b, p.
     if ((rc = enqueue_fwa(p, wst, fwa_ctas(p, 4)))) return rc;
     TLK_CUDA(cudaEventRecord(p.ev_tail, wst));
   }
-  TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
-  p.mark(st, "conv2_dgrad");
-  TLK_CUDA(cudaGetLastError());
+  if (!dgrad_first) {
+    TLK_CUDA(launch(conv2_tc_kernel<false>, dim3(CONV_CTAS_PER_LANE, L), CONV_FD_THREADS, ConvPolicy<false>::SMEM, st, ca));
+    p.mark(st, "conv2_dgrad");
+    TLK_CUDA(cudaGetLastError());
+  }
   // TLK_CNN_SPLIT_OPT=1: the optimizer of every parameter but conv1's runs
   // on the side branch once the conv2 dgrad (which reads this step's conv2
   // weights) is done, beside the conv1 wgrad; the chain then ends with the

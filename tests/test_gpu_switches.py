@@ -44,7 +44,7 @@ def _curves(env, *args):
 @pytest.mark.parametrize("env", [{"TLK_PDL": "0"}, {"TLK_CNN_NOFORK": "1"}, {"TLK_CNN_FWA_SIDE": "0"},
                                  {"TLK_CNN_FWA_SIDE": "1"}, {"TLK_CNN_FWA_SIDE": "2", "TLK_FWA_CTAS": "37"},
                                  {"TLK_FWA_CTAS": "23"}, {"TLK_CNN_SPLIT_OPT": "1"}, {"TLK_FWA_DEFER_AT": "0"}, {"TLK_FWA_DEFER_AT": "2", "TLK_FWA_CTAS": "120"},
-                                 {"TLK_CNN_FWA_SIDE": "4"}, {"TLK_CNN_JOIN_EARLY": "1"}, {"TLK_CNN_FLAG_JOIN": "1"}])
+                                 {"TLK_CNN_FWA_SIDE": "4"}, {"TLK_CNN_JOIN_EARLY": "1"}, {"TLK_CNN_FLAG_JOIN": "1"}, {"TLK_CNN_FORK_LATE": "1"}])
 def test_launch_switches_are_bit_identical(env):
     base = _curves({}, "cnn", 3, 64, 6)
     assert np.array_equal(_curves(env, "cnn", 3, 64, 6), base)
